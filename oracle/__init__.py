@@ -1,0 +1,94 @@
+"""CPU oracle for the batched Eigen-benchmark update — TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+and ``--impl reference`` legs may import this package.  The product package
+``paper_1904_08555_b200`` never imports it (tests/test_boundary.py checks).
+
+The arithmetic lives in ``jm_oracle.c`` (plain C triple loop, compiled with
+``-O2 -ffp-contract=off``; see its header for the paper passages and the
+readings R1-R9).  This module only builds/loads it and marshals numpy arrays.
+
+Pinned by tests/test_oracle_pins.py (O1-O12 of SURVEY.md §8(c)); no function
+here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "jm_oracle.c")
+_LIB = os.path.join(_HERE, "libjm_oracle.so")
+_lock = threading.Lock()
+_lib = None
+
+ONES = 0
+IDENTITY = 1
+ADDENDS = {"ones": ONES, "identity": IDENTITY}
+
+
+def build(force: bool = False) -> str:
+    """Compile jm_oracle.c -> libjm_oracle.so (gcc, no fast-math, no FMA contraction)."""
+    if (not force and os.path.exists(_LIB)
+            and os.path.getmtime(_LIB) >= os.path.getmtime(_SRC)):
+        return _LIB
+    tmp = _LIB + f".tmp{os.getpid()}"
+    cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC",
+           "-shared", "-pthread", "-o", tmp, _SRC]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            lib.jm_oracle_run.restype = ctypes.c_int
+            lib.jm_oracle_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+            _lib = lib
+    return _lib
+
+
+def default_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def run(x: np.ndarray, repeat: int, addend: str | int = "ones",
+        threads: int | None = None) -> np.ndarray:
+    """Return f^repeat applied to every matrix of ``x`` (shape (batch, n, n)).
+
+    ``x`` must be float32 or float64; the update is computed in that type
+    (the element type is the template argument T).
+    """
+    lib = _load()
+    x = np.ascontiguousarray(x)
+    if x.ndim != 3 or x.shape[1] != x.shape[2]:
+        raise ValueError("expected (batch, n, n)")
+    if x.dtype == np.float32:
+        dt = 0
+    elif x.dtype == np.float64:
+        dt = 1
+    else:
+        raise ValueError("oracle supports float32/float64")
+    a = ADDENDS[addend] if isinstance(addend, str) else int(addend)
+    batch, n, _ = x.shape
+    out = np.empty_like(x)
+    th = default_threads() if threads is None else int(threads)
+    rc = lib.jm_oracle_run(n, dt, a, batch, int(repeat),
+                           x.ctypes.data_as(ctypes.c_void_p),
+                           out.ctypes.data_as(ctypes.c_void_p), th)
+    if rc != 0:
+        raise ValueError(f"jm_oracle_run rejected arguments (rc={rc})")
+    return out

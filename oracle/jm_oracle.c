@@ -1,0 +1,147 @@
+/*
+ * jm_oracle.c — plain, slow, obviously-correct CPU ORACLE for the Eigen
+ * benchmark update of ClangJIT (Finkel, Poliakoff, Richards, arXiv 1904.08555).
+ *
+ *   TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ *   bench.py's cpu_baseline / --impl reference legs may load this library.
+ *   The product path (paper_1904_08555_b200/) never links, imports or calls
+ *   it, and shares no code, header, constant or helper with it.
+ *
+ * What it computes (PAPER.md:362 prose; Listing 4; Listing 5
+ * lines 406-408):
+ *
+ *     for r < repeat:   m = Ones + T(0.00005) * (m + (m*m))
+ *
+ * applied independently to each of `batch` n-by-n matrices, in the element
+ * type T the caller names (float or double).  Readings
+ * taken where the paper is silent:
+ *   R1 (Q1) the addend is the listings' Matrix::Ones (all-ones J); the prose
+ *           "I" (identity) is offered as addend=1.
+ *   R2 (Q2) c = T(0.00005): the literal is rounded to T before use.
+ *   R6 (Q6) the product sums k in ascending order with a separate multiply
+ *           and add (this file is compiled with -ffp-contract=off, no
+ *           -ffast-math, IEEE denormals).
+ *   R7 (Q7) elementwise order: t = m + p; u = c*t; r = A + u  (as written).
+ *   R8 (Q8) m*m is formed from the PRE-update m (Eigen evaluates products
+ *           into a temporary), so the update is simultaneous.
+ *   R5 (Q5) buffers are read as row-major m[i][j] = in[i*n + j]; reading them
+ *           column-major gives the transposed result bitwise (O9), so both
+ *           storage readings agree on the flat buffer.
+ *   R9 (Q9) IEEE inf/NaN propagate; there is no convergence early exit.
+ *
+ * Pins (tests/test_oracle_pins.py): O1 SPEC.md:537 worked example, O3 the
+ * hand-expanded n=2 step, O4/O5 closed-form fixed points, O6/O7/O8 invariant
+ * families, O9 transpose equivariance, O10 exact rational brute force for
+ * n=1..4, O11 R=0 / batch independence, O12 divergence for n>=35.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+#define ORACLE_F32 0
+#define ORACLE_F64 1
+#define ORACLE_ONES 0
+#define ORACLE_IDENTITY 1
+
+/* One update m -> r of one matrix, type double. */
+static void step_f64(int n, int addend, const double *m, double *r) {
+    const double c = (double)0.00005;
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) {
+            double p = 0.0;
+            for (int k = 0; k < n; ++k) {      /* (m*m)(i,j), ascending k */
+                double prod = m[i * n + k] * m[k * n + j];
+                p = p + prod;
+            }
+            double t = m[i * n + j] + p;        /* m + m*m */
+            double u = c * t;                   /* T(0.00005) * (...) */
+            /* Ones + u, or (prose reading) I + u */
+            r[i * n + j] = (addend == ORACLE_ONES || i == j) ? 1.0 + u : u;
+        }
+    }
+}
+
+/* Same, type float: every operation rounds to float (T = float). */
+static void step_f32(int n, int addend, const float *m, float *r) {
+    const float c = (float)0.00005;
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) {
+            float p = 0.0f;
+            for (int k = 0; k < n; ++k) {
+                float prod = m[i * n + k] * m[k * n + j];
+                p = p + prod;
+            }
+            float t = m[i * n + j] + p;
+            float u = c * t;
+            r[i * n + j] = (addend == ORACLE_ONES || i == j) ? 1.0f + u : u;
+        }
+    }
+}
+
+typedef struct {
+    int n, dtype, addend;
+    int64_t b0, b1, repeat;
+    const void *in;
+    void *out;
+} job_t;
+
+static void *run_range(void *arg) {
+    job_t *j = (job_t *)arg;
+    const int n = j->n;
+    const size_t nn = (size_t)n * (size_t)n;
+    if (j->dtype == ORACLE_F64) {
+        double *a = (double *)malloc(nn * sizeof(double));
+        double *b = (double *)malloc(nn * sizeof(double));
+        for (int64_t bi = j->b0; bi < j->b1; ++bi) {
+            memcpy(a, (const double *)j->in + (size_t)bi * nn, nn * sizeof(double));
+            for (int64_t r = 0; r < j->repeat; ++r) {
+                step_f64(n, j->addend, a, b);
+                double *t = a; a = b; b = t;    /* m = r */
+            }
+            memcpy((double *)j->out + (size_t)bi * nn, a, nn * sizeof(double));
+        }
+        free(a); free(b);
+    } else {
+        float *a = (float *)malloc(nn * sizeof(float));
+        float *b = (float *)malloc(nn * sizeof(float));
+        for (int64_t bi = j->b0; bi < j->b1; ++bi) {
+            memcpy(a, (const float *)j->in + (size_t)bi * nn, nn * sizeof(float));
+            for (int64_t r = 0; r < j->repeat; ++r) {
+                step_f32(n, j->addend, a, b);
+                float *t = a; a = b; b = t;
+            }
+            memcpy((float *)j->out + (size_t)bi * nn, a, nn * sizeof(float));
+        }
+        free(a); free(b);
+    }
+    return NULL;
+}
+
+/*
+ * out[b] = f^repeat(in[b]) for b in [0, batch).  `in` and `out` are host
+ * buffers of batch*n*n elements of the named type; they may be the same
+ * buffer.  threads <= 0 means 1.  Returns 0, or -1 on bad arguments.
+ */
+int jm_oracle_run(int n, int dtype, int addend, int64_t batch, int64_t repeat,
+                  const void *in, void *out, int threads) {
+    if (n < 1 || batch < 0 || repeat < 0) return -1;
+    if (dtype != ORACLE_F32 && dtype != ORACLE_F64) return -1;
+    if (addend != ORACLE_ONES && addend != ORACLE_IDENTITY) return -1;
+    if (batch == 0) return 0;
+    if (threads < 1) threads = 1;
+    if ((int64_t)threads > batch) threads = (int)batch;
+    job_t *jobs = (job_t *)calloc((size_t)threads, sizeof(job_t));
+    pthread_t *tids = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    for (int t = 0; t < threads; ++t) {
+        jobs[t].n = n; jobs[t].dtype = dtype; jobs[t].addend = addend;
+        jobs[t].b0 = batch * t / threads;
+        jobs[t].b1 = batch * (t + 1) / threads;
+        jobs[t].repeat = repeat; jobs[t].in = in; jobs[t].out = out;
+    }
+    for (int t = 1; t < threads; ++t) pthread_create(&tids[t], NULL, run_range, &jobs[t]);
+    run_range(&jobs[0]);
+    for (int t = 1; t < threads; ++t) pthread_join(tids[t], NULL);
+    free(jobs); free(tids);
+    return 0;
+}
