@@ -1,0 +1,217 @@
+/*
+ * jit_mat.h — C ABI of libjitmat: the batched, runtime-specialized Eigen
+ * benchmark update of ClangJIT (Finkel, Poliakoff, Richards, arXiv 1904.08555)
+ * on NVIDIA B200 (sm_100a).
+ *
+ * THE OPERATION (Listing 4, Listing 5 lines
+ * 406-408):  for every matrix b in [0, batch)
+ *
+ *     M <- A + c * (M + M*M)      repeated `repeat` times,   c = T(0.00005)
+ *
+ * with A = Ones (the all-ones matrix the listings add; default) or, under the
+ * prose reading of PAPER.md:362, A = I.  M*M is formed from the pre-update M
+ * (Eigen evaluates products into a temporary).  There is no convergence early
+ * exit.  T is float or double, chosen at run time by name like Listing 4's
+ * test_aot(std::string &type, ...) and Listing 5's
+ * test_jit.
+ *
+ * THE SPECIALIZATION (§2, §4 Algorithm 1 lines
+ * 308-349, §4.1): the first call for a key {n, dtype, addend,
+ * kind} instantiates the kernel template for that N and T through NVRTC —
+ * from source embedded in the library, no file-system access (PAPER.md:83,
+ * 351) — straight to an sm_100a cubin, loads it, and caches the function in a
+ * process-global table (Algorithm 1 lines 319 and 347).  Later
+ * calls with the same key hit the cache.  The GENERIC kind is a runtime-N
+ * kernel compiled ahead of time (the analog of Listing 4's dynamic-size
+ * path); it never compiles at run time.
+ *
+ * LAYOUT: `in` and `out` each hold `batch` matrices of n*n elements of type T,
+ * contiguous, no padding between matrices (element (i,j) of matrix b at
+ * b*n*n + i*n + j, or the column-major reading — both give the same buffer
+ * result because f(M^T) = f(M)^T).
+ *
+ * OWNERSHIP: the library never allocates or frees caller memory and keeps no
+ * reference to `in`/`out` after the work it enqueued completes.  `in == out`
+ * (exact alias) is allowed; a partial overlap is JM_E_INVALID.
+ *
+ * ERRORS (an answer to PAPER.md:806, "no place to get out an error"): every
+ * entry returns JM_OK (0) or a negative JM_E_* code; nothing aborts and no
+ * exception crosses the ABI.  jit_mat_last_error() returns a thread-local
+ * message (with the NVRTC log on JM_E_COMPILE).  Argument and compile errors
+ * are detected before anything is enqueued.  Kernel faults are asynchronous
+ * and surface at the caller's next synchronization, or at once with
+ * JM_FLAG_SYNC / environment JIT_MAT_SYNC=1.  There is no CPU fallback: a
+ * device that is not compute capability 10.x is JM_E_ARCH.
+ *
+ * THREADING: every function is thread-safe.  The first call for a key blocks
+ * the calling host thread while it compiles (as __clang_jit does); concurrent
+ * callers of the same key wait for that one compile; distinct keys compile in
+ * parallel.  One process drives one device (jit_mat_init's).
+ */
+#ifndef JIT_MAT_H
+#define JIT_MAT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(JM_BUILDING_LIB) && defined(__GNUC__)
+#define JM_API __attribute__((visibility("default")))
+#else
+#define JM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element types: the names of Listing 4's type switch */
+enum { JM_F32 = 0, JM_F64 = 1 };
+
+/* addend A: the listings' Matrix::Ones (default) or the prose "I" */
+enum { JM_ADDEND_ONES = 0, JM_ADDEND_IDENTITY = 1 };
+
+/* kernel kind: the NVRTC-specialized template (Listing 5) or the AoT
+ * runtime-N generic kernel (Listing 4) */
+enum { JM_KIND_SPECIALIZED = 0, JM_KIND_GENERIC = 1 };
+
+/* status codes */
+enum {
+  JM_OK = 0,
+  JM_E_INVALID = -1,          /* bad argument (n <= 0, batch < 0, repeat out of range, NULL, overlap) */
+  JM_E_UNSUPPORTED = -2,      /* n > 64, dtype not f32/f64 ("long double"), unknown type name */
+  JM_E_NOT_INITIALIZED = -3,  /* jit_mat_init not called, or after jit_mat_shutdown */
+  JM_E_ARCH = -4,             /* device is not sm_100 (compute capability 10.x) */
+  JM_E_COMPILE = -5,          /* NVRTC or module load failed; log in jit_mat_last_error() */
+  JM_E_CUDA = -6,             /* CUDA driver error (message in jit_mat_last_error()) */
+  JM_E_ALIGN = -7             /* in/out not 16-byte aligned */
+};
+
+#define JM_N_MAX 64
+#define JM_REPEAT_MAX 2147483647LL
+
+/* run flags */
+#define JM_FLAG_SYNC 1u          /* synchronize the stream before returning; report kernel faults */
+#define JM_FLAG_HOST_BUFFERS 2u  /* in/out are HOST pointers: the library stages them through
+                                    device buffers it owns, chunked and overlapped (see run_host) */
+
+/* Initialise for `device` (-1 = the calling thread's current CUDA device, else
+ * device 0).  Loads the CUDA driver, retains the device's primary context (the
+ * one PyTorch uses), checks compute capability 10.x (else JM_E_ARCH), loads the
+ * ahead-of-time generic and auxiliary kernels and pre-seeds the generic cache
+ * slots.  No NVRTC work.  Idempotent for the same device; a different device
+ * while initialised is JM_E_INVALID. */
+JM_API int jit_mat_init(int device);
+
+/* out[b] = f^repeat(in[b]) for b in [0, batch): the specialized kernel for
+ * (n, dtype), addend Ones, on the stream set by jit_mat_set_stream (default:
+ * the legacy default stream).  `in`/`out` are device pointers (16-byte
+ * aligned) on the initialised device.  n in [1, 64]; batch >= 0 (0: no-op);
+ * repeat in [0, 2^31) (0: out is a bitwise copy of in).  Asynchronous. */
+JM_API int jit_mat_run(int n, int dtype, int64_t batch, int64_t repeat, const void *in, void *out);
+
+/* Unload every module, drop the cache and release the primary context.  Later
+ * calls return JM_E_NOT_INITIALIZED until jit_mat_init is called again. */
+JM_API int jit_mat_shutdown(void);
+
+/* ---- extensions ---------------------------------------------------------- */
+
+typedef struct {
+  int n, dtype, addend, kind;
+  int64_t batch, repeat;
+  const void *in;
+  void *out;
+  void *stream;      /* CUstream / cudaStream_t; NULL = the stream set by jit_mat_set_stream */
+  unsigned flags;    /* JM_FLAG_* */
+} jm_run_desc;
+
+/* General entry: any addend / kind / stream / flags.  With JM_FLAG_HOST_BUFFERS
+ * `in`/`out` are host pointers (pinned or pageable) and the call is
+ * synchronous: the input streams host->device in chunks, each chunk is updated
+ * on the device, and results stream back, with copies and compute overlapped on
+ * library-owned streams and staging buffers. */
+JM_API int jit_mat_run_ex(const jm_run_desc *d);
+
+/* Convenience for the host-buffer path = run_ex(kind SPECIALIZED, addend Ones,
+ * JM_FLAG_HOST_BUFFERS).  Synchronous. */
+JM_API int jit_mat_run_host(int n, int dtype, int64_t batch, int64_t repeat, const void *in, void *out);
+
+/* Stream used by jit_mat_run (e.g. torch.cuda.current_stream().cuda_stream). */
+JM_API int jit_mat_set_stream(void *cuda_stream);
+
+/* Look up (and on a miss, compile and load) the kernel for a key without
+ * launching.  The analog of forcing an instantiation ahead of use. */
+JM_API int jit_mat_prepare(int n, int dtype, int addend, int kind);
+
+/* "float" -> JM_F32, "double" -> JM_F64; "long double" and anything else ->
+ * JM_E_UNSUPPORTED (the GPU path supports two of Listing 4's three types). */
+JM_API int jit_mat_dtype_from_name(const char *name);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+JM_API const char *jit_mat_last_error(void);
+
+/* Cache statistics (SPEC.md:540-545 analog). */
+typedef struct {
+  int64_t compilations;      /* NVRTC compiles performed (successful or not) */
+  int64_t hits;              /* lookups answered from the cache */
+  int64_t misses;            /* lookups that had to compile (or wait for a compile) */
+  int64_t launches;          /* kernels launched by this library */
+  double compile_ms_total;   /* wall time inside NVRTC + module load */
+  int32_t keys_ready;        /* cache slots in READY state */
+  int32_t keys_failed;       /* cache slots in FAILED state */
+} jm_stats;
+
+typedef struct {
+  int32_t n, dtype, addend, kind;
+  int32_t state;             /* 0 empty, 1 compiling, 2 ready, 3 failed */
+  int32_t regs;              /* CU_FUNC_ATTRIBUTE_NUM_REGS (the Fig. 5 analog) */
+  int32_t local_bytes;       /* CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES (spills) */
+  int32_t smem_bytes;        /* dynamic shared memory per CTA of the launch plan */
+  int32_t threads;           /* threads per CTA of the launch plan */
+  int32_t tile;              /* tiling kind (JM_TILE_*) chosen by the planner */
+  int64_t cubin_bytes;
+  double compile_ms;
+} jm_key_info;
+
+/* tiling kinds reported in jm_key_info.tile */
+enum { JM_TILE_GENERIC = 0, JM_TILE_TPM = 1, JM_TILE_WARP_DMMA = 2, JM_TILE_CTA_DMMA = 3,
+       JM_TILE_WARP_F32 = 4, JM_TILE_CTA_F32 = 5, JM_TILE_ROWS = 6 };
+
+JM_API int jit_mat_stats(jm_stats *out);
+/* Copy up to `cap` non-empty slots into `keys`; returns the number of
+ * non-empty slots (may exceed cap). */
+JM_API int jit_mat_key_info(jm_key_info *keys, int cap);
+/* Reset counters (not the cache). */
+JM_API int jit_mat_reset_stats(void);
+
+/* ---- driver support (untimed plumbing) ----------- */
+
+/* Fill out[0 .. batch*n*n) on the device with the counter-hash input generator
+ * keyed by the GLOBAL matrix index (global_first + b), so a batch split across
+ * ranks equals the unsplit batch.  dist: 0 paper (iota), 1 bench (U[-1,1)),
+ * 2 hard (U[0,1) * 2*4000/n).  The definition is written out in
+ * jm_synth/__init__.py (host side); this is an independent device
+ * implementation of the same definition.  Asynchronous on the set stream. */
+JM_API int jit_mat_fill(int n, int dtype, int dist, uint64_t seed, int64_t global_first,
+                 int64_t batch, void *out);
+
+/* Order-independent checksum of x[0 .. batch*n*n):
+ *   S = sum_e splitmix64(bits(x_e) ^ PHI*(global_first*n*n + e)) mod 2^64,
+ * plus the plain f64 sum.  Synchronous; results written to host pointers. */
+JM_API int jit_mat_checksum(int n, int dtype, int64_t global_first, int64_t batch, const void *x,
+                     uint64_t *host_u64, double *host_f64);
+
+/* Device / library facts: SM count, CC major/minor, library version string. */
+JM_API int jit_mat_device_info(int *sm_count, int *cc_major, int *cc_minor);
+JM_API const char *jit_mat_version(void);
+
+/* ---- test hook ------------------------------------------------------------ */
+
+/* NVRTC-compile the specialized kernel for a key to an sm_100a cubin WITHOUT a
+ * device or jit_mat_init (nothing is loaded or cached).  Lets a CPU-only test
+ * tier prove that every specialization compiles.  cubin_bytes may be NULL. */
+JM_API int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JIT_MAT_H */

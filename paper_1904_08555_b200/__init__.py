@@ -1,0 +1,183 @@
+"""paper_1904_08555_b200 — JIT-specialized batched small-matrix update on B200.
+
+A thin ctypes binding over ``libjitmat.so`` (C ABI: ``include/jit_mat.h``).
+Every name below mirrors the C entry point of the same name; the functions do
+argument marshalling only — all work (NVRTC specialization, caching, every
+kernel) happens inside the library.  There is no CPU fallback: if the library
+is missing the import fails, and without a B200 ``jit_mat_init`` returns
+``JM_E_ARCH`` / ``JM_E_CUDA``.
+
+The operation is the Eigen benchmark update of ClangJIT (arXiv 1904.08555,
+PAPER.md:362, Listings 4/5 lines 364-414): ``M <- Ones + T(0.00005)*(M + M*M)``
+repeated ``repeat`` times on each of ``batch`` independent N x N matrices.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from ._lib import (  # noqa: F401  (re-exported C ABI)
+    JM_ADDEND_IDENTITY, JM_ADDEND_ONES, JM_E_ALIGN, JM_E_ARCH, JM_E_COMPILE, JM_E_CUDA,
+    JM_E_INVALID, JM_E_NOT_INITIALIZED, JM_E_UNSUPPORTED, JM_F32, JM_F64, JM_FLAG_HOST_BUFFERS,
+    JM_FLAG_SYNC, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK, JM_TILE_NAMES, JitMatError,
+    jm_key_info, jm_run_desc, jm_stats, lib, lib_path,
+)
+
+__all__ = [
+    "jit_mat_init", "jit_mat_run", "jit_mat_shutdown", "jit_mat_run_ex", "jit_mat_run_host",
+    "jit_mat_set_stream", "jit_mat_prepare", "jit_mat_dtype_from_name", "jit_mat_last_error",
+    "jit_mat_stats", "jit_mat_key_info", "jit_mat_reset_stats", "jit_mat_fill",
+    "jit_mat_checksum", "jit_mat_device_info", "jit_mat_version", "jit_mat_compile_check",
+    "run", "JitMatError",
+]
+
+_DTYPES = {"float": JM_F32, "f32": JM_F32, "float32": JM_F32,
+           "double": JM_F64, "f64": JM_F64, "float64": JM_F64}
+_ADDENDS = {"ones": JM_ADDEND_ONES, "identity": JM_ADDEND_IDENTITY}
+_KINDS = {"specialized": JM_KIND_SPECIALIZED, "generic": JM_KIND_GENERIC}
+
+
+def _check(rc: int, what: str) -> int:
+    if rc < 0:
+        raise JitMatError(rc, f"{what}: {jit_mat_last_error()}")
+    return rc
+
+
+def _dt(dtype) -> int:
+    if isinstance(dtype, int):
+        return dtype
+    name = getattr(dtype, "__name__", None) or str(dtype).replace("torch.", "")
+    if name in _DTYPES:
+        return _DTYPES[name]
+    return _check(lib.jit_mat_dtype_from_name(str(dtype).encode()), "dtype")
+
+
+# ---------------------------------------------------------------- C ABI mirror
+def jit_mat_init(device: int = -1) -> None:
+    _check(lib.jit_mat_init(int(device)), "jit_mat_init")
+
+
+def jit_mat_shutdown() -> None:
+    _check(lib.jit_mat_shutdown(), "jit_mat_shutdown")
+
+
+def jit_mat_run(n: int, dtype, batch: int, repeat: int, in_ptr: int, out_ptr: int) -> None:
+    _check(lib.jit_mat_run(int(n), _dt(dtype), int(batch), int(repeat), ctypes.c_void_p(in_ptr),
+                           ctypes.c_void_p(out_ptr)), "jit_mat_run")
+
+
+def jit_mat_run_ex(n: int, dtype, batch: int, repeat: int, in_ptr: int, out_ptr: int, *,
+                   addend="ones", kind="specialized", stream: int | None = None,
+                   flags: int = 0) -> None:
+    d = jm_run_desc(int(n), _dt(dtype), _ADDENDS.get(addend, addend), _KINDS.get(kind, kind),
+                    int(batch), int(repeat), ctypes.c_void_p(in_ptr), ctypes.c_void_p(out_ptr),
+                    ctypes.c_void_p(stream or 0), int(flags))
+    _check(lib.jit_mat_run_ex(ctypes.byref(d)), "jit_mat_run_ex")
+
+
+def jit_mat_run_host(n: int, dtype, batch: int, repeat: int, in_ptr: int, out_ptr: int) -> None:
+    _check(lib.jit_mat_run_host(int(n), _dt(dtype), int(batch), int(repeat),
+                                ctypes.c_void_p(in_ptr), ctypes.c_void_p(out_ptr)),
+           "jit_mat_run_host")
+
+
+def jit_mat_set_stream(stream: int | None) -> None:
+    _check(lib.jit_mat_set_stream(ctypes.c_void_p(stream or 0)), "jit_mat_set_stream")
+
+
+def jit_mat_prepare(n: int, dtype, addend="ones", kind="specialized") -> None:
+    _check(lib.jit_mat_prepare(int(n), _dt(dtype), _ADDENDS.get(addend, addend),
+                               _KINDS.get(kind, kind)), "jit_mat_prepare")
+
+
+def jit_mat_dtype_from_name(name: str) -> int:
+    return lib.jit_mat_dtype_from_name(name.encode())
+
+
+def jit_mat_last_error() -> str:
+    return lib.jit_mat_last_error().decode(errors="replace")
+
+
+def jit_mat_stats() -> dict:
+    s = jm_stats()
+    _check(lib.jit_mat_stats(ctypes.byref(s)), "jit_mat_stats")
+    return {f: getattr(s, f) for f, _ in jm_stats._fields_}
+
+
+def jit_mat_key_info() -> list[dict]:
+    cnt = lib.jit_mat_key_info(None, 0)
+    arr = (jm_key_info * max(cnt, 1))()
+    cnt = lib.jit_mat_key_info(arr, cnt)
+    out = []
+    for i in range(cnt):
+        d = {f: getattr(arr[i], f) for f, _ in jm_key_info._fields_}
+        d["tile_name"] = JM_TILE_NAMES.get(d["tile"], "?")
+        out.append(d)
+    return out
+
+
+def jit_mat_reset_stats() -> None:
+    _check(lib.jit_mat_reset_stats(), "jit_mat_reset_stats")
+
+
+def jit_mat_fill(n: int, dtype, dist: int, seed: int, global_first: int, batch: int,
+                 out_ptr: int) -> None:
+    _check(lib.jit_mat_fill(int(n), _dt(dtype), int(dist), ctypes.c_uint64(seed),
+                            int(global_first), int(batch), ctypes.c_void_p(out_ptr)),
+           "jit_mat_fill")
+
+
+def jit_mat_checksum(n: int, dtype, global_first: int, batch: int, x_ptr: int) -> tuple[int, float]:
+    u = ctypes.c_uint64(0)
+    f = ctypes.c_double(0.0)
+    _check(lib.jit_mat_checksum(int(n), _dt(dtype), int(global_first), int(batch),
+                                ctypes.c_void_p(x_ptr), ctypes.byref(u), ctypes.byref(f)),
+           "jit_mat_checksum")
+    return int(u.value), float(f.value)
+
+
+def jit_mat_device_info() -> dict:
+    sm, ma, mi = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _check(lib.jit_mat_device_info(ctypes.byref(sm), ctypes.byref(ma), ctypes.byref(mi)),
+           "jit_mat_device_info")
+    return {"sm_count": sm.value, "cc": (ma.value, mi.value)}
+
+
+def jit_mat_version() -> str:
+    return lib.jit_mat_version().decode()
+
+
+def jit_mat_compile_check(n: int, dtype, addend="ones") -> int:
+    cb = ctypes.c_longlong(0)
+    _check(lib.jit_mat_compile_check(int(n), _dt(dtype), _ADDENDS.get(addend, addend),
+                                     ctypes.byref(cb)), "jit_mat_compile_check")
+    return int(cb.value)
+
+
+# ---------------------------------------------------------------- convenience
+def run(x, repeat: int, out=None, *, addend: str = "ones", kind: str = "specialized",
+        stream=None, sync: bool = False):
+    """Apply the update to a CUDA tensor ``x`` of shape (batch, n, n) (float32/float64).
+
+    Marshals the tensor pointers into :func:`jit_mat_run_ex`; ``out`` may be ``x``
+    (in place).  Runs on ``stream`` (default: torch's current stream).
+    """
+    import torch
+
+    if x.dim() != 3 or x.shape[1] != x.shape[2]:
+        raise ValueError("expected a (batch, n, n) tensor")
+    if not x.is_cuda or not x.is_contiguous():
+        raise ValueError("expected a contiguous CUDA tensor")
+    if out is None:
+        out = torch.empty_like(x)
+    if out.shape != x.shape or out.dtype != x.dtype or not out.is_contiguous():
+        raise ValueError("out must match x")
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    jit_mat_run_ex(x.shape[1], str(x.dtype), x.shape[0], repeat, x.data_ptr(), out.data_ptr(),
+                   addend=addend, kind=kind, stream=st.cuda_stream,
+                   flags=JM_FLAG_SYNC if sync else 0)
+    return out
+
+
+def _selftest_loaded() -> str:
+    return os.path.abspath(lib_path)

@@ -1,0 +1,105 @@
+// jm_plan.h — launch/tiling plan shared by the host runtime (g++) and the
+// device kernels (nvcc and NVRTC).  Pure constexpr C++: no CUDA, no std headers
+// (NVRTC compiles it from the in-library source string).
+//
+// The plan picks, per (N, dtype), how a batch of independent N x N matrices is
+// mapped onto the B200:
+//   TPM   thread-per-matrix, whole matrix in registers      f64 N<=6, f32 N<=8
+//   DMMA  FP64 tensor-core DMMA.8x8x4 (mma.sync m8n8k4.f64), N padded to 8k;
+//         W warps per matrix (W=1 for N<=32, else one CTA per matrix)
+//   F32   FP32 register-tiled outer products with FFMA2, W warps per matrix
+//   GENERIC the AoT runtime-N kernel (never NVRTC-compiled)
+#ifndef JM_PLAN_H
+#define JM_PLAN_H
+
+#if defined(__CUDACC__) || defined(__CUDACC_RTC__)
+#define JM_HD __host__ __device__
+#else
+#define JM_HD
+#endif
+
+namespace jm {
+
+enum class Addend : int { Ones = 0, Identity = 1 };
+enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, F32 = 4 };
+
+struct Plan {
+  int tile;      // Tile
+  int threads;   // threads per CTA
+  int mpc;       // matrices per CTA chunk
+  int smem;      // dynamic shared memory bytes per CTA
+  int w;         // warps cooperating on one matrix
+};
+
+JM_HD constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+JM_HD constexpr int rup(int a, int b) { return cdiv(a, b) * b; }
+
+// Bytes per matrix in a shared-memory staging area.  When the matrix is a
+// multiple of 16 B the stride is an ODD multiple of 16 B, so a thread-per-matrix
+// read of 16-B pieces is bank-conflict free; otherwise (odd N) the matrices are
+// packed and element reads at an odd element stride are conflict free.
+JM_HD constexpr int stage_stride(int n, int es) {
+  return ((n * n * es) % 16) ? n * n * es
+                             : ((((n * n * es) / 16) & 1) ? n * n * es : n * n * es + 16);
+}
+
+// A chunk's staging area, rounded to 16 B so the buffers after it stay aligned.
+JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage_stride(n, es), 16); }
+
+JM_HD constexpr Tile tile_for(int n, int dtype) {
+  return dtype == 1 ? (n <= 6 ? Tile::TPM : Tile::Dmma) : (n <= 8 ? Tile::TPM : Tile::F32);
+}
+
+// ---- TPM ----
+constexpr int TPM_THREADS = 128;
+
+// ---- DMMA (FP64) ----
+constexpr int DMMA_WPC = 4;                       // warps per CTA when W == 1
+JM_HD constexpr int dmma_t8(int n) { return cdiv(n, 8); }
+JM_HD constexpr int dmma_rt(int n) { return n <= 32 ? dmma_t8(n) : ((dmma_t8(n) % 2 == 0) ? 2 : 1); }
+JM_HD constexpr int dmma_w(int n) { return dmma_t8(n) / dmma_rt(n); }
+JM_HD constexpr int dmma_rsc(int n) { return rup(4 * dmma_t8(n), 8); }     // scratch row stride, 16-B chunks
+JM_HD constexpr int dmma_scr(int n) { return 8 * dmma_t8(n) * dmma_rsc(n) * 16; }  // one scratch buffer
+
+// ---- F32 tiles ----
+JM_HD constexpr int f32_w(int n) { return n <= 32 ? 1 : 4; }
+constexpr int F32_WPC = 4;                        // warps per CTA when W == 1
+JM_HD constexpr int f32_rg(int n) { return f32_w(n) == 1 ? 8 : 16; }   // thread rows
+JM_HD constexpr int f32_cg(int n) { return f32_w(n) == 1 ? 4 : 8; }    // thread cols
+JM_HD constexpr int f32_ra(int n) { return cdiv(n, f32_rg(n)); }       // rows per thread
+JM_HD constexpr int f32_cb(int n) { return rup(cdiv(n, f32_cg(n)), 2); }  // cols per thread (even: FFMA2)
+JM_HD constexpr int f32_ldm(int n) { return f32_cg(n) * f32_cb(n) + 4; }  // sM row stride (floats)
+JM_HD constexpr int f32_ldt(int n) { return f32_rg(n) * f32_ra(n) + 4; }  // sMT row stride (floats)
+JM_HD constexpr int f32_buf(int n) { return n * (f32_ldm(n) + f32_ldt(n)) * 4; }  // one M + M^T buffer
+
+JM_HD constexpr Plan plan_specialized(int n, int dtype) {
+  const int es = dtype == 1 ? 8 : 4;
+  const Tile t = tile_for(n, dtype);
+  if (t == Tile::TPM) {
+    return Plan{(int)t, TPM_THREADS, TPM_THREADS, stage_bytes(TPM_THREADS, n, es), 1};
+  }
+  if (t == Tile::Dmma) {
+    const int w = dmma_w(n);
+    if (w == 1)
+      return Plan{(int)t, 32 * DMMA_WPC, DMMA_WPC,
+                  stage_bytes(DMMA_WPC, n, es) + DMMA_WPC * dmma_scr(n), 1};
+    return Plan{(int)t, 32 * w, 1, stage_bytes(1, n, es) + 2 * dmma_scr(n), w};
+  }
+  const int w = f32_w(n);
+  if (w == 1)
+    return Plan{(int)t, 32 * F32_WPC, F32_WPC,
+                stage_bytes(F32_WPC, n, es) + F32_WPC * f32_buf(n), 1};
+  return Plan{(int)t, 32 * w, 1, stage_bytes(1, n, es) + 2 * f32_buf(n), w};
+}
+
+// ---- GENERIC (runtime N; AoT) ----
+constexpr int GENERIC_THREADS = 256;
+JM_HD constexpr int generic_mpc(int n) { return (n * n >= GENERIC_THREADS) ? 1 : GENERIC_THREADS / (n * n); }
+JM_HD constexpr Plan plan_generic(int n, int dtype) {
+  // staging area + product buffer, both packed n*n per matrix
+  return Plan{(int)Tile::Generic, GENERIC_THREADS, generic_mpc(n),
+              2 * generic_mpc(n) * n * n * (dtype == 1 ? 8 : 4), 1};
+}
+
+}  // namespace jm
+#endif  // JM_PLAN_H

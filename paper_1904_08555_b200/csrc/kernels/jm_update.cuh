@@ -1,0 +1,509 @@
+// jm_update.cuh — device kernels for the batched Eigen-benchmark update
+//
+//     M <- A + c * (M + M*M),  c = T(0.00005),  repeated `repeat` times
+//
+// (Listing 4; Listing 5) over
+// `batch` independent N x N matrices.  This text is embedded in libjitmat and
+// compiled at run time by NVRTC, once per key {N, T, addend} — the B200 analog
+// of ClangJIT instantiating `test_jit_sz<type, size>` on first use (Listing 5,
+// PAPER.md:397-413; Algorithm 1).  It must stay free of
+// #include so NVRTC never touches the file system; jm_plan.h
+// is prepended to it when the library embeds the source.
+//
+// Arithmetic per update: the accumulator starts at M, so
+// P = M + M*M costs N^2*N FMAs, then M' = fma(c, P, a_ij) with a_ij = 1 (Ones)
+// or [i == j] (Identity) — N^2 (N+1) FMAs per matrix-update in total, the
+// algorithmic count.  M*M always reads the pre-update M (Q8 / R8).
+#ifndef JM_UPDATE_CUH
+#define JM_UPDATE_CUH
+
+namespace jm {
+
+typedef unsigned long long u64;
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ double fmaT(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float fmaT(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
+__device__ __forceinline__ uint4 ldg_nc16(const void *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg16(void *p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Copy `cnt` packed matrices (MB bytes each) between global memory and a
+// shared staging area whose matrices sit SB bytes apart.  Cooperative over NT
+// threads; every global access is coalesced.  ALIGNED: the chunk's global start
+// is 16-B aligned, so 16-B vectors are used (128-bit LDG/STG).
+template <int N, int ES, int SB, int NT, bool ALIGNED>
+__device__ __forceinline__ void stage_in(const char *__restrict__ g, char *s, int cnt, int tid) {
+  constexpr int MB = N * N * ES;
+  if constexpr (ALIGNED && (MB % 16) == 0) {
+    constexpr int PPM = MB / 16;
+    const int pieces = cnt * PPM;
+#pragma unroll 4
+    for (int p = tid; p < pieces; p += NT) {
+      const int m = p / PPM, q = p - m * PPM;
+      *reinterpret_cast<uint4 *>(s + m * SB + q * 16) = ldg_nc16(g + (size_t)p * 16);
+    }
+  } else if constexpr (ALIGNED && SB == MB) {
+    const int bytes = cnt * MB, pieces = bytes >> 4;
+#pragma unroll 4
+    for (int p = tid; p < pieces; p += NT)
+      *reinterpret_cast<uint4 *>(s + p * 16) = ldg_nc16(g + (size_t)p * 16);
+    for (int o = pieces * 16 + tid * ES; o < bytes; o += NT * ES) {
+      if constexpr (ES == 8) *reinterpret_cast<u64 *>(s + o) = *reinterpret_cast<const u64 *>(g + o);
+      else *reinterpret_cast<unsigned *>(s + o) = *reinterpret_cast<const unsigned *>(g + o);
+    }
+  } else {
+    const int elems = cnt * N * N;
+    for (int e = tid; e < elems; e += NT) {
+      const int m = e / (N * N), q = e - m * (N * N);
+      if constexpr (ES == 8)
+        *reinterpret_cast<u64 *>(s + m * SB + q * 8) = reinterpret_cast<const u64 *>(g)[e];
+      else
+        *reinterpret_cast<unsigned *>(s + m * SB + q * 4) = reinterpret_cast<const unsigned *>(g)[e];
+    }
+  }
+}
+
+template <int N, int ES, int SB, int NT, bool ALIGNED>
+__device__ __forceinline__ void stage_out(char *__restrict__ g, const char *s, int cnt, int tid) {
+  constexpr int MB = N * N * ES;
+  if constexpr (ALIGNED && (MB % 16) == 0) {
+    constexpr int PPM = MB / 16;
+    const int pieces = cnt * PPM;
+#pragma unroll 4
+    for (int p = tid; p < pieces; p += NT) {
+      const int m = p / PPM, q = p - m * PPM;
+      stg16(g + (size_t)p * 16, *reinterpret_cast<const uint4 *>(s + m * SB + q * 16));
+    }
+  } else if constexpr (ALIGNED && SB == MB) {
+    const int bytes = cnt * MB, pieces = bytes >> 4;
+#pragma unroll 4
+    for (int p = tid; p < pieces; p += NT)
+      stg16(g + (size_t)p * 16, *reinterpret_cast<const uint4 *>(s + p * 16));
+    for (int o = pieces * 16 + tid * ES; o < bytes; o += NT * ES) {
+      if constexpr (ES == 8) *reinterpret_cast<u64 *>(g + o) = *reinterpret_cast<const u64 *>(s + o);
+      else *reinterpret_cast<unsigned *>(g + o) = *reinterpret_cast<const unsigned *>(s + o);
+    }
+  } else {
+    const int elems = cnt * N * N;
+    for (int e = tid; e < elems; e += NT) {
+      const int m = e / (N * N), q = e - m * (N * N);
+      if constexpr (ES == 8)
+        reinterpret_cast<u64 *>(g)[e] = *reinterpret_cast<const u64 *>(s + m * SB + q * 8);
+      else
+        reinterpret_cast<unsigned *>(g)[e] = *reinterpret_cast<const unsigned *>(s + m * SB + q * 4);
+    }
+  }
+}
+
+// ======================================================================
+// TPM: thread per matrix.  The whole matrix (and the product) lives in
+// registers for all `repeat` updates; fully unrolled for the compile-time N
+// (the register analog of Eigen's fixed-size Matrix<T,size,size>).
+// ======================================================================
+template <int N, class T, Addend A>
+__device__ __forceinline__ void tpm_iterate(T (&m)[N * N], int repeat) {
+  const T c = T(0.00005);
+  for (int r = 0; r < repeat; ++r) {
+    T p[N * N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        T acc = m[i * N + j];  // P = M + M*M: accumulator starts at M
+#pragma unroll
+        for (int k = 0; k < N; ++k) acc = fmaT(m[i * N + k], m[k * N + j], acc);
+        p[i * N + j] = acc;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        if (A == Addend::Ones || i == j) m[i * N + j] = fmaT(c, p[i * N + j], T(1));
+        else m[i * N + j] = c * p[i * N + j];
+      }
+    }
+  }
+}
+
+// FP32 variant: pairs of columns go through FFMA2 (sm_100 packed FP32 FMA):
+// half the issue slots of scalar FFMA for the same FMA count.
+template <int N, Addend A>
+__device__ __forceinline__ void tpm_iterate_f32x2(float (&m)[N * N], int repeat) {
+  const float c = float(0.00005);
+  constexpr int NH = N / 2;
+  for (int r = 0; r < repeat; ++r) {
+    float p[N * N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int jj = 0; jj < NH; ++jj) {
+        float2 acc = make_float2(m[i * N + 2 * jj], m[i * N + 2 * jj + 1]);
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+          acc = __ffma2_rn(make_float2(m[i * N + k], m[i * N + k]),
+                           make_float2(m[k * N + 2 * jj], m[k * N + 2 * jj + 1]), acc);
+        p[i * N + 2 * jj] = acc.x;
+        p[i * N + 2 * jj + 1] = acc.y;
+      }
+      if constexpr (N % 2) {
+        float acc = m[i * N + N - 1];
+#pragma unroll
+        for (int k = 0; k < N; ++k) acc = fmaT(m[i * N + k], m[k * N + N - 1], acc);
+        p[i * N + N - 1] = acc;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        if (A == Addend::Ones || i == j) m[i * N + j] = fmaT(c, p[i * N + j], 1.0f);
+        else m[i * N + j] = c * p[i * N + j];
+      }
+    }
+  }
+}
+
+template <int N, class T, Addend A>
+__device__ __forceinline__ void run_tpm(const T *__restrict__ in, T *__restrict__ out,
+                                        long long batch, int repeat) {
+  constexpr int ES = sizeof(T), MB = N * N * ES, SB = stage_stride(N, ES);
+  constexpr int NT = TPM_THREADS, MPC = TPM_THREADS;
+  extern __shared__ __align__(16) char smem[];
+  const int tid = threadIdx.x;
+  const long long nchunks = (batch + MPC - 1) / MPC;
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long b0 = ch * MPC;
+    const int cnt = (int)((batch - b0) < MPC ? (batch - b0) : MPC);
+    stage_in<N, ES, SB, NT, true>(reinterpret_cast<const char *>(in) + b0 * MB, smem, cnt, tid);
+    __syncthreads();
+    if (tid < cnt) {
+      T m[N * N];
+      char *mine = smem + tid * SB;
+      if constexpr (MB % 16 == 0) {  // 16-B pieces at an odd 16-B stride: conflict free
+#pragma unroll
+        for (int q = 0; q < MB / 16; ++q) {
+          if constexpr (ES == 8) {
+            const double2 v = *reinterpret_cast<const double2 *>(mine + 16 * q);
+            m[2 * q] = v.x; m[2 * q + 1] = v.y;
+          } else {
+            const float4 v = *reinterpret_cast<const float4 *>(mine + 16 * q);
+            m[4 * q] = v.x; m[4 * q + 1] = v.y; m[4 * q + 2] = v.z; m[4 * q + 3] = v.w;
+          }
+        }
+      } else {  // odd N: packed, odd element stride: conflict free
+#pragma unroll
+        for (int e = 0; e < N * N; ++e) m[e] = reinterpret_cast<const T *>(mine)[e];
+      }
+      if constexpr (ES == 4 && N >= 2) tpm_iterate_f32x2<N, A>(m, repeat);
+      else tpm_iterate<N, T, A>(m, repeat);
+      if constexpr (MB % 16 == 0) {
+#pragma unroll
+        for (int q = 0; q < MB / 16; ++q) {
+          if constexpr (ES == 8)
+            *reinterpret_cast<double2 *>(mine + 16 * q) = make_double2(m[2 * q], m[2 * q + 1]);
+          else
+            *reinterpret_cast<float4 *>(mine + 16 * q) =
+                make_float4(m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < N * N; ++e) reinterpret_cast<T *>(mine)[e] = m[e];
+      }
+    }
+    __syncthreads();
+    stage_out<N, ES, SB, NT, true>(reinterpret_cast<char *>(out) + b0 * MB, smem, cnt, tid);
+    __syncthreads();
+  }
+}
+
+// ======================================================================
+// DMMA: FP64 tensor cores (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4).
+//
+// M is padded to NP = 8*T8 and held in registers as DMMA accumulator
+// fragments: lane (g = lane/4, t = lane%4) holds M[8I+g][8J+2t+s], s = 0,1.
+// k-permutation: the k-step (J, s) sums over k in {8J + 2t + s : t = 0..3}.
+// With that grouping the A fragment A[g][t] = M[8I+g][8J+2t+s] is exactly the
+// lane's own accumulator element s of tile (I, J) — no data movement.  The B
+// fragment B[t][g] = M[8J+2t+s][8J'+g] is the transpose-side read; it goes
+// through a shared-memory copy of M that each update republishes, in an
+// XOR-swizzled layout that makes both the 128-bit publish stores and the 64-bit
+// fragment loads bank-conflict free.
+// W warps share one matrix (each owns RT row tiles); W == 1 for N <= 32.
+// ======================================================================
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// byte offset of 16-B chunk `cc` of row `r` in the swizzled scratch
+template <int RSC>
+__device__ __forceinline__ int scr_off(int r, int cc) {
+  return (r * RSC + (cc ^ ((r & 6) ^ ((r & 1) << 2)))) * 16;
+}
+
+template <int N, Addend A, int W>
+__device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *__restrict__ out,
+                                         long long batch, int repeat) {
+  constexpr int T8 = dmma_t8(N), RT = dmma_rt(N), RSC = dmma_rsc(N), SCR = dmma_scr(N);
+  constexpr int ES = 8, MB = N * N * 8, SB = stage_stride(N, 8);
+  constexpr int WPC = (W == 1) ? DMMA_WPC : W;
+  constexpr int NT = 32 * WPC;
+  constexpr int MPC = (W == 1) ? DMMA_WPC : 1;
+  constexpr bool AL = ((MPC * MB) % 16) == 0;
+  static_assert(RT * W == T8, "row tiles must cover the matrix");
+  extern __shared__ __align__(16) char smem[];
+  char *stage = smem;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mi = (W == 1) ? warp : 0;        // matrix slot in the chunk
+  const int wr = (W == 1) ? 0 : warp;        // this warp's rank within the matrix
+  char *scr = smem + stage_bytes(MPC, N, 8) + ((W == 1) ? warp * SCR : 0);
+  const double c = 0.00005;
+  const long long nchunks = (batch + MPC - 1) / MPC;
+
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long b0 = ch * MPC;
+    const int cnt = (int)((batch - b0) < MPC ? (batch - b0) : MPC);
+    stage_in<N, ES, SB, NT, AL>(reinterpret_cast<const char *>(in) + b0 * MB, stage, cnt, tid);
+    __syncthreads();
+    if (mi < cnt) {
+      double *sm = reinterpret_cast<double *>(stage + mi * SB);
+      double acc[RT][T8][2];
+#pragma unroll
+      for (int I = 0; I < RT; ++I)
+#pragma unroll
+        for (int J = 0; J < T8; ++J)
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const int row = 8 * (wr * RT + I) + g, col = 8 * J + 2 * t + s;
+            acc[I][J][s] = (row < N && col < N) ? sm[row * N + col] : 0.0;
+          }
+      for (int r = 0; r < repeat; ++r) {
+        char *sb = scr + ((W > 1) ? (r & 1) * SCR : 0);
+        // publish M (own rows) for the B-fragment reads
+#pragma unroll
+        for (int I = 0; I < RT; ++I)
+#pragma unroll
+          for (int J = 0; J < T8; ++J)
+            *reinterpret_cast<double2 *>(sb + scr_off<RSC>(8 * (wr * RT + I) + g, 4 * J + t)) =
+                make_double2(acc[I][J][0], acc[I][J][1]);
+        if constexpr (W == 1) __syncwarp(); else __syncthreads();
+        double p[RT][T8][2];
+#pragma unroll
+        for (int I = 0; I < RT; ++I)
+#pragma unroll
+          for (int J = 0; J < T8; ++J) { p[I][J][0] = acc[I][J][0]; p[I][J][1] = acc[I][J][1]; }
+#pragma unroll
+        for (int J = 0; J < T8; ++J) {
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            double b[T8];
+#pragma unroll
+            for (int J2 = 0; J2 < T8; ++J2)
+              b[J2] = *reinterpret_cast<const double *>(
+                  sb + scr_off<RSC>(8 * J + 2 * t + s, 4 * J2 + (g >> 1)) + 8 * (g & 1));
+#pragma unroll
+            for (int I = 0; I < RT; ++I)
+#pragma unroll
+              for (int J2 = 0; J2 < T8; ++J2) dmma884(p[I][J2][0], p[I][J2][1], acc[I][J][s], b[J2]);
+          }
+        }
+        // M' = A + c * P  (padding stays exactly zero)
+#pragma unroll
+        for (int I = 0; I < RT; ++I)
+#pragma unroll
+          for (int J = 0; J < T8; ++J)
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const int row = 8 * (wr * RT + I) + g, col = 8 * J + 2 * t + s;
+              const double a = (A == Addend::Ones || row == col) ? 1.0 : 0.0;
+              double v = fmaT(c, p[I][J][s], a);
+              if constexpr (N % 8 != 0) v = (row < N && col < N) ? v : 0.0;
+              acc[I][J][s] = v;
+            }
+        if constexpr (W == 1) __syncwarp();
+      }
+#pragma unroll
+      for (int I = 0; I < RT; ++I)
+#pragma unroll
+        for (int J = 0; J < T8; ++J)
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const int row = 8 * (wr * RT + I) + g, col = 8 * J + 2 * t + s;
+            if (row < N && col < N) sm[row * N + col] = acc[I][J][s];
+          }
+    }
+    __syncthreads();
+    stage_out<N, ES, SB, NT, AL>(reinterpret_cast<char *>(out) + b0 * MB, stage, cnt, tid);
+    __syncthreads();
+  }
+}
+
+// ======================================================================
+// F32: FP32 register-tiled outer products.  The RG x CG threads of a matrix
+// each own an RA x CB block of M (registers).  Every update republishes M and
+// M^T to shared memory; then for k < N each thread reads RA values of column k
+// (a row of M^T) and CB values of row k (broadcast loads) and issues RA*CB/2
+// FFMA2.  W warps per matrix (W == 1 for N <= 32).
+// ======================================================================
+template <int N, Addend A, int W>
+__device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__restrict__ out,
+                                        long long batch, int repeat) {
+  constexpr int RG = f32_rg(N), CG = f32_cg(N), RA = f32_ra(N), CB = f32_cb(N);
+  constexpr int LDM = f32_ldm(N), LDT = f32_ldt(N), BUF = f32_buf(N);
+  constexpr int ES = 4, MB = N * N * 4, SB = stage_stride(N, 4);
+  constexpr int WPC = (W == 1) ? F32_WPC : W;
+  constexpr int NT = 32 * WPC;
+  constexpr int MPC = (W == 1) ? F32_WPC : 1;
+  constexpr bool AL = ((MPC * MB) % 16) == 0;
+  static_assert(RG * CG == 32 * W, "thread grid must match the warps per matrix");
+  static_assert(CB % 2 == 0, "FFMA2 needs column pairs");
+  extern __shared__ __align__(16) char smem[];
+  char *stage = smem;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int mi = (W == 1) ? warp : 0;
+  const int tr = (W == 1) ? (tid & 31) : tid;   // rank within the matrix
+  const int r0 = (tr / CG) * RA, c0 = (tr % CG) * CB;
+  char *bufs = smem + stage_bytes(MPC, N, 4) + ((W == 1) ? warp * BUF : 0);
+  const float c = float(0.00005);
+  const long long nchunks = (batch + MPC - 1) / MPC;
+
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long b0 = ch * MPC;
+    const int cnt = (int)((batch - b0) < MPC ? (batch - b0) : MPC);
+    stage_in<N, ES, SB, NT, AL>(reinterpret_cast<const char *>(in) + b0 * MB, stage, cnt, tid);
+    __syncthreads();
+    if (mi < cnt) {
+      float *sm = reinterpret_cast<float *>(stage + mi * SB);
+      float m[RA][CB];
+#pragma unroll
+      for (int i = 0; i < RA; ++i)
+#pragma unroll
+        for (int j = 0; j < CB; ++j) {
+          const int row = r0 + i, col = c0 + j;
+          m[i][j] = (row < N && col < N) ? sm[row * N + col] : 0.0f;
+        }
+      for (int r = 0; r < repeat; ++r) {
+        float *sM = reinterpret_cast<float *>(bufs + ((W > 1) ? (r & 1) * BUF : 0));
+        float *sMT = sM + N * LDM;
+        // publish M (row blocks) and M^T (column blocks)
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+          if (r0 + i < N) {
+#pragma unroll
+            for (int j = 0; j < CB; j += 2)
+              *reinterpret_cast<float2 *>(sM + (r0 + i) * LDM + c0 + j) = make_float2(m[i][j], m[i][j + 1]);
+          }
+#pragma unroll
+        for (int j = 0; j < CB; ++j)
+          if (c0 + j < N) {
+            if constexpr (RA % 2 == 0) {
+#pragma unroll
+              for (int i = 0; i < RA; i += 2)
+                *reinterpret_cast<float2 *>(sMT + (c0 + j) * LDT + r0 + i) = make_float2(m[i][j], m[i + 1][j]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < RA; ++i) sMT[(c0 + j) * LDT + r0 + i] = m[i][j];
+            }
+          }
+        if constexpr (W == 1) __syncwarp(); else __syncthreads();
+        float2 p[RA][CB / 2];
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+#pragma unroll
+          for (int j = 0; j < CB / 2; ++j) p[i][j] = make_float2(m[i][2 * j], m[i][2 * j + 1]);
+#pragma unroll 4
+        for (int k = 0; k < N; ++k) {
+          float a[RA], b[CB];
+          if constexpr (RA % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < RA; i += 4) {
+              const float4 v = *reinterpret_cast<const float4 *>(sMT + k * LDT + r0 + i);
+              a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
+            }
+          } else if constexpr (RA % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < RA; i += 2) {
+              const float2 v = *reinterpret_cast<const float2 *>(sMT + k * LDT + r0 + i);
+              a[i] = v.x; a[i + 1] = v.y;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < RA; ++i) a[i] = sMT[k * LDT + r0 + i];
+          }
+          if constexpr (CB % 4 == 0) {
+#pragma unroll
+            for (int j = 0; j < CB; j += 4) {
+              const float4 v = *reinterpret_cast<const float4 *>(sM + k * LDM + c0 + j);
+              b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < CB; j += 2) {
+              const float2 v = *reinterpret_cast<const float2 *>(sM + k * LDM + c0 + j);
+              b[j] = v.x; b[j + 1] = v.y;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < RA; ++i)
+#pragma unroll
+            for (int j = 0; j < CB / 2; ++j)
+              p[i][j] = __ffma2_rn(make_float2(a[i], a[i]), make_float2(b[2 * j], b[2 * j + 1]), p[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+#pragma unroll
+          for (int j = 0; j < CB; ++j) {
+            const int row = r0 + i, col = c0 + j;
+            const float pv = (j & 1) ? p[i][j / 2].y : p[i][j / 2].x;
+            const float a = (A == Addend::Ones || row == col) ? 1.0f : 0.0f;
+            float v = fmaT(c, pv, a);
+            m[i][j] = (row < N && col < N) ? v : 0.0f;
+          }
+        if constexpr (W == 1) __syncwarp();
+      }
+#pragma unroll
+      for (int i = 0; i < RA; ++i)
+#pragma unroll
+        for (int j = 0; j < CB; ++j) {
+          const int row = r0 + i, col = c0 + j;
+          if (row < N && col < N) sm[row * N + col] = m[i][j];
+        }
+    }
+    __syncthreads();
+    stage_out<N, ES, SB, NT, AL>(reinterpret_cast<char *>(out) + b0 * MB, stage, cnt, tid);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ entry
+// The NVRTC name expression is "jm::k_update<N, T, jm::Addend::X, jm::Tile::Y>"
+// with Y = tile_for(N, dtype); the host launches it with plan_specialized().
+template <int N, class T, Addend A, Tile K>
+__global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).threads)
+    k_update(const T *__restrict__ in, T *__restrict__ out, long long batch, int repeat) {
+  static_assert(N >= 1 && N <= 64, "N in [1, 64]");
+  static_assert(K == tile_for(N, sizeof(T) == 8 ? 1 : 0), "tile must match the plan");
+  if constexpr (K == Tile::TPM) {
+    run_tpm<N, T, A>(in, out, batch, repeat);
+  } else if constexpr (K == Tile::Dmma) {
+    run_dmma<N, A, dmma_w(N)>(in, out, batch, repeat);
+  } else {
+    run_f32<N, A, f32_w(N)>(in, out, batch, repeat);
+  }
+}
+
+}  // namespace jm
+#endif  // JM_UPDATE_CUH

@@ -1,0 +1,759 @@
+// jm_runtime.cpp — libjitmat: the C ABI (include/jit_mat.h) and the
+// specialization runtime behind it.
+//
+// The paper's runtime (§4; Algorithm 1, 308-349) looks
+// up a program-global instantiation cache (line 306, "a DenseMap ... protected
+// by a mutex"; Algorithm 1 lines 319 and 347) and on a miss instantiates the
+// template from embedded compiler state, optimizes it and JITs it; for CUDA it
+// picks the device compiler state by compute capability and emits PTX that the
+// driver turns into a fatbin (lines 353-354).  Here:
+//   * the cache is a direct-indexed table of slots [kind][addend][dtype][N],
+//     published with release/acquire atomics; a hit is one acquire load (no
+//     lock), a miss takes the slot's own mutex, so distinct keys compile in
+//     parallel and concurrent callers of one key wait for a single compile;
+//   * the "embedded compiler state" is the kernel template source, embedded in
+//     this library at build time; NVRTC instantiates the name expression
+//     "jm::k_update<N, T, jm::Addend::X, jm::Tile::Y>" straight to an sm_100a
+//     CUBIN (no PTX JIT, no fatbin), with no include paths (no file access at
+//     JIT time);
+//   * the CUDA driver API is reached through dlopen("libcuda.so.1"), so the
+//     library loads (and its symbols can be checked) on a machine without a
+//     GPU; NVRTC is statically linked.
+#include "jit_mat.h"
+
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../kernels/jm_plan.h"
+
+extern "C" {
+extern const unsigned char jm_embedded_kernel_src[];
+extern const unsigned long long jm_embedded_kernel_src_len;
+extern const unsigned char jm_embedded_aot_cubin[];
+extern const unsigned long long jm_embedded_aot_cubin_len;
+}
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+thread_local std::string t_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return code;
+}
+
+// ------------------------------------------------------------------ driver API
+struct Driver {
+  void *handle = nullptr;
+  decltype(&cuInit) Init = nullptr;
+  decltype(&cuDeviceGet) DeviceGet = nullptr;
+  decltype(&cuDeviceGetAttribute) DeviceGetAttribute = nullptr;
+  decltype(&cuDevicePrimaryCtxRetain) PrimaryCtxRetain = nullptr;
+  decltype(&cuDevicePrimaryCtxRelease) PrimaryCtxRelease = nullptr;
+  decltype(&cuCtxGetCurrent) CtxGetCurrent = nullptr;
+  decltype(&cuCtxSetCurrent) CtxSetCurrent = nullptr;
+  decltype(&cuCtxGetDevice) CtxGetDevice = nullptr;
+  decltype(&cuModuleLoadData) ModuleLoadData = nullptr;
+  decltype(&cuModuleUnload) ModuleUnload = nullptr;
+  decltype(&cuModuleGetFunction) ModuleGetFunction = nullptr;
+  decltype(&cuFuncGetAttribute) FuncGetAttribute = nullptr;
+  decltype(&cuFuncSetAttribute) FuncSetAttribute = nullptr;
+  decltype(&cuLaunchKernel) LaunchKernel = nullptr;
+  decltype(&cuStreamSynchronize) StreamSynchronize = nullptr;
+  decltype(&cuStreamCreate) StreamCreate = nullptr;
+  decltype(&cuStreamDestroy) StreamDestroy = nullptr;
+  decltype(&cuStreamWaitEvent) StreamWaitEvent = nullptr;
+  decltype(&cuEventCreate) EventCreate = nullptr;
+  decltype(&cuEventDestroy) EventDestroy = nullptr;
+  decltype(&cuEventRecord) EventRecord = nullptr;
+  decltype(&cuMemAlloc) MemAlloc = nullptr;
+  decltype(&cuMemFree) MemFree = nullptr;
+  decltype(&cuMemcpyHtoDAsync) MemcpyHtoDAsync = nullptr;
+  decltype(&cuMemcpyDtoHAsync) MemcpyDtoHAsync = nullptr;
+  decltype(&cuMemsetD8Async) MemsetD8Async = nullptr;
+  decltype(&cuGetErrorString) GetErrorString = nullptr;
+  decltype(&cuOccupancyMaxActiveBlocksPerMultiprocessor) OccupancyMaxActiveBlocks = nullptr;
+  decltype(&cuPointerGetAttribute) PointerGetAttribute = nullptr;
+};
+
+Driver D;
+std::mutex g_driver_mu;
+
+typedef CUresult (*GetProcFn)(const char *, void **, int, cuuint64_t, CUdriverProcAddressQueryResult *);
+
+int load_driver() {
+  std::lock_guard<std::mutex> lk(g_driver_mu);
+  if (D.handle) return JM_OK;
+  void *h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_LOCAL);
+  if (!h) return fail(JM_E_CUDA, "CUDA driver libcuda.so.1 not found: %s", dlerror());
+  GetProcFn gp = (GetProcFn)dlsym(h, "cuGetProcAddress_v2");
+  if (!gp) return fail(JM_E_CUDA, "driver lacks cuGetProcAddress_v2 (driver too old for CUDA 12)");
+  bool ok = true;
+  auto get = [&](const char *name, auto &fp) {
+    void *p = nullptr;
+    CUdriverProcAddressQueryResult st;
+    CUresult r = gp(name, &p, CUDA_VERSION, CU_GET_PROC_ADDRESS_DEFAULT, &st);
+    if (r != CUDA_SUCCESS || !p) ok = false;
+    fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(p);
+  };
+  get("cuInit", D.Init);
+  get("cuDeviceGet", D.DeviceGet);
+  get("cuDeviceGetAttribute", D.DeviceGetAttribute);
+  get("cuDevicePrimaryCtxRetain", D.PrimaryCtxRetain);
+  get("cuDevicePrimaryCtxRelease", D.PrimaryCtxRelease);
+  get("cuCtxGetCurrent", D.CtxGetCurrent);
+  get("cuCtxSetCurrent", D.CtxSetCurrent);
+  get("cuCtxGetDevice", D.CtxGetDevice);
+  get("cuModuleLoadData", D.ModuleLoadData);
+  get("cuModuleUnload", D.ModuleUnload);
+  get("cuModuleGetFunction", D.ModuleGetFunction);
+  get("cuFuncGetAttribute", D.FuncGetAttribute);
+  get("cuFuncSetAttribute", D.FuncSetAttribute);
+  get("cuLaunchKernel", D.LaunchKernel);
+  get("cuStreamSynchronize", D.StreamSynchronize);
+  get("cuStreamCreate", D.StreamCreate);
+  get("cuStreamDestroy", D.StreamDestroy);
+  get("cuStreamWaitEvent", D.StreamWaitEvent);
+  get("cuEventCreate", D.EventCreate);
+  get("cuEventDestroy", D.EventDestroy);
+  get("cuEventRecord", D.EventRecord);
+  get("cuMemAlloc", D.MemAlloc);
+  get("cuMemFree", D.MemFree);
+  get("cuMemcpyHtoDAsync", D.MemcpyHtoDAsync);
+  get("cuMemcpyDtoHAsync", D.MemcpyDtoHAsync);
+  get("cuMemsetD8Async", D.MemsetD8Async);
+  get("cuGetErrorString", D.GetErrorString);
+  get("cuOccupancyMaxActiveBlocksPerMultiprocessor", D.OccupancyMaxActiveBlocks);
+  get("cuPointerGetAttribute", D.PointerGetAttribute);
+  if (!ok) {
+    dlclose(h);
+    return fail(JM_E_CUDA, "could not resolve the CUDA driver entry points");
+  }
+  D.handle = h;
+  return JM_OK;
+}
+
+int cu_fail(CUresult r, const char *what) {
+  const char *s = nullptr;
+  if (D.GetErrorString) D.GetErrorString(r, &s);
+  return fail(JM_E_CUDA, "%s: CUDA error %d (%s)", what, (int)r, s ? s : "?");
+}
+#define CU_TRY(expr, what)                      \
+  do {                                          \
+    CUresult _r = (expr);                       \
+    if (_r != CUDA_SUCCESS) return cu_fail(_r, what); \
+  } while (0)
+
+// ------------------------------------------------------------------ cache
+enum SlotState { S_EMPTY = 0, S_COMPILING = 1, S_READY = 2, S_FAILED = 3 };
+
+struct Slot {
+  std::atomic<int> state{S_EMPTY};
+  std::mutex mu;
+  CUmodule mod = nullptr;     // owned (specialized kind only)
+  CUfunction fn = nullptr;
+  jm::Plan plan{};
+  int grid_cap = 0;           // SM count x resident CTAs per SM
+  int regs = 0, local_bytes = 0;
+  long long cubin_bytes = 0;
+  double compile_ms = 0.0;
+  std::string err;
+};
+
+constexpr int NKIND = 2, NADD = 2, NDT = 2, NMAX = JM_N_MAX;
+Slot g_slots[NKIND][NADD][NDT][NMAX + 1];
+
+struct State {
+  std::mutex mu;
+  std::atomic<bool> inited{false};
+  CUdevice dev = 0;
+  int ordinal = -1;
+  CUcontext ctx = nullptr;
+  int sms = 0, cc_major = 0, cc_minor = 0;
+  CUmodule aot = nullptr;
+  CUfunction generic[NDT][NADD] = {};
+  CUfunction fill[NDT] = {};
+  CUfunction checksum[NDT] = {};
+  CUdeviceptr sum_buf = 0;    // u64 + f64 for checksum
+  std::atomic<void *> stream{nullptr};
+  // host-buffer staging (run_host)
+  std::mutex host_mu;
+  CUdeviceptr hbuf[3] = {0, 0, 0};
+  size_t hbuf_bytes = 0;
+  CUstream hs[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
+  CUevent ev_h2d[3] = {}, ev_cmp[3] = {}, ev_d2h[3] = {};
+};
+State G;
+
+std::atomic<long long> c_compilations{0}, c_hits{0}, c_misses{0}, c_launches{0};
+std::atomic<long long> c_compile_us{0};
+
+bool env_flag(const char *name) {
+  const char *v = getenv(name);
+  return v && *v && strcmp(v, "0") != 0;
+}
+
+int ensure_ctx() {
+  CUcontext cur = nullptr;
+  CU_TRY(D.CtxGetCurrent(&cur), "cuCtxGetCurrent");
+  if (cur != G.ctx) CU_TRY(D.CtxSetCurrent(G.ctx), "cuCtxSetCurrent");
+  return JM_OK;
+}
+
+const char *tile_name(int t) {
+  switch ((jm::Tile)t) {
+    case jm::Tile::TPM: return "TPM";
+    case jm::Tile::Dmma: return "Dmma";
+    case jm::Tile::F32: return "F32";
+    default: return "Generic";
+  }
+}
+
+std::string name_expression(int n, int dtype, int addend) {
+  char buf[160];
+  snprintf(buf, sizeof buf, "jm::k_update<%d, %s, jm::Addend::%s, jm::Tile::%s>", n,
+           dtype == JM_F64 ? "double" : "float", addend == JM_ADDEND_ONES ? "Ones" : "Identity",
+           tile_name((int)jm::tile_for(n, dtype)));
+  return buf;
+}
+
+// NVRTC: instantiate the template for (n, dtype, addend) -> sm_100a cubin.
+int nvrtc_compile(int n, int dtype, int addend, std::vector<char> &cubin, std::string &lowered,
+                  std::string &log) {
+  const std::string src((const char *)jm_embedded_kernel_src, (size_t)jm_embedded_kernel_src_len);
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "jm_update.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) {
+    log = nvrtcGetErrorString(r);
+    return JM_E_COMPILE;
+  }
+  const std::string expr = name_expression(n, dtype, addend);
+  nvrtcAddNameExpression(prog, expr.c_str());
+  const char *opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=true", "-lineinfo",
+                        "--ftz=false", "--prec-div=true", "--prec-sqrt=true"};
+  r = nvrtcCompileProgram(prog, (int)(sizeof opts / sizeof opts[0]), opts);
+  size_t lsz = 0;
+  nvrtcGetProgramLogSize(prog, &lsz);
+  if (lsz > 1) {
+    log.resize(lsz);
+    nvrtcGetProgramLog(prog, &log[0]);
+  }
+  if (r != NVRTC_SUCCESS) {
+    log = std::string("NVRTC failed for ") + expr + ": " + nvrtcGetErrorString(r) + "\n" + log;
+    nvrtcDestroyProgram(&prog);
+    return JM_E_COMPILE;
+  }
+  const char *low = nullptr;
+  nvrtcGetLoweredName(prog, expr.c_str(), &low);
+  lowered = low ? low : "";
+  size_t csz = 0;
+  nvrtcGetCUBINSize(prog, &csz);
+  cubin.resize(csz);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  return JM_OK;
+}
+
+int finish_function(Slot &s, CUfunction fn) {
+  int v = 0;
+  D.FuncGetAttribute(&v, CU_FUNC_ATTRIBUTE_NUM_REGS, fn);
+  s.regs = v;
+  D.FuncGetAttribute(&v, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, fn);
+  s.local_bytes = v;
+  if (s.plan.smem > 48 * 1024)
+    CU_TRY(D.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, s.plan.smem),
+           "cuFuncSetAttribute(max dynamic smem)");
+  int nb = 0;
+  CU_TRY(D.OccupancyMaxActiveBlocks(&nb, fn, s.plan.threads, (size_t)s.plan.smem),
+         "cuOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (nb < 1) return fail(JM_E_CUDA, "kernel cannot be resident (threads %d, smem %d)", s.plan.threads, s.plan.smem);
+  s.grid_cap = nb * G.sms;
+  s.fn = fn;
+  return JM_OK;
+}
+
+int compile_slot(Slot &s, int n, int dtype, int addend) {
+  const auto t0 = std::chrono::steady_clock::now();
+  c_compilations++;
+  std::vector<char> cubin;
+  std::string lowered, log;
+  int rc = nvrtc_compile(n, dtype, addend, cubin, lowered, log);
+  if (rc != JM_OK) {
+    s.err = log;
+    return fail(rc, "%s", log.c_str());
+  }
+  if ((rc = ensure_ctx()) != JM_OK) return rc;
+  CUmodule mod = nullptr;
+  CUresult cr = D.ModuleLoadData(&mod, cubin.data());
+  if (cr != CUDA_SUCCESS) {
+    cu_fail(cr, "cuModuleLoadData(NVRTC cubin)");
+    s.err = t_err;
+    return JM_E_COMPILE;
+  }
+  CUfunction fn = nullptr;
+  cr = D.ModuleGetFunction(&fn, mod, lowered.c_str());
+  if (cr != CUDA_SUCCESS) {
+    D.ModuleUnload(mod);
+    cu_fail(cr, "cuModuleGetFunction");
+    s.err = t_err;
+    return JM_E_COMPILE;
+  }
+  s.plan = jm::plan_specialized(n, dtype);
+  s.mod = mod;
+  s.cubin_bytes = (long long)cubin.size();
+  rc = finish_function(s, fn);
+  if (rc != JM_OK) {
+    D.ModuleUnload(mod);
+    s.mod = nullptr;
+    s.err = t_err;
+    return rc;
+  }
+  const double ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  s.compile_ms = ms;
+  c_compile_us += (long long)(ms * 1000.0);
+  if (env_flag("JIT_MAT_LOG"))
+    fprintf(stderr, "[jitmat] compiled %s in %.1f ms (%lld B cubin, %d regs, %d B local)\n",
+            name_expression(n, dtype, addend).c_str(), ms, s.cubin_bytes, s.regs, s.local_bytes);
+  return JM_OK;
+}
+
+int check_key(int n, int dtype, int addend, int kind) {
+  if (n <= 0) return fail(JM_E_INVALID, "n must be >= 1 (got %d)", n);
+  if (n > JM_N_MAX) return fail(JM_E_UNSUPPORTED, "n = %d exceeds the supported maximum %d", n, JM_N_MAX);
+  if (dtype != JM_F32 && dtype != JM_F64) return fail(JM_E_UNSUPPORTED, "dtype %d not supported (f32/f64 only)", dtype);
+  if (addend != JM_ADDEND_ONES && addend != JM_ADDEND_IDENTITY) return fail(JM_E_INVALID, "addend %d invalid", addend);
+  if (kind != JM_KIND_SPECIALIZED && kind != JM_KIND_GENERIC) return fail(JM_E_INVALID, "kind %d invalid", kind);
+  return JM_OK;
+}
+
+// Algorithm 1 (PAPER.md:319 lookup, :347 store) with per-key once semantics.
+int lookup(int n, int dtype, int addend, int kind, Slot **out) {
+  int rc = check_key(n, dtype, addend, kind);
+  if (rc != JM_OK) return rc;
+  if (!G.inited.load(std::memory_order_acquire)) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
+  Slot &s = g_slots[kind][addend][dtype][n];
+  int st = s.state.load(std::memory_order_acquire);
+  if (st == S_READY) {
+    c_hits++;
+    *out = &s;
+    return JM_OK;
+  }
+  if (st == S_FAILED) return fail(JM_E_COMPILE, "%s", s.err.c_str());
+  c_misses++;
+  std::lock_guard<std::mutex> lk(s.mu);
+  st = s.state.load(std::memory_order_acquire);
+  if (st == S_READY) { *out = &s; return JM_OK; }
+  if (st == S_FAILED) return fail(JM_E_COMPILE, "%s", s.err.c_str());
+  if (kind == JM_KIND_GENERIC) return fail(JM_E_INVALID, "generic slot not seeded");
+  s.state.store(S_COMPILING, std::memory_order_relaxed);
+  rc = compile_slot(s, n, dtype, addend);
+  if (rc != JM_OK) {
+    if (rc == JM_E_COMPILE) {
+      s.state.store(S_FAILED, std::memory_order_release);
+    } else {
+      s.state.store(S_EMPTY, std::memory_order_release);   // transient (driver) error: retry later
+    }
+    return rc;
+  }
+  s.state.store(S_READY, std::memory_order_release);
+  *out = &s;
+  return JM_OK;
+}
+
+int launch(Slot &s, int n, int64_t batch, int64_t repeat, const void *in, void *out, CUstream stream,
+           int kind) {
+  const long long mpc = s.plan.mpc;
+  const long long nchunks = (batch + mpc - 1) / mpc;
+  const unsigned grid = (unsigned)(nchunks < s.grid_cap ? nchunks : s.grid_cap);
+  long long b = batch;
+  int r = (int)repeat;
+  CUdeviceptr pin = (CUdeviceptr)in, pout = (CUdeviceptr)out;
+  void *args_spec[] = {&pin, &pout, &b, &r};
+  int nn = n;
+  void *args_gen[] = {&pin, &pout, &b, &r, &nn};
+  CU_TRY(D.LaunchKernel(s.fn, grid, 1, 1, (unsigned)s.plan.threads, 1, 1, (unsigned)s.plan.smem, stream,
+                        kind == JM_KIND_GENERIC ? args_gen : args_spec, nullptr),
+         "cuLaunchKernel(update)");
+  c_launches++;
+  return JM_OK;
+}
+
+int validate_run(const jm_run_desc *d) {
+  if (!d) return fail(JM_E_INVALID, "NULL descriptor");
+  int rc = check_key(d->n, d->dtype, d->addend, d->kind);
+  if (rc != JM_OK) return rc;
+  if (d->batch < 0) return fail(JM_E_INVALID, "batch must be >= 0 (got %lld)", (long long)d->batch);
+  if (d->repeat < 0 || d->repeat > JM_REPEAT_MAX)
+    return fail(JM_E_INVALID, "repeat must be in [0, 2^31) (got %lld)", (long long)d->repeat);
+  if (!G.inited.load(std::memory_order_acquire)) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
+  if (d->batch == 0) return JM_OK;
+  if (!d->in || !d->out) return fail(JM_E_INVALID, "NULL buffer");
+  const size_t es = d->dtype == JM_F64 ? 8 : 4;
+  const unsigned long long bytes = (unsigned long long)d->batch * d->n * d->n * es;
+  const unsigned long long a = (unsigned long long)d->in, b = (unsigned long long)d->out;
+  if (a != b && a < b + bytes && b < a + bytes)
+    return fail(JM_E_INVALID, "in and out partially overlap (only exact aliasing is allowed)");
+  if (!(d->flags & JM_FLAG_HOST_BUFFERS) && ((a | b) & 15))
+    return fail(JM_E_ALIGN, "in/out must be 16-byte aligned");
+  return JM_OK;
+}
+
+int sync_if(unsigned flags, CUstream st) {
+  if ((flags & JM_FLAG_SYNC) || env_flag("JIT_MAT_SYNC")) CU_TRY(D.StreamSynchronize(st), "kernel execution");
+  return JM_OK;
+}
+
+// Host buffers: stream chunks H2D -> update in place on the device -> D2H,
+// three library-owned device buffers in rotation on three streams so the two
+// copy directions and the kernel overlap.
+int run_host(const jm_run_desc *d, Slot &s) {
+  std::lock_guard<std::mutex> lk(G.host_mu);
+  const size_t es = d->dtype == JM_F64 ? 8 : 4;
+  const size_t mb = (size_t)d->n * d->n * es;
+  size_t chunk_bytes = (size_t)64 << 20;
+  if (const char *e = getenv("JIT_MAT_HOST_CHUNK_MB")) chunk_bytes = (size_t)atoll(e) << 20;
+  long long per = (long long)(chunk_bytes / mb);
+  per -= per % 4;                        // keep chunk starts 16-B aligned
+  if (per < 4) per = 4;
+  const size_t need = (size_t)per * mb;
+  if (G.hbuf_bytes < need) {
+    for (int i = 0; i < 3; ++i)
+      if (G.hbuf[i]) { D.MemFree(G.hbuf[i]); G.hbuf[i] = 0; }
+    G.hbuf_bytes = 0;
+    for (int i = 0; i < 3; ++i) CU_TRY(D.MemAlloc(&G.hbuf[i], need), "cuMemAlloc(host staging)");
+    G.hbuf_bytes = need;
+  }
+  if (!G.hs[0]) {
+    for (int i = 0; i < 3; ++i) {
+      CU_TRY(D.StreamCreate(&G.hs[i], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+      CU_TRY(D.EventCreate(&G.ev_h2d[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+      CU_TRY(D.EventCreate(&G.ev_cmp[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+      CU_TRY(D.EventCreate(&G.ev_d2h[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    }
+  }
+  const char *hin = (const char *)d->in;
+  char *hout = (char *)d->out;
+  long long c = 0;
+  for (long long b0 = 0; b0 < d->batch; b0 += per, ++c) {
+    const long long cnt = (d->batch - b0) < per ? (d->batch - b0) : per;
+    const size_t bytes = (size_t)cnt * mb;
+    const int k = (int)(c % 3);
+    if (c >= 3) CU_TRY(D.StreamWaitEvent(G.hs[0], G.ev_d2h[k], 0), "cuStreamWaitEvent");
+    CU_TRY(D.MemcpyHtoDAsync(G.hbuf[k], hin + (size_t)b0 * mb, bytes, G.hs[0]), "cuMemcpyHtoDAsync");
+    CU_TRY(D.EventRecord(G.ev_h2d[k], G.hs[0]), "cuEventRecord");
+    CU_TRY(D.StreamWaitEvent(G.hs[1], G.ev_h2d[k], 0), "cuStreamWaitEvent");
+    int rc = launch(s, d->n, cnt, d->repeat, (const void *)G.hbuf[k], (void *)G.hbuf[k], G.hs[1], d->kind);
+    if (rc != JM_OK) return rc;
+    CU_TRY(D.EventRecord(G.ev_cmp[k], G.hs[1]), "cuEventRecord");
+    CU_TRY(D.StreamWaitEvent(G.hs[2], G.ev_cmp[k], 0), "cuStreamWaitEvent");
+    CU_TRY(D.MemcpyDtoHAsync(hout + (size_t)b0 * mb, G.hbuf[k], bytes, G.hs[2]), "cuMemcpyDtoHAsync");
+    CU_TRY(D.EventRecord(G.ev_d2h[k], G.hs[2]), "cuEventRecord");
+  }
+  CU_TRY(D.StreamSynchronize(G.hs[2]), "host-buffer pipeline");
+  CU_TRY(D.StreamSynchronize(G.hs[1]), "host-buffer pipeline");
+  return JM_OK;
+}
+
+int run_impl(const jm_run_desc *d) {
+  int rc = validate_run(d);
+  if (rc != JM_OK || d->batch == 0) return rc;
+  Slot *s = nullptr;
+  if ((rc = lookup(d->n, d->dtype, d->addend, d->kind, &s)) != JM_OK) return rc;
+  if ((rc = ensure_ctx()) != JM_OK) return rc;
+  if (d->flags & JM_FLAG_HOST_BUFFERS) return run_host(d, *s);
+  CUstream st = (CUstream)(d->stream ? d->stream : G.stream.load(std::memory_order_relaxed));
+  if ((rc = launch(*s, d->n, d->batch, d->repeat, d->in, d->out, st, d->kind)) != JM_OK) return rc;
+  return sync_if(d->flags, st);
+}
+
+void seed_generic_slots() {
+  for (int dt = 0; dt < NDT; ++dt)
+    for (int ad = 0; ad < NADD; ++ad)
+      for (int n = 1; n <= NMAX; ++n) {
+        Slot &s = g_slots[JM_KIND_GENERIC][ad][dt][n];
+        s.plan = jm::plan_generic(n, dt);
+        s.mod = nullptr;
+        s.cubin_bytes = (long long)jm_embedded_aot_cubin_len;
+        if (finish_function(s, G.generic[dt][ad]) == JM_OK) s.state.store(S_READY, std::memory_order_release);
+        else { s.err = t_err; s.state.store(S_FAILED, std::memory_order_release); }
+      }
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+int jit_mat_init(int device) {
+  std::lock_guard<std::mutex> lk(G.mu);
+  if (G.inited.load()) {
+    if (device >= 0 && device != G.ordinal)
+      return fail(JM_E_INVALID, "already initialised on device %d", G.ordinal);
+    return ensure_ctx();
+  }
+  int rc = load_driver();
+  if (rc != JM_OK) return rc;
+  CU_TRY(D.Init(0), "cuInit");
+  int ord = device;
+  if (ord < 0) {
+    CUcontext cur = nullptr;
+    CUdevice cd = 0;
+    ord = 0;
+    if (D.CtxGetCurrent(&cur) == CUDA_SUCCESS && cur && D.CtxGetDevice(&cd) == CUDA_SUCCESS) ord = (int)cd;
+  }
+  CU_TRY(D.DeviceGet(&G.dev, ord), "cuDeviceGet");
+  CU_TRY(D.DeviceGetAttribute(&G.cc_major, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, G.dev), "cuDeviceGetAttribute");
+  CU_TRY(D.DeviceGetAttribute(&G.cc_minor, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR, G.dev), "cuDeviceGetAttribute");
+  CU_TRY(D.DeviceGetAttribute(&G.sms, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, G.dev), "cuDeviceGetAttribute");
+  int major = G.cc_major;
+  if (const char *e = getenv("JIT_MAT_FAKE_CC_MAJOR")) major = atoi(e);   // tests of the JM_E_ARCH path
+  if (major != 10)
+    return fail(JM_E_ARCH, "device %d has compute capability %d.%d; this library targets sm_100a (B200) only",
+                ord, major, G.cc_minor);
+  CU_TRY(D.PrimaryCtxRetain(&G.ctx, G.dev), "cuDevicePrimaryCtxRetain");
+  G.ordinal = ord;
+  if ((rc = ensure_ctx()) != JM_OK) return rc;
+  CU_TRY(D.ModuleLoadData(&G.aot, jm_embedded_aot_cubin), "cuModuleLoadData(AoT cubin)");
+  static const char *gnames[NDT][NADD] = {{"jm_generic_f32_ones", "jm_generic_f32_identity"},
+                                          {"jm_generic_f64_ones", "jm_generic_f64_identity"}};
+  for (int dt = 0; dt < NDT; ++dt)
+    for (int ad = 0; ad < NADD; ++ad) CU_TRY(D.ModuleGetFunction(&G.generic[dt][ad], G.aot, gnames[dt][ad]), gnames[dt][ad]);
+  CU_TRY(D.ModuleGetFunction(&G.fill[0], G.aot, "jm_fill_f32"), "jm_fill_f32");
+  CU_TRY(D.ModuleGetFunction(&G.fill[1], G.aot, "jm_fill_f64"), "jm_fill_f64");
+  CU_TRY(D.ModuleGetFunction(&G.checksum[0], G.aot, "jm_checksum_f32"), "jm_checksum_f32");
+  CU_TRY(D.ModuleGetFunction(&G.checksum[1], G.aot, "jm_checksum_f64"), "jm_checksum_f64");
+  CU_TRY(D.MemAlloc(&G.sum_buf, 16), "cuMemAlloc(checksum)");
+  seed_generic_slots();
+  G.inited.store(true, std::memory_order_release);
+  return JM_OK;
+}
+
+int jit_mat_shutdown(void) {
+  std::lock_guard<std::mutex> lk(G.mu);
+  if (!G.inited.load()) return fail(JM_E_NOT_INITIALIZED, "not initialised");
+  ensure_ctx();
+  G.inited.store(false, std::memory_order_release);
+  for (int k = 0; k < NKIND; ++k)
+    for (int a = 0; a < NADD; ++a)
+      for (int t = 0; t < NDT; ++t)
+        for (int n = 0; n <= NMAX; ++n) {
+          Slot &s = g_slots[k][a][t][n];
+          std::lock_guard<std::mutex> sl(s.mu);
+          if (s.mod) D.ModuleUnload(s.mod);
+          s.mod = nullptr;
+          s.fn = nullptr;
+          s.err.clear();
+          s.regs = s.local_bytes = 0;
+          s.cubin_bytes = 0;
+          s.compile_ms = 0;
+          s.state.store(S_EMPTY, std::memory_order_release);
+        }
+  {
+    std::lock_guard<std::mutex> hl(G.host_mu);
+    for (int i = 0; i < 3; ++i) {
+      if (G.hbuf[i]) D.MemFree(G.hbuf[i]);
+      G.hbuf[i] = 0;
+      if (G.hs[i]) {
+        D.StreamDestroy(G.hs[i]);
+        D.EventDestroy(G.ev_h2d[i]);
+        D.EventDestroy(G.ev_cmp[i]);
+        D.EventDestroy(G.ev_d2h[i]);
+      }
+      G.hs[i] = nullptr;
+    }
+    G.hbuf_bytes = 0;
+  }
+  if (G.sum_buf) D.MemFree(G.sum_buf);
+  G.sum_buf = 0;
+  if (G.aot) D.ModuleUnload(G.aot);
+  G.aot = nullptr;
+  D.PrimaryCtxRelease(G.dev);
+  G.ctx = nullptr;
+  G.ordinal = -1;
+  G.stream.store(nullptr);
+  return JM_OK;
+}
+
+int jit_mat_run(int n, int dtype, int64_t batch, int64_t repeat, const void *in, void *out) {
+  jm_run_desc d{n, dtype, JM_ADDEND_ONES, JM_KIND_SPECIALIZED, batch, repeat, in, out, nullptr, 0u};
+  return run_impl(&d);
+}
+
+int jit_mat_run_ex(const jm_run_desc *d) { return run_impl(d); }
+
+int jit_mat_run_host(int n, int dtype, int64_t batch, int64_t repeat, const void *in, void *out) {
+  jm_run_desc d{n, dtype, JM_ADDEND_ONES, JM_KIND_SPECIALIZED, batch, repeat, in, out, nullptr,
+                JM_FLAG_HOST_BUFFERS};
+  return run_impl(&d);
+}
+
+int jit_mat_set_stream(void *cuda_stream) {
+  G.stream.store(cuda_stream, std::memory_order_relaxed);
+  return JM_OK;
+}
+
+int jit_mat_prepare(int n, int dtype, int addend, int kind) {
+  Slot *s = nullptr;
+  return lookup(n, dtype, addend, kind, &s);
+}
+
+int jit_mat_dtype_from_name(const char *name) {
+  if (!name) return fail(JM_E_INVALID, "NULL type name");
+  if (strcmp(name, "float") == 0) return JM_F32;
+  if (strcmp(name, "double") == 0) return JM_F64;
+  return fail(JM_E_UNSUPPORTED, "%s not supported on the GPU path (float, double)", name);
+}
+
+const char *jit_mat_last_error(void) { return t_err.c_str(); }
+
+int jit_mat_stats(jm_stats *out) {
+  if (!out) return fail(JM_E_INVALID, "NULL stats");
+  out->compilations = c_compilations.load();
+  out->hits = c_hits.load();
+  out->misses = c_misses.load();
+  out->launches = c_launches.load();
+  out->compile_ms_total = c_compile_us.load() / 1000.0;
+  int ready = 0, failed = 0;
+  for (int a = 0; a < NADD; ++a)
+    for (int t = 0; t < NDT; ++t)
+      for (int n = 1; n <= NMAX; ++n) {
+        const int st = g_slots[JM_KIND_SPECIALIZED][a][t][n].state.load();
+        ready += st == S_READY;
+        failed += st == S_FAILED;
+      }
+  out->keys_ready = ready;
+  out->keys_failed = failed;
+  return JM_OK;
+}
+
+int jit_mat_key_info(jm_key_info *keys, int cap) {
+  int cnt = 0;
+  for (int k = 0; k < NKIND; ++k)
+    for (int a = 0; a < NADD; ++a)
+      for (int t = 0; t < NDT; ++t)
+        for (int n = 1; n <= NMAX; ++n) {
+          Slot &s = g_slots[k][a][t][n];
+          const int st = s.state.load(std::memory_order_acquire);
+          if (st == S_EMPTY) continue;
+          if (keys && cnt < cap) {
+            jm_key_info &o = keys[cnt];
+            o.n = n; o.dtype = t; o.addend = a; o.kind = k; o.state = st;
+            o.regs = s.regs; o.local_bytes = s.local_bytes; o.smem_bytes = s.plan.smem;
+            o.threads = s.plan.threads;
+            o.tile = k == JM_KIND_GENERIC ? JM_TILE_GENERIC
+                     : (s.plan.tile == (int)jm::Tile::TPM ? JM_TILE_TPM
+                        : s.plan.tile == (int)jm::Tile::Dmma ? (s.plan.w > 1 ? JM_TILE_CTA_DMMA : JM_TILE_WARP_DMMA)
+                        : (s.plan.w > 1 ? JM_TILE_CTA_F32 : JM_TILE_WARP_F32));
+            o.cubin_bytes = s.cubin_bytes;
+            o.compile_ms = s.compile_ms;
+          }
+          ++cnt;
+        }
+  return cnt;
+}
+
+int jit_mat_reset_stats(void) {
+  c_compilations = 0; c_hits = 0; c_misses = 0; c_launches = 0; c_compile_us = 0;
+  return JM_OK;
+}
+
+int jit_mat_fill(int n, int dtype, int dist, uint64_t seed, int64_t global_first, int64_t batch, void *out) {
+  int rc = check_key(n, dtype, JM_ADDEND_ONES, JM_KIND_SPECIALIZED);
+  if (rc != JM_OK) return rc;
+  if (dist < 0 || dist > 2) return fail(JM_E_INVALID, "dist %d invalid", dist);
+  if (batch < 0 || global_first < 0) return fail(JM_E_INVALID, "negative batch/global_first");
+  if (!G.inited.load()) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
+  if (batch == 0) return JM_OK;
+  if (!out) return fail(JM_E_INVALID, "NULL buffer");
+  if ((rc = ensure_ctx()) != JM_OK) return rc;
+  long long total = (long long)batch * n * n, gf = global_first;
+  unsigned long long sd = seed;
+  int nn = n, ds = dist;
+  CUdeviceptr p = (CUdeviceptr)out;
+  void *args[] = {&p, &nn, &ds, &sd, &gf, &total};
+  long long blocks = (total + 255) / 256;
+  if (blocks > (long long)G.sms * 16) blocks = (long long)G.sms * 16;
+  CUstream st = (CUstream)G.stream.load();
+  CU_TRY(D.LaunchKernel(G.fill[dtype], (unsigned)blocks, 1, 1, 256, 1, 1, 0, st, args, nullptr), "cuLaunchKernel(fill)");
+  c_launches++;
+  return sync_if(0, st);
+}
+
+int jit_mat_checksum(int n, int dtype, int64_t global_first, int64_t batch, const void *x,
+                     uint64_t *host_u64, double *host_f64) {
+  int rc = check_key(n, dtype, JM_ADDEND_ONES, JM_KIND_SPECIALIZED);
+  if (rc != JM_OK) return rc;
+  if (batch < 0 || global_first < 0) return fail(JM_E_INVALID, "negative batch/global_first");
+  if (!G.inited.load()) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
+  if (!host_u64 || !host_f64 || (batch > 0 && !x)) return fail(JM_E_INVALID, "NULL pointer");
+  if ((rc = ensure_ctx()) != JM_OK) return rc;
+  CUstream st = (CUstream)G.stream.load();
+  CU_TRY(D.MemsetD8Async(G.sum_buf, 0, 16, st), "cuMemsetD8Async");
+  long long total = (long long)batch * n * n, gf = global_first;
+  if (total > 0) {
+    int nn = n;
+    CUdeviceptr px = (CUdeviceptr)x, pu = G.sum_buf, pf = G.sum_buf + 8;
+    void *args[] = {&px, &nn, &gf, &total, &pu, &pf};
+    long long blocks = (total + 255) / 256;
+    if (blocks > (long long)G.sms * 8) blocks = (long long)G.sms * 8;
+    CU_TRY(D.LaunchKernel(G.checksum[dtype], (unsigned)blocks, 1, 1, 256, 1, 1, 0, st, args, nullptr),
+           "cuLaunchKernel(checksum)");
+    c_launches++;
+  }
+  unsigned long long hv[2] = {0, 0};
+  CU_TRY(D.MemcpyDtoHAsync(hv, G.sum_buf, 16, st), "cuMemcpyDtoHAsync(checksum)");
+  CU_TRY(D.StreamSynchronize(st), "checksum");
+  *host_u64 = hv[0];
+  memcpy(host_f64, &hv[1], 8);
+  return JM_OK;
+}
+
+int jit_mat_device_info(int *sm_count, int *cc_major, int *cc_minor) {
+  if (!G.inited.load()) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
+  if (sm_count) *sm_count = G.sms;
+  if (cc_major) *cc_major = G.cc_major;
+  if (cc_minor) *cc_minor = G.cc_minor;
+  return JM_OK;
+}
+
+const char *jit_mat_version(void) {
+  static char buf[96];
+  int maj = 0, min = 0;
+  nvrtcVersion(&maj, &min);
+  snprintf(buf, sizeof buf, "jitmat 0.1 (sm_100a; NVRTC %d.%d static)", maj, min);
+  return buf;
+}
+
+// Test hook: NVRTC-compile a key without a device (no module load).  Lets the
+// CPU-only test tier prove every specialization compiles for sm_100a.
+int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes) {
+  int rc = check_key(n, dtype, addend, JM_KIND_SPECIALIZED);
+  if (rc != JM_OK) return rc;
+  std::vector<char> cubin;
+  std::string lowered, log;
+  rc = nvrtc_compile(n, dtype, addend, cubin, lowered, log);
+  if (rc != JM_OK) return fail(rc, "%s", log.c_str());
+  if (cubin_bytes) *cubin_bytes = (long long)cubin.size();
+  return JM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+"""C ABI behaviour on the GPU: cache laws, error codes, concurrency, key info.
+
+Cache-law ideas follow SPEC.md:644 (1000 calls over 10 keys -> 10
+compilations) and SPEC.md:561 (concurrent lookup, mutually exclusive
+insertion); the paper's program-global cache is PAPER.md:306 / Algorithm 1
+lines 319 and 347.
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+
+import jm_synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture()
+def jm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1904_08555_b200 as jm
+    torch.cuda.init()
+    jm.jit_mat_init(0)
+    yield jm
+
+
+def _fresh(jm):
+    jm.jit_mat_shutdown()
+    jm.jit_mat_init(0)
+    jm.jit_mat_reset_stats()
+
+
+def test_single_compilation_law(jm):
+    _fresh(jm)
+    rng = np.random.default_rng(1904)
+    keys = [(n, dt) for n, dt in zip([2, 3, 5, 8, 11, 16, 21, 32, 40, 64],
+                                     ["f64", "f32"] * 5)]
+    bufs = {}
+    for n, dt in keys:
+        tdt = torch.float64 if dt == "f64" else torch.float32
+        bufs[(n, dt)] = torch.zeros(4, n, n, dtype=tdt, device="cuda")
+    trace = rng.integers(0, len(keys), 1000)
+    for i in trace:
+        n, dt = keys[i]
+        x = bufs[(n, dt)]
+        jm.jit_mat_run(n, dt, 4, 1, x.data_ptr(), x.data_ptr())
+    torch.cuda.synchronize()
+    st = jm.jit_mat_stats()
+    assert st["compilations"] == 10
+    assert st["misses"] == 10
+    assert st["hits"] == 990
+    assert st["launches"] == 1000
+    assert st["keys_ready"] == 10
+
+
+def test_concurrent_cold_key_compiles_once(jm):
+    _fresh(jm)
+    errs = []
+
+    def worker():
+        try:
+            jm.jit_mat_prepare(24, "double")
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=worker) for _ in range(16)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs
+    st = jm.jit_mat_stats()
+    assert st["compilations"] == 1
+    assert st["hits"] + st["misses"] == 16
+
+
+def test_distinct_keys_compile_in_parallel_threads(jm):
+    _fresh(jm)
+    keys = [(n, dt) for n in (6, 9, 14, 27) for dt in ("double", "float")]
+    ts = [threading.Thread(target=jm.jit_mat_prepare, args=k) for k in keys]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert jm.jit_mat_stats()["compilations"] == len(keys)
+
+
+def test_generic_is_preseeded(jm):
+    _fresh(jm)
+    for n in (1, 7, 64):
+        jm.jit_mat_prepare(n, "double", kind="generic")
+    assert jm.jit_mat_stats()["compilations"] == 0
+
+
+def test_key_info_reports_registers(jm):
+    _fresh(jm)
+    for n, dt in ((4, "double"), (16, "double"), (16, "float"), (64, "double")):
+        jm.jit_mat_prepare(n, dt)
+    info = {(k["n"], k["dtype"], k["kind"]): k for k in jm.jit_mat_key_info()}
+    k16 = info[(16, 1, 0)]
+    assert k16["state"] == 2 and k16["regs"] > 0 and k16["cubin_bytes"] > 0
+    assert k16["tile_name"] == "warp_dmma"
+    assert info[(64, 1, 0)]["tile_name"] == "cta_dmma"
+    assert info[(4, 1, 0)]["tile_name"] == "tpm"
+    assert info[(16, 0, 0)]["tile_name"] == "warp_f32"
+    for k in info.values():
+        assert k["local_bytes"] == 0, f"spill in {k}"
+
+
+def test_error_codes(jm):
+    x = torch.zeros(8, 4, 4, dtype=torch.float64, device="cuda")
+    p = x.data_ptr()
+    lib = jm.lib
+    assert lib.jit_mat_run(0, 1, 8, 1, p, p) == jm.JM_E_INVALID
+    assert lib.jit_mat_run(65, 1, 8, 1, p, p) == jm.JM_E_UNSUPPORTED
+    assert lib.jit_mat_run(4, 2, 8, 1, p, p) == jm.JM_E_UNSUPPORTED
+    assert lib.jit_mat_run(4, 1, -1, 1, p, p) == jm.JM_E_INVALID
+    assert lib.jit_mat_run(4, 1, 8, -1, p, p) == jm.JM_E_INVALID
+    assert lib.jit_mat_run(4, 1, 8, 1 << 31, p, p) == jm.JM_E_INVALID
+    assert lib.jit_mat_run(4, 1, 4, 1, p + 8, p + 8) == jm.JM_E_ALIGN
+    assert lib.jit_mat_run(4, 1, 4, 1, p, p + 128) == jm.JM_E_INVALID   # partial overlap
+    assert lib.jit_mat_run(4, 1, 4, 1, None, p) == jm.JM_E_INVALID
+    assert lib.jit_mat_run(4, 1, 0, 1, None, None) == jm.JM_OK            # empty batch
+    assert lib.jit_mat_dtype_from_name(b"long double") == jm.JM_E_UNSUPPORTED
+    assert "long double" in jm.jit_mat_last_error()
+    assert lib.jit_mat_dtype_from_name(b"double") == jm.JM_F64
+    assert lib.jit_mat_dtype_from_name(b"float") == jm.JM_F32
+    assert lib.jit_mat_init(1 if torch.cuda.device_count() == 1 else 0) in (jm.JM_E_INVALID, jm.JM_OK)
+
+
+def test_shutdown_then_not_initialized(jm):
+    x = torch.zeros(2, 3, 3, dtype=torch.float32, device="cuda")
+    jm.jit_mat_shutdown()
+    assert jm.lib.jit_mat_run(3, 0, 2, 1, x.data_ptr(), x.data_ptr()) == jm.JM_E_NOT_INITIALIZED
+    assert jm.lib.jit_mat_prepare(3, 0, 0, 0) == jm.JM_E_NOT_INITIALIZED
+    jm.jit_mat_init(0)
+    y = jm.run(x, 1, sync=True)
+    assert torch.all(y == 1.0)   # O1: zero input, one repeat -> all ones
+
+
+def test_device_info(jm):
+    info = jm.jit_mat_device_info()
+    assert info["cc"][0] == 10
+    assert info["sm_count"] == torch.cuda.get_device_properties(0).multi_processor_count
+
+
+def test_set_stream_is_honoured(jm):
+    s = torch.cuda.Stream()
+    x = jm_synth.generate(16, "f64", "bench", 1, 0, 4096)
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty_like(xd)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        jm.jit_mat_set_stream(s.cuda_stream)
+        jm.jit_mat_run(16, "f64", 4096, 10, xd.data_ptr(), out.data_ptr())
+        ev = torch.cuda.Event()
+        ev.record(s)
+    ev.synchronize()
+    ref = torch.empty_like(xd)
+    jm.run(xd, 10, ref, sync=True)
+    assert torch.equal(out, ref)
+    jm.jit_mat_set_stream(torch.cuda.current_stream().cuda_stream)
