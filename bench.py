@@ -226,6 +226,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1904_08555_b200 as jm
+    from paper_1904_08555_b200 import shard
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -239,7 +240,7 @@ def main():
     n, dt, B, R = a.n, a.dtype, a.batch, a.repeat
     tdt = torch.float64 if dt == "f64" else torch.float32
     es = 8 if dt == "f64" else 4
-    gfirst = rank * B
+    gfirst, _ = shard.weak_slice(rank, B)
     x = torch.empty(B, n, n, dtype=tdt, device=dev)
     y = torch.empty_like(x)
 
@@ -289,21 +290,15 @@ def main():
     ms_step = el_ms / a.steps
 
     # max over ranks + checksum gather (NCCL, outside the data path)
-    csum, fsum = jm.jit_mat_checksum(n, dt, gfirst, B, y.data_ptr())
-    rec = torch.tensor([ms_step, float(B)], dtype=torch.float64, device=dev)
-    ck = torch.tensor([csum - (1 << 64) if csum >= (1 << 63) else csum], dtype=torch.int64, device=dev)
+    csum, _ = jm.jit_mat_checksum(n, dt, gfirst, B, y.data_ptr())
     if world > 1:
-        recs = torch.empty(world, 2, dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(recs, rec)
-        cks = torch.empty(world, dtype=torch.int64, device=dev)
-        dist.all_gather_into_tensor(cks, ck)
-        recs, cks = recs.cpu().tolist(), cks.cpu().tolist()
+        recs, cks = shard.gather_record(dist, [ms_step, float(B)], [csum], dev)
     else:
-        recs, cks = [rec.cpu().tolist()], ck.cpu().tolist()
+        recs, cks = [[ms_step, float(B)]], [[csum]]
     ms_max = max(r[0] for r in recs)
     total_units = sum(r[1] for r in recs) * R
     value = total_units / (ms_max / 1e3)
-    global_checksum = sum(c & ((1 << 64) - 1) for c in cks) & ((1 << 64) - 1)
+    global_checksum = shard.combine_checksums(c[0] for c in cks)
 
     fpu = flops_per_update(n, a.addend)
     achieved_tf = B * R * fpu / (ms_step / 1e3) / 1e12       # this rank's kernel
@@ -361,13 +356,8 @@ def main():
         gsteps = max(2, min(5, a.steps))
         g_ms, _ = timed("generic", gsteps, 1)
         g_ms_step = g_ms / gsteps
-        recg = torch.tensor([g_ms_step], dtype=torch.float64, device=dev)
-        if world > 1:
-            allg = torch.empty(world, dtype=torch.float64, device=dev)
-            dist.all_gather_into_tensor(allg, recg)
-            g_max = float(allg.max())
-        else:
-            g_max = g_ms_step
+        g_max = (max(r[0] for r in shard.gather_record(dist, [g_ms_step], [], dev)[0])
+                 if world > 1 else g_ms_step)
         gval = B * world * R / (g_max / 1e3)
         line["generic"] = {"value": gval, "unit": UNIT, "ms_per_step": g_max,
                            "gflops": gval * fpu / 1e9,
@@ -385,13 +375,8 @@ def main():
         for _ in range(e2e_steps):
             jm.jit_mat_run_host(n, dt, B, R, hx.data_ptr(), hy.data_ptr())
         el = time.perf_counter() - t0
-        rece = torch.tensor([el / e2e_steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            alle = torch.empty(world, dtype=torch.float64, device=dev)
-            dist.all_gather_into_tensor(alle, rece)
-            e_max = float(alle.max())
-        else:
-            e_max = el / e2e_steps
+        e_max = (max(r[0] for r in shard.gather_record(dist, [el / e2e_steps], [], dev)[0])
+                 if world > 1 else el / e2e_steps)
         line["e2e"] = {"value": B * world * R / e_max, "unit": UNIT,
                        "h2d_bytes_per_step": B * n * n * es, "d2h_bytes_per_step": B * n * n * es,
                        "ms_per_step": e_max * 1e3, "steps": e2e_steps,
