@@ -72,7 +72,11 @@ enum { JM_ADDEND_ONES = 0, JM_ADDEND_IDENTITY = 1 };
 
 /* kernel kind: the NVRTC-specialized template (Listing 5) or the AoT
  * runtime-N generic kernel (Listing 4) */
-enum { JM_KIND_SPECIALIZED = 0, JM_KIND_GENERIC = 1 };
+enum { JM_KIND_SPECIALIZED = 0, JM_KIND_GENERIC = 1,
+       /* the same template compiled AHEAD of time by nvcc for Fig. 3's sizes
+        * (n = 3, 7, 16, double): pre-seeded at init, never
+        * compiled at run time; other keys -> JM_E_UNSUPPORTED */
+       JM_KIND_AOT_SPECIALIZED = 2 };
 
 /* status codes */
 enum {
@@ -134,6 +138,18 @@ JM_API int jit_mat_run_ex(const jm_run_desc *d);
 /* Convenience for the host-buffer path = run_ex(kind SPECIALIZED, addend Ones,
  * JM_FLAG_HOST_BUFFERS).  Synchronous. */
 JM_API int jit_mat_run_host(int n, int dtype, int64_t batch, int64_t repeat, const void *in, void *out);
+
+/* Mixed-N batch (BASELINE.json configs[3]): `count` independent groups, each a
+ * device-buffer descriptor with its own n / dtype / addend / kind / batch /
+ * repeat (the per-descriptor `stream` and JM_FLAG_HOST_BUFFERS are not allowed).
+ * All cold keys are specialized first, concurrently on host threads (distinct
+ * keys compile in parallel, "roughly additive" compile times
+ * become overlapped); then the groups are launched concurrently on a pool of
+ * library streams forked from and joined back into `stream` (NULL = the set
+ * stream), so small groups fill the GPU together.  Asynchronous w.r.t. the
+ * host unless `flags` has JM_FLAG_SYNC.  Every descriptor is validated before
+ * anything is compiled or launched. */
+JM_API int jit_mat_run_many(const jm_run_desc *descs, int count, void *stream, unsigned flags);
 
 /* Stream used by jit_mat_run (e.g. torch.cuda.current_stream().cuda_stream). */
 JM_API int jit_mat_set_stream(void *cuda_stream);

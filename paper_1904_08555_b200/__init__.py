@@ -19,12 +19,14 @@ import os
 from ._lib import (  # noqa: F401  (re-exported C ABI)
     JM_ADDEND_IDENTITY, JM_ADDEND_ONES, JM_E_ALIGN, JM_E_ARCH, JM_E_COMPILE, JM_E_CUDA,
     JM_E_INVALID, JM_E_NOT_INITIALIZED, JM_E_UNSUPPORTED, JM_F32, JM_F64, JM_FLAG_HOST_BUFFERS,
-    JM_FLAG_SYNC, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK, JM_TILE_NAMES, JitMatError,
+    JM_FLAG_SYNC, JM_KIND_AOT_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK,
+    JM_TILE_NAMES, JitMatError,
     jm_key_info, jm_run_desc, jm_stats, lib, lib_path,
 )
 
 __all__ = [
     "jit_mat_init", "jit_mat_run", "jit_mat_shutdown", "jit_mat_run_ex", "jit_mat_run_host",
+    "jit_mat_run_many",
     "jit_mat_set_stream", "jit_mat_prepare", "jit_mat_dtype_from_name", "jit_mat_last_error",
     "jit_mat_stats", "jit_mat_key_info", "jit_mat_reset_stats", "jit_mat_fill",
     "jit_mat_checksum", "jit_mat_device_info", "jit_mat_version", "jit_mat_compile_check",
@@ -34,7 +36,8 @@ __all__ = [
 _DTYPES = {"float": JM_F32, "f32": JM_F32, "float32": JM_F32,
            "double": JM_F64, "f64": JM_F64, "float64": JM_F64}
 _ADDENDS = {"ones": JM_ADDEND_ONES, "identity": JM_ADDEND_IDENTITY}
-_KINDS = {"specialized": JM_KIND_SPECIALIZED, "generic": JM_KIND_GENERIC}
+_KINDS = {"specialized": JM_KIND_SPECIALIZED, "generic": JM_KIND_GENERIC,
+          "aot_specialized": JM_KIND_AOT_SPECIALIZED}
 
 
 def _check(rc: int, what: str) -> int:
@@ -79,6 +82,19 @@ def jit_mat_run_host(n: int, dtype, batch: int, repeat: int, in_ptr: int, out_pt
     _check(lib.jit_mat_run_host(int(n), _dt(dtype), int(batch), int(repeat),
                                 ctypes.c_void_p(in_ptr), ctypes.c_void_p(out_ptr)),
            "jit_mat_run_host")
+
+
+def jit_mat_run_many(groups, stream: int | None = None, sync: bool = False) -> None:
+    """Mixed-N batch: ``groups`` is a sequence of dicts with keys n, dtype, batch,
+    repeat, in_ptr, out_ptr and optional addend / kind (C: jit_mat_run_many)."""
+    arr = (jm_run_desc * max(1, len(groups)))()
+    for i, g in enumerate(groups):
+        arr[i] = jm_run_desc(int(g["n"]), _dt(g["dtype"]), _ADDENDS.get(g.get("addend", "ones"), 0),
+                             _KINDS.get(g.get("kind", "specialized"), 0), int(g["batch"]),
+                             int(g["repeat"]), ctypes.c_void_p(g["in_ptr"]),
+                             ctypes.c_void_p(g["out_ptr"]), None, 0)
+    _check(lib.jit_mat_run_many(arr, len(groups), ctypes.c_void_p(stream or 0),
+                                JM_FLAG_SYNC if sync else 0), "jit_mat_run_many")
 
 
 def jit_mat_set_stream(stream: int | None) -> None:

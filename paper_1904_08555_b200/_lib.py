@@ -14,7 +14,7 @@ lib = ctypes.CDLL(lib_path)
 
 JM_F32, JM_F64 = 0, 1
 JM_ADDEND_ONES, JM_ADDEND_IDENTITY = 0, 1
-JM_KIND_SPECIALIZED, JM_KIND_GENERIC = 0, 1
+JM_KIND_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_AOT_SPECIALIZED = 0, 1, 2
 JM_OK = 0
 JM_E_INVALID, JM_E_UNSUPPORTED, JM_E_NOT_INITIALIZED = -1, -2, -3
 JM_E_ARCH, JM_E_COMPILE, JM_E_CUDA, JM_E_ALIGN = -4, -5, -6, -7
@@ -58,6 +58,7 @@ _SIGS = {
     "jit_mat_shutdown": (_I, []),
     "jit_mat_run_ex": (_I, [ctypes.POINTER(jm_run_desc)]),
     "jit_mat_run_host": (_I, [_I, _I, _I64, _I64, _P, _P]),
+    "jit_mat_run_many": (_I, [ctypes.POINTER(jm_run_desc), _I, _P, ctypes.c_uint]),
     "jit_mat_set_stream": (_I, [_P]),
     "jit_mat_prepare": (_I, [_I, _I, _I, _I]),
     "jit_mat_dtype_from_name": (_I, [ctypes.c_char_p]),

@@ -122,6 +122,24 @@ JM_GENERIC(jm_generic_f32_identity, float, jm::Addend::Identity)
 JM_GENERIC(jm_generic_f64_ones, double, jm::Addend::Ones)
 JM_GENERIC(jm_generic_f64_identity, double, jm::Addend::Identity)
 
+// AoT SPECIALIZATIONS ("explicit
+// specializations ... are used instead", Fig. 3 "AoT specialization" bar,
+// PAPER.md:440-466): the very same template body the NVRTC path instantiates,
+// compiled here by nvcc for the sizes of Fig. 3 (3, 7, 16) in double, so the
+// three-way comparison JIT / AoT-specialization / AoT-generic can be made.
+#define JM_AOT_SPEC(N, T, TN, ADD, AN)                                                           \
+  extern "C" __global__ void __launch_bounds__(jm::plan_specialized(N, TN).threads)              \
+      jm_aotspec_##T##_n##N##_##AN(const T *__restrict__ in, T *__restrict__ out, long long batch, \
+                                   int repeat) {                                                 \
+    jm::update_body<N, T, ADD, jm::tile_for(N, TN)>(in, out, batch, repeat);                     \
+  }
+JM_AOT_SPEC(3, double, 1, jm::Addend::Ones, ones)
+JM_AOT_SPEC(7, double, 1, jm::Addend::Ones, ones)
+JM_AOT_SPEC(16, double, 1, jm::Addend::Ones, ones)
+JM_AOT_SPEC(3, double, 1, jm::Addend::Identity, identity)
+JM_AOT_SPEC(7, double, 1, jm::Addend::Identity, identity)
+JM_AOT_SPEC(16, double, 1, jm::Addend::Identity, identity)
+
 extern "C" __global__ void jm_fill_f32(float *out, int n, int dist, unsigned long long seed,
                                        long long gfirst, long long total) {
   jm::fill_impl<float>(out, n, dist, seed, gfirst, total);

@@ -56,7 +56,12 @@ constexpr int TPM_THREADS = 128;
 // ---- DMMA (FP64) ----
 constexpr int DMMA_WPC = 4;                       // warps per CTA when W == 1
 JM_HD constexpr int dmma_t8(int n) { return cdiv(n, 8); }
-JM_HD constexpr int dmma_rt(int n) { return n <= 32 ? dmma_t8(n) : ((dmma_t8(n) % 2 == 0) ? 2 : 1); }
+// row tiles per warp: whole matrix per warp up to n = 24; two warps of two
+// row tiles for 25..32 (keeps the accumulators + product copy under ~128 regs);
+// above 32 one CTA per matrix, two (even T8) or one (odd T8) row tile per warp.
+JM_HD constexpr int dmma_rt(int n) {
+  return n <= 24 ? dmma_t8(n) : ((dmma_t8(n) % 2 == 0) ? 2 : 1);
+}
 JM_HD constexpr int dmma_w(int n) { return dmma_t8(n) / dmma_rt(n); }
 JM_HD constexpr int dmma_rsc(int n) { return rup(4 * dmma_t8(n), 8); }     // scratch row stride, 16-B chunks
 JM_HD constexpr int dmma_scr(int n) { return 8 * dmma_t8(n) * dmma_rsc(n) * 16; }  // one scratch buffer
@@ -90,6 +95,11 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
     return Plan{(int)t, 32 * F32_WPC, F32_WPC,
                 stage_bytes(F32_WPC, n, es) + F32_WPC * f32_buf(n), 1};
   return Plan{(int)t, 32 * w, 1, stage_bytes(1, n, es) + 2 * f32_buf(n), w};
+}
+
+// ---- AoT specializations (nvcc-compiled at build time; Fig. 3's sizes) ----
+JM_HD constexpr bool aot_spec_available(int n, int dtype) {
+  return dtype == 1 && (n == 3 || n == 7 || n == 16);
 }
 
 // ---- GENERIC (runtime N; AoT) ----

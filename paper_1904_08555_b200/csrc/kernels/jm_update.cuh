@@ -31,6 +31,12 @@ __device__ __forceinline__ uint4 ldg_nc16(const void *p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;
 }
+// 128-bit shared store of two doubles (keeps ptxas from splitting it into two
+// 64-bit stores when it cannot prove the swizzled offset is 16-B aligned).
+__device__ __forceinline__ void sts_f64x2(void *p, double a, double b) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(s), "d"(a), "d"(b) : "memory");
+}
 __device__ __forceinline__ void stg16(void *p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
@@ -297,8 +303,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
         for (int I = 0; I < RT; ++I)
 #pragma unroll
           for (int J = 0; J < T8; ++J)
-            *reinterpret_cast<double2 *>(sb + scr_off<RSC>(8 * (wr * RT + I) + g, 4 * J + t)) =
-                make_double2(acc[I][J][0], acc[I][J][1]);
+            sts_f64x2(sb + scr_off<RSC>(8 * (wr * RT + I) + g, 4 * J + t), acc[I][J][0], acc[I][J][1]);
         if constexpr (W == 1) __syncwarp(); else __syncthreads();
         double p[RT][T8][2];
 #pragma unroll
@@ -492,8 +497,8 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
 // The NVRTC name expression is "jm::k_update<N, T, jm::Addend::X, jm::Tile::Y>"
 // with Y = tile_for(N, dtype); the host launches it with plan_specialized().
 template <int N, class T, Addend A, Tile K>
-__global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).threads)
-    k_update(const T *__restrict__ in, T *__restrict__ out, long long batch, int repeat) {
+__device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restrict__ out,
+                                            long long batch, int repeat) {
   static_assert(N >= 1 && N <= 64, "N in [1, 64]");
   static_assert(K == tile_for(N, sizeof(T) == 8 ? 1 : 0), "tile must match the plan");
   if constexpr (K == Tile::TPM) {
@@ -503,6 +508,12 @@ __global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).th
   } else {
     run_f32<N, A, f32_w(N)>(in, out, batch, repeat);
   }
+}
+
+template <int N, class T, Addend A, Tile K>
+__global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).threads)
+    k_update(const T *__restrict__ in, T *__restrict__ out, long long batch, int repeat) {
+  update_body<N, T, A, K>(in, out, batch, repeat);
 }
 
 }  // namespace jm

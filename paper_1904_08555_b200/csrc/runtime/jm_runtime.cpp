@@ -25,6 +25,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdarg>
@@ -33,6 +34,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -178,7 +180,7 @@ struct Slot {
   std::string err;
 };
 
-constexpr int NKIND = 2, NADD = 2, NDT = 2, NMAX = JM_N_MAX;
+constexpr int NKIND = 3, NADD = 2, NDT = 2, NMAX = JM_N_MAX;
 Slot g_slots[NKIND][NADD][NDT][NMAX + 1];
 
 struct State {
@@ -341,7 +343,8 @@ int check_key(int n, int dtype, int addend, int kind) {
   if (n > JM_N_MAX) return fail(JM_E_UNSUPPORTED, "n = %d exceeds the supported maximum %d", n, JM_N_MAX);
   if (dtype != JM_F32 && dtype != JM_F64) return fail(JM_E_UNSUPPORTED, "dtype %d not supported (f32/f64 only)", dtype);
   if (addend != JM_ADDEND_ONES && addend != JM_ADDEND_IDENTITY) return fail(JM_E_INVALID, "addend %d invalid", addend);
-  if (kind != JM_KIND_SPECIALIZED && kind != JM_KIND_GENERIC) return fail(JM_E_INVALID, "kind %d invalid", kind);
+  if (kind != JM_KIND_SPECIALIZED && kind != JM_KIND_GENERIC && kind != JM_KIND_AOT_SPECIALIZED)
+    return fail(JM_E_INVALID, "kind %d invalid", kind);
   return JM_OK;
 }
 
@@ -364,6 +367,9 @@ int lookup(int n, int dtype, int addend, int kind, Slot **out) {
   if (st == S_READY) { *out = &s; return JM_OK; }
   if (st == S_FAILED) return fail(JM_E_COMPILE, "%s", s.err.c_str());
   if (kind == JM_KIND_GENERIC) return fail(JM_E_INVALID, "generic slot not seeded");
+  if (kind == JM_KIND_AOT_SPECIALIZED)
+    return fail(JM_E_UNSUPPORTED, "no ahead-of-time specialization for n=%d %s (available: n = 3, 7, 16, double)",
+                n, dtype == JM_F64 ? "double" : "float");
   s.state.store(S_COMPILING, std::memory_order_relaxed);
   rc = compile_slot(s, n, dtype, addend);
   if (rc != JM_OK) {
@@ -485,6 +491,85 @@ int run_impl(const jm_run_desc *d) {
   return sync_if(d->flags, st);
 }
 
+// Mixed-N: resolve every key (cold keys compile concurrently), then fork the
+// groups over a pool of streams and join them back into the caller's stream.
+constexpr int POOL = 8;
+std::mutex g_pool_mu;
+CUstream g_pool[POOL] = {};
+CUevent g_fork = nullptr, g_join[POOL] = {};
+
+int run_many_impl(const jm_run_desc *d, int count, void *stream, unsigned flags) {
+  if (count < 0 || (count > 0 && !d)) return fail(JM_E_INVALID, "bad descriptor array");
+  for (int i = 0; i < count; ++i) {
+    if (d[i].flags & JM_FLAG_HOST_BUFFERS) return fail(JM_E_INVALID, "descriptor %d: host buffers not allowed", i);
+    if (d[i].stream) return fail(JM_E_INVALID, "descriptor %d: per-descriptor stream not allowed", i);
+    int rc = validate_run(&d[i]);
+    if (rc != JM_OK) {
+      t_err = "descriptor " + std::to_string(i) + ": " + t_err;
+      return rc;
+    }
+  }
+  // 1. specialize: distinct cold keys in parallel (one host thread per key)
+  std::vector<Slot *> slots((size_t)count, nullptr);
+  std::vector<int> todo;
+  for (int i = 0; i < count; ++i) {
+    if (d[i].batch == 0) continue;
+    Slot &s = g_slots[d[i].kind][d[i].addend][d[i].dtype][d[i].n];
+    if (s.state.load(std::memory_order_acquire) != S_READY) todo.push_back(i);
+  }
+  if (todo.size() > 1) {
+    std::vector<std::thread> th;
+    std::vector<int> rcs(todo.size(), JM_OK);
+    std::vector<std::string> errs(todo.size());
+    for (size_t t = 0; t < todo.size(); ++t)
+      th.emplace_back([&, t] {
+        Slot *s = nullptr;
+        const jm_run_desc &x = d[todo[t]];
+        rcs[t] = lookup(x.n, x.dtype, x.addend, x.kind, &s);
+        if (rcs[t] != JM_OK) errs[t] = t_err;
+      });
+    for (auto &t : th) t.join();
+    for (size_t t = 0; t < todo.size(); ++t)
+      if (rcs[t] != JM_OK) return fail(rcs[t], "descriptor %d: %s", todo[t], errs[t].c_str());
+  }
+  for (int i = 0; i < count; ++i) {
+    if (d[i].batch == 0) continue;
+    int rc = lookup(d[i].n, d[i].dtype, d[i].addend, d[i].kind, &slots[(size_t)i]);
+    if (rc != JM_OK) return rc;
+  }
+  int rc = ensure_ctx();
+  if (rc != JM_OK) return rc;
+  CUstream st = (CUstream)(stream ? stream : G.stream.load(std::memory_order_relaxed));
+  // 2. fork / launch / join; biggest groups first, round-robin over the pool
+  std::vector<int> order;
+  for (int i = 0; i < count; ++i)
+    if (d[i].batch > 0) order.push_back(i);
+  auto work = [&](int i) { return (double)d[i].batch * d[i].n * d[i].n * (d[i].n + 1) * (double)(d[i].repeat + 1); };
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return work(a) > work(b); });
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_fork) {
+    CU_TRY(D.EventCreate(&g_fork, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    for (int p = 0; p < POOL; ++p) {
+      CU_TRY(D.StreamCreate(&g_pool[p], CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+      CU_TRY(D.EventCreate(&g_join[p], CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    }
+  }
+  const int used = (int)std::min<size_t>(order.size(), POOL);
+  if (used == 0) return JM_OK;
+  CU_TRY(D.EventRecord(g_fork, st), "cuEventRecord(fork)");
+  for (int p = 0; p < used; ++p) CU_TRY(D.StreamWaitEvent(g_pool[p], g_fork, 0), "cuStreamWaitEvent(fork)");
+  for (size_t k = 0; k < order.size(); ++k) {
+    const jm_run_desc &x = d[order[k]];
+    rc = launch(*slots[(size_t)order[k]], x.n, x.batch, x.repeat, x.in, x.out, g_pool[k % used], x.kind);
+    if (rc != JM_OK) return rc;
+  }
+  for (int p = 0; p < used; ++p) {
+    CU_TRY(D.EventRecord(g_join[p], g_pool[p]), "cuEventRecord(join)");
+    CU_TRY(D.StreamWaitEvent(st, g_join[p], 0), "cuStreamWaitEvent(join)");
+  }
+  return sync_if(flags, st);
+}
+
 void seed_generic_slots() {
   for (int dt = 0; dt < NDT; ++dt)
     for (int ad = 0; ad < NADD; ++ad)
@@ -496,6 +581,27 @@ void seed_generic_slots() {
         if (finish_function(s, G.generic[dt][ad]) == JM_OK) s.state.store(S_READY, std::memory_order_release);
         else { s.err = t_err; s.state.store(S_FAILED, std::memory_order_release); }
       }
+}
+
+// Explicit (ahead-of-time) specializations take precedence over compiling
+// (PAPER.md:176): their slots are READY from the start.
+int seed_aot_spec_slots() {
+  for (int ad = 0; ad < NADD; ++ad)
+    for (int n = 1; n <= NMAX; ++n) {
+      if (!jm::aot_spec_available(n, JM_F64)) continue;
+      char name[96];
+      snprintf(name, sizeof name, "jm_aotspec_double_n%d_%s", n, ad == JM_ADDEND_ONES ? "ones" : "identity");
+      CUfunction fn = nullptr;
+      CU_TRY(D.ModuleGetFunction(&fn, G.aot, name), name);
+      Slot &s = g_slots[JM_KIND_AOT_SPECIALIZED][ad][JM_F64][n];
+      s.plan = jm::plan_specialized(n, JM_F64);
+      s.mod = nullptr;
+      s.cubin_bytes = (long long)jm_embedded_aot_cubin_len;
+      int rc = finish_function(s, fn);
+      if (rc != JM_OK) return rc;
+      s.state.store(S_READY, std::memory_order_release);
+    }
+  return JM_OK;
 }
 
 }  // namespace
@@ -543,6 +649,7 @@ int jit_mat_init(int device) {
   CU_TRY(D.ModuleGetFunction(&G.checksum[1], G.aot, "jm_checksum_f64"), "jm_checksum_f64");
   CU_TRY(D.MemAlloc(&G.sum_buf, 16), "cuMemAlloc(checksum)");
   seed_generic_slots();
+  if ((rc = seed_aot_spec_slots()) != JM_OK) return rc;
   G.inited.store(true, std::memory_order_release);
   return JM_OK;
 }
@@ -582,6 +689,17 @@ int jit_mat_shutdown(void) {
     }
     G.hbuf_bytes = 0;
   }
+  {
+    std::lock_guard<std::mutex> pl(g_pool_mu);
+    for (int p = 0; p < POOL; ++p) {
+      if (g_pool[p]) D.StreamDestroy(g_pool[p]);
+      if (g_join[p]) D.EventDestroy(g_join[p]);
+      g_pool[p] = nullptr;
+      g_join[p] = nullptr;
+    }
+    if (g_fork) D.EventDestroy(g_fork);
+    g_fork = nullptr;
+  }
   if (G.sum_buf) D.MemFree(G.sum_buf);
   G.sum_buf = 0;
   if (G.aot) D.ModuleUnload(G.aot);
@@ -599,6 +717,10 @@ int jit_mat_run(int n, int dtype, int64_t batch, int64_t repeat, const void *in,
 }
 
 int jit_mat_run_ex(const jm_run_desc *d) { return run_impl(d); }
+
+int jit_mat_run_many(const jm_run_desc *descs, int count, void *stream, unsigned flags) {
+  return run_many_impl(descs, count, stream, flags);
+}
 
 int jit_mat_run_host(int n, int dtype, int64_t batch, int64_t repeat, const void *in, void *out) {
   jm_run_desc d{n, dtype, JM_ADDEND_ONES, JM_KIND_SPECIALIZED, batch, repeat, in, out, nullptr,

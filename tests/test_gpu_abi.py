@@ -164,3 +164,27 @@ def test_set_stream_is_honoured(jm):
     jm.run(xd, 10, ref, sync=True)
     assert torch.equal(out, ref)
     jm.jit_mat_set_stream(torch.cuda.current_stream().cuda_stream)
+
+
+def test_aot_specializations_preseeded_and_identical(jm):
+    """F3's three-way comparison: JIT (NVRTC) vs AoT specialization (nvcc) vs generic.
+
+    The AoT specializations are the same template body compiled ahead of time, so
+    their outputs must equal the NVRTC ones bit for bit; they never compile
+    (explicit specializations are used instead of JIT-compiling).
+    """
+    _fresh(jm)
+    for n in (3, 7, 16):
+        jm.jit_mat_prepare(n, "double", kind="aot_specialized")
+    assert jm.jit_mat_stats()["compilations"] == 0
+    for n in (3, 7, 16):
+        for addend in ("ones", "identity"):
+            x = torch.from_numpy(jm_synth.generate(n, "f64", "hard", 9, 0, 999)).cuda()
+            a = jm.run(x, 5, addend=addend, kind="aot_specialized", sync=True)
+            b = jm.run(x, 5, addend=addend, kind="specialized", sync=True)
+            assert torch.equal(a, b), (n, addend)
+    with pytest.raises(jm.JitMatError) as e:
+        jm.jit_mat_prepare(8, "double", kind="aot_specialized")
+    assert e.value.code == jm.JM_E_UNSUPPORTED
+    with pytest.raises(jm.JitMatError):
+        jm.jit_mat_prepare(16, "float", kind="aot_specialized")

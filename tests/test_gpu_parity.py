@@ -190,3 +190,36 @@ def test_specialized_and_generic_agree_closely(jm):
     a = _gpu_run(jm, x, 50, kind="specialized")
     b = _gpu_run(jm, x, 50, kind="generic")
     assert max_rel_err(a, b) <= TOL[np.dtype(np.float64)]
+
+
+def test_run_many_mixed_sizes_matches_single_runs(jm):
+    """Mixed-N batch (configs[3]) through jit_mat_run_many == per-group runs, bitwise."""
+    rng = np.random.default_rng(5)
+    groups, bufs = [], []
+    for n in [2, 3, 5, 8, 13, 16, 24, 31, 33, 64]:
+        for dt in ("f64", "f32"):
+            b = int(rng.integers(1, 300))
+            x = torch.from_numpy(jm_synth.generate(n, dt, "hard", 3 + n, 0, b)).cuda()
+            y = torch.empty_like(x)
+            groups.append(dict(n=n, dtype=dt, batch=b, repeat=3, in_ptr=x.data_ptr(),
+                               out_ptr=y.data_ptr(), kind="specialized" if n % 2 else "generic"))
+            bufs.append((x, y))
+    groups.append(dict(n=7, dtype="f64", batch=0, repeat=3, in_ptr=0, out_ptr=0))
+    jm.jit_mat_run_many(groups, stream=torch.cuda.current_stream().cuda_stream, sync=True)
+    for (x, y), g in zip(bufs, groups):
+        ref = torch.empty_like(x)
+        jm.run(x, 3, ref, kind=g["kind"], sync=True)
+        assert torch.equal(y, ref), g
+        if g["n"] <= 16:
+            assert_parity(y.cpu().numpy(), oracle.run(x.cpu().numpy(), 3), what=str(g))
+
+
+def test_run_many_rejects_bad_descriptor_before_launch(jm):
+    x = torch.zeros(4, 4, 4, dtype=torch.float64, device="cuda")
+    y = torch.full_like(x, 7.0)
+    bad = [dict(n=4, dtype="f64", batch=4, repeat=1, in_ptr=x.data_ptr(), out_ptr=y.data_ptr()),
+           dict(n=99, dtype="f64", batch=4, repeat=1, in_ptr=x.data_ptr(), out_ptr=y.data_ptr())]
+    with pytest.raises(jm.JitMatError):
+        jm.jit_mat_run_many(bad, sync=True)
+    torch.cuda.synchronize()
+    assert torch.all(y == 7.0)
