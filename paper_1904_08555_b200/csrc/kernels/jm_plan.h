@@ -77,6 +77,27 @@ JM_HD constexpr int f32_ldm(int n) { return f32_cg(n) * f32_cb(n) + 4; }  // sM 
 JM_HD constexpr int f32_ldt(int n) { return f32_rg(n) * f32_ra(n) + 4; }  // sMT row stride (floats)
 JM_HD constexpr int f32_buf(int n) { return n * (f32_ldm(n) + f32_ldt(n)) * 4; }  // one M + M^T buffer
 
+// ---- F32 row panels (9 <= n <= 32) ----
+// A thread owns RP = 4 FULL rows of M (the A operand is local); row k of M
+// (the B operand) is a shared-memory broadcast.  G threads per matrix,
+// 32 / G matrices per warp, P computed in `f32p_halves` column halves so the
+// accumulators fit next to the 4 full rows.
+constexpr int F32P_RP = 4;
+constexpr int F32P_WPC = 2;                       // warps per CTA
+constexpr int F32P_KSTEP = 4;                     // k steps between scheduling fences
+// (n > 16 needs more than 4 x 16 resident floats next to the accumulators: spills)
+JM_HD constexpr bool f32p_use(int n) { return n >= 9 && n <= 16; }
+JM_HD constexpr int f32p_g(int n) { return n <= 16 ? 4 : 8; }                 // threads per matrix
+JM_HD constexpr int f32p_mpw(int n) { return 32 / f32p_g(n); }                // matrices per warp
+JM_HD constexpr int f32p_ncr(int n) { return cdiv(n, 4); }                    // real 16-B chunks per row
+JM_HD constexpr int f32p_ncs(int n) { return f32p_ncr(n) <= 4 ? 4 : 8; }      // stored chunks (pow2: XOR swizzle)
+// column groups of (at most) two 16-B chunks: 8 accumulator columns live at a time
+JM_HD constexpr int f32p_halves(int n) { return n <= 16 ? 1 : cdiv(f32p_ncr(n), 2); }
+// one matrix buffer, +32 B skew: a matrix's PAIR of buffers is then an odd
+// multiple of 64 B, so the two matrices sharing a quarter-warp land in
+// opposite halves of the 128-B bank window
+JM_HD constexpr int f32p_mbuf(int n) { return n * f32p_ncs(n) * 16 + 32; }
+
 JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   const int es = dtype == 1 ? 8 : 4;
   const Tile t = tile_for(n, dtype);
@@ -90,12 +111,21 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
                   stage_bytes(DMMA_WPC, n, es) + DMMA_WPC * dmma_scr(n), 1};
     return Plan{(int)t, 32 * w, 1, stage_bytes(1, n, es) + 2 * dmma_scr(n), w};
   }
+  if (f32p_use(n)) {
+    const int mpc = F32P_WPC * f32p_mpw(n);
+    return Plan{(int)t, 32 * F32P_WPC, mpc, stage_bytes(mpc, n, es) + 2 * mpc * f32p_mbuf(n), 1};
+  }
   const int w = f32_w(n);
   if (w == 1)
     return Plan{(int)t, 32 * F32_WPC, F32_WPC,
                 stage_bytes(F32_WPC, n, es) + F32_WPC * f32_buf(n), 1};
   return Plan{(int)t, 32 * w, 1, stage_bytes(1, n, es) + 2 * f32_buf(n), w};
 }
+
+// __launch_bounds__ minimum resident CTAs per SM.  Registers are granted per
+// SMSP (16384 each): a cap only bites in steps of warps-per-SMSP (2 -> 255,
+// 3 -> 168), and 168 makes the FP32 row panels spill, so no kernel asks for one.
+JM_HD constexpr int launch_min_blocks(int, int) { return 1; }
 
 // ---- AoT specializations (nvcc-compiled at build time; Fig. 3's sizes) ----
 JM_HD constexpr bool aot_spec_available(int n, int dtype) {

@@ -357,6 +357,161 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
 }
 
 // ======================================================================
+// F32P: FP32 row panels (9 <= N <= 32).  Each of the G threads of a matrix
+// owns RP = 4 FULL rows of M in registers, so the A operand of P = M + M*M
+// (M[i][k] for its rows) is local; the B operand (row k of M) is a
+// shared-memory broadcast: the G threads of a matrix read the same 16-B
+// chunks.  Per update a thread issues 4*N/2 FFMA2 per k against N/4 LDS.128.
+// Rows live in a double-buffered shared copy (one __syncwarp per update):
+// update r reads buffer r&1 and writes its new rows into buffer (r&1)^1.
+// 16-B chunk q of row r is stored at chunk q ^ ((r >> 2) & (NCS-1)), so the
+// 4 (or 8) threads of a matrix publishing row r0+i hit distinct bank groups.
+// For N > 16 the accumulators are formed in two column halves (the 4 full
+// rows of the A operand stay in registers for both).
+// ======================================================================
+template <int NCS>
+__device__ __forceinline__ int f32p_off(int row, int q) {
+  return (row * NCS + (q ^ ((row >> 2) & (NCS - 1)))) * 16;
+}
+
+template <int N, Addend A>
+__device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__restrict__ out,
+                                         long long batch, int repeat) {
+  constexpr int RP = F32P_RP, G = f32p_g(N), MPW = f32p_mpw(N), NCR = f32p_ncr(N);
+  constexpr int NCS = f32p_ncs(N), HALVES = f32p_halves(N), MBUF = f32p_mbuf(N);
+  constexpr int NC = 4 * NCR;                          // computed columns (16-B padded)
+  constexpr int QH = cdiv(NCR, HALVES);                     // chunks per column group
+  constexpr int ES = 4, MB = N * N * 4, SB = stage_stride(N, 4);
+  constexpr int NT = 32 * F32P_WPC, MPC = F32P_WPC * MPW;
+  constexpr bool AL = ((MPC * MB) % 16) == 0;
+  static_assert(G * RP >= N, "row panels must cover the matrix");
+  extern __shared__ __align__(16) char smem[];
+  char *stage = smem;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int mw = lane / G, tg = lane - mw * G;
+  const int mi = warp * MPW + mw;                      // matrix slot in the chunk
+  const int r0 = tg * RP;
+  char *bufs = smem + stage_bytes(MPC, N, 4) + mi * 2 * MBUF;
+  const float c = float(0.00005);
+  const long long nchunks = (batch + MPC - 1) / MPC;
+
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long b0 = ch * MPC;
+    const int cnt = (int)((batch - b0) < MPC ? (batch - b0) : MPC);
+    stage_in<N, ES, SB, NT, AL>(reinterpret_cast<const char *>(in) + b0 * MB, stage, cnt, tid);
+    __syncthreads();
+    // every lane runs the loop (a warp holds several matrices and syncs as one);
+    // slots past the batch end compute on zeros and are never written back
+    const bool live = mi < cnt;
+    float *sm = reinterpret_cast<float *>(stage + mi * SB);
+    float m[RP][NC];
+#pragma unroll
+    for (int i = 0; i < RP; ++i)
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const int row = r0 + i;
+        m[i][j] = (live && row < N && j < N) ? sm[row * N + j] : 0.0f;
+      }
+#pragma unroll
+    for (int i = 0; i < RP; ++i)
+      if (r0 + i < N) {
+#pragma unroll
+        for (int q = 0; q < NCR; ++q)
+          *reinterpret_cast<float4 *>(bufs + f32p_off<NCS>(r0 + i, q)) =
+              make_float4(m[i][4 * q], m[i][4 * q + 1], m[i][4 * q + 2], m[i][4 * q + 3]);
+      }
+    __syncwarp();
+#pragma unroll 1
+    for (int r = 0; r < repeat; ++r) {
+      const char *cur = bufs + (r & 1) * MBUF;
+      char *nxt = bufs + ((r & 1) ^ 1) * MBUF;
+#pragma unroll
+      for (int h = 0; h < HALVES; ++h) {
+        constexpr int QMAX = QH;
+        const int qlo = h * QH;
+        const int qn = (NCR - qlo) < QH ? (NCR - qlo) : QH;
+        float2 p[RP][2 * QMAX];
+#pragma unroll
+        for (int i = 0; i < RP; ++i)
+#pragma unroll
+          for (int jp = 0; jp < 2 * QMAX; ++jp)
+            if (jp < 2 * qn) p[i][jp] = make_float2(m[i][4 * qlo + 2 * jp], m[i][4 * qlo + 2 * jp + 1]);
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          // keep ptxas from hoisting every row-k load of the group at once
+          // (register pressure next to the 4 resident rows)
+          if (k % F32P_KSTEP == 0) asm volatile("" ::: "memory");
+          float b[4 * QMAX];
+#pragma unroll
+          for (int q = 0; q < QMAX; ++q)
+            if (q < qn) {
+              const float4 v = *reinterpret_cast<const float4 *>(cur + f32p_off<NCS>(k, qlo + q));
+              b[4 * q] = v.x; b[4 * q + 1] = v.y; b[4 * q + 2] = v.z; b[4 * q + 3] = v.w;
+            }
+#pragma unroll
+          for (int i = 0; i < RP; ++i)
+#pragma unroll
+            for (int jp = 0; jp < 2 * QMAX; ++jp)
+              if (jp < 2 * qn)
+                p[i][jp] = __ffma2_rn(make_float2(m[i][k], m[i][k]),
+                                      make_float2(b[2 * jp], b[2 * jp + 1]), p[i][jp]);
+        }
+        // M' = A + c * P (padding stays zero) -> next buffer
+#pragma unroll
+        for (int i = 0; i < RP; ++i) {
+          const int row = r0 + i;
+#pragma unroll
+          for (int q = 0; q < QMAX; ++q)
+            if (q < qn) {
+              // the diagonal element of row r0+i sits in chunk tg, lane e == i
+              const bool dchunk = (qlo + q) == tg;
+              float v[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int col = 4 * (qlo + q) + e;
+                const float pv = (e & 1) ? p[i][2 * q + e / 2].y : p[i][2 * q + e / 2].x;
+                const float a = (A == Addend::Ones || (e == i && dchunk)) ? 1.0f : 0.0f;
+                v[e] = ((G * RP == N || row < N) && col < N) ? fmaT(c, pv, a) : 0.0f;
+              }
+              if (row < N)
+                *reinterpret_cast<float4 *>(nxt + f32p_off<NCS>(row, qlo + q)) =
+                    make_float4(v[0], v[1], v[2], v[3]);
+              if constexpr (HALVES == 1) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) m[i][4 * (qlo + q) + e] = v[e];
+              }
+            }
+        }
+      }
+      if constexpr (HALVES > 1) {   // own rows back from the next buffer (written by this thread)
+#pragma unroll
+        for (int i = 0; i < RP; ++i)
+          if (r0 + i < N) {
+#pragma unroll
+            for (int q = 0; q < NCR; ++q) {
+              const float4 v = *reinterpret_cast<const float4 *>(nxt + f32p_off<NCS>(r0 + i, q));
+              m[i][4 * q] = v.x; m[i][4 * q + 1] = v.y; m[i][4 * q + 2] = v.z; m[i][4 * q + 3] = v.w;
+            }
+          }
+      }
+      __syncwarp();
+    }
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < RP; ++i)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const int row = r0 + i;
+          if (row < N && j < N) sm[row * N + j] = m[i][j];
+        }
+    }
+    __syncthreads();
+    stage_out<N, ES, SB, NT, AL>(reinterpret_cast<char *>(out) + b0 * MB, stage, cnt, tid);
+    __syncthreads();
+  }
+}
+
+// ======================================================================
 // F32: FP32 register-tiled outer products.  The RG x CG threads of a matrix
 // each own an RA x CB block of M (registers).  Every update republishes M and
 // M^T to shared memory; then for k < N each thread reads RA values of column k
@@ -505,13 +660,16 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
     run_tpm<N, T, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Dmma) {
     run_dmma<N, A, dmma_w(N)>(in, out, batch, repeat);
+  } else if constexpr (f32p_use(N)) {
+    run_f32p<N, A>(in, out, batch, repeat);
   } else {
     run_f32<N, A, f32_w(N)>(in, out, batch, repeat);
   }
 }
 
 template <int N, class T, Addend A, Tile K>
-__global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).threads)
+__global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).threads,
+                                  launch_min_blocks(N, sizeof(T) == 8 ? 1 : 0))
     k_update(const T *__restrict__ in, T *__restrict__ out, long long batch, int repeat) {
   update_body<N, T, A, K>(in, out, batch, repeat);
 }
