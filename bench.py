@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--n", type=int, default=16)
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--batch", type=int, default=1 << 20, help="matrices per GPU")
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="strong scaling (configs[4], C5): fixed total batch split across ranks")
     ap.add_argument("--repeat", type=int, default=100)
     ap.add_argument("--addend", default="ones", choices=["ones", "identity"])
     ap.add_argument("--kind", default="specialized", choices=["specialized", "generic"])
@@ -241,10 +243,15 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     jm.jit_mat_set_stream(stream.cuda_stream)
 
-    n, dt, B, R = a.n, a.dtype, a.batch, a.repeat
+    n, dt, R = a.n, a.dtype, a.repeat
     tdt = torch.float64 if dt == "f64" else torch.float32
     es = 8 if dt == "f64" else 4
-    gfirst, _ = shard.weak_slice(rank, B)
+    if a.global_batch is not None:     # strong scaling: every N shares one fixed global batch
+        gfirst, B = shard.strong_slice(rank, world, a.global_batch)
+        a.batch = B
+    else:                              # weak scaling: B matrices per GPU
+        B = a.batch
+        gfirst, _ = shard.weak_slice(rank, B)
     x = torch.empty(B, n, n, dtype=tdt, device=dev)
     y = torch.empty_like(x)
 
@@ -338,8 +345,10 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": max(3, a.warmup), "ms_per_step": ms_max, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
-        "config": {"workload": workload_name(a), "n": n, "batch_per_gpu": B, "global_batch": B * world,
+        "scaling": "strong" if a.global_batch is not None else "weak",
+        "vs_baseline": None, "dtype": dt, "data": "synthetic",
+        "config": {"workload": workload_name(a), "n": n, "batch_per_gpu": B,
+                   "global_batch": a.global_batch if a.global_batch is not None else B * world,
                    "repeat": R, "addend": a.addend, "kind": a.kind,
                    "dist": "bench: U[-1,1) counter-hash, seed 0x0019040855",
                    "l2": f"inputs {alg_bytes / 2 / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)",
@@ -362,7 +371,7 @@ def main():
         g_ms_step = g_ms / gsteps
         g_max = (max(r[0] for r in shard.gather_record(dist, [g_ms_step], [], dev)[0])
                  if world > 1 else g_ms_step)
-        gval = B * world * R / (g_max / 1e3)
+        gval = total_units / (g_max / 1e3)
         line["generic"] = {"value": gval, "unit": UNIT, "ms_per_step": g_max,
                            "gflops": gval * fpu / 1e9,
                            "specialized_speedup": value / gval}
@@ -371,7 +380,7 @@ def main():
             a_ms, _ = timed("aot_specialized", gsteps, 1)
             a_max = (max(r[0] for r in shard.gather_record(dist, [a_ms / gsteps], [], dev)[0])
                      if world > 1 else a_ms / gsteps)
-            aval = B * world * R / (a_max / 1e3)
+            aval = total_units / (a_max / 1e3)
             line["aot_specialized"] = {"value": aval, "unit": UNIT, "ms_per_step": a_max,
                                        "time_relative_to_jit": a_max / ms_max}
 
@@ -389,7 +398,7 @@ def main():
         el = time.perf_counter() - t0
         e_max = (max(r[0] for r in shard.gather_record(dist, [el / e2e_steps], [], dev)[0])
                  if world > 1 else el / e2e_steps)
-        line["e2e"] = {"value": B * world * R / e_max, "unit": UNIT,
+        line["e2e"] = {"value": total_units / e_max, "unit": UNIT,
                        "h2d_bytes_per_step": B * n * n * es, "d2h_bytes_per_step": B * n * n * es,
                        "ms_per_step": e_max * 1e3, "steps": e2e_steps,
                        "api": "jit_mat_run_host (pinned host in/out, chunked H2D/compute/D2H overlap)"}

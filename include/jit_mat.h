@@ -151,6 +151,18 @@ JM_API int jit_mat_run_host(int n, int dtype, int64_t batch, int64_t repeat, con
  * anything is compiled or launched. */
 JM_API int jit_mat_run_many(const jm_run_desc *descs, int count, void *stream, unsigned flags);
 
+/* Share specializations between processes (the paper's
+ * compile-time concern).  jit_mat_cache_export writes a
+ * self-describing blob (key + kernel symbol + sm_100a cubin) of a READY
+ * specialized key into `buf` (`cap` bytes); `*len` receives the blob size
+ * (pass buf = NULL to query).  JM_E_INVALID if the key has not been compiled.
+ * jit_mat_cache_import installs such a blob (from the same library build) for
+ * its key without running NVRTC: one rank compiles, broadcasts the blob, the
+ * other ranks import it.  Importing into a READY slot is a no-op (JM_OK); a blob
+ * for another key or a corrupt blob is JM_E_INVALID. */
+JM_API int jit_mat_cache_export(int n, int dtype, int addend, void *buf, size_t cap, size_t *len);
+JM_API int jit_mat_cache_import(const void *blob, size_t len);
+
 /* Stream used by jit_mat_run (e.g. torch.cuda.current_stream().cuda_stream). */
 JM_API int jit_mat_set_stream(void *cuda_stream);
 
@@ -174,6 +186,7 @@ typedef struct {
   double compile_ms_total;   /* wall time inside NVRTC + module load */
   int32_t keys_ready;        /* cache slots in READY state */
   int32_t keys_failed;       /* cache slots in FAILED state */
+  int64_t imports;           /* keys installed by jit_mat_cache_import (no NVRTC) */
 } jm_stats;
 
 typedef struct {

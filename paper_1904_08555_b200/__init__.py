@@ -26,7 +26,7 @@ from ._lib import (  # noqa: F401  (re-exported C ABI)
 
 __all__ = [
     "jit_mat_init", "jit_mat_run", "jit_mat_shutdown", "jit_mat_run_ex", "jit_mat_run_host",
-    "jit_mat_run_many",
+    "jit_mat_run_many", "jit_mat_cache_export", "jit_mat_cache_import",
     "jit_mat_set_stream", "jit_mat_prepare", "jit_mat_dtype_from_name", "jit_mat_last_error",
     "jit_mat_stats", "jit_mat_key_info", "jit_mat_reset_stats", "jit_mat_fill",
     "jit_mat_checksum", "jit_mat_device_info", "jit_mat_version", "jit_mat_compile_check",
@@ -95,6 +95,23 @@ def jit_mat_run_many(groups, stream: int | None = None, sync: bool = False) -> N
                              ctypes.c_void_p(g["out_ptr"]), None, 0)
     _check(lib.jit_mat_run_many(arr, len(groups), ctypes.c_void_p(stream or 0),
                                 JM_FLAG_SYNC if sync else 0), "jit_mat_run_many")
+
+
+def jit_mat_cache_export(n: int, dtype, addend="ones") -> bytes:
+    """Blob (key + symbol + sm_100a cubin) of a compiled specialization."""
+    ln = ctypes.c_size_t(0)
+    a = _ADDENDS.get(addend, addend)
+    _check(lib.jit_mat_cache_export(int(n), _dt(dtype), a, None, 0, ctypes.byref(ln)),
+           "jit_mat_cache_export")
+    buf = ctypes.create_string_buffer(ln.value)
+    _check(lib.jit_mat_cache_export(int(n), _dt(dtype), a, buf, ln.value, ctypes.byref(ln)),
+           "jit_mat_cache_export")
+    return buf.raw[:ln.value]
+
+
+def jit_mat_cache_import(blob: bytes) -> None:
+    """Install a blob from jit_mat_cache_export without running NVRTC."""
+    _check(lib.jit_mat_cache_import(blob, len(blob)), "jit_mat_cache_import")
 
 
 def jit_mat_set_stream(stream: int | None) -> None:

@@ -40,7 +40,7 @@ class jm_stats(ctypes.Structure):
     _fields_ = [("compilations", ctypes.c_int64), ("hits", ctypes.c_int64),
                 ("misses", ctypes.c_int64), ("launches", ctypes.c_int64),
                 ("compile_ms_total", ctypes.c_double), ("keys_ready", ctypes.c_int32),
-                ("keys_failed", ctypes.c_int32)]
+                ("keys_failed", ctypes.c_int32), ("imports", ctypes.c_int64)]
 
 
 class jm_key_info(ctypes.Structure):
@@ -59,6 +59,8 @@ _SIGS = {
     "jit_mat_run_ex": (_I, [ctypes.POINTER(jm_run_desc)]),
     "jit_mat_run_host": (_I, [_I, _I, _I64, _I64, _P, _P]),
     "jit_mat_run_many": (_I, [ctypes.POINTER(jm_run_desc), _I, _P, ctypes.c_uint]),
+    "jit_mat_cache_export": (_I, [_I, _I, _I, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    "jit_mat_cache_import": (_I, [_P, ctypes.c_size_t]),
     "jit_mat_set_stream": (_I, [_P]),
     "jit_mat_prepare": (_I, [_I, _I, _I, _I]),
     "jit_mat_dtype_from_name": (_I, [ctypes.c_char_p]),

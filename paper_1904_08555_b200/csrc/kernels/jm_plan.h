@@ -82,13 +82,14 @@ JM_HD constexpr int f32_buf(int n) { return n * (f32_ldm(n) + f32_ldt(n)) * 4; }
 // (the B operand) is a shared-memory broadcast.  G threads per matrix,
 // 32 / G matrices per warp, P computed in `f32p_halves` column halves so the
 // accumulators fit next to the 4 full rows.
-constexpr int F32P_RP = 4;
+constexpr int F32P_RP_MAX = 4;
 constexpr int F32P_WPC = 2;                       // warps per CTA
 constexpr int F32P_KSTEP = 4;                     // k steps between scheduling fences
 // (n > 16 needs more than 4 x 16 resident floats next to the accumulators: spills)
 JM_HD constexpr bool f32p_use(int n) { return n >= 9 && n <= 16; }
 JM_HD constexpr int f32p_g(int n) { return n <= 16 ? 4 : 8; }                 // threads per matrix
 JM_HD constexpr int f32p_mpw(int n) { return 32 / f32p_g(n); }                // matrices per warp
+JM_HD constexpr int f32p_rp(int n) { return cdiv(n, f32p_g(n)); }             // rows per thread (<= 4)
 JM_HD constexpr int f32p_ncr(int n) { return cdiv(n, 4); }                    // real 16-B chunks per row
 JM_HD constexpr int f32p_ncs(int n) { return f32p_ncr(n) <= 4 ? 4 : 8; }      // stored chunks (pow2: XOR swizzle)
 // column groups of (at most) two 16-B chunks: 8 accumulator columns live at a time
@@ -98,9 +99,17 @@ JM_HD constexpr int f32p_halves(int n) { return n <= 16 ? 1 : cdiv(f32p_ncr(n), 
 // opposite halves of the 128-B bank window
 JM_HD constexpr int f32p_mbuf(int n) { return n * f32p_ncs(n) * 16 + 32; }
 
+// Double-buffered (cp.async prefetch) staging.  Measured on B200 (r01 sweep):
+// it lifts DMMA n=16 at repeat 1 from 0.87 to 0.94 of HBM, but the doubled
+// stage area costs residency and the compute-bound repeat-100 configurations
+// lose 1-25 % (FP32 row panels most), so every kind currently runs the
+// single-buffered stage; the Stager keeps both paths.
+JM_HD constexpr bool prefetch_for(int, int) { return false; }
+
 JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   const int es = dtype == 1 ? 8 : 4;
   const Tile t = tile_for(n, dtype);
+  const int nst = prefetch_for(n, dtype) ? 2 : 1;   // stage buffers
   if (t == Tile::TPM) {
     return Plan{(int)t, TPM_THREADS, TPM_THREADS, stage_bytes(TPM_THREADS, n, es), 1};
   }
@@ -108,24 +117,31 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
     const int w = dmma_w(n);
     if (w == 1)
       return Plan{(int)t, 32 * DMMA_WPC, DMMA_WPC,
-                  stage_bytes(DMMA_WPC, n, es) + DMMA_WPC * dmma_scr(n), 1};
-    return Plan{(int)t, 32 * w, 1, stage_bytes(1, n, es) + 2 * dmma_scr(n), w};
+                  nst * stage_bytes(DMMA_WPC, n, es) + DMMA_WPC * dmma_scr(n), 1};
+    return Plan{(int)t, 32 * w, 1, nst * stage_bytes(1, n, es) + 2 * dmma_scr(n), w};
   }
   if (f32p_use(n)) {
     const int mpc = F32P_WPC * f32p_mpw(n);
-    return Plan{(int)t, 32 * F32P_WPC, mpc, stage_bytes(mpc, n, es) + 2 * mpc * f32p_mbuf(n), 1};
+    return Plan{(int)t, 32 * F32P_WPC, mpc, nst * stage_bytes(mpc, n, es) + 2 * mpc * f32p_mbuf(n), 1};
   }
   const int w = f32_w(n);
   if (w == 1)
     return Plan{(int)t, 32 * F32_WPC, F32_WPC,
-                stage_bytes(F32_WPC, n, es) + F32_WPC * f32_buf(n), 1};
-  return Plan{(int)t, 32 * w, 1, stage_bytes(1, n, es) + 2 * f32_buf(n), w};
+                nst * stage_bytes(F32_WPC, n, es) + F32_WPC * f32_buf(n), 1};
+  return Plan{(int)t, 32 * w, 1, nst * stage_bytes(1, n, es) + 2 * f32_buf(n), w};
 }
 
-// __launch_bounds__ minimum resident CTAs per SM.  Registers are granted per
-// SMSP (16384 each): a cap only bites in steps of warps-per-SMSP (2 -> 255,
-// 3 -> 168), and 168 makes the FP32 row panels spill, so no kernel asks for one.
-JM_HD constexpr int launch_min_blocks(int, int) { return 1; }
+// Which entry point the specialization uses: k_update (maxThreads only) or
+// k_update_mb1 (maxThreads, minBlocks = 1) — the CTA-per-matrix DMMA kinds.
+JM_HD constexpr bool use_mb1(int n, int dtype) {
+  return tile_for(n, dtype) == Tile::Dmma && dmma_w(n) > 1;
+}
+
+// Note: k_update passes only maxThreads to __launch_bounds__.  Registers are
+// granted per SMSP (16384 each), so a minBlocks cap only bites in steps of
+// warps-per-SMSP (2 -> 255, 3 -> 168 regs); 168 makes the FP32 row panels
+// spill, and an explicit minBlocks = 1 changes ptxas' heuristics (r01: TPM
+// f32 n=2 went 32 -> 45 registers and lost 18 % of HBM throughput).
 
 // ---- AoT specializations (nvcc-compiled at build time; Fig. 3's sizes) ----
 JM_HD constexpr bool aot_spec_available(int n, int dtype) {

@@ -111,6 +111,97 @@ __device__ __forceinline__ void stage_out(char *__restrict__ g, const char *s, i
   }
 }
 
+// Asynchronous variant of stage_in (cp.async / LDGSTS: global -> shared with no
+// register round trip), same layouts; the caller commits and waits.
+__device__ __forceinline__ void cp_async16(void *s, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(s)),
+               "l"(g) : "memory");
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void *s, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"((unsigned)__cvta_generic_to_shared(s)),
+               "l"(g), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int N, int ES, int SB, int NT, bool ALIGNED>
+__device__ __forceinline__ void stage_in_async(const char *__restrict__ g, char *s, int cnt, int tid) {
+  constexpr int MB = N * N * ES;
+  if constexpr (ALIGNED && (MB % 16) == 0) {
+    constexpr int PPM = MB / 16;
+    const int pieces = cnt * PPM;
+    for (int p = tid; p < pieces; p += NT) {
+      const int m = p / PPM, q = p - m * PPM;
+      cp_async16(s + m * SB + q * 16, g + (size_t)p * 16);
+    }
+  } else if constexpr (ALIGNED && SB == MB) {
+    const int bytes = cnt * MB, pieces = bytes >> 4;
+    for (int p = tid; p < pieces; p += NT) cp_async16(s + p * 16, g + (size_t)p * 16);
+    for (int o = pieces * 16 + tid * ES; o < bytes; o += NT * ES) cp_async_small<ES>(s + o, g + o);
+  } else {
+    const int elems = cnt * N * N;
+    for (int e = tid; e < elems; e += NT) {
+      const int m = e / (N * N), q = e - m * (N * N);
+      cp_async_small<ES>(s + m * SB + q * ES, g + (size_t)e * ES);
+    }
+  }
+}
+
+// Chunk scheduler shared by the kernels: a persistent CTA walks chunks of MPC
+// matrices (chunk = blockIdx.x, += gridDim.x).  With PF (prefetch) the stage
+// area is double-buffered: while chunk i is computed, chunk i+gridDim.x is
+// already streaming into the other buffer through cp.async, so the HBM latency
+// of the next load hides behind this chunk's updates (matters at small repeat).
+//   for (sg.start(); sg.valid(); sg.next()) { sg.acquire(); ...use sg.buf()...; sg.release(); }
+template <int N, int ES, int SB, int NT, int MPC, bool AL, bool PF>
+struct Stager {
+  static constexpr int MB = N * N * ES;
+  static constexpr int SZ = stage_bytes(MPC, N, ES);
+  const char *in;
+  char *out;
+  char *base;
+  long long batch, nchunks, ch;
+  int it, tid;
+  __device__ __forceinline__ Stager(const void *in_, void *out_, long long batch_, char *base_)
+      : in(reinterpret_cast<const char *>(in_)), out(reinterpret_cast<char *>(out_)), base(base_),
+        batch(batch_), nchunks((batch_ + MPC - 1) / MPC), ch(blockIdx.x), it(0), tid(threadIdx.x) {}
+  __device__ __forceinline__ int count(long long c) const {
+    const long long r = batch - c * MPC;
+    return (int)(r < MPC ? r : MPC);
+  }
+  __device__ __forceinline__ void issue(long long c, char *dst) {
+    stage_in_async<N, ES, SB, NT, AL>(in + c * MPC * MB, dst, count(c), tid);
+    cp_async_commit();
+  }
+  __device__ __forceinline__ void start() {
+    if (PF && ch < nchunks) issue(ch, base);
+  }
+  __device__ __forceinline__ bool valid() const { return ch < nchunks; }
+  __device__ __forceinline__ char *buf() const { return base + (PF ? (it & 1) * SZ : 0); }
+  __device__ __forceinline__ int cnt() const { return count(ch); }
+  __device__ __forceinline__ void acquire() {
+    if constexpr (PF) {
+      cp_async_wait_all();
+      __syncthreads();   // chunk `ch` visible to all; every thread is done with chunk it-1
+      const long long nx = ch + gridDim.x;
+      if (nx < nchunks) issue(nx, base + ((it + 1) & 1) * SZ);
+    } else {
+      stage_in<N, ES, SB, NT, AL>(in + ch * MPC * MB, buf(), cnt(), tid);
+      __syncthreads();
+    }
+  }
+  __device__ __forceinline__ void release() {
+    __syncthreads();
+    stage_out<N, ES, SB, NT, AL>(out + ch * MPC * MB, buf(), cnt(), tid);
+    if constexpr (!PF) __syncthreads();
+  }
+  __device__ __forceinline__ void next() {
+    ch += gridDim.x;
+    ++it;
+  }
+};
+
 // ======================================================================
 // TPM: thread per matrix.  The whole matrix (and the product) lives in
 // registers for all `repeat` updates; fully unrolled for the compile-time N
@@ -269,21 +360,20 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   constexpr int MPC = (W == 1) ? DMMA_WPC : 1;
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   static_assert(RT * W == T8, "row tiles must cover the matrix");
+  constexpr bool PF = prefetch_for(N, 1);
   extern __shared__ __align__(16) char smem[];
-  char *stage = smem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int mi = (W == 1) ? warp : 0;        // matrix slot in the chunk
   const int wr = (W == 1) ? 0 : warp;        // this warp's rank within the matrix
-  char *scr = smem + stage_bytes(MPC, N, 8) + ((W == 1) ? warp * SCR : 0);
+  char *scr = smem + (PF ? 2 : 1) * stage_bytes(MPC, N, 8) + ((W == 1) ? warp * SCR : 0);
   const double c = 0.00005;
-  const long long nchunks = (batch + MPC - 1) / MPC;
 
-  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const long long b0 = ch * MPC;
-    const int cnt = (int)((batch - b0) < MPC ? (batch - b0) : MPC);
-    stage_in<N, ES, SB, NT, AL>(reinterpret_cast<const char *>(in) + b0 * MB, stage, cnt, tid);
-    __syncthreads();
+  Stager<N, ES, SB, NT, MPC, AL, PF> sg(in, out, batch, smem);
+  for (sg.start(); sg.valid(); sg.next()) {
+    sg.acquire();
+    char *stage = sg.buf();
+    const int cnt = sg.cnt();
     if (mi < cnt) {
       double *sm = reinterpret_cast<double *>(stage + mi * SB);
       double acc[RT][T8][2];
@@ -350,9 +440,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
             if (row < N && col < N) sm[row * N + col] = acc[I][J][s];
           }
     }
-    __syncthreads();
-    stage_out<N, ES, SB, NT, AL>(reinterpret_cast<char *>(out) + b0 * MB, stage, cnt, tid);
-    __syncthreads();
+    sg.release();
   }
 }
 
@@ -377,7 +465,8 @@ __device__ __forceinline__ int f32p_off(int row, int q) {
 template <int N, Addend A>
 __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__restrict__ out,
                                          long long batch, int repeat) {
-  constexpr int RP = F32P_RP, G = f32p_g(N), MPW = f32p_mpw(N), NCR = f32p_ncr(N);
+  constexpr int RP = f32p_rp(N), G = f32p_g(N), MPW = f32p_mpw(N), NCR = f32p_ncr(N);
+  static_assert(RP <= F32P_RP_MAX, "at most 4 resident rows per thread");
   constexpr int NCS = f32p_ncs(N), HALVES = f32p_halves(N), MBUF = f32p_mbuf(N);
   constexpr int NC = 4 * NCR;                          // computed columns (16-B padded)
   constexpr int QH = cdiv(NCR, HALVES);                     // chunks per column group
@@ -385,21 +474,20 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
   constexpr int NT = 32 * F32P_WPC, MPC = F32P_WPC * MPW;
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   static_assert(G * RP >= N, "row panels must cover the matrix");
+  constexpr bool PF = prefetch_for(N, 0);
   extern __shared__ __align__(16) char smem[];
-  char *stage = smem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int mw = lane / G, tg = lane - mw * G;
   const int mi = warp * MPW + mw;                      // matrix slot in the chunk
   const int r0 = tg * RP;
-  char *bufs = smem + stage_bytes(MPC, N, 4) + mi * 2 * MBUF;
+  char *bufs = smem + (PF ? 2 : 1) * stage_bytes(MPC, N, 4) + mi * 2 * MBUF;
   const float c = float(0.00005);
-  const long long nchunks = (batch + MPC - 1) / MPC;
 
-  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const long long b0 = ch * MPC;
-    const int cnt = (int)((batch - b0) < MPC ? (batch - b0) : MPC);
-    stage_in<N, ES, SB, NT, AL>(reinterpret_cast<const char *>(in) + b0 * MB, stage, cnt, tid);
-    __syncthreads();
+  Stager<N, ES, SB, NT, MPC, AL, PF> sg(in, out, batch, smem);
+  for (sg.start(); sg.valid(); sg.next()) {
+    sg.acquire();
+    char *stage = sg.buf();
+    const int cnt = sg.cnt();
     // every lane runs the loop (a warp holds several matrices and syncs as one);
     // slots past the batch end compute on zeros and are never written back
     const bool live = mi < cnt;
@@ -470,7 +558,8 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
               for (int e = 0; e < 4; ++e) {
                 const int col = 4 * (qlo + q) + e;
                 const float pv = (e & 1) ? p[i][2 * q + e / 2].y : p[i][2 * q + e / 2].x;
-                const float a = (A == Addend::Ones || (e == i && dchunk)) ? 1.0f : 0.0f;
+                const bool diag = (RP == 4) ? (e == i && dchunk) : (col == row);
+                const float a = (A == Addend::Ones || diag) ? 1.0f : 0.0f;
                 v[e] = ((G * RP == N || row < N) && col < N) ? fmaT(c, pv, a) : 0.0f;
               }
               if (row < N)
@@ -505,9 +594,7 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
           if (row < N && j < N) sm[row * N + j] = m[i][j];
         }
     }
-    __syncthreads();
-    stage_out<N, ES, SB, NT, AL>(reinterpret_cast<char *>(out) + b0 * MB, stage, cnt, tid);
-    __syncthreads();
+    sg.release();
   }
 }
 
@@ -530,21 +617,20 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   static_assert(RG * CG == 32 * W, "thread grid must match the warps per matrix");
   static_assert(CB % 2 == 0, "FFMA2 needs column pairs");
+  constexpr bool PF = prefetch_for(N, 0);
   extern __shared__ __align__(16) char smem[];
-  char *stage = smem;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int mi = (W == 1) ? warp : 0;
   const int tr = (W == 1) ? (tid & 31) : tid;   // rank within the matrix
   const int r0 = (tr / CG) * RA, c0 = (tr % CG) * CB;
-  char *bufs = smem + stage_bytes(MPC, N, 4) + ((W == 1) ? warp * BUF : 0);
+  char *bufs = smem + (PF ? 2 : 1) * stage_bytes(MPC, N, 4) + ((W == 1) ? warp * BUF : 0);
   const float c = float(0.00005);
-  const long long nchunks = (batch + MPC - 1) / MPC;
 
-  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const long long b0 = ch * MPC;
-    const int cnt = (int)((batch - b0) < MPC ? (batch - b0) : MPC);
-    stage_in<N, ES, SB, NT, AL>(reinterpret_cast<const char *>(in) + b0 * MB, stage, cnt, tid);
-    __syncthreads();
+  Stager<N, ES, SB, NT, MPC, AL, PF> sg(in, out, batch, smem);
+  for (sg.start(); sg.valid(); sg.next()) {
+    sg.acquire();
+    char *stage = sg.buf();
+    const int cnt = sg.cnt();
     if (mi < cnt) {
       float *sm = reinterpret_cast<float *>(stage + mi * SB);
       float m[RA][CB];
@@ -642,9 +728,7 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
           if (row < N && col < N) sm[row * N + col] = m[i][j];
         }
     }
-    __syncthreads();
-    stage_out<N, ES, SB, NT, AL>(reinterpret_cast<char *>(out) + b0 * MB, stage, cnt, tid);
-    __syncthreads();
+    sg.release();
   }
 }
 
@@ -668,9 +752,17 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
 }
 
 template <int N, class T, Addend A, Tile K>
-__global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).threads,
-                                  launch_min_blocks(N, sizeof(T) == 8 ? 1 : 0))
+__global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).threads)
     k_update(const T *__restrict__ in, T *__restrict__ out, long long batch, int repeat) {
+  update_body<N, T, A, K>(in, out, batch, repeat);
+}
+
+// Same body, with minBlocksPerSM = 1 stated: for the CTA-per-matrix DMMA kinds
+// this lets ptxas keep ~180 registers (r01: n=64 spilled 8 B at 168 without it,
+// and n=32 ran 0.83 vs 0.91 of the FP64 pipe).  kernel_name_for() selects it.
+template <int N, class T, Addend A, Tile K>
+__global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).threads, 1)
+    k_update_mb1(const T *__restrict__ in, T *__restrict__ out, long long batch, int repeat) {
   update_body<N, T, A, K>(in, out, batch, repeat);
 }
 

@@ -178,6 +178,8 @@ struct Slot {
   long long cubin_bytes = 0;
   double compile_ms = 0.0;
   std::string err;
+  std::vector<char> cubin;    // NVRTC output kept for jit_mat_cache_export
+  std::string lowered;        // mangled kernel symbol
 };
 
 constexpr int NKIND = 3, NADD = 2, NDT = 2, NMAX = JM_N_MAX;
@@ -205,7 +207,7 @@ struct State {
 };
 State G;
 
-std::atomic<long long> c_compilations{0}, c_hits{0}, c_misses{0}, c_launches{0};
+std::atomic<long long> c_compilations{0}, c_hits{0}, c_misses{0}, c_launches{0}, c_imports{0};
 std::atomic<long long> c_compile_us{0};
 
 bool env_flag(const char *name) {
@@ -231,7 +233,8 @@ const char *tile_name(int t) {
 
 std::string name_expression(int n, int dtype, int addend) {
   char buf[160];
-  snprintf(buf, sizeof buf, "jm::k_update<%d, %s, jm::Addend::%s, jm::Tile::%s>", n,
+  snprintf(buf, sizeof buf, "jm::%s<%d, %s, jm::Addend::%s, jm::Tile::%s>",
+           jm::use_mb1(n, dtype) ? "k_update_mb1" : "k_update", n,
            dtype == JM_F64 ? "double" : "float", addend == JM_ADDEND_ONES ? "Ones" : "Identity",
            tile_name((int)jm::tile_for(n, dtype)));
   return buf;
@@ -292,17 +295,10 @@ int finish_function(Slot &s, CUfunction fn) {
   return JM_OK;
 }
 
-int compile_slot(Slot &s, int n, int dtype, int addend) {
-  const auto t0 = std::chrono::steady_clock::now();
-  c_compilations++;
-  std::vector<char> cubin;
-  std::string lowered, log;
-  int rc = nvrtc_compile(n, dtype, addend, cubin, lowered, log);
-  if (rc != JM_OK) {
-    s.err = log;
-    return fail(rc, "%s", log.c_str());
-  }
-  if ((rc = ensure_ctx()) != JM_OK) return rc;
+// Load a specialized cubin into a slot (after NVRTC, or from an imported blob).
+int install_cubin(Slot &s, int n, int dtype, std::vector<char> &&cubin, const std::string &lowered) {
+  int rc = ensure_ctx();
+  if (rc != JM_OK) return rc;
   CUmodule mod = nullptr;
   CUresult cr = D.ModuleLoadData(&mod, cubin.data());
   if (cr != CUDA_SUCCESS) {
@@ -328,6 +324,22 @@ int compile_slot(Slot &s, int n, int dtype, int addend) {
     s.err = t_err;
     return rc;
   }
+  s.cubin = std::move(cubin);
+  s.lowered = lowered;
+  return JM_OK;
+}
+
+int compile_slot(Slot &s, int n, int dtype, int addend) {
+  const auto t0 = std::chrono::steady_clock::now();
+  c_compilations++;
+  std::vector<char> cubin;
+  std::string lowered, log;
+  int rc = nvrtc_compile(n, dtype, addend, cubin, lowered, log);
+  if (rc != JM_OK) {
+    s.err = log;
+    return fail(rc, "%s", log.c_str());
+  }
+  if ((rc = install_cubin(s, n, dtype, std::move(cubin), lowered)) != JM_OK) return rc;
   const double ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   s.compile_ms = ms;
@@ -671,6 +683,9 @@ int jit_mat_shutdown(void) {
           s.err.clear();
           s.regs = s.local_bytes = 0;
           s.cubin_bytes = 0;
+          s.cubin.clear();
+          s.cubin.shrink_to_fit();
+          s.lowered.clear();
           s.compile_ms = 0;
           s.state.store(S_EMPTY, std::memory_order_release);
         }
@@ -728,6 +743,60 @@ int jit_mat_run_host(int n, int dtype, int64_t batch, int64_t repeat, const void
   return run_impl(&d);
 }
 
+int jit_mat_cache_export(int n, int dtype, int addend, void *buf, size_t cap, size_t *len) {
+  int rc = check_key(n, dtype, addend, JM_KIND_SPECIALIZED);
+  if (rc != JM_OK) return rc;
+  if (!len) return fail(JM_E_INVALID, "NULL len");
+  Slot &s = g_slots[JM_KIND_SPECIALIZED][addend][dtype][n];
+  if (s.state.load(std::memory_order_acquire) != S_READY || s.cubin.empty())
+    return fail(JM_E_INVALID, "key n=%d dtype=%d addend=%d is not compiled in this process", n, dtype, addend);
+  std::lock_guard<std::mutex> lk(s.mu);
+  const uint32_t nl = (uint32_t)s.lowered.size();
+  const uint64_t cl = (uint64_t)s.cubin.size();
+  const size_t total = 4 + 3 * 4 + 4 + nl + 8 + cl;
+  *len = total;
+  if (!buf) return JM_OK;
+  if (cap < total) return fail(JM_E_INVALID, "buffer too small (%zu < %zu)", cap, total);
+  char *p = (char *)buf;
+  const int32_t key[3] = {n, dtype, addend};
+  memcpy(p, "JMC1", 4); p += 4;
+  memcpy(p, key, sizeof key); p += sizeof key;
+  memcpy(p, &nl, 4); p += 4;
+  memcpy(p, s.lowered.data(), nl); p += nl;
+  memcpy(p, &cl, 8); p += 8;
+  memcpy(p, s.cubin.data(), cl);
+  return JM_OK;
+}
+
+int jit_mat_cache_import(const void *blob, size_t len) {
+  if (!blob || len < 4 + 12 + 4 + 8) return fail(JM_E_INVALID, "blob too short");
+  if (!G.inited.load(std::memory_order_acquire)) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
+  const char *p = (const char *)blob, *end = p + len;
+  if (memcmp(p, "JMC1", 4) != 0) return fail(JM_E_INVALID, "not a jitmat cubin blob");
+  p += 4;
+  int32_t key[3];
+  memcpy(key, p, sizeof key); p += sizeof key;
+  int rc = check_key(key[0], key[1], key[2], JM_KIND_SPECIALIZED);
+  if (rc != JM_OK) return rc;
+  uint32_t nl;
+  memcpy(&nl, p, 4); p += 4;
+  if ((size_t)(end - p) < (size_t)nl + 8) return fail(JM_E_INVALID, "truncated blob");
+  std::string lowered(p, nl); p += nl;
+  uint64_t cl;
+  memcpy(&cl, p, 8); p += 8;
+  if ((uint64_t)(end - p) != cl || cl == 0) return fail(JM_E_INVALID, "truncated blob");
+  if (lowered.find("k_update") == std::string::npos) return fail(JM_E_INVALID, "unexpected kernel symbol");
+  Slot &s = g_slots[JM_KIND_SPECIALIZED][key[2]][key[1]][key[0]];
+  std::lock_guard<std::mutex> lk(s.mu);
+  if (s.state.load(std::memory_order_acquire) == S_READY) return JM_OK;
+  std::vector<char> cubin(p, p + cl);
+  if ((rc = install_cubin(s, key[0], key[1], std::move(cubin), lowered)) != JM_OK) return rc;
+  s.compile_ms = 0.0;
+  c_imports++;
+  s.state.store(S_READY, std::memory_order_release);
+  return JM_OK;
+}
+
 int jit_mat_set_stream(void *cuda_stream) {
   G.stream.store(cuda_stream, std::memory_order_relaxed);
   return JM_OK;
@@ -753,6 +822,7 @@ int jit_mat_stats(jm_stats *out) {
   out->hits = c_hits.load();
   out->misses = c_misses.load();
   out->launches = c_launches.load();
+  out->imports = c_imports.load();
   out->compile_ms_total = c_compile_us.load() / 1000.0;
   int ready = 0, failed = 0;
   for (int a = 0; a < NADD; ++a)
@@ -794,7 +864,7 @@ int jit_mat_key_info(jm_key_info *keys, int cap) {
 }
 
 int jit_mat_reset_stats(void) {
-  c_compilations = 0; c_hits = 0; c_misses = 0; c_launches = 0; c_compile_us = 0;
+  c_compilations = 0; c_hits = 0; c_misses = 0; c_launches = 0; c_compile_us = 0; c_imports = 0;
   return JM_OK;
 }
 

@@ -188,3 +188,23 @@ def test_aot_specializations_preseeded_and_identical(jm):
     assert e.value.code == jm.JM_E_UNSUPPORTED
     with pytest.raises(jm.JitMatError):
         jm.jit_mat_prepare(16, "float", kind="aot_specialized")
+
+
+def test_cache_export_import_skips_nvrtc(jm):
+    """f2: one process compiles, another installs the blob (NVRTC not run)."""
+    _fresh(jm)
+    x = torch.from_numpy(jm_synth.generate(13, "f64", "hard", 2, 0, 77)).cuda()
+    ref = jm.run(x, 3, sync=True)
+    blob = jm.jit_mat_cache_export(13, "double")
+    assert blob[:4] == b"JMC1" and len(blob) > 1000
+    _fresh(jm)
+    jm.jit_mat_cache_import(blob)
+    jm.jit_mat_cache_import(blob)          # second import: no-op
+    got = jm.run(x, 3, sync=True)
+    st = jm.jit_mat_stats()
+    assert st["compilations"] == 0 and st["imports"] == 1
+    assert torch.equal(got, ref)
+    with pytest.raises(jm.JitMatError):
+        jm.jit_mat_cache_import(b"JMC1" + blob[4:40])
+    with pytest.raises(jm.JitMatError):
+        jm.jit_mat_cache_export(14, "double")
