@@ -54,8 +54,38 @@ def _load():
             lib.jm_oracle_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int64, ctypes.c_int64,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+            lib.jm_oracle_matmul.restype = ctypes.c_int
+            lib.jm_oracle_matmul.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_int]
             _lib = lib
     return _lib
+
+
+def matmul_acc(c: np.ndarray, a: np.ndarray, b: np.ndarray, threads: int | None = None) -> np.ndarray:
+    """Return c + a @ b per batch entry (Listing 8, batch reading R16).
+
+    Computed in the arrays' dtype by jm_oracle.c (ascending k, separate
+    multiply and add); the inputs are not modified.
+    """
+    lib = _load()
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    out = np.array(c, copy=True, order="C")
+    if not (a.shape == b.shape == out.shape and a.dtype == b.dtype == out.dtype):
+        raise ValueError("a, b, c must share shape (batch, n, n) and dtype")
+    if a.ndim != 3 or a.shape[1] != a.shape[2]:
+        raise ValueError("expected (batch, n, n)")
+    dt = {np.dtype(np.float32): 0, np.dtype(np.float64): 1}.get(a.dtype)
+    if dt is None:
+        raise ValueError("oracle supports float32/float64")
+    th = default_threads() if threads is None else int(threads)
+    rc = lib.jm_oracle_matmul(a.shape[1], dt, a.shape[0], a.ctypes.data_as(ctypes.c_void_p),
+                              b.ctypes.data_as(ctypes.c_void_p),
+                              out.ctypes.data_as(ctypes.c_void_p), th)
+    if rc != 0:
+        raise ValueError(f"jm_oracle_matmul rejected arguments (rc={rc})")
+    return out
 
 
 def default_threads() -> int:

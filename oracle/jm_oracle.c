@@ -119,6 +119,73 @@ static void *run_range(void *arg) {
 }
 
 /*
+ * Batched small matrix multiply-accumulate — the RAJA benchmark of PAPER.md
+ * §5.1, Listing 8 (lines 562-600):
+ *     out_matrix[MAT2D(i,j,size)] += input_matrix1[MAT2D(i,k,size)] *
+ *                                    input_matrix2[MAT2D(k,j,size)]
+ * over the loop nest (matrices, i, j, k), innermost k ascending, one multiply
+ * and one add per iteration (separate roundings).  Reading R16:
+ * the listing's lambda ignores the `matrices` index, so as printed every batch
+ * entry accumulates into ONE output; the batch form c[b] += a[b] * b[b] (each
+ * entry its own three matrices) is the evident intent and is what this
+ * computes.  Row-major MAT2D(r,c,size) = r*size + c, as in the listing.
+ */
+static void *mm_range(void *arg) {
+    job_t *j = (job_t *)arg;
+    const int n = j->n;
+    const size_t nn = (size_t)n * (size_t)n;
+    const void *const *ab = (const void *const *)j->in;   /* {a, b} */
+    for (int64_t bi = j->b0; bi < j->b1; ++bi) {
+        if (j->dtype == ORACLE_F64) {
+            const double *a = (const double *)ab[0] + (size_t)bi * nn;
+            const double *b = (const double *)ab[1] + (size_t)bi * nn;
+            double *c = (double *)j->out + (size_t)bi * nn;
+            for (int i = 0; i < n; ++i)
+                for (int jj = 0; jj < n; ++jj)
+                    for (int k = 0; k < n; ++k) {
+                        double prod = a[i * n + k] * b[k * n + jj];
+                        c[i * n + jj] = c[i * n + jj] + prod;
+                    }
+        } else {
+            const float *a = (const float *)ab[0] + (size_t)bi * nn;
+            const float *b = (const float *)ab[1] + (size_t)bi * nn;
+            float *c = (float *)j->out + (size_t)bi * nn;
+            for (int i = 0; i < n; ++i)
+                for (int jj = 0; jj < n; ++jj)
+                    for (int k = 0; k < n; ++k) {
+                        float prod = a[i * n + k] * b[k * n + jj];
+                        c[i * n + jj] = c[i * n + jj] + prod;
+                    }
+        }
+    }
+    return NULL;
+}
+
+/* c[b] += a[b] * b[b] for b in [0, batch) (host buffers, c updated in place). */
+int jm_oracle_matmul(int n, int dtype, int64_t batch, const void *a, const void *b, void *c,
+                     int threads) {
+    if (n < 1 || batch < 0) return -1;
+    if (dtype != ORACLE_F32 && dtype != ORACLE_F64) return -1;
+    if (batch == 0) return 0;
+    if (threads < 1) threads = 1;
+    if ((int64_t)threads > batch) threads = (int)batch;
+    const void *ab[2] = {a, b};
+    job_t *jobs = (job_t *)calloc((size_t)threads, sizeof(job_t));
+    pthread_t *tids = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    for (int t = 0; t < threads; ++t) {
+        jobs[t].n = n; jobs[t].dtype = dtype; jobs[t].addend = 0;
+        jobs[t].b0 = batch * t / threads;
+        jobs[t].b1 = batch * (t + 1) / threads;
+        jobs[t].repeat = 0; jobs[t].in = ab; jobs[t].out = c;
+    }
+    for (int t = 1; t < threads; ++t) pthread_create(&tids[t], NULL, mm_range, &jobs[t]);
+    mm_range(&jobs[0]);
+    for (int t = 1; t < threads; ++t) pthread_join(tids[t], NULL);
+    free(jobs); free(tids);
+    return 0;
+}
+
+/*
  * out[b] = f^repeat(in[b]) for b in [0, batch).  `in` and `out` are host
  * buffers of batch*n*n elements of the named type; they may be the same
  * buffer.  threads <= 0 means 1.  Returns 0, or -1 on bad arguments.
