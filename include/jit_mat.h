@@ -163,6 +163,20 @@ JM_API int jit_mat_run_many(const jm_run_desc *descs, int count, void *stream, u
 JM_API int jit_mat_cache_export(int n, int dtype, int addend, void *buf, size_t cap, size_t *len);
 JM_API int jit_mat_cache_import(const void *blob, size_t len);
 
+/* Batched small matrix multiply-accumulate, the RAJA benchmark of PAPER.md
+ * §5.1 (Listing 8):
+ *     c[b] += a[b] * b[b]        for b in [0, batch)
+ * each a n x n row-major matrix of `dtype` (Listing 8's MAT2D(r,c,size) =
+ * r*size + c), contiguous per batch.  kind JM_KIND_SPECIALIZED instantiates
+ * jm::k_matmul<n, T> through NVRTC on first use (cached like jit_mat_run);
+ * JM_KIND_GENERIC is the runtime-n kernel.  Device pointers, 16-byte aligned; c
+ * must not overlap a or b (a and b may alias each other).  Asynchronous on
+ * `stream` (NULL = the set stream).  As printed, Listing 8's lambda ignores the
+ * batch index and accumulates every entry into one output; the batched form is
+ * the evident intent (reading R16). */
+JM_API int jit_mat_matmul(int n, int dtype, int kind, int64_t batch, const void *a, const void *b,
+                          void *c, void *stream);
+
 /* Stream used by jit_mat_run (e.g. torch.cuda.current_stream().cuda_stream). */
 JM_API int jit_mat_set_stream(void *cuda_stream);
 
@@ -199,11 +213,13 @@ typedef struct {
   int32_t tile;              /* tiling kind (JM_TILE_*) chosen by the planner */
   int64_t cubin_bytes;
   double compile_ms;
+  int32_t op;                /* 0 = update (jit_mat_run), 1 = multiply-accumulate (jit_mat_matmul) */
+  int32_t reserved;
 } jm_key_info;
 
 /* tiling kinds reported in jm_key_info.tile */
 enum { JM_TILE_GENERIC = 0, JM_TILE_TPM = 1, JM_TILE_WARP_DMMA = 2, JM_TILE_CTA_DMMA = 3,
-       JM_TILE_WARP_F32 = 4, JM_TILE_CTA_F32 = 5, JM_TILE_ROWS = 6 };
+       JM_TILE_WARP_F32 = 4, JM_TILE_CTA_F32 = 5, JM_TILE_ROWS = 6, JM_TILE_MATMUL = 7 };
 
 JM_API int jit_mat_stats(jm_stats *out);
 /* Copy up to `cap` non-empty slots into `keys`; returns the number of
@@ -237,8 +253,16 @@ JM_API const char *jit_mat_version(void);
 
 /* NVRTC-compile the specialized kernel for a key to an sm_100a cubin WITHOUT a
  * device or jit_mat_init (nothing is loaded or cached).  Lets a CPU-only test
- * tier prove that every specialization compiles.  cubin_bytes may be NULL. */
+ * tier prove that every specialization compiles.  addend = JM_OP_MATMUL selects
+ * the multiply-accumulate template instead.  cubin_bytes may be NULL. */
+#define JM_OP_MATMUL 2
 JM_API int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes);
+
+/* Cache-hit cost of the key lookup (the paper calls the
+ * lookup overhead "noticeable", and dominant for small work,
+ * PAPER.md:560): `iters` lookups of a READY key (compiled first if needed),
+ * average nanoseconds per lookup written to *ns. */
+JM_API int jit_mat_time_lookup(int n, int dtype, int addend, int kind, int64_t iters, double *ns);
 
 #ifdef __cplusplus
 }

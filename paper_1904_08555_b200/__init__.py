@@ -19,14 +19,15 @@ import os
 from ._lib import (  # noqa: F401  (re-exported C ABI)
     JM_ADDEND_IDENTITY, JM_ADDEND_ONES, JM_E_ALIGN, JM_E_ARCH, JM_E_COMPILE, JM_E_CUDA,
     JM_E_INVALID, JM_E_NOT_INITIALIZED, JM_E_UNSUPPORTED, JM_F32, JM_F64, JM_FLAG_HOST_BUFFERS,
-    JM_FLAG_SYNC, JM_KIND_AOT_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK,
+    JM_FLAG_SYNC, JM_KIND_AOT_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK, JM_OP_MATMUL,
     JM_TILE_NAMES, JitMatError,
     jm_key_info, jm_run_desc, jm_stats, lib, lib_path,
 )
 
 __all__ = [
     "jit_mat_init", "jit_mat_run", "jit_mat_shutdown", "jit_mat_run_ex", "jit_mat_run_host",
-    "jit_mat_run_many", "jit_mat_cache_export", "jit_mat_cache_import",
+    "jit_mat_run_many", "jit_mat_cache_export", "jit_mat_cache_import", "jit_mat_matmul",
+    "jit_mat_time_lookup", "matmul",
     "jit_mat_set_stream", "jit_mat_prepare", "jit_mat_dtype_from_name", "jit_mat_last_error",
     "jit_mat_stats", "jit_mat_key_info", "jit_mat_reset_stats", "jit_mat_fill",
     "jit_mat_checksum", "jit_mat_device_info", "jit_mat_version", "jit_mat_compile_check",
@@ -114,6 +115,38 @@ def jit_mat_cache_import(blob: bytes) -> None:
     _check(lib.jit_mat_cache_import(blob, len(blob)), "jit_mat_cache_import")
 
 
+def jit_mat_matmul(n: int, dtype, batch: int, a_ptr: int, b_ptr: int, c_ptr: int, *,
+                   kind="specialized", stream: int | None = None) -> None:
+    """c[b] += a[b] @ b[b] (Listing 8; C: jit_mat_matmul)."""
+    _check(lib.jit_mat_matmul(int(n), _dt(dtype), _KINDS.get(kind, kind), int(batch),
+                              ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), ctypes.c_void_p(c_ptr),
+                              ctypes.c_void_p(stream or 0)), "jit_mat_matmul")
+
+
+def jit_mat_time_lookup(n: int, dtype, addend="ones", kind="specialized", iters: int = 1_000_000) -> float:
+    """Average ns per cache-hit lookup, timed inside the library (row a1)."""
+    ns = ctypes.c_double(0.0)
+    _check(lib.jit_mat_time_lookup(int(n), _dt(dtype), _ADDENDS.get(addend, addend),
+                                   _KINDS.get(kind, kind), int(iters), ctypes.byref(ns)),
+           "jit_mat_time_lookup")
+    return float(ns.value)
+
+
+def matmul(a, b, c, *, kind: str = "specialized", stream=None, sync: bool = False):
+    """c += a @ b for CUDA tensors of shape (batch, n, n); returns c."""
+    import torch
+
+    for t in (a, b, c):
+        if t.dim() != 3 or t.shape != a.shape or t.dtype != a.dtype or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("a, b, c must be contiguous CUDA tensors of one (batch, n, n) shape and dtype")
+    st = stream if stream is not None else torch.cuda.current_stream(a.device)
+    jit_mat_matmul(a.shape[1], str(a.dtype), a.shape[0], a.data_ptr(), b.data_ptr(), c.data_ptr(),
+                   kind=kind, stream=st.cuda_stream)
+    if sync:
+        st.synchronize()
+    return c
+
+
 def jit_mat_set_stream(stream: int | None) -> None:
     _check(lib.jit_mat_set_stream(ctypes.c_void_p(stream or 0)), "jit_mat_set_stream")
 
@@ -181,9 +214,10 @@ def jit_mat_version() -> str:
 
 
 def jit_mat_compile_check(n: int, dtype, addend="ones") -> int:
+    """NVRTC-compile a key without a GPU; addend="matmul" selects k_matmul."""
     cb = ctypes.c_longlong(0)
-    _check(lib.jit_mat_compile_check(int(n), _dt(dtype), _ADDENDS.get(addend, addend),
-                                     ctypes.byref(cb)), "jit_mat_compile_check")
+    a = JM_OP_MATMUL if addend == "matmul" else _ADDENDS.get(addend, addend)
+    _check(lib.jit_mat_compile_check(int(n), _dt(dtype), a, ctypes.byref(cb)), "jit_mat_compile_check")
     return int(cb.value)
 
 

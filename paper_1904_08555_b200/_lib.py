@@ -20,7 +20,8 @@ JM_E_INVALID, JM_E_UNSUPPORTED, JM_E_NOT_INITIALIZED = -1, -2, -3
 JM_E_ARCH, JM_E_COMPILE, JM_E_CUDA, JM_E_ALIGN = -4, -5, -6, -7
 JM_FLAG_SYNC, JM_FLAG_HOST_BUFFERS = 1, 2
 JM_TILE_NAMES = {0: "generic", 1: "tpm", 2: "warp_dmma", 3: "cta_dmma", 4: "warp_f32",
-                 5: "cta_f32", 6: "rows"}
+                 5: "cta_f32", 6: "rows", 7: "matmul"}
+JM_OP_MATMUL = 2
 
 
 class JitMatError(RuntimeError):
@@ -48,7 +49,8 @@ class jm_key_info(ctypes.Structure):
                 ("kind", ctypes.c_int32), ("state", ctypes.c_int32), ("regs", ctypes.c_int32),
                 ("local_bytes", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("tile", ctypes.c_int32),
-                ("cubin_bytes", ctypes.c_int64), ("compile_ms", ctypes.c_double)]
+                ("cubin_bytes", ctypes.c_int64), ("compile_ms", ctypes.c_double),
+                ("op", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 _I, _I64, _P, _U64 = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_uint64
@@ -74,6 +76,8 @@ _SIGS = {
     "jit_mat_device_info": (_I, [ctypes.POINTER(_I)] * 3),
     "jit_mat_version": (ctypes.c_char_p, []),
     "jit_mat_compile_check": (_I, [_I, _I, _I, ctypes.POINTER(ctypes.c_longlong)]),
+    "jit_mat_matmul": (_I, [_I, _I, _I, _I64, _P, _P, _P, _P]),
+    "jit_mat_time_lookup": (_I, [_I, _I, _I, _I, _I64, ctypes.POINTER(ctypes.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)

@@ -11,6 +11,7 @@
 //   * fill / checksum — driver plumbing.
 #include "jm_plan.h"
 #include "jm_update.cuh"
+#include "jm_matmul.cuh"
 
 namespace jm {
 
@@ -48,6 +49,38 @@ __device__ __forceinline__ void generic_update(const T *__restrict__ in, T *__re
       __syncthreads();
     }
     for (int e = tid; e < total; e += NT) out[b0 * nn + e] = M[e];
+    __syncthreads();
+  }
+}
+
+// Generic (runtime-N) batched multiply-accumulate: the un-specialized
+// comparison for matmul_body (same staging, runtime loop bounds).
+template <class T>
+__device__ __forceinline__ void matmul_generic(const T *__restrict__ a, const T *__restrict__ b,
+                                               T *__restrict__ c, long long batch, int n) {
+  constexpr int NT = MM_THREADS;
+  const int nn = n * n, mpc = mm_mpc(n);
+  extern __shared__ __align__(16) char smem[];
+  T *A = reinterpret_cast<T *>(smem);
+  T *B = reinterpret_cast<T *>(smem + stage_bytes(mpc, n, (int)sizeof(T)));
+  const int tid = threadIdx.x;
+  const long long nchunks = (batch + mpc - 1) / mpc;
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long b0 = ch * mpc;
+    const int cnt = (int)((batch - b0) < mpc ? (batch - b0) : mpc);
+    const int total = cnt * nn;
+    for (int e = tid; e < total; e += NT) {
+      A[e] = a[b0 * nn + e];
+      B[e] = b[b0 * nn + e];
+    }
+    __syncthreads();
+    T *C = c + b0 * nn;
+    for (int e = tid; e < total; e += NT) {
+      const int mi = e / nn, q = e - mi * nn, i = q / n, j = q - i * n;
+      T acc = C[e];
+      for (int k = 0; k < n; ++k) acc = fmaT(A[mi * nn + i * n + k], B[mi * nn + k * n + j], acc);
+      C[e] = acc;
+    }
     __syncthreads();
   }
 }
@@ -139,6 +172,17 @@ JM_AOT_SPEC(16, double, 1, jm::Addend::Ones, ones)
 JM_AOT_SPEC(3, double, 1, jm::Addend::Identity, identity)
 JM_AOT_SPEC(7, double, 1, jm::Addend::Identity, identity)
 JM_AOT_SPEC(16, double, 1, jm::Addend::Identity, identity)
+
+extern "C" __global__ void __launch_bounds__(jm::MM_THREADS)
+    jm_mm_generic_f32(const float *__restrict__ a, const float *__restrict__ b, float *__restrict__ c,
+                      long long batch, int n) {
+  jm::matmul_generic<float>(a, b, c, batch, n);
+}
+extern "C" __global__ void __launch_bounds__(jm::MM_THREADS)
+    jm_mm_generic_f64(const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ c,
+                      long long batch, int n) {
+  jm::matmul_generic<double>(a, b, c, batch, n);
+}
 
 extern "C" __global__ void jm_fill_f32(float *out, int n, int dist, unsigned long long seed,
                                        long long gfirst, long long total) {

@@ -148,6 +148,14 @@ JM_HD constexpr bool aot_spec_available(int n, int dtype) {
   return dtype == 1 && (n == 3 || n == 7 || n == 16);
 }
 
+// ---- batched multiply-accumulate (Listing 8) ----
+constexpr int MM_THREADS = 256;
+JM_HD constexpr int mm_mpc(int n) { return (n * n >= MM_THREADS) ? 1 : MM_THREADS / (n * n); }
+JM_HD constexpr Plan plan_matmul(int n, int dtype) {
+  // A and B chunks staged packed; C is streamed by the owning threads
+  return Plan{(int)Tile::Generic, MM_THREADS, mm_mpc(n), 2 * stage_bytes(mm_mpc(n), n, dtype == 1 ? 8 : 4), 1};
+}
+
 // ---- GENERIC (runtime N; AoT) ----
 constexpr int GENERIC_THREADS = 256;
 JM_HD constexpr int generic_mpc(int n) { return (n * n >= GENERIC_THREADS) ? 1 : GENERIC_THREADS / (n * n); }

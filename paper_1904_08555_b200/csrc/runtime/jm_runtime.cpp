@@ -184,6 +184,7 @@ struct Slot {
 
 constexpr int NKIND = 3, NADD = 2, NDT = 2, NMAX = JM_N_MAX;
 Slot g_slots[NKIND][NADD][NDT][NMAX + 1];
+Slot g_mm_slots[2][NDT][NMAX + 1];     // multiply-accumulate: [specialized|generic][dtype][n]
 
 struct State {
   std::mutex mu;
@@ -240,9 +241,16 @@ std::string name_expression(int n, int dtype, int addend) {
   return buf;
 }
 
-// NVRTC: instantiate the template for (n, dtype, addend) -> sm_100a cubin.
-int nvrtc_compile(int n, int dtype, int addend, std::vector<char> &cubin, std::string &lowered,
-                  std::string &log) {
+std::string mm_name_expression(int n, int dtype) {
+  char buf[96];
+  snprintf(buf, sizeof buf, "jm::k_matmul<%d, %s>", n, dtype == JM_F64 ? "double" : "float");
+  return buf;
+}
+
+// NVRTC: instantiate one name expression of the embedded template source ->
+// sm_100a cubin (+ the lowered, i.e. mangled, symbol).
+int nvrtc_compile_expr(const std::string &expr, std::vector<char> &cubin, std::string &lowered,
+                       std::string &log) {
   const std::string src((const char *)jm_embedded_kernel_src, (size_t)jm_embedded_kernel_src_len);
   nvrtcProgram prog;
   nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "jm_update.cu", 0, nullptr, nullptr);
@@ -250,7 +258,6 @@ int nvrtc_compile(int n, int dtype, int addend, std::vector<char> &cubin, std::s
     log = nvrtcGetErrorString(r);
     return JM_E_COMPILE;
   }
-  const std::string expr = name_expression(n, dtype, addend);
   nvrtcAddNameExpression(prog, expr.c_str());
   const char *opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=true", "-lineinfo",
                         "--ftz=false", "--prec-div=true", "--prec-sqrt=true"};
@@ -295,8 +302,16 @@ int finish_function(Slot &s, CUfunction fn) {
   return JM_OK;
 }
 
+// ops: the Eigen-benchmark update (k_update) and the batched multiply-accumulate
+// of the RAJA benchmark (k_matmul, Listing 8)
+enum { OP_UPDATE = 0, OP_MATMUL = 1 };
+
+jm::Plan plan_for(int op, int n, int dtype) {
+  return op == OP_MATMUL ? jm::plan_matmul(n, dtype) : jm::plan_specialized(n, dtype);
+}
+
 // Load a specialized cubin into a slot (after NVRTC, or from an imported blob).
-int install_cubin(Slot &s, int n, int dtype, std::vector<char> &&cubin, const std::string &lowered) {
+int install_cubin(Slot &s, int op, int n, int dtype, std::vector<char> &&cubin, const std::string &lowered) {
   int rc = ensure_ctx();
   if (rc != JM_OK) return rc;
   CUmodule mod = nullptr;
@@ -314,7 +329,7 @@ int install_cubin(Slot &s, int n, int dtype, std::vector<char> &&cubin, const st
     s.err = t_err;
     return JM_E_COMPILE;
   }
-  s.plan = jm::plan_specialized(n, dtype);
+  s.plan = plan_for(op, n, dtype);
   s.mod = mod;
   s.cubin_bytes = (long long)cubin.size();
   rc = finish_function(s, fn);
@@ -329,24 +344,25 @@ int install_cubin(Slot &s, int n, int dtype, std::vector<char> &&cubin, const st
   return JM_OK;
 }
 
-int compile_slot(Slot &s, int n, int dtype, int addend) {
+int compile_slot(Slot &s, int op, int n, int dtype, int addend) {
   const auto t0 = std::chrono::steady_clock::now();
   c_compilations++;
   std::vector<char> cubin;
   std::string lowered, log;
-  int rc = nvrtc_compile(n, dtype, addend, cubin, lowered, log);
+  const std::string expr = op == OP_MATMUL ? mm_name_expression(n, dtype) : name_expression(n, dtype, addend);
+  int rc = nvrtc_compile_expr(expr, cubin, lowered, log);
   if (rc != JM_OK) {
     s.err = log;
     return fail(rc, "%s", log.c_str());
   }
-  if ((rc = install_cubin(s, n, dtype, std::move(cubin), lowered)) != JM_OK) return rc;
+  if ((rc = install_cubin(s, op, n, dtype, std::move(cubin), lowered)) != JM_OK) return rc;
   const double ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   s.compile_ms = ms;
   c_compile_us += (long long)(ms * 1000.0);
   if (env_flag("JIT_MAT_LOG"))
     fprintf(stderr, "[jitmat] compiled %s in %.1f ms (%lld B cubin, %d regs, %d B local)\n",
-            name_expression(n, dtype, addend).c_str(), ms, s.cubin_bytes, s.regs, s.local_bytes);
+            expr.c_str(), ms, s.cubin_bytes, s.regs, s.local_bytes);
   return JM_OK;
 }
 
@@ -361,11 +377,13 @@ int check_key(int n, int dtype, int addend, int kind) {
 }
 
 // Algorithm 1 (PAPER.md:319 lookup, :347 store) with per-key once semantics.
-int lookup(int n, int dtype, int addend, int kind, Slot **out) {
+int lookup_op(int op, int n, int dtype, int addend, int kind, Slot **out) {
   int rc = check_key(n, dtype, addend, kind);
   if (rc != JM_OK) return rc;
   if (!G.inited.load(std::memory_order_acquire)) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
-  Slot &s = g_slots[kind][addend][dtype][n];
+  if (op == OP_MATMUL && kind == JM_KIND_AOT_SPECIALIZED)
+    return fail(JM_E_UNSUPPORTED, "no ahead-of-time specialization of the multiply-accumulate");
+  Slot &s = op == OP_MATMUL ? g_mm_slots[kind][dtype][n] : g_slots[kind][addend][dtype][n];
   int st = s.state.load(std::memory_order_acquire);
   if (st == S_READY) {
     c_hits++;
@@ -383,7 +401,7 @@ int lookup(int n, int dtype, int addend, int kind, Slot **out) {
     return fail(JM_E_UNSUPPORTED, "no ahead-of-time specialization for n=%d %s (available: n = 3, 7, 16, double)",
                 n, dtype == JM_F64 ? "double" : "float");
   s.state.store(S_COMPILING, std::memory_order_relaxed);
-  rc = compile_slot(s, n, dtype, addend);
+  rc = compile_slot(s, op, n, dtype, addend);
   if (rc != JM_OK) {
     if (rc == JM_E_COMPILE) {
       s.state.store(S_FAILED, std::memory_order_release);
@@ -395,6 +413,10 @@ int lookup(int n, int dtype, int addend, int kind, Slot **out) {
   s.state.store(S_READY, std::memory_order_release);
   *out = &s;
   return JM_OK;
+}
+
+int lookup(int n, int dtype, int addend, int kind, Slot **out) {
+  return lookup_op(OP_UPDATE, n, dtype, addend, kind, out);
 }
 
 int launch(Slot &s, int n, int64_t batch, int64_t repeat, const void *in, void *out, CUstream stream,
@@ -659,6 +681,19 @@ int jit_mat_init(int device) {
   CU_TRY(D.ModuleGetFunction(&G.fill[1], G.aot, "jm_fill_f64"), "jm_fill_f64");
   CU_TRY(D.ModuleGetFunction(&G.checksum[0], G.aot, "jm_checksum_f32"), "jm_checksum_f32");
   CU_TRY(D.ModuleGetFunction(&G.checksum[1], G.aot, "jm_checksum_f64"), "jm_checksum_f64");
+  {
+    CUfunction mmg[NDT] = {};
+    CU_TRY(D.ModuleGetFunction(&mmg[0], G.aot, "jm_mm_generic_f32"), "jm_mm_generic_f32");
+    CU_TRY(D.ModuleGetFunction(&mmg[1], G.aot, "jm_mm_generic_f64"), "jm_mm_generic_f64");
+    for (int dt = 0; dt < NDT; ++dt)
+      for (int n = 1; n <= NMAX; ++n) {
+        Slot &s = g_mm_slots[JM_KIND_GENERIC][dt][n];
+        s.plan = jm::plan_matmul(n, dt);
+        s.cubin_bytes = (long long)jm_embedded_aot_cubin_len;
+        if ((rc = finish_function(s, mmg[dt])) != JM_OK) return rc;
+        s.state.store(S_READY, std::memory_order_release);
+      }
+  }
   CU_TRY(D.MemAlloc(&G.sum_buf, 16), "cuMemAlloc(checksum)");
   seed_generic_slots();
   if ((rc = seed_aot_spec_slots()) != JM_OK) return rc;
@@ -671,24 +706,27 @@ int jit_mat_shutdown(void) {
   if (!G.inited.load()) return fail(JM_E_NOT_INITIALIZED, "not initialised");
   ensure_ctx();
   G.inited.store(false, std::memory_order_release);
+  auto reset = [](Slot &s) {
+    std::lock_guard<std::mutex> sl(s.mu);
+    if (s.mod) D.ModuleUnload(s.mod);
+    s.mod = nullptr;
+    s.fn = nullptr;
+    s.err.clear();
+    s.regs = s.local_bytes = 0;
+    s.cubin_bytes = 0;
+    s.cubin.clear();
+    s.cubin.shrink_to_fit();
+    s.lowered.clear();
+    s.compile_ms = 0;
+    s.state.store(S_EMPTY, std::memory_order_release);
+  };
   for (int k = 0; k < NKIND; ++k)
     for (int a = 0; a < NADD; ++a)
       for (int t = 0; t < NDT; ++t)
-        for (int n = 0; n <= NMAX; ++n) {
-          Slot &s = g_slots[k][a][t][n];
-          std::lock_guard<std::mutex> sl(s.mu);
-          if (s.mod) D.ModuleUnload(s.mod);
-          s.mod = nullptr;
-          s.fn = nullptr;
-          s.err.clear();
-          s.regs = s.local_bytes = 0;
-          s.cubin_bytes = 0;
-          s.cubin.clear();
-          s.cubin.shrink_to_fit();
-          s.lowered.clear();
-          s.compile_ms = 0;
-          s.state.store(S_EMPTY, std::memory_order_release);
-        }
+        for (int n = 0; n <= NMAX; ++n) reset(g_slots[k][a][t][n]);
+  for (int k = 0; k < 2; ++k)
+    for (int t = 0; t < NDT; ++t)
+      for (int n = 0; n <= NMAX; ++n) reset(g_mm_slots[k][t][n]);
   {
     std::lock_guard<std::mutex> hl(G.host_mu);
     for (int i = 0; i < 3; ++i) {
@@ -790,7 +828,7 @@ int jit_mat_cache_import(const void *blob, size_t len) {
   std::lock_guard<std::mutex> lk(s.mu);
   if (s.state.load(std::memory_order_acquire) == S_READY) return JM_OK;
   std::vector<char> cubin(p, p + cl);
-  if ((rc = install_cubin(s, key[0], key[1], std::move(cubin), lowered)) != JM_OK) return rc;
+  if ((rc = install_cubin(s, OP_UPDATE, key[0], key[1], std::move(cubin), lowered)) != JM_OK) return rc;
   s.compile_ms = 0.0;
   c_imports++;
   s.state.store(S_READY, std::memory_order_release);
@@ -857,9 +895,28 @@ int jit_mat_key_info(jm_key_info *keys, int cap) {
                         : (s.plan.w > 1 ? JM_TILE_CTA_F32 : JM_TILE_WARP_F32));
             o.cubin_bytes = s.cubin_bytes;
             o.compile_ms = s.compile_ms;
+            o.op = 0;
           }
           ++cnt;
         }
+  for (int k = 0; k < 2; ++k)
+    for (int t = 0; t < NDT; ++t)
+      for (int n = 1; n <= NMAX; ++n) {
+        Slot &s = g_mm_slots[k][t][n];
+        const int st = s.state.load(std::memory_order_acquire);
+        if (st == S_EMPTY || (k == JM_KIND_GENERIC)) continue;   // generic mm slots: always seeded
+        if (keys && cnt < cap) {
+          jm_key_info &o = keys[cnt];
+          o.n = n; o.dtype = t; o.addend = 0; o.kind = k; o.state = st;
+          o.regs = s.regs; o.local_bytes = s.local_bytes; o.smem_bytes = s.plan.smem;
+          o.threads = s.plan.threads;
+          o.tile = JM_TILE_MATMUL;
+          o.cubin_bytes = s.cubin_bytes;
+          o.compile_ms = s.compile_ms;
+          o.op = 1;
+        }
+        ++cnt;
+      }
   return cnt;
 }
 
@@ -938,13 +995,67 @@ const char *jit_mat_version(void) {
 // Test hook: NVRTC-compile a key without a device (no module load).  Lets the
 // CPU-only test tier prove every specialization compiles for sm_100a.
 int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes) {
-  int rc = check_key(n, dtype, addend, JM_KIND_SPECIALIZED);
+  int rc = check_key(n, dtype, addend == JM_OP_MATMUL ? JM_ADDEND_ONES : addend, JM_KIND_SPECIALIZED);
   if (rc != JM_OK) return rc;
   std::vector<char> cubin;
   std::string lowered, log;
-  rc = nvrtc_compile(n, dtype, addend, cubin, lowered, log);
+  rc = nvrtc_compile_expr(addend == JM_OP_MATMUL ? mm_name_expression(n, dtype) : name_expression(n, dtype, addend),
+                          cubin, lowered, log);
   if (rc != JM_OK) return fail(rc, "%s", log.c_str());
   if (cubin_bytes) *cubin_bytes = (long long)cubin.size();
+  return JM_OK;
+}
+
+int jit_mat_matmul(int n, int dtype, int kind, int64_t batch, const void *a, const void *b, void *c,
+                   void *stream) {
+  int rc = check_key(n, dtype, JM_ADDEND_ONES, kind);
+  if (rc != JM_OK) return rc;
+  if (batch < 0) return fail(JM_E_INVALID, "batch must be >= 0 (got %lld)", (long long)batch);
+  if (!G.inited.load(std::memory_order_acquire)) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
+  if (batch == 0) return JM_OK;
+  if (!a || !b || !c) return fail(JM_E_INVALID, "NULL buffer");
+  if (((unsigned long long)a | (unsigned long long)b | (unsigned long long)c) & 15)
+    return fail(JM_E_ALIGN, "a/b/c must be 16-byte aligned");
+  const unsigned long long bytes = (unsigned long long)batch * n * n * (dtype == JM_F64 ? 8 : 4);
+  const unsigned long long pc = (unsigned long long)c;
+  for (const void *p : {a, b}) {
+    const unsigned long long q = (unsigned long long)p;
+    if (q < pc + bytes && pc < q + bytes) return fail(JM_E_INVALID, "c must not overlap a or b");
+  }
+  Slot *s = nullptr;
+  if ((rc = lookup_op(OP_MATMUL, n, dtype, JM_ADDEND_ONES, kind, &s)) != JM_OK) return rc;
+  if ((rc = ensure_ctx()) != JM_OK) return rc;
+  CUstream st = (CUstream)(stream ? stream : G.stream.load(std::memory_order_relaxed));
+  const long long mpc = s->plan.mpc;
+  const long long nchunks = (batch + mpc - 1) / mpc;
+  const unsigned grid = (unsigned)(nchunks < s->grid_cap ? nchunks : s->grid_cap);
+  CUdeviceptr pa = (CUdeviceptr)a, pb = (CUdeviceptr)b, pcc = (CUdeviceptr)c;
+  long long bt = batch;
+  int nn = n;
+  void *args_spec[] = {&pa, &pb, &pcc, &bt};
+  void *args_gen[] = {&pa, &pb, &pcc, &bt, &nn};
+  CU_TRY(D.LaunchKernel(s->fn, grid, 1, 1, (unsigned)s->plan.threads, 1, 1, (unsigned)s->plan.smem, st,
+                        kind == JM_KIND_GENERIC ? args_gen : args_spec, nullptr),
+         "cuLaunchKernel(matmul)");
+  c_launches++;
+  return sync_if(0, st);
+}
+
+// Cache-hit cost of the key lookup (row a1), measured in C: `iters` lookups of
+// an already-READY key, average nanoseconds per lookup into *ns.
+int jit_mat_time_lookup(int n, int dtype, int addend, int kind, int64_t iters, double *ns) {
+  if (!ns || iters <= 0) return fail(JM_E_INVALID, "bad arguments");
+  Slot *s = nullptr;
+  int rc = lookup(n, dtype, addend, kind, &s);   // make sure it is READY
+  if (rc != JM_OK) return rc;
+  const auto t0 = std::chrono::steady_clock::now();
+  uintptr_t sink = 0;
+  for (int64_t i = 0; i < iters; ++i) {
+    rc = lookup(n, dtype, addend, kind, &s);
+    sink += (uintptr_t)s + (uintptr_t)rc;
+  }
+  const double el = std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
+  *ns = el / (double)iters + (sink == 1 ? 1e-300 : 0.0);
   return JM_OK;
 }
 
