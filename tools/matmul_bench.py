@@ -59,14 +59,15 @@ def graph_us(fn, calls_per_graph, replays, stream):
     with torch.cuda.graph(g, stream=stream):
         for _ in range(calls_per_graph):
             fn()
-    g.replay()
-    stream.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(replays):
+    with torch.cuda.stream(stream):   # replay() launches on the current stream
         g.replay()
-    e1.record(stream)
-    e1.synchronize()
+        stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(replays):
+            g.replay()
+        e1.record(stream)
+        e1.synchronize()
     return e0.elapsed_time(e1) * 1e3 / (calls_per_graph * replays)
 
 
