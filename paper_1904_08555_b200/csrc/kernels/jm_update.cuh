@@ -213,15 +213,16 @@ __device__ __forceinline__ void tpm_iterate(T (&m)[N * N], int repeat) {
   for (int r = 0; r < repeat; ++r) {
     T p[N * N];
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
+    for (int e = 0; e < N * N; ++e) p[e] = m[e];   // P = M + M*M: accumulators start at M
+    // k outermost: consecutive DFMAs share the operand m[i][k] (operand-reuse
+    // cache; a DFMA reading three distinct register pairs is register-bank bound)
+    // and target independent accumulators; per element the k order is unchanged.
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        T acc = m[i * N + j];  // P = M + M*M: accumulator starts at M
+    for (int k = 0; k < N; ++k)
 #pragma unroll
-        for (int k = 0; k < N; ++k) acc = fmaT(m[i * N + k], m[k * N + j], acc);
-        p[i * N + j] = acc;
-      }
-    }
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j) p[i * N + j] = fmaT(m[i * N + k], m[k * N + j], p[i * N + j]);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
 #pragma unroll
@@ -241,25 +242,33 @@ __device__ __forceinline__ void tpm_iterate_f32x2(float (&m)[N * N], int repeat)
   constexpr int NH = N / 2;
   for (int r = 0; r < repeat; ++r) {
     float p[N * N];
+    float2 p2[N][NH > 0 ? NH : 1];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
 #pragma unroll
-      for (int jj = 0; jj < NH; ++jj) {
-        float2 acc = make_float2(m[i * N + 2 * jj], m[i * N + 2 * jj + 1]);
-#pragma unroll
-        for (int k = 0; k < N; ++k)
-          acc = __ffma2_rn(make_float2(m[i * N + k], m[i * N + k]),
-                           make_float2(m[k * N + 2 * jj], m[k * N + 2 * jj + 1]), acc);
-        p[i * N + 2 * jj] = acc.x;
-        p[i * N + 2 * jj + 1] = acc.y;
-      }
-      if constexpr (N % 2) {
-        float acc = m[i * N + N - 1];
-#pragma unroll
-        for (int k = 0; k < N; ++k) acc = fmaT(m[i * N + k], m[k * N + N - 1], acc);
-        p[i * N + N - 1] = acc;
-      }
+      for (int jj = 0; jj < NH; ++jj) p2[i][jj] = make_float2(m[i * N + 2 * jj], m[i * N + 2 * jj + 1]);
+      if constexpr (N % 2) p[i * N + N - 1] = m[i * N + N - 1];
     }
+    // k outermost (operand reuse of m[i][k], independent accumulators); per
+    // element the k order is unchanged
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int jj = 0; jj < NH; ++jj)
+          p2[i][jj] = __ffma2_rn(make_float2(m[i * N + k], m[i * N + k]),
+                                 make_float2(m[k * N + 2 * jj], m[k * N + 2 * jj + 1]), p2[i][jj]);
+        if constexpr (N % 2)
+          p[i * N + N - 1] = fmaT(m[i * N + k], m[k * N + N - 1], p[i * N + N - 1]);
+      }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int jj = 0; jj < NH; ++jj) {
+        p[i * N + 2 * jj] = p2[i][jj].x;
+        p[i * N + 2 * jj + 1] = p2[i][jj].y;
+      }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
 #pragma unroll

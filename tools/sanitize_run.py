@@ -1,0 +1,68 @@
+#!/usr/bin/env python3
+"""Small invocation of every kernel kind, for compute-sanitizer.
+
+    compute-sanitizer --tool memcheck  python tools/sanitize_run.py
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py
+    compute-sanitizer --tool synccheck python tools/sanitize_run.py
+
+Covers TPM, warp/CTA DMMA, FP32 row panels and tiles, the generic kernels, the
+AoT specializations, the multiply-accumulate, fill, checksum, run_many and the
+host-buffer path, each on a ragged batch (several chunks + a partial one).
+Exits non-zero on any library error; the sanitizer reports the rest.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1904_08555_b200 as jm  # noqa: E402
+
+CASES = [(2, "f64"), (3, "f64"), (5, "f64"), (7, "f64"), (16, "f64"), (13, "f64"), (32, "f64"),
+         (40, "f64"), (64, "f64"), (3, "f32"), (8, "f32"), (12, "f32"), (16, "f32"), (24, "f32"),
+         (33, "f32"), (64, "f32")]
+
+
+def main():
+    torch.cuda.init()
+    jm.jit_mat_init(0)
+    for n, dt in CASES:
+        tdt = torch.float64 if dt == "f64" else torch.float32
+        batch = 37 if n <= 16 else 5
+        x = torch.empty(batch, n, n, dtype=tdt, device="cuda")
+        jm.jit_mat_fill(n, dt, 2, 7, 0, batch, x.data_ptr())
+        for kind in ("specialized", "generic"):
+            for addend in ("ones", "identity"):
+                jm.run(x, 2, addend=addend, kind=kind, sync=True)
+        y = x.clone()
+        jm.run(y, 2, y, sync=True)                       # in place
+        jm.jit_mat_checksum(n, dt, 0, batch, y.data_ptr())
+        c = torch.zeros_like(x)
+        jm.matmul(x, x, c, sync=True)
+        jm.matmul(x, x, c, kind="generic", sync=True)
+        print(f"ok n={n} {dt}", flush=True)
+    x = torch.rand(11, 16, 16, dtype=torch.float64, device="cuda")
+    jm.run(x, 3, kind="aot_specialized", sync=True)
+    groups = []
+    bufs = []
+    for n in (2, 9, 17, 40):
+        a = torch.rand(6, n, n, dtype=torch.float64, device="cuda")
+        b = torch.empty_like(a)
+        bufs.append((a, b))
+        groups.append(dict(n=n, dtype="f64", batch=6, repeat=2, in_ptr=a.data_ptr(), out_ptr=b.data_ptr()))
+    jm.jit_mat_run_many(groups, sync=True)
+    h = np.random.default_rng(0).random((300, 4, 4))
+    out = np.empty_like(h)
+    os.environ["JIT_MAT_HOST_CHUNK_MB"] = "0"
+    jm.jit_mat_run_host(4, "f64", 300, 2, h.ctypes.data, out.ctypes.data)
+    torch.cuda.synchronize()
+    print("sanitize_run: all kinds exercised")
+
+
+if __name__ == "__main__":
+    main()
