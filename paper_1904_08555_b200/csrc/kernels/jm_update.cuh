@@ -352,6 +352,14 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));
 }
+// D = A*B + C with D != C: the first k-step reads the accumulator init (M)
+// from the A-operand registers directly, so P needs no separate copy of M.
+__device__ __forceinline__ void dmma884_c(double &d0, double &d1, double a, double b, double c0,
+                                          double c1) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
+      : "=d"(d0), "=d"(d1)
+      : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
 
 // byte offset of 16-B chunk `cc` of row `r` in the swizzled scratch
 template <int RSC>
@@ -406,10 +414,6 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
         if constexpr (W == 1) __syncwarp(); else __syncthreads();
         double p[RT][T8][2];
 #pragma unroll
-        for (int I = 0; I < RT; ++I)
-#pragma unroll
-          for (int J = 0; J < T8; ++J) { p[I][J][0] = acc[I][J][0]; p[I][J][1] = acc[I][J][1]; }
-#pragma unroll
         for (int J = 0; J < T8; ++J) {
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
@@ -421,7 +425,12 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
 #pragma unroll
             for (int I = 0; I < RT; ++I)
 #pragma unroll
-              for (int J2 = 0; J2 < T8; ++J2) dmma884(p[I][J2][0], p[I][J2][1], acc[I][J][s], b[J2]);
+              for (int J2 = 0; J2 < T8; ++J2) {
+                if (J == 0 && s == 0)   // P = M + (first k-step): accumulator init is M itself
+                  dmma884_c(p[I][J2][0], p[I][J2][1], acc[I][J][s], b[J2], acc[I][J2][0], acc[I][J2][1]);
+                else
+                  dmma884(p[I][J2][0], p[I][J2][1], acc[I][J][s], b[J2]);
+              }
           }
         }
         // M' = A + c * P  (padding stays exactly zero)

@@ -67,6 +67,34 @@ __global__ void k_mix(double *out, double av, double bv) {
   if (s == 12345.678) out[0] = s;
 }
 
+// The C2 kernel's FP64 instruction mix per warp and update: 16 DMMA.8x8x4
+// (4 accumulator chains x 4 k-steps) + 8 DFMA (epilogue).  Upper bound for
+// the warp-DMMA n=16 kernel when nothing else stalls.
+__global__ void k_mix16_8(double *out, double av, double bv) {
+  double c[4][2], d[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { c[i][0] = threadIdx.x; c[i][1] = i; }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) d[i] = i;
+  double a = av * threadIdx.x, b = bv;
+  for (int it = 0; it < ITER / 8; ++it) {
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) d[j] = fma(d[j], b, a);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s += c[i][0] + c[i][1];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += d[i];
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void k_ffma(float *out, float b, float c) {
   float a[16];
 #pragma unroll
@@ -187,6 +215,9 @@ int main() {
   ms = timeit([&] { k_mix<<<blocks, threads>>>(dd, 1e-3, 1e-3); });
   printf("  \"dmma_dfma_mix_tflops\": %.3f,\n",
          (nwarp * (ITER / 4) * 4 * 512.0 + nthr * (ITER / 4) * 4 * 8 * 2.0) / (ms * 1e-3) / 1e12);
+  ms = timeit([&] { k_mix16_8<<<blocks, threads>>>(dd, 1e-3, 1e-3); });
+  printf("  \"dmma16_dfma8_mix_tflops\": %.3f,\n",
+         (nwarp * (ITER / 8) * 16 * 512.0 + nthr * (ITER / 8) * 8 * 2.0) / (ms * 1e-3) / 1e12);
   ms = timeit([&] { k_ffma<<<blocks, threads>>>(df, 1.0000001f, 1e-9f); });
   printf("  \"ffma_tflops\": %.3f,\n", nthr * ITER * 16 * 2 / (ms * 1e-3) / 1e12);
   ms = timeit([&] { k_ffma2<<<blocks, threads>>>(df, 1.0000001f, 1e-9f); });
