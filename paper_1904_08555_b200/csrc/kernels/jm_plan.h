@@ -21,7 +21,7 @@
 namespace jm {
 
 enum class Addend : int { Ones = 0, Identity = 1 };
-enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, F32 = 4 };
+enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, F32 = 4, Rows = 6 };
 
 struct Plan {
   int tile;      // Tile
@@ -46,21 +46,44 @@ JM_HD constexpr int stage_stride(int n, int es) {
 // A chunk's staging area, rounded to 16 B so the buffers after it stay aligned.
 JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage_stride(n, es), 16); }
 
+// FP64: thread-per-matrix up to n = 7 (166 registers, no spill; DMMA would pad
+// 7 -> 8), FP64 tensor cores above.  The FP64 row panels (Tile::Rows) are kept
+// selectable through JM_F64_ROWS_MAX but off: measured on B200 they reach only
+// 0.26-0.35 of the FP64 pipe for n = 9..12 (shared-memory operand bound, three
+// FMAs per loaded double), not better than the padded DMMA tiles.
+#ifndef JM_F64_ROWS_MAX
+#define JM_F64_ROWS_MAX 0
+#endif
 JM_HD constexpr Tile tile_for(int n, int dtype) {
-  return dtype == 1 ? (n <= 6 ? Tile::TPM : Tile::Dmma) : (n <= 8 ? Tile::TPM : Tile::F32);
+  return dtype == 1 ? (n <= 7 ? Tile::TPM : ((n >= 9 && n <= JM_F64_ROWS_MAX) ? Tile::Rows : Tile::Dmma))
+                    : (n <= 8 ? Tile::TPM : Tile::F32);
 }
+
+// ---- F64 row panels (9 <= n <= 12): DFMA, where DMMA padding wastes most ----
+constexpr int F64P_G = 4;                          // threads per matrix
+constexpr int F64P_WPC = 2;                        // warps per CTA
+JM_HD constexpr int f64p_rp(int n) { return cdiv(n, F64P_G); }             // rows per thread (3)
+JM_HD constexpr int f64p_ncr(int n) { return cdiv(n, 2); }                 // 16-B chunks per row
+JM_HD constexpr int f64p_ncs(int n) { return f64p_ncr(n) <= 4 ? 4 : 8; }   // stored chunks (pow2)
+JM_HD constexpr int f64p_groups(int n) { return cdiv(f64p_ncr(n), 2); }    // 4-column groups
+JM_HD constexpr int f64p_mbuf(int n) { return n * f64p_ncs(n) * 16 + 32; }
 
 // ---- TPM ----
 constexpr int TPM_THREADS = 128;
 
 // ---- DMMA (FP64) ----
+#ifndef JM_DMMA_RT_LARGE
+#define JM_DMMA_RT_LARGE 1   // row tiles per warp for n > 32 (one warp per 8-row tile)
+#endif
 constexpr int DMMA_WPC = 4;                       // warps per CTA when W == 1
 JM_HD constexpr int dmma_t8(int n) { return cdiv(n, 8); }
 // row tiles per warp: whole matrix per warp up to n = 24; two warps of two
-// row tiles for 25..32 (keeps the accumulators + product copy under ~128 regs);
-// above 32 one CTA per matrix, two (even T8) or one (odd T8) row tile per warp.
+// row tiles for 25..32 (keeps the accumulators + product under ~128 regs);
+// above 32 one CTA per matrix: 4 warps x 2 row tiles for 57..64, one row tile
+// per warp otherwise (r01 sweep: n=48 0.69 -> 0.72 of the FP64 pipe with one
+// tile per warp, n=64 0.92 with two vs 0.87 with one).
 JM_HD constexpr int dmma_rt(int n) {
-  return n <= 24 ? dmma_t8(n) : ((dmma_t8(n) % 2 == 0) ? 2 : 1);
+  return n <= 24 ? dmma_t8(n) : ((n <= 32 || dmma_t8(n) == 8) ? 2 : JM_DMMA_RT_LARGE);
 }
 JM_HD constexpr int dmma_w(int n) { return dmma_t8(n) / dmma_rt(n); }
 JM_HD constexpr int dmma_rsc(int n) { return rup(4 * dmma_t8(n), 8); }     // scratch row stride, 16-B chunks
@@ -112,6 +135,10 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   const int nst = prefetch_for(n, dtype) ? 2 : 1;   // stage buffers
   if (t == Tile::TPM) {
     return Plan{(int)t, TPM_THREADS, TPM_THREADS, stage_bytes(TPM_THREADS, n, es), 1};
+  }
+  if (t == Tile::Rows) {
+    const int mpc = F64P_WPC * (32 / F64P_G);
+    return Plan{(int)t, 32 * F64P_WPC, mpc, stage_bytes(mpc, n, es) + 2 * mpc * f64p_mbuf(n), 1};
   }
   if (t == Tile::Dmma) {
     const int w = dmma_w(n);

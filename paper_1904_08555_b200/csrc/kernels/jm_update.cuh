@@ -417,6 +417,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
         for (int J = 0; J < T8; ++J) {
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
+            if (8 * J + s >= N) continue;   // every k of this k-step is padding: skip (compile time)
             double b[T8];
 #pragma unroll
             for (int J2 = 0; J2 < T8; ++J2)
@@ -617,6 +618,125 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
 }
 
 // ======================================================================
+// F64P: FP64 row panels (9 <= N <= 12), the DFMA counterpart of F32P for the
+// sizes where DMMA's 8x8x4 granularity wastes most of the pipe (n = 9 pads to
+// 16: 24 % useful).  G = 4 threads per matrix, RP = 3 full rows each (A operand
+// local), row k of M broadcast from a double-buffered, chunk-swizzled shared
+// copy (16-B chunk = 2 doubles); accumulators in column groups of 2 chunks.
+// ======================================================================
+template <int N, Addend A>
+__device__ __forceinline__ void run_f64p(const double *__restrict__ in, double *__restrict__ out,
+                                         long long batch, int repeat) {
+  constexpr int RP = f64p_rp(N), G = F64P_G, MPW = 32 / F64P_G, NCR = f64p_ncr(N);
+  constexpr int NCS = f64p_ncs(N), GROUPS = f64p_groups(N), MBUF = f64p_mbuf(N);
+  constexpr int NC = 2 * NCR;                          // computed columns (16-B padded)
+  constexpr int QH = cdiv(NCR, GROUPS);                // chunks per column group
+  constexpr int ES = 8, MB = N * N * 8, SB = stage_stride(N, 8);
+  constexpr int NT = 32 * F64P_WPC, MPC = F64P_WPC * MPW;
+  constexpr bool AL = ((MPC * MB) % 16) == 0;
+  static_assert(G * RP >= N, "row panels must cover the matrix");
+  extern __shared__ __align__(16) char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int mw = lane / G, tg = lane - mw * G;
+  const int mi = warp * MPW + mw;
+  const int r0 = tg * RP;
+  char *bufs = smem + stage_bytes(MPC, N, 8) + mi * 2 * MBUF;
+  const double c = 0.00005;
+
+  Stager<N, ES, SB, NT, MPC, AL, false> sg(in, out, batch, smem);
+  for (sg.start(); sg.valid(); sg.next()) {
+    sg.acquire();
+    char *stage = sg.buf();
+    const int cnt = sg.cnt();
+    const bool live = mi < cnt;      // all lanes run the loop; dead slots are never stored
+    double *sm = reinterpret_cast<double *>(stage + mi * SB);
+    double m[RP][NC];
+#pragma unroll
+    for (int i = 0; i < RP; ++i)
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const int row = r0 + i;
+        m[i][j] = (live && row < N && j < N) ? sm[row * N + j] : 0.0;
+      }
+#pragma unroll
+    for (int i = 0; i < RP; ++i)
+      if (r0 + i < N) {
+#pragma unroll
+        for (int q = 0; q < NCR; ++q)
+          sts_f64x2(bufs + f32p_off<NCS>(r0 + i, q), m[i][2 * q], m[i][2 * q + 1]);
+      }
+    __syncwarp();
+#pragma unroll 1
+    for (int r = 0; r < repeat; ++r) {
+      const char *cur = bufs + (r & 1) * MBUF;
+      char *nxt = bufs + ((r & 1) ^ 1) * MBUF;
+#pragma unroll
+      for (int h = 0; h < GROUPS; ++h) {
+        const int qlo = h * QH;
+        const int qn = (NCR - qlo) < QH ? (NCR - qlo) : QH;
+        double p[RP][2 * QH];
+#pragma unroll
+        for (int i = 0; i < RP; ++i)
+#pragma unroll
+          for (int j = 0; j < 2 * QH; ++j)
+            if (j < 2 * qn) p[i][j] = m[i][2 * qlo + j];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double b[2 * QH];
+#pragma unroll
+          for (int q = 0; q < QH; ++q)
+            if (q < qn) {
+              const double2 v = *reinterpret_cast<const double2 *>(cur + f32p_off<NCS>(k, qlo + q));
+              b[2 * q] = v.x; b[2 * q + 1] = v.y;
+            }
+#pragma unroll
+          for (int i = 0; i < RP; ++i)
+#pragma unroll
+            for (int j = 0; j < 2 * QH; ++j)
+              if (j < 2 * qn) p[i][j] = fmaT(m[i][k], b[j], p[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < RP; ++i) {
+          const int row = r0 + i;
+#pragma unroll
+          for (int q = 0; q < QH; ++q)
+            if (q < qn) {
+              double v[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int col = 2 * (qlo + q) + e;
+                const double a = (A == Addend::Ones || col == row) ? 1.0 : 0.0;
+                v[e] = (row < N && col < N) ? fmaT(c, p[i][2 * q + e], a) : 0.0;
+              }
+              if (row < N) sts_f64x2(nxt + f32p_off<NCS>(row, qlo + q), v[0], v[1]);
+            }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RP; ++i)   // own rows back from the next buffer (written by this thread)
+        if (r0 + i < N) {
+#pragma unroll
+          for (int q = 0; q < NCR; ++q) {
+            const double2 v = *reinterpret_cast<const double2 *>(nxt + f32p_off<NCS>(r0 + i, q));
+            m[i][2 * q] = v.x; m[i][2 * q + 1] = v.y;
+          }
+        }
+      __syncwarp();
+    }
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < RP; ++i)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const int row = r0 + i;
+          if (row < N && j < N) sm[row * N + j] = m[i][j];
+        }
+    }
+    sg.release();
+  }
+}
+
+// ======================================================================
 // F32: FP32 register-tiled outer products.  The RG x CG threads of a matrix
 // each own an RA x CB block of M (registers).  Every update republishes M and
 // M^T to shared memory; then for k < N each thread reads RA values of column k
@@ -760,6 +880,8 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
   static_assert(K == tile_for(N, sizeof(T) == 8 ? 1 : 0), "tile must match the plan");
   if constexpr (K == Tile::TPM) {
     run_tpm<N, T, A>(in, out, batch, repeat);
+  } else if constexpr (K == Tile::Rows) {
+    run_f64p<N, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Dmma) {
     run_dmma<N, A, dmma_w(N)>(in, out, batch, repeat);
   } else if constexpr (f32p_use(N)) {
