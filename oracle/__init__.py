@@ -58,8 +58,37 @@ def _load():
             lib.jm_oracle_matmul.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                              ctypes.c_int]
+            lib.jm_oracle_mass.restype = ctypes.c_int
+            lib.jm_oracle_mass.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_int]
             _lib = lib
     return _lib
+
+
+def mass_apply(y: np.ndarray, B: np.ndarray, op: np.ndarray, x: np.ndarray,
+               threads: int | None = None) -> np.ndarray:
+    """Return y + (Laghos 2D mass action on x) per element (reading R18; float64).
+
+    Shapes: B (Q, D) = dofToQuad, op (E, Q, Q), x and y (E, D, D).  Follows
+    jm_oracle.c's rMassMultAdd2D loop order; inputs are not modified.
+    """
+    lib = _load()
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    op = np.ascontiguousarray(op, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.array(y, dtype=np.float64, copy=True, order="C")
+    Q, D = B.shape
+    E = x.shape[0]
+    if x.shape != (E, D, D) or out.shape != (E, D, D) or op.shape != (E, Q, Q):
+        raise ValueError("shapes: B (Q,D), op (E,Q,Q), x/y (E,D,D)")
+    th = default_threads() if threads is None else int(threads)
+    rc = lib.jm_oracle_mass(D, Q, E, B.ctypes.data_as(ctypes.c_void_p),
+                            op.ctypes.data_as(ctypes.c_void_p), x.ctypes.data_as(ctypes.c_void_p),
+                            out.ctypes.data_as(ctypes.c_void_p), th)
+    if rc != 0:
+        raise ValueError(f"jm_oracle_mass rejected arguments (rc={rc})")
+    return out
 
 
 def matmul_acc(c: np.ndarray, a: np.ndarray, b: np.ndarray, threads: int | None = None) -> np.ndarray:

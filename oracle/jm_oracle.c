@@ -186,6 +186,90 @@ int jm_oracle_matmul(int n, int dtype, int64_t batch, const void *a, const void 
 }
 
 /*
+ * Laghos 2D mass-operator action, rMassMultAdd2D<NUM_DOFS_1D, NUM_QUAD_1D>
+ * (§5.3, Listing 12: the kernel whose ~32 explicit
+ * instantiations ClangJIT replaces; Fig. 7 lines 765-785 time it on 10,000
+ * elements).  The paper names the kernel but does not print it; reading R18
+ * takes the standard sum-factorised partial-assembly mass action
+ * of Laghos/MFEM, with D = NUM_DOFS_1D, Q = NUM_QUAD_1D, for each element e:
+ *     S[qy][qx] = sum_dy sum_dx B[qy][dy] B[qx][dx] X[e][dy][dx]   (x to quad points)
+ *     S[qy][qx] *= op[e][qy][qx]                                    (quadrature weights)
+ *     Y[e][dy][dx] += sum_qy sum_qx B[qy][dy] B[qx][dx] S[qy][qx]   (back to dofs)
+ * evaluated in Laghos' loop order: first contract dx, then dy (and qx, then
+ * qy on the way back), ascending indices, separate multiply and add.  Layouts
+ * (row-major here): B is Q x D (B[q*D + d], Laghos' dofToQuad), op is E x Q x Q
+ * (op[e*Q*Q + qy*Q + qx]), x and y are E x D x D (x[e*D*D + dy*D + dx]); the
+ * transposed basis (quadToDof) is B^T.  y is updated in place.
+ */
+typedef struct {
+    int D, Q;
+    int64_t e0, e1;
+    const double *B, *op, *x;
+    double *y;
+} mass_job_t;
+
+static void *mass_range(void *arg) {
+    mass_job_t *j = (mass_job_t *)arg;
+    const int D = j->D, Q = j->Q;
+    double *sol_xy = (double *)malloc((size_t)Q * Q * sizeof(double));
+    double *sol_x = (double *)malloc((size_t)(Q > D ? Q : D) * sizeof(double));
+    for (int64_t e = j->e0; e < j->e1; ++e) {
+        const double *x = j->x + (size_t)e * D * D;
+        const double *op = j->op + (size_t)e * Q * Q;
+        double *y = j->y + (size_t)e * D * D;
+        for (int i = 0; i < Q * Q; ++i) sol_xy[i] = 0.0;
+        for (int dy = 0; dy < D; ++dy) {
+            for (int qx = 0; qx < Q; ++qx) sol_x[qx] = 0.0;
+            for (int dx = 0; dx < D; ++dx) {
+                const double s = x[dy * D + dx];
+                for (int qx = 0; qx < Q; ++qx) sol_x[qx] = sol_x[qx] + j->B[qx * D + dx] * s;
+            }
+            for (int qy = 0; qy < Q; ++qy) {
+                const double d2q = j->B[qy * D + dy];
+                for (int qx = 0; qx < Q; ++qx) sol_xy[qy * Q + qx] = sol_xy[qy * Q + qx] + d2q * sol_x[qx];
+            }
+        }
+        for (int qy = 0; qy < Q; ++qy)
+            for (int qx = 0; qx < Q; ++qx) sol_xy[qy * Q + qx] = sol_xy[qy * Q + qx] * op[qy * Q + qx];
+        for (int qy = 0; qy < Q; ++qy) {
+            for (int dx = 0; dx < D; ++dx) sol_x[dx] = 0.0;
+            for (int qx = 0; qx < Q; ++qx) {
+                const double s = sol_xy[qy * Q + qx];
+                for (int dx = 0; dx < D; ++dx) sol_x[dx] = sol_x[dx] + j->B[qx * D + dx] * s;
+            }
+            for (int dy = 0; dy < D; ++dy) {
+                const double q2d = j->B[qy * D + dy];
+                for (int dx = 0; dx < D; ++dx) y[dy * D + dx] = y[dy * D + dx] + q2d * sol_x[dx];
+            }
+        }
+    }
+    free(sol_xy);
+    free(sol_x);
+    return NULL;
+}
+
+int jm_oracle_mass(int D, int Q, int64_t elements, const double *B, const double *op, const double *x,
+                   double *y, int threads) {
+    if (D < 1 || Q < 1 || elements < 0) return -1;
+    if (elements == 0) return 0;
+    if (threads < 1) threads = 1;
+    if ((int64_t)threads > elements) threads = (int)elements;
+    mass_job_t *jobs = (mass_job_t *)calloc((size_t)threads, sizeof(mass_job_t));
+    pthread_t *tids = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    for (int t = 0; t < threads; ++t) {
+        jobs[t].D = D; jobs[t].Q = Q;
+        jobs[t].e0 = elements * t / threads;
+        jobs[t].e1 = elements * (t + 1) / threads;
+        jobs[t].B = B; jobs[t].op = op; jobs[t].x = x; jobs[t].y = y;
+    }
+    for (int t = 1; t < threads; ++t) pthread_create(&tids[t], NULL, mass_range, &jobs[t]);
+    mass_range(&jobs[0]);
+    for (int t = 1; t < threads; ++t) pthread_join(tids[t], NULL);
+    free(jobs); free(tids);
+    return 0;
+}
+
+/*
  * out[b] = f^repeat(in[b]) for b in [0, batch).  `in` and `out` are host
  * buffers of batch*n*n elements of the named type; they may be the same
  * buffer.  threads <= 0 means 1.  Returns 0, or -1 on bad arguments.
