@@ -177,6 +177,21 @@ JM_API int jit_mat_cache_import(const void *blob, size_t len);
 JM_API int jit_mat_matmul(int n, int dtype, int kind, int64_t batch, const void *a, const void *b,
                           void *c, void *stream);
 
+/* Laghos 2D mass-operator action rMassMultAdd2D<NUM_DOFS_1D, NUM_QUAD_1D>
+ * (§5.3, Listing 12, Fig. 7; SURVEY.md §8(f) f4;
+ * DESIGN.md reading R18), FP64, for each element e in [0, elements):
+ *     S = (B X_e B^T) .* op_e ;   y_e += B^T S B
+ * B: quads x dofs row-major (Laghos' dofToQuad; its transpose is quadToDof),
+ * op: elements x quads x quads, x and y: elements x dofs x dofs, all row-major
+ * doubles, device pointers (op/x/y 16-byte aligned; y must not overlap B, op
+ * or x).  kind JM_KIND_SPECIALIZED instantiates jm::k_mass<dofs, quads>
+ * through NVRTC (replacing Laghos' ~32-entry dispatch map of explicit
+ * instantiations, Listing 12); JM_KIND_GENERIC is the runtime-(dofs, quads)
+ * kernel.  1 <= dofs, quads <= 8 (Fig. 7's d, q in {2, 4, 8}); larger is
+ * JM_E_UNSUPPORTED.  Asynchronous on `stream` (NULL = the set stream). */
+JM_API int jit_mat_mass(int dofs, int quads, int kind, int64_t elements, const double *B,
+                        const double *op, const double *x, double *y, void *stream);
+
 /* Stream used by jit_mat_run (e.g. torch.cuda.current_stream().cuda_stream). */
 JM_API int jit_mat_set_stream(void *cuda_stream);
 
@@ -256,6 +271,7 @@ JM_API const char *jit_mat_version(void);
  * tier prove that every specialization compiles.  addend = JM_OP_MATMUL selects
  * the multiply-accumulate template instead.  cubin_bytes may be NULL. */
 #define JM_OP_MATMUL 2
+#define JM_OP_MASS 3     /* compile_check(dofs, quads, JM_OP_MASS, ...): k_mass<dofs, quads> */
 JM_API int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes);
 
 /* Cache-hit cost of the key lookup (the paper calls the

@@ -27,7 +27,7 @@ from ._lib import (  # noqa: F401  (re-exported C ABI)
 __all__ = [
     "jit_mat_init", "jit_mat_run", "jit_mat_shutdown", "jit_mat_run_ex", "jit_mat_run_host",
     "jit_mat_run_many", "jit_mat_cache_export", "jit_mat_cache_import", "jit_mat_matmul",
-    "jit_mat_time_lookup", "matmul",
+    "jit_mat_time_lookup", "matmul", "jit_mat_mass", "mass",
     "jit_mat_set_stream", "jit_mat_prepare", "jit_mat_dtype_from_name", "jit_mat_last_error",
     "jit_mat_stats", "jit_mat_key_info", "jit_mat_reset_stats", "jit_mat_fill",
     "jit_mat_checksum", "jit_mat_device_info", "jit_mat_version", "jit_mat_compile_check",
@@ -123,6 +123,31 @@ def jit_mat_matmul(n: int, dtype, batch: int, a_ptr: int, b_ptr: int, c_ptr: int
                               ctypes.c_void_p(stream or 0)), "jit_mat_matmul")
 
 
+def jit_mat_mass(dofs: int, quads: int, elements: int, B_ptr: int, op_ptr: int, x_ptr: int,
+                 y_ptr: int, *, kind="specialized", stream: int | None = None) -> None:
+    """Laghos 2D mass action y_e += B^T((B x_e B^T) .* op_e) B (C: jit_mat_mass)."""
+    _check(lib.jit_mat_mass(int(dofs), int(quads), _KINDS.get(kind, kind), int(elements),
+                            ctypes.c_void_p(B_ptr), ctypes.c_void_p(op_ptr), ctypes.c_void_p(x_ptr),
+                            ctypes.c_void_p(y_ptr), ctypes.c_void_p(stream or 0)), "jit_mat_mass")
+
+
+def mass(B, op, x, y, *, kind: str = "specialized", stream=None, sync: bool = False):
+    """y += mass action of x for float64 CUDA tensors B (Q,D), op (E,Q,Q), x/y (E,D,D)."""
+    import torch
+
+    Q, D = B.shape
+    E = x.shape[0]
+    for t, shp in ((B, (Q, D)), (op, (E, Q, Q)), (x, (E, D, D)), (y, (E, D, D))):
+        if tuple(t.shape) != shp or t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("expected contiguous float64 CUDA tensors B (Q,D), op (E,Q,Q), x/y (E,D,D)")
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    jit_mat_mass(D, Q, E, B.data_ptr(), op.data_ptr(), x.data_ptr(), y.data_ptr(), kind=kind,
+                 stream=st.cuda_stream)
+    if sync:
+        st.synchronize()
+    return y
+
+
 def jit_mat_time_lookup(n: int, dtype, addend="ones", kind="specialized", iters: int = 1_000_000) -> float:
     """Average ns per cache-hit lookup, timed inside the library (row a1)."""
     ns = ctypes.c_double(0.0)
@@ -214,8 +239,12 @@ def jit_mat_version() -> str:
 
 
 def jit_mat_compile_check(n: int, dtype, addend="ones") -> int:
-    """NVRTC-compile a key without a GPU; addend="matmul" selects k_matmul."""
+    """NVRTC-compile a key without a GPU; addend="matmul" selects k_matmul and
+    addend="mass" selects k_mass<n, dtype> (dtype = quads, an int)."""
     cb = ctypes.c_longlong(0)
+    if addend == "mass":
+        _check(lib.jit_mat_compile_check(int(n), int(dtype), 3, ctypes.byref(cb)), "jit_mat_compile_check")
+        return int(cb.value)
     a = JM_OP_MATMUL if addend == "matmul" else _ADDENDS.get(addend, addend)
     _check(lib.jit_mat_compile_check(int(n), _dt(dtype), a, ctypes.byref(cb)), "jit_mat_compile_check")
     return int(cb.value)

@@ -22,6 +22,7 @@ JM_FLAG_SYNC, JM_FLAG_HOST_BUFFERS = 1, 2
 JM_TILE_NAMES = {0: "generic", 1: "tpm", 2: "warp_dmma", 3: "cta_dmma", 4: "warp_f32",
                  5: "cta_f32", 6: "rows", 7: "matmul"}
 JM_OP_MATMUL = 2
+JM_OP_MASS = 3
 
 
 class JitMatError(RuntimeError):
@@ -77,6 +78,7 @@ _SIGS = {
     "jit_mat_version": (ctypes.c_char_p, []),
     "jit_mat_compile_check": (_I, [_I, _I, _I, ctypes.POINTER(ctypes.c_longlong)]),
     "jit_mat_matmul": (_I, [_I, _I, _I, _I64, _P, _P, _P, _P]),
+    "jit_mat_mass": (_I, [_I, _I, _I, _I64, _P, _P, _P, _P, _P]),
     "jit_mat_time_lookup": (_I, [_I, _I, _I, _I, _I64, ctypes.POINTER(ctypes.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():

@@ -12,6 +12,7 @@
 #include "jm_plan.h"
 #include "jm_update.cuh"
 #include "jm_matmul.cuh"
+#include "jm_mass.cuh"
 
 namespace jm {
 
@@ -81,6 +82,57 @@ __device__ __forceinline__ void matmul_generic(const T *__restrict__ a, const T 
       for (int k = 0; k < n; ++k) acc = fmaT(A[mi * nn + i * n + k], B[mi * nn + k * n + j], acc);
       C[e] = acc;
     }
+    __syncthreads();
+  }
+}
+
+// Generic (runtime D, Q) Laghos mass action: the non-specialized comparison of
+// Fig. 7 — same algorithm as mass_body with runtime loop
+// bounds, so the per-element quadrature array lives in local memory.
+__device__ __forceinline__ void mass_generic(const double *__restrict__ B, const double *__restrict__ op,
+                                             const double *__restrict__ x, double *__restrict__ y,
+                                             long long elements, int D, int Q) {
+  constexpr int NT = MASS_THREADS, MPC = MASS_THREADS;
+  extern __shared__ __align__(16) char smem[];
+  double *sx = reinterpret_cast<double *>(smem);
+  double *sy = sx + MPC * D * D;
+  double *so = sy + MPC * D * D;
+  double *sB = so + MPC * Q * Q;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < Q * D; i += NT) sB[i] = B[i];
+  const long long nchunks = (elements + MPC - 1) / MPC;
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long e0 = ch * MPC;
+    const int cnt = (int)((elements - e0) < MPC ? (elements - e0) : MPC);
+    for (int i = tid; i < cnt * D * D; i += NT) {
+      sx[i] = x[e0 * D * D + i];
+      sy[i] = y[e0 * D * D + i];
+    }
+    for (int i = tid; i < cnt * Q * Q; i += NT) so[i] = op[e0 * Q * Q + i];
+    __syncthreads();
+    if (tid < cnt) {
+      const double *X = sx + tid * D * D, *O = so + tid * Q * Q;
+      double *Y = sy + tid * D * D;
+      double S[MASS_MAX * MASS_MAX], sol[MASS_MAX];
+      for (int i = 0; i < Q * Q; ++i) S[i] = 0.0;
+      for (int dy = 0; dy < D; ++dy) {
+        for (int qx = 0; qx < Q; ++qx) sol[qx] = 0.0;
+        for (int dx = 0; dx < D; ++dx)
+          for (int qx = 0; qx < Q; ++qx) sol[qx] = fmaT(sB[qx * D + dx], X[dy * D + dx], sol[qx]);
+        for (int qy = 0; qy < Q; ++qy)
+          for (int qx = 0; qx < Q; ++qx) S[qy * Q + qx] = fmaT(sB[qy * D + dy], sol[qx], S[qy * Q + qx]);
+      }
+      for (int i = 0; i < Q * Q; ++i) S[i] *= O[i];
+      for (int qy = 0; qy < Q; ++qy) {
+        for (int dx = 0; dx < D; ++dx) sol[dx] = 0.0;
+        for (int qx = 0; qx < Q; ++qx)
+          for (int dx = 0; dx < D; ++dx) sol[dx] = fmaT(sB[qx * D + dx], S[qy * Q + qx], sol[dx]);
+        for (int dy = 0; dy < D; ++dy)
+          for (int dx = 0; dx < D; ++dx) Y[dy * D + dx] = fmaT(sB[qy * D + dy], sol[dx], Y[dy * D + dx]);
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < cnt * D * D; i += NT) y[e0 * D * D + i] = sy[i];
     __syncthreads();
   }
 }
@@ -182,6 +234,12 @@ extern "C" __global__ void __launch_bounds__(jm::MM_THREADS)
     jm_mm_generic_f64(const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ c,
                       long long batch, int n) {
   jm::matmul_generic<double>(a, b, c, batch, n);
+}
+
+extern "C" __global__ void __launch_bounds__(jm::MASS_THREADS)
+    jm_mass_generic(const double *__restrict__ B, const double *__restrict__ op, const double *__restrict__ x,
+                    double *__restrict__ y, long long elements, int D, int Q) {
+  jm::mass_generic(B, op, x, y, elements, D, Q);
 }
 
 extern "C" __global__ void jm_fill_f32(float *out, int n, int dist, unsigned long long seed,

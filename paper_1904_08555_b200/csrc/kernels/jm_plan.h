@@ -183,6 +183,15 @@ JM_HD constexpr Plan plan_matmul(int n, int dtype) {
   return Plan{(int)Tile::Generic, MM_THREADS, mm_mpc(n), 2 * stage_bytes(mm_mpc(n), n, dtype == 1 ? 8 : 4), 1};
 }
 
+// ---- Laghos 2D mass operator (Listing 12) ----
+// one thread per element, MASS_THREADS elements per CTA chunk
+constexpr int MASS_MAX = 8;                        // 1 <= D, Q <= 8 (Fig. 7: d,q in {2,4,8})
+constexpr int MASS_THREADS = 64;
+JM_HD constexpr Plan plan_mass(int d, int q) {
+  return Plan{(int)Tile::Generic, MASS_THREADS, MASS_THREADS,
+              2 * stage_bytes(MASS_THREADS, d, 8) + stage_bytes(MASS_THREADS, q, 8) + rup(q * d * 8, 16), 1};
+}
+
 // ---- GENERIC (runtime N; AoT) ----
 constexpr int GENERIC_THREADS = 256;
 JM_HD constexpr int generic_mpc(int n) { return (n * n >= GENERIC_THREADS) ? 1 : GENERIC_THREADS / (n * n); }

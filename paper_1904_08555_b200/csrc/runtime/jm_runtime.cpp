@@ -185,6 +185,7 @@ struct Slot {
 constexpr int NKIND = 3, NADD = 2, NDT = 2, NMAX = JM_N_MAX;
 Slot g_slots[NKIND][NADD][NDT][NMAX + 1];
 Slot g_mm_slots[2][NDT][NMAX + 1];     // multiply-accumulate: [specialized|generic][dtype][n]
+Slot g_mass_slots[2][jm::MASS_MAX + 1][jm::MASS_MAX + 1];   // Laghos mass action: [kind][D][Q]
 
 struct State {
   std::mutex mu;
@@ -305,14 +306,24 @@ int finish_function(Slot &s, CUfunction fn) {
 
 // ops: the Eigen-benchmark update (k_update) and the batched multiply-accumulate
 // of the RAJA benchmark (k_matmul, Listing 8)
-enum { OP_UPDATE = 0, OP_MATMUL = 1 };
+enum { OP_UPDATE = 0, OP_MATMUL = 1, OP_MASS = 2 };
 
-jm::Plan plan_for(int op, int n, int dtype) {
-  return op == OP_MATMUL ? jm::plan_matmul(n, dtype) : jm::plan_specialized(n, dtype);
+// (for OP_MASS: n = D = NUM_DOFS_1D, extra = Q = NUM_QUAD_1D)
+jm::Plan plan_for(int op, int n, int dtype, int extra) {
+  return op == OP_MATMUL ? jm::plan_matmul(n, dtype)
+         : op == OP_MASS ? jm::plan_mass(n, extra)
+                         : jm::plan_specialized(n, dtype);
+}
+
+std::string mass_name_expression(int d, int q) {
+  char buf[64];
+  snprintf(buf, sizeof buf, "jm::k_mass<%d, %d>", d, q);
+  return buf;
 }
 
 // Load a specialized cubin into a slot (after NVRTC, or from an imported blob).
-int install_cubin(Slot &s, int op, int n, int dtype, std::vector<char> &&cubin, const std::string &lowered) {
+int install_cubin(Slot &s, int op, int n, int dtype, int extra, std::vector<char> &&cubin,
+                  const std::string &lowered) {
   int rc = ensure_ctx();
   if (rc != JM_OK) return rc;
   CUmodule mod = nullptr;
@@ -330,7 +341,7 @@ int install_cubin(Slot &s, int op, int n, int dtype, std::vector<char> &&cubin, 
     s.err = t_err;
     return JM_E_COMPILE;
   }
-  s.plan = plan_for(op, n, dtype);
+  s.plan = plan_for(op, n, dtype, extra);
   s.mod = mod;
   s.cubin_bytes = (long long)cubin.size();
   rc = finish_function(s, fn);
@@ -350,13 +361,15 @@ int compile_slot(Slot &s, int op, int n, int dtype, int addend) {
   c_compilations++;
   std::vector<char> cubin;
   std::string lowered, log;
-  const std::string expr = op == OP_MATMUL ? mm_name_expression(n, dtype) : name_expression(n, dtype, addend);
+  const std::string expr = op == OP_MATMUL ? mm_name_expression(n, dtype)
+                           : op == OP_MASS ? mass_name_expression(n, addend)
+                                           : name_expression(n, dtype, addend);
   int rc = nvrtc_compile_expr(expr, cubin, lowered, log);
   if (rc != JM_OK) {
     s.err = log;
     return fail(rc, "%s", log.c_str());
   }
-  if ((rc = install_cubin(s, op, n, dtype, std::move(cubin), lowered)) != JM_OK) return rc;
+  if ((rc = install_cubin(s, op, n, dtype, addend, std::move(cubin), lowered)) != JM_OK) return rc;
   const double ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   s.compile_ms = ms;
@@ -377,6 +390,8 @@ int check_key(int n, int dtype, int addend, int kind) {
   return JM_OK;
 }
 
+int acquire_slot(Slot &s, int op, int n, int dtype, int addend, int kind, Slot **out);
+
 // Algorithm 1 (PAPER.md:319 lookup, :347 store) with per-key once semantics.
 int lookup_op(int op, int n, int dtype, int addend, int kind, Slot **out) {
   int rc = check_key(n, dtype, addend, kind);
@@ -385,6 +400,13 @@ int lookup_op(int op, int n, int dtype, int addend, int kind, Slot **out) {
   if (op == OP_MATMUL && kind == JM_KIND_AOT_SPECIALIZED)
     return fail(JM_E_UNSUPPORTED, "no ahead-of-time specialization of the multiply-accumulate");
   Slot &s = op == OP_MATMUL ? g_mm_slots[kind][dtype][n] : g_slots[kind][addend][dtype][n];
+  return acquire_slot(s, op, n, dtype, addend, kind, out);
+}
+
+// The slot state machine of Algorithm 1 (hit: one acquire load; miss: the
+// slot's mutex, then compile once).  For OP_MASS, n = D and `addend` = Q.
+int acquire_slot(Slot &s, int op, int n, int dtype, int addend, int kind, Slot **out) {
+  int rc = JM_OK;
   int st = s.state.load(std::memory_order_acquire);
   if (st == S_READY) {
     c_hits++;
@@ -694,6 +716,17 @@ int jit_mat_init(int device) {
         if ((rc = finish_function(s, mmg[dt])) != JM_OK) return rc;
         s.state.store(S_READY, std::memory_order_release);
       }
+    CUfunction mg = nullptr;
+    CU_TRY(D.ModuleGetFunction(&mg, G.aot, "jm_mass_generic"), "jm_mass_generic");
+    for (int d = 1; d <= jm::MASS_MAX; ++d)
+      for (int q = 1; q <= jm::MASS_MAX; ++q) {
+        Slot &s = g_mass_slots[JM_KIND_GENERIC][d][q];
+        s.plan = jm::Plan{(int)jm::Tile::Generic, jm::MASS_THREADS, jm::MASS_THREADS,
+                          jm::MASS_THREADS * (2 * d * d + q * q) * 8 + q * d * 8, 1};
+        s.cubin_bytes = (long long)jm_embedded_aot_cubin_len;
+        if ((rc = finish_function(s, mg)) != JM_OK) return rc;
+        s.state.store(S_READY, std::memory_order_release);
+      }
   }
   CU_TRY(D.MemAlloc(&G.sum_buf, 16), "cuMemAlloc(checksum)");
   seed_generic_slots();
@@ -728,6 +761,9 @@ int jit_mat_shutdown(void) {
   for (int k = 0; k < 2; ++k)
     for (int t = 0; t < NDT; ++t)
       for (int n = 0; n <= NMAX; ++n) reset(g_mm_slots[k][t][n]);
+  for (int k = 0; k < 2; ++k)
+    for (int d = 0; d <= jm::MASS_MAX; ++d)
+      for (int q = 0; q <= jm::MASS_MAX; ++q) reset(g_mass_slots[k][d][q]);
   {
     std::lock_guard<std::mutex> hl(G.host_mu);
     for (int i = 0; i < 3; ++i) {
@@ -829,7 +865,7 @@ int jit_mat_cache_import(const void *blob, size_t len) {
   std::lock_guard<std::mutex> lk(s.mu);
   if (s.state.load(std::memory_order_acquire) == S_READY) return JM_OK;
   std::vector<char> cubin(p, p + cl);
-  if ((rc = install_cubin(s, OP_UPDATE, key[0], key[1], std::move(cubin), lowered)) != JM_OK) return rc;
+  if ((rc = install_cubin(s, OP_UPDATE, key[0], key[1], key[2], std::move(cubin), lowered)) != JM_OK) return rc;
   s.compile_ms = 0.0;
   c_imports++;
   s.state.store(S_READY, std::memory_order_release);
@@ -997,12 +1033,20 @@ const char *jit_mat_version(void) {
 // Test hook: NVRTC-compile a key without a device (no module load).  Lets the
 // CPU-only test tier prove every specialization compiles for sm_100a.
 int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes) {
-  int rc = check_key(n, dtype, addend == JM_OP_MATMUL ? JM_ADDEND_ONES : addend, JM_KIND_SPECIALIZED);
-  if (rc != JM_OK) return rc;
+  int rc = JM_OK;
+  std::string expr;
+  if (addend == JM_OP_MASS) {   // n = dofs, dtype = quads
+    if (n < 1 || dtype < 1 || n > jm::MASS_MAX || dtype > jm::MASS_MAX)
+      return fail(JM_E_UNSUPPORTED, "dofs/quads must be in [1, %d]", jm::MASS_MAX);
+    expr = mass_name_expression(n, dtype);
+  } else {
+    rc = check_key(n, dtype, addend == JM_OP_MATMUL ? JM_ADDEND_ONES : addend, JM_KIND_SPECIALIZED);
+    if (rc != JM_OK) return rc;
+    expr = addend == JM_OP_MATMUL ? mm_name_expression(n, dtype) : name_expression(n, dtype, addend);
+  }
   std::vector<char> cubin;
   std::string lowered, log;
-  rc = nvrtc_compile_expr(addend == JM_OP_MATMUL ? mm_name_expression(n, dtype) : name_expression(n, dtype, addend),
-                          cubin, lowered, log);
+  rc = nvrtc_compile_expr(expr, cubin, lowered, log);
   if (rc != JM_OK) return fail(rc, "%s", log.c_str());
   if (cubin_bytes) *cubin_bytes = (long long)cubin.size();
   return JM_OK;
@@ -1039,6 +1083,45 @@ int jit_mat_matmul(int n, int dtype, int kind, int64_t batch, const void *a, con
   CU_TRY(D.LaunchKernel(s->fn, grid, 1, 1, (unsigned)s->plan.threads, 1, 1, (unsigned)s->plan.smem, st,
                         kind == JM_KIND_GENERIC ? args_gen : args_spec, nullptr),
          "cuLaunchKernel(matmul)");
+  c_launches++;
+  return sync_if(0, st);
+}
+
+int jit_mat_mass(int dofs, int quads, int kind, int64_t elements, const double *B, const double *op,
+                 const double *x, double *y, void *stream) {
+  if (dofs < 1 || quads < 1) return fail(JM_E_INVALID, "dofs and quads must be >= 1");
+  if (dofs > jm::MASS_MAX || quads > jm::MASS_MAX)
+    return fail(JM_E_UNSUPPORTED, "dofs/quads up to %d supported (got %d, %d)", jm::MASS_MAX, dofs, quads);
+  if (kind != JM_KIND_SPECIALIZED && kind != JM_KIND_GENERIC)
+    return fail(kind == JM_KIND_AOT_SPECIALIZED ? JM_E_UNSUPPORTED : JM_E_INVALID, "kind %d not available", kind);
+  if (elements < 0) return fail(JM_E_INVALID, "elements must be >= 0");
+  if (!G.inited.load(std::memory_order_acquire)) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
+  if (elements == 0) return JM_OK;
+  if (!B || !op || !x || !y) return fail(JM_E_INVALID, "NULL buffer");
+  if (((unsigned long long)op | (unsigned long long)x | (unsigned long long)y) & 15)
+    return fail(JM_E_ALIGN, "op/x/y must be 16-byte aligned");
+  const unsigned long long yb = (unsigned long long)elements * dofs * dofs * 8, py = (unsigned long long)y;
+  const unsigned long long spans[3][2] = {{(unsigned long long)x, yb},
+                                          {(unsigned long long)op, (unsigned long long)elements * quads * quads * 8},
+                                          {(unsigned long long)B, (unsigned long long)dofs * quads * 8}};
+  for (auto &sp : spans)
+    if (sp[0] < py + yb && py < sp[0] + sp[1]) return fail(JM_E_INVALID, "y must not overlap B, op or x");
+  Slot *s = nullptr;
+  int rc = acquire_slot(g_mass_slots[kind][dofs][quads], OP_MASS, dofs, JM_F64, quads, kind, &s);
+  if (rc != JM_OK) return rc;
+  if ((rc = ensure_ctx()) != JM_OK) return rc;
+  CUstream st = (CUstream)(stream ? stream : G.stream.load(std::memory_order_relaxed));
+  const long long mpc = s->plan.mpc;
+  const long long nchunks = (elements + mpc - 1) / mpc;
+  const unsigned grid = (unsigned)(nchunks < s->grid_cap ? nchunks : s->grid_cap);
+  CUdeviceptr pb = (CUdeviceptr)B, po = (CUdeviceptr)op, px = (CUdeviceptr)x, pyy = (CUdeviceptr)y;
+  long long ne = elements;
+  int dd = dofs, qq = quads;
+  void *args_spec[] = {&pb, &po, &px, &pyy, &ne};
+  void *args_gen[] = {&pb, &po, &px, &pyy, &ne, &dd, &qq};
+  CU_TRY(D.LaunchKernel(s->fn, grid, 1, 1, (unsigned)s->plan.threads, 1, 1, (unsigned)s->plan.smem, st,
+                        kind == JM_KIND_GENERIC ? args_gen : args_spec, nullptr),
+         "cuLaunchKernel(mass)");
   c_launches++;
   return sync_if(0, st);
 }
