@@ -361,11 +361,9 @@ __device__ __forceinline__ void dmma884_c(double &d0, double &d1, double a, doub
       : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }
 
-// byte offset of 16-B chunk `cc` of row `r` in the swizzled scratch
-template <int RSC>
-__device__ __forceinline__ int scr_off(int r, int cc) {
-  return (r * RSC + (cc ^ ((r & 6) ^ ((r & 1) << 2)))) * 16;
-}
+// Scratch layout: 16-B chunk `cc` of row `r` lives at byte
+//   (r * RSC + (cc ^ ((r & 6) ^ ((r & 1) << 2)))) * 16
+// (run_dmma precomputes this as lane constants + immediates: bofs / pofs).
 
 template <int N, Addend A, int W>
 __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *__restrict__ out,
@@ -385,6 +383,21 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   const int wr = (W == 1) ? 0 : warp;        // this warp's rank within the matrix
   char *scr = smem + (PF ? 2 : 1) * stage_bytes(MPC, N, 8) + ((W == 1) ? warp * SCR : 0);
   const double c = 0.00005;
+  // Swizzled-scratch offsets factored into a few lane constants plus
+  // compile-time immediates (chunk c ^ f only touches c's low 3 bits, and the
+  // row swizzle f depends on the row mod 8 alone):
+  //   B fragment, k-step (J,s), column tile J2:  bofs[s][J2&1] + (8J*RSC + 8(J2>>1))*16
+  //   publish, own row tile I, column tile J:    pofs[J&1] + (8I*RSC + 8(J>>1))*16
+  // so ptxas keeps 6 registers of addresses instead of one per (J, s, J2).
+  const int gh = g >> 1, gl = g & 1, fg = (g & 6) ^ ((g & 1) << 2);
+  int bofs[2][2], pofs[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int j1 = 0; j1 < 2; ++j1)
+      bofs[s][j1] = ((2 * t + s) * RSC + ((j1 * 4 + gh) ^ (2 * t ^ (s << 2)))) * 16 + 8 * gl;
+#pragma unroll
+  for (int j1 = 0; j1 < 2; ++j1) pofs[j1] = ((8 * wr * RT + g) * RSC + ((j1 * 4 + t) ^ fg)) * 16;
 
   Stager<N, ES, SB, NT, MPC, AL, PF> sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
@@ -410,7 +423,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
         for (int I = 0; I < RT; ++I)
 #pragma unroll
           for (int J = 0; J < T8; ++J)
-            sts_f64x2(sb + scr_off<RSC>(8 * (wr * RT + I) + g, 4 * J + t), acc[I][J][0], acc[I][J][1]);
+            sts_f64x2(sb + pofs[J & 1] + (8 * I * RSC + 8 * (J >> 1)) * 16, acc[I][J][0], acc[I][J][1]);
         if constexpr (W == 1) __syncwarp(); else __syncthreads();
         double p[RT][T8][2];
 #pragma unroll
@@ -421,8 +434,8 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
             double b[T8];
 #pragma unroll
             for (int J2 = 0; J2 < T8; ++J2)
-              b[J2] = *reinterpret_cast<const double *>(
-                  sb + scr_off<RSC>(8 * J + 2 * t + s, 4 * J2 + (g >> 1)) + 8 * (g & 1));
+              b[J2] = *reinterpret_cast<const double *>(sb + bofs[s][J2 & 1] +
+                                                        (8 * J * RSC + 8 * (J2 >> 1)) * 16);
 #pragma unroll
             for (int I = 0; I < RT; ++I)
 #pragma unroll
