@@ -72,6 +72,9 @@ JM_HD constexpr int f64p_mbuf(int n) { return n * f64p_ncs(n) * 16 + 32; }
 constexpr int TPM_THREADS = 128;
 
 // ---- DMMA (FP64) ----
+#ifndef JM_DMMA_WARP_MAX
+#define JM_DMMA_WARP_MAX 32  // whole matrix in one warp up to this n
+#endif
 #ifndef JM_DMMA_RT_LARGE
 #define JM_DMMA_RT_LARGE 1   // row tiles per warp for n > 32 (one warp per 8-row tile)
 #endif
@@ -83,7 +86,7 @@ JM_HD constexpr int dmma_t8(int n) { return cdiv(n, 8); }
 // per warp otherwise (r01 sweep: n=48 0.69 -> 0.72 of the FP64 pipe with one
 // tile per warp, n=64 0.92 with two vs 0.87 with one).
 JM_HD constexpr int dmma_rt(int n) {
-  return n <= 24 ? dmma_t8(n) : ((n <= 32 || dmma_t8(n) == 8) ? 2 : JM_DMMA_RT_LARGE);
+  return n <= JM_DMMA_WARP_MAX ? dmma_t8(n) : ((n <= 32 || dmma_t8(n) == 8) ? 2 : JM_DMMA_RT_LARGE);
 }
 JM_HD constexpr int dmma_w(int n) { return dmma_t8(n) / dmma_rt(n); }
 JM_HD constexpr int dmma_rsc(int n) { return rup(4 * dmma_t8(n), 8); }     // scratch row stride, 16-B chunks
