@@ -1,6 +1,6 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider -k "f64" > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
-timeout 900 python tools/sweep.py --only c3 --sizes 24,25,28,32 --dtypes f64 --out gpurun_out/sweep_w1.jsonl > /dev/null 2>&1; python -c "
-import json
-for l in open('gpurun_out/sweep_w1.jsonl'):
-    d=json.loads(l)
-    s=d['specialized']; print(d['n'], d['dtype'], d['repeat'], d['tile'], d['regs'], d['smem'], round(s['ms'],2), round(s['tflops'],2), 'pipe', round(s['frac_pipe'],3), 'hbm', round(s['frac_hbm'],3))"
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
+timeout 1200 python tools/sweep.py --out gpurun_out/sweep_r01d.jsonl > gpurun_out/sweep_d.log 2>&1; wc -l gpurun_out/sweep_r01d.jsonl
+python bench.py > gpurun_out/bench4.log 2> gpurun_out/bench4.err; tail -c 1500 gpurun_out/bench4.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2b.csv python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_update -s 3 -c 1 -o gpurun_out/prof_c2b python bench.py --steps 2 --warmup 3 --no-generic --no-e2e --no-cpu > /dev/null 2>&1
+ls gpurun_out/*c2b*
