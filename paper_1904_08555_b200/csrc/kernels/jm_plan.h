@@ -181,8 +181,44 @@ JM_HD constexpr bool aot_spec_available(int n, int dtype) {
 // ---- batched multiply-accumulate (Listing 8) ----
 constexpr int MM_THREADS = 256;
 JM_HD constexpr int mm_mpc(int n) { return (n * n >= MM_THREADS) ? 1 : MM_THREADS / (n * n); }
+// Specialized multiply-accumulate: a bulk-copy (TMA, cp.async.bulk) ring of
+// MM_STAGES chunk buffers, each holding MPC packed matrices of A, B and C.  A
+// chunk's byte count must be a multiple of 16, so MPC is a multiple of
+// 16 / gcd(MB, 16); about MM_CHUNK_BYTES per operand per chunk.
+constexpr int MM_CHUNK_BYTES = 8192;
+constexpr int MM_STAGES_MAX = 4;
+constexpr int MM_SMEM_BUDGET = 200 * 1024;
+constexpr int MM_BAR_BYTES = 64;  // MM_STAGES_MAX mbarriers, padded
+JM_HD constexpr int mm_align_mult(int mb) { return (mb % 16 == 0) ? 1 : (mb % 8 == 0) ? 2 : 4; }
+JM_HD constexpr int mm_bulk_mpc(int n, int es) {
+  const int mb = n * n * es, m = mm_align_mult(mb);
+  const int k = (MM_CHUNK_BYTES / mb) / m * m;
+  return k > 0 ? k : m;
+}
+JM_HD constexpr int mm_bulk_stages(int n, int es) {
+  const int s = MM_SMEM_BUDGET / (3 * mm_bulk_mpc(n, es) * n * n * es);
+  return s > MM_STAGES_MAX ? MM_STAGES_MAX : s;
+}
+// sizes whose chunk ring does not fit twice (large odd n) keep the staged path
+JM_HD constexpr bool mm_bulk(int n, int es) { return mm_bulk_stages(n, es) >= 2; }
+// Small batches (fewer full chunks than SMs) are latency-bound: the ring would
+// leave most SMs idle, so the kernel computes straight from global memory over
+// the whole grid instead and is launched without the ring's shared memory.
+constexpr int MM_DIRECT_CHUNKS = 148;
+JM_HD constexpr bool mm_direct(long long batch, int n, int es) {
+  return !mm_bulk(n, es) ? false : batch < (long long)MM_DIRECT_CHUNKS * mm_bulk_mpc(n, es);
+}
+constexpr int MM_DIRECT_GRID = 148 * 8;  // 2048 threads per SM
 JM_HD constexpr Plan plan_matmul(int n, int dtype) {
-  // A and B chunks staged packed; C is streamed by the owning threads
+  const int es = dtype == 1 ? 8 : 4;
+  if (mm_bulk(n, es)) {
+    const int mpc = mm_bulk_mpc(n, es);
+    return Plan{(int)Tile::Generic, MM_THREADS, mpc, mm_bulk_stages(n, es) * 3 * mpc * n * n * es + MM_BAR_BYTES, 1};
+  }
+  return Plan{(int)Tile::Generic, MM_THREADS, mm_mpc(n), 2 * stage_bytes(mm_mpc(n), n, es), 1};
+}
+// the AoT generic (runtime n) kernel: A and B staged per chunk, C streamed
+JM_HD constexpr Plan plan_matmul_generic(int n, int dtype) {
   return Plan{(int)Tile::Generic, MM_THREADS, mm_mpc(n), 2 * stage_bytes(mm_mpc(n), n, dtype == 1 ? 8 : 4), 1};
 }
 

@@ -711,7 +711,7 @@ int jit_mat_init(int device) {
     for (int dt = 0; dt < NDT; ++dt)
       for (int n = 1; n <= NMAX; ++n) {
         Slot &s = g_mm_slots[JM_KIND_GENERIC][dt][n];
-        s.plan = jm::plan_matmul(n, dt);
+        s.plan = jm::plan_matmul_generic(n, dt);
         s.cubin_bytes = (long long)jm_embedded_aot_cubin_len;
         if ((rc = finish_function(s, mmg[dt])) != JM_OK) return rc;
         s.state.store(S_READY, std::memory_order_release);
@@ -1074,13 +1074,21 @@ int jit_mat_matmul(int n, int dtype, int kind, int64_t batch, const void *a, con
   CUstream st = (CUstream)(stream ? stream : G.stream.load(std::memory_order_relaxed));
   const long long mpc = s->plan.mpc;
   const long long nchunks = (batch + mpc - 1) / mpc;
-  const unsigned grid = (unsigned)(nchunks < s->grid_cap ? nchunks : s->grid_cap);
+  unsigned grid = (unsigned)(nchunks < s->grid_cap ? nchunks : s->grid_cap);
+  unsigned smem = (unsigned)s->plan.smem;
+  const int es = dtype == JM_F64 ? 8 : 4;
+  if (kind != JM_KIND_GENERIC && jm::mm_direct(batch, n, es)) {
+    // small batch: the kernel's grid-wide direct path, no bulk-copy ring
+    const long long blocks = (batch * n * n + jm::MM_THREADS - 1) / jm::MM_THREADS;
+    grid = (unsigned)(blocks < jm::MM_DIRECT_GRID ? blocks : jm::MM_DIRECT_GRID);
+    smem = 0;
+  }
   CUdeviceptr pa = (CUdeviceptr)a, pb = (CUdeviceptr)b, pcc = (CUdeviceptr)c;
   long long bt = batch;
   int nn = n;
   void *args_spec[] = {&pa, &pb, &pcc, &bt};
   void *args_gen[] = {&pa, &pb, &pcc, &bt, &nn};
-  CU_TRY(D.LaunchKernel(s->fn, grid, 1, 1, (unsigned)s->plan.threads, 1, 1, (unsigned)s->plan.smem, st,
+  CU_TRY(D.LaunchKernel(s->fn, grid, 1, 1, (unsigned)s->plan.threads, 1, 1, smem, st,
                         kind == JM_KIND_GENERIC ? args_gen : args_spec, nullptr),
          "cuLaunchKernel(matmul)");
   c_launches++;

@@ -99,3 +99,21 @@ def test_lookup_hit_cost_is_small(jm):
     jm.jit_mat_prepare(16, "double")
     ns = jm.jit_mat_time_lookup(16, "double", iters=200_000)
     assert 0 < ns < 1000, ns
+
+
+@pytest.mark.parametrize("n,dt,batch", [(2, "f64", (1 << 20) + 13), (8, "f32", 300_001), (16, "f64", 60_007),
+                                        (33, "f32", 2_003), (1, "f32", 5_000_001), (64, "f64", 701),
+                                        (63, "f64", 301), (63, "f32", 150)])
+def test_matmul_bulk_ring_wraps(jm, n, dt, batch):
+    """Batches large enough that every CTA cycles its bulk-copy ring many times
+    (chunks per CTA >> MM_STAGES) plus a ragged tail; checked on a sample of
+    matrices (each matrix is independent, R16) including the first, the last and
+    the whole tail.  n = 63 has no ring (chunk too large): the staged loop."""
+    a, b, c = _inputs(n, dt, batch, 55 + n)
+    ta, tb, tc = (torch.from_numpy(x).cuda() for x in (a, b, c))
+    jm.matmul(ta, tb, tc, sync=True)
+    rng = np.random.default_rng(n)
+    idx = np.unique(np.concatenate([rng.integers(0, batch, 2000), np.arange(max(0, batch - 300), batch), [0]]))
+    got = tc[torch.from_numpy(idx).cuda()].cpu().numpy()
+    want = oracle.matmul_acc(c[idx], a[idx], b[idx])
+    assert_mm_parity(got, want, a[idx], b[idx], c[idx], what=f"bulk ring n={n} {dt} batch={batch}")

@@ -1,2 +1,3 @@
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 5 --warmup 3 --no-cpu > gpurun_out/torchrun1.log 2> gpurun_out/torchrun1.err; echo rc=$?; tail -c 600 gpurun_out/torchrun1.log; tail -3 gpurun_out/torchrun1.err
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29534 bench.py --impl reference --gpus 1 --steps 3 --warmup 1 > gpurun_out/torchrun_ref.log 2>&1; echo rc=$?; tail -c 400 gpurun_out/torchrun_ref.log
+set -x
+timeout 900 python -m pytest tests/test_gpu_matmul.py -x -q 2>&1 | tail -15
+timeout 600 python tools/matmul_bench.py --out gpurun_out/matmul.jsonl > gpurun_out/matmul.log 2>&1; echo rc=$?; grep HBM gpurun_out/matmul.jsonl
