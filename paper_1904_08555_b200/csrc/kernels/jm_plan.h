@@ -92,16 +92,58 @@ JM_HD constexpr int dmma_w(int n) { return dmma_t8(n) / dmma_rt(n); }
 JM_HD constexpr int dmma_rsc(int n) { return rup(4 * dmma_t8(n), 8); }     // scratch row stride, 16-B chunks
 JM_HD constexpr int dmma_scr(int n) { return 8 * dmma_t8(n) * dmma_rsc(n) * 16; }  // one scratch buffer
 
-// ---- F32 tiles ----
-JM_HD constexpr int f32_w(int n) { return n <= 32 ? 1 : 4; }
-constexpr int F32_WPC = 4;                        // warps per CTA when W == 1
-JM_HD constexpr int f32_rg(int n) { return f32_w(n) == 1 ? 8 : 16; }   // thread rows
-JM_HD constexpr int f32_cg(int n) { return f32_w(n) == 1 ? 4 : 8; }    // thread cols
-JM_HD constexpr int f32_ra(int n) { return cdiv(n, f32_rg(n)); }       // rows per thread
-JM_HD constexpr int f32_cb(int n) { return rup(cdiv(n, f32_cg(n)), 2); }  // cols per thread (even: FFMA2)
-JM_HD constexpr int f32_ldm(int n) { return f32_cg(n) * f32_cb(n) + 4; }  // sM row stride (floats)
-JM_HD constexpr int f32_ldt(int n) { return f32_rg(n) * f32_ra(n) + 4; }  // sMT row stride (floats)
-JM_HD constexpr int f32_buf(int n) { return n * (f32_ldm(n) + f32_ldt(n)) * 4; }  // one M + M^T buffer
+// ---- F32 tiles (17 <= n <= 64) ----
+// RG x CG threads per matrix, each owning an RA x CB block of P (RA <= 8,
+// CB <= 16, CB a multiple of 4) in registers; padding rows/columns are
+// computed and discarded.  Only M itself is published to shared memory
+// (row-major, row stride LDM): the A operand M[i][k..k+3] is one 16-B load per
+// owned row per four k steps, the B operand is row k (16-B pieces).  Shared
+// memory traffic per FFMA2 is what bounds these tiles (sm_100a: an LDS.128
+// costs 2.7-4 SM clocks, r01_microbench_lds_patterns.json), hence the large
+// 8 x 16 register tiles.  Whole matrices per warp: 32 / (RG*CG) of them.
+// The tile is chosen per n by a small model: useful / padded FMAs x used lanes
+// x min(1, FMA clocks / LDS clocks), with an LDS.128 costing ~4.5 SM clocks
+// per warp in context and an FFMA2 0.5; accumulators + operands <= 200 regs.
+struct F32Tile {
+  int rg, ra, cg, cb;
+};
+JM_HD constexpr F32Tile f32_tile(int n) {
+  F32Tile best{cdiv(n, 8), cdiv(n, cdiv(n, 8)), cdiv(n, 16), rup(cdiv(n, cdiv(n, 16)), 4)};
+  double bs = -1.0;
+  for (int ra = 8; ra >= 2; --ra)
+    for (int cb = 16; cb >= 4; cb -= 4) {
+      const int rg = cdiv(n, ra), cg = cdiv(n, cb), t = rg * cg;
+      if (t > 32 || ra * cb + 4 * ra + 2 * cb > 200) continue;
+      const double pad = (double)n * n * n / ((double)(rg * ra) * (cg * cb) * rup(n, 4));
+      const double lane = (double)((32 / t) * t) / 32.0;
+      double lsu = (double)(ra * cb) / (4.5 * (ra + cb));
+      if (lsu > 1.0) lsu = 1.0;
+      const double sc = pad * lane * lsu;
+      if (sc > bs + 1e-9) {
+        bs = sc;
+        best = F32Tile{rg, ra, cg, cb};
+      }
+    }
+  return best;
+}
+JM_HD constexpr int f32_rg(int n) { return f32_tile(n).rg; }   // thread rows
+JM_HD constexpr int f32_ra(int n) { return f32_tile(n).ra; }   // rows per thread
+JM_HD constexpr int f32_cg(int n) { return f32_tile(n).cg; }   // thread cols
+JM_HD constexpr int f32_cb(int n) { return f32_tile(n).cb; }   // cols per thread
+JM_HD constexpr int f32_tpm(int n) { return f32_rg(n) * f32_cg(n); }      // threads per matrix
+JM_HD constexpr int f32_mpw(int n) { return 32 / f32_tpm(n); }            // matrices per warp
+constexpr int F32_WPC = 2;                                                // warps per CTA
+JM_HD constexpr int f32_rows(int n) { return f32_rg(n) * f32_ra(n); }     // padded rows
+JM_HD constexpr int f32_cols(int n) { return f32_cg(n) * f32_cb(n); }     // padded cols
+JM_HD constexpr int f32_kp(int n) { return rup(n, 4); }                   // k steps (blocks of 4)
+JM_HD constexpr int f32_srows(int n) { return f32_rows(n) > f32_kp(n) ? f32_rows(n) : f32_kp(n); }
+// row stride in floats: LDM / 4 odd, so eight consecutive rows' 16-B A loads
+// fall in eight different 16-B bank groups
+JM_HD constexpr int f32_ldm(int n) { return f32_cols(n) + (((f32_cols(n) / 4) % 2 == 0) ? 4 : 8); }
+// one matrix region: holds the staged matrix, then the published M
+JM_HD constexpr int f32_region(int n) {
+  return rup(f32_srows(n) * f32_ldm(n) * 4 > n * n * 4 ? f32_srows(n) * f32_ldm(n) * 4 : n * n * 4, 16);
+}
 
 // ---- F32 row panels (9 <= n <= 32) ----
 // A thread owns RP = 4 FULL rows of M (the A operand is local); row k of M
@@ -154,11 +196,9 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
     const int mpc = F32P_WPC * f32p_mpw(n);
     return Plan{(int)t, 32 * F32P_WPC, mpc, nst * stage_bytes(mpc, n, es) + 2 * mpc * f32p_mbuf(n), 1};
   }
-  const int w = f32_w(n);
-  if (w == 1)
-    return Plan{(int)t, 32 * F32_WPC, F32_WPC,
-                nst * stage_bytes(F32_WPC, n, es) + F32_WPC * f32_buf(n), 1};
-  return Plan{(int)t, 32 * w, 1, nst * stage_bytes(1, n, es) + 2 * f32_buf(n), w};
+  // F32 tiles: the stage area IS the per-matrix region (stride f32_region)
+  const int mpc = F32_WPC * f32_mpw(n);
+  return Plan{(int)t, 32 * F32_WPC, mpc, mpc * f32_region(n), 1};
 }
 
 // Which entry point the specialization uses: k_update (maxThreads only) or

@@ -750,133 +750,127 @@ __device__ __forceinline__ void run_f64p(const double *__restrict__ in, double *
 }
 
 // ======================================================================
-// F32: FP32 register-tiled outer products.  The RG x CG threads of a matrix
-// each own an RA x CB block of M (registers).  Every update republishes M and
-// M^T to shared memory; then for k < N each thread reads RA values of column k
-// (a row of M^T) and CB values of row k (broadcast loads) and issues RA*CB/2
-// FFMA2.  W warps per matrix (W == 1 for N <= 32).
+// F32 (17 <= n <= 64): FP32 register-tiled outer products with FFMA2.  The
+// RG x CG threads of a matrix each own an RA x CB block of P = M + M*M in
+// registers (the accumulators start at M, so P is the only state); thread
+// (tr, tc) owns rows i*RG + tr and columns in 16-B pieces (h*CG + tc)*4.
+// Every update republishes M row-major into the matrix's shared-memory region
+// (the region the chunk was staged into); then per block of four k steps a
+// thread loads M[row][k..k+3] for its RA rows (one LDS.128 each) and, one k
+// ahead of the math, row k's CB/4 pieces, and issues RA*CB/2 FFMA2 per k.
+// Steps k in [N, rup(N,4)) read zero padding (exact no-ops).  A warp holds
+// 32 / (RG*CG) whole matrices, so only __syncwarp is needed.
 // ======================================================================
-template <int N, Addend A, int W>
+template <int N, Addend A>
 __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__restrict__ out,
                                         long long batch, int repeat) {
-  constexpr int RG = f32_rg(N), CG = f32_cg(N), RA = f32_ra(N), CB = f32_cb(N);
-  constexpr int LDM = f32_ldm(N), LDT = f32_ldt(N), BUF = f32_buf(N);
-  constexpr int ES = 4, MB = N * N * 4, SB = stage_stride(N, 4);
-  constexpr int WPC = (W == 1) ? F32_WPC : W;
-  constexpr int NT = 32 * WPC;
-  constexpr int MPC = (W == 1) ? F32_WPC : 1;
+  constexpr int RG = f32_rg(N), RA = f32_ra(N), CG = f32_cg(N), CB = f32_cb(N);
+  constexpr int TPMAT = RG * CG, MPW = f32_mpw(N);
+  constexpr int ROWS = f32_rows(N), COLS = f32_cols(N), KP = f32_kp(N), SROWS = f32_srows(N);
+  constexpr int LDM = f32_ldm(N), REG = f32_region(N);
+  constexpr int ES = 4, MB = N * N * 4;
+  constexpr int NT = 32 * F32_WPC, MPC = F32_WPC * MPW;
   constexpr bool AL = ((MPC * MB) % 16) == 0;
-  static_assert(RG * CG == 32 * W, "thread grid must match the warps per matrix");
-  static_assert(CB % 2 == 0, "FFMA2 needs column pairs");
-  constexpr bool PF = prefetch_for(N, 0);
+  constexpr bool PAD = (ROWS != N) || (COLS != N);
+  static_assert(CB % 4 == 0 && MPW >= 1, "tile shape");
   extern __shared__ __align__(16) char smem[];
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int mi = (W == 1) ? warp : 0;
-  const int tr = (W == 1) ? (tid & 31) : tid;   // rank within the matrix
-  const int r0 = (tr / CG) * RA, c0 = (tr % CG) * CB;
-  char *bufs = smem + (PF ? 2 : 1) * stage_bytes(MPC, N, 4) + ((W == 1) ? warp * BUF : 0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = lane / TPMAT, t = lane - m * TPMAT;
+  const int tr = t % RG, tc = t / RG;
+  const int mi = warp * MPW + m;
   const float c = float(0.00005);
+  auto row_of = [&](int i) { return i * RG + tr; };
+  auto col_of = [&](int j) { return ((j >> 2) * CG + tc) * 4 + (j & 3); };
 
-  Stager<N, ES, SB, NT, MPC, AL, PF> sg(in, out, batch, smem);
+  Stager<N, ES, REG, NT, MPC, AL, false> sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
-    char *stage = sg.buf();
-    const int cnt = sg.cnt();
-    if (mi < cnt) {
-      float *sm = reinterpret_cast<float *>(stage + mi * SB);
-      float m[RA][CB];
+    const bool live = (m < MPW) && (mi < sg.cnt());
+    float *sm = reinterpret_cast<float *>(sg.buf() + (m < MPW ? mi : 0) * REG);
+    float2 p[RA][CB / 2];
+    if (live) {
 #pragma unroll
       for (int i = 0; i < RA; ++i)
 #pragma unroll
-        for (int j = 0; j < CB; ++j) {
-          const int row = r0 + i, col = c0 + j;
-          m[i][j] = (row < N && col < N) ? sm[row * N + col] : 0.0f;
+        for (int j = 0; j < CB; j += 2) {
+          const int row = row_of(i), c0 = col_of(j), c1 = c0 + 1;
+          p[i][j / 2].x = (row < N && c0 < N) ? sm[row * N + c0] : 0.0f;
+          p[i][j / 2].y = (row < N && c1 < N) ? sm[row * N + c1] : 0.0f;
         }
-      for (int r = 0; r < repeat; ++r) {
-        float *sM = reinterpret_cast<float *>(bufs + ((W > 1) ? (r & 1) * BUF : 0));
-        float *sMT = sM + N * LDM;
-        // publish M (row blocks) and M^T (column blocks)
-#pragma unroll
-        for (int i = 0; i < RA; ++i)
-          if (r0 + i < N) {
-#pragma unroll
-            for (int j = 0; j < CB; j += 2)
-              *reinterpret_cast<float2 *>(sM + (r0 + i) * LDM + c0 + j) = make_float2(m[i][j], m[i][j + 1]);
-          }
-#pragma unroll
-        for (int j = 0; j < CB; ++j)
-          if (c0 + j < N) {
-            if constexpr (RA % 2 == 0) {
-#pragma unroll
-              for (int i = 0; i < RA; i += 2)
-                *reinterpret_cast<float2 *>(sMT + (c0 + j) * LDT + r0 + i) = make_float2(m[i][j], m[i + 1][j]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < RA; ++i) sMT[(c0 + j) * LDT + r0 + i] = m[i][j];
-            }
-          }
-        if constexpr (W == 1) __syncwarp(); else __syncthreads();
-        float2 p[RA][CB / 2];
+    }
+    __syncwarp();                        // staged matrix in registers: reuse the region as sM
+    if constexpr (SROWS > ROWS) {        // rows read as padding by k in [ROWS, KP): zero once
+      if (live)
+        for (int e = t; e < (SROWS - ROWS) * LDM; e += TPMAT) sm[ROWS * LDM + e] = 0.0f;
+    }
+    for (int r = 0; r < repeat; ++r) {
+      if (live) {
 #pragma unroll
         for (int i = 0; i < RA; ++i)
 #pragma unroll
-          for (int j = 0; j < CB / 2; ++j) p[i][j] = make_float2(m[i][2 * j], m[i][2 * j + 1]);
-#pragma unroll 4
-        for (int k = 0; k < N; ++k) {
-          float a[RA], b[CB];
-          if constexpr (RA % 4 == 0) {
-#pragma unroll
-            for (int i = 0; i < RA; i += 4) {
-              const float4 v = *reinterpret_cast<const float4 *>(sMT + k * LDT + r0 + i);
-              a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
-            }
-          } else if constexpr (RA % 2 == 0) {
-#pragma unroll
-            for (int i = 0; i < RA; i += 2) {
-              const float2 v = *reinterpret_cast<const float2 *>(sMT + k * LDT + r0 + i);
-              a[i] = v.x; a[i + 1] = v.y;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < RA; ++i) a[i] = sMT[k * LDT + r0 + i];
-          }
-          if constexpr (CB % 4 == 0) {
-#pragma unroll
-            for (int j = 0; j < CB; j += 4) {
-              const float4 v = *reinterpret_cast<const float4 *>(sM + k * LDM + c0 + j);
-              b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < CB; j += 2) {
-              const float2 v = *reinterpret_cast<const float2 *>(sM + k * LDM + c0 + j);
-              b[j] = v.x; b[j + 1] = v.y;
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < RA; ++i)
-#pragma unroll
-            for (int j = 0; j < CB / 2; ++j)
-              p[i][j] = __ffma2_rn(make_float2(a[i], a[i]), make_float2(b[2 * j], b[2 * j + 1]), p[i][j]);
-        }
-#pragma unroll
-        for (int i = 0; i < RA; ++i)
-#pragma unroll
-          for (int j = 0; j < CB; ++j) {
-            const int row = r0 + i, col = c0 + j;
-            const float pv = (j & 1) ? p[i][j / 2].y : p[i][j / 2].x;
-            const float a = (A == Addend::Ones || row == col) ? 1.0f : 0.0f;
-            float v = fmaT(c, pv, a);
-            m[i][j] = (row < N && col < N) ? v : 0.0f;
-          }
-        if constexpr (W == 1) __syncwarp();
+          for (int h = 0; h < CB / 4; ++h)
+            *reinterpret_cast<float4 *>(sm + row_of(i) * LDM + (h * CG + tc) * 4) =
+                make_float4(p[i][2 * h].x, p[i][2 * h].y, p[i][2 * h + 1].x, p[i][2 * h + 1].y);
       }
+      __syncwarp();
+      if (live) {
+        float b[CB], bn[CB];
+        auto load_b = [&](float (&dst)[CB], int k) {
+#pragma unroll
+          for (int h = 0; h < CB / 4; ++h) {
+            const float4 v = *reinterpret_cast<const float4 *>(sm + k * LDM + (h * CG + tc) * 4);
+            dst[4 * h] = v.x; dst[4 * h + 1] = v.y; dst[4 * h + 2] = v.z; dst[4 * h + 3] = v.w;
+          }
+        };
+        load_b(b, 0);
+#pragma unroll 1
+        for (int kb = 0; kb < KP; kb += 4) {
+          float4 av[RA];
+#pragma unroll
+          for (int i = 0; i < RA; ++i) av[i] = *reinterpret_cast<const float4 *>(sm + row_of(i) * LDM + kb);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const int kn = kb + kk + 1 < KP ? kb + kk + 1 : kb + kk;
+            load_b(bn, kn);              // next step's B row ahead of this step's math
+#pragma unroll
+            for (int i = 0; i < RA; ++i) {
+              const float a = kk == 0 ? av[i].x : kk == 1 ? av[i].y : kk == 2 ? av[i].z : av[i].w;
+#pragma unroll
+              for (int j = 0; j < CB / 2; ++j)
+                p[i][j] = __ffma2_rn(make_float2(a, a), make_float2(b[2 * j], b[2 * j + 1]), p[i][j]);
+            }
+#pragma unroll
+            for (int j = 0; j < CB; ++j) b[j] = bn[j];
+          }
+        }
+      }
+      __syncwarp();                      // all reads of this update done before the next publish
+      if (live) {
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+#pragma unroll
+          for (int j = 0; j < CB; j += 2) {
+            const int row = row_of(i), c0 = col_of(j), c1 = c0 + 1;
+            float2 &q = p[i][j / 2];
+            const float a0 = (A == Addend::Ones || row == c0) ? 1.0f : 0.0f;
+            const float a1 = (A == Addend::Ones || row == c1) ? 1.0f : 0.0f;
+            q.x = fmaT(c, q.x, a0);
+            q.y = fmaT(c, q.y, a1);
+            if constexpr (PAD) {         // padding stays exactly zero
+              if (row >= N || c0 >= N) q.x = 0.0f;
+              if (row >= N || c1 >= N) q.y = 0.0f;
+            }
+          }
+      }
+    }
+    if (live) {
 #pragma unroll
       for (int i = 0; i < RA; ++i)
 #pragma unroll
-        for (int j = 0; j < CB; ++j) {
-          const int row = r0 + i, col = c0 + j;
-          if (row < N && col < N) sm[row * N + col] = m[i][j];
+        for (int j = 0; j < CB; j += 2) {
+          const int row = row_of(i), c0 = col_of(j), c1 = c0 + 1;
+          if (row < N && c0 < N) sm[row * N + c0] = p[i][j / 2].x;
+          if (row < N && c1 < N) sm[row * N + c1] = p[i][j / 2].y;
         }
     }
     sg.release();
@@ -900,7 +894,7 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
   } else if constexpr (f32p_use(N)) {
     run_f32p<N, A>(in, out, batch, repeat);
   } else {
-    run_f32<N, A, f32_w(N)>(in, out, batch, repeat);
+    run_f32<N, A>(in, out, batch, repeat);
   }
 }
 

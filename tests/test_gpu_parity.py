@@ -96,6 +96,16 @@ def test_divergence_to_inf(jm, n, rep, kind):
         assert_parity(_gpu_run(jm, x, r, kind=kind), oracle.run(x, r), what=f"pre-divergence R={r}")
 
 
+@pytest.mark.parametrize("n", [17, 24, 32, 33, 48, 64])
+def test_f32_overflow_positions_match(jm, n):
+    # FP32 paper init overflows within a few updates at these n; the tiles pad
+    # to multiples of 8 / 4, and the padding must never leak NaN or inf into
+    # the real entries: every non-finite position must match the oracle's.
+    x = jm_synth.generate(n, "f32", "paper", 0, 0, 3)
+    for r in (1, 2, 4, 8, 16):
+        assert_parity(_gpu_run(jm, x, r), oracle.run(x, r), what=f"f32 paper n={n} R={r}")
+
+
 @pytest.mark.parametrize("dt", ["f64", "f32"])
 @pytest.mark.parametrize("n", [1, 3, 4, 5, 8, 16, 33, 64])
 def test_repeat_zero_is_bitwise_copy(jm, n, dt):
