@@ -97,6 +97,8 @@ enum {
 #define JM_FLAG_SYNC 1u          /* synchronize the stream before returning; report kernel faults */
 #define JM_FLAG_HOST_BUFFERS 2u  /* in/out are HOST pointers: the library stages them through
                                     device buffers it owns, chunked and overlapped (see run_host) */
+#define JM_FLAG_RESIDENT 4u      /* use the resident kernel whatever the repeat count (see VARIANT) */
+#define JM_FLAG_STREAMING 8u     /* use the streaming kernel where the kind has one (see VARIANT) */
 
 /* Initialise for `device` (-1 = the calling thread's current CUDA device, else
  * device 0).  Loads the CUDA driver, retains the device's primary context (the
@@ -110,7 +112,20 @@ JM_API int jit_mat_init(int device);
  * (n, dtype), addend Ones, on the stream set by jit_mat_set_stream (default:
  * the legacy default stream).  `in`/`out` are device pointers (16-byte
  * aligned) on the initialised device.  n in [1, 64]; batch >= 0 (0: no-op);
- * repeat in [0, 2^31) (0: out is a bitwise copy of in).  Asynchronous. */
+ * repeat in [0, 2^31) (0: out is a bitwise copy of in).  Asynchronous.
+ *
+ * VARIANT (every specialized entry point): where the tiling kind has one (the
+ * DMMA and FP32-tile kinds: f64 n >= 8, f32 n >= 9), a call whose
+ * repeat * (n + 1) is below the kind's measured switch point (jm_plan.h
+ * stream_rn: 600 for f64 n = 9..32, 200 for f64 n >= 33, 64 for f32
+ * n = 9..16, 140 for f32 n >= 17; the HBM-bound side of the roofline and
+ * somewhat beyond) runs the STREAMING variant of the same
+ * specialization — the same tile code behind a bulk-copy (TMA) ring — which is
+ * a second cache key, compiled on its first such call.  Results agree with the
+ * resident kernel bit for bit (same arithmetic in the same order).  Environment
+ * JIT_MAT_STREAM=0/1 forces resident/streaming, JIT_MAT_STREAM_RN moves the
+ * switch point (read once per process); per call, jm_run_desc.flags
+ * JM_FLAG_RESIDENT / JM_FLAG_STREAMING force it. */
 JM_API int jit_mat_run(int n, int dtype, int64_t batch, int64_t repeat, const void *in, void *out);
 
 /* Unload every module, drop the cache and release the primary context.  Later
@@ -153,9 +168,10 @@ JM_API int jit_mat_run_many(const jm_run_desc *descs, int count, void *stream, u
 
 /* Share specializations between processes (the paper's
  * compile-time concern).  jit_mat_cache_export writes a
- * self-describing blob (key + kernel symbol + sm_100a cubin) of a READY
- * specialized key into `buf` (`cap` bytes); `*len` receives the blob size
- * (pass buf = NULL to query).  JM_E_INVALID if the key has not been compiled.
+ * self-describing blob ("JMC2": key + per compiled variant — resident and/or
+ * streaming — the kernel symbol and sm_100a cubin) of a specialized key into
+ * `buf` (`cap` bytes); `*len` receives the blob size (pass buf = NULL to
+ * query).  JM_E_INVALID if neither variant of the key has been compiled.
  * jit_mat_cache_import installs such a blob (from the same library build) for
  * its key without running NVRTC: one rank compiles, broadcasts the blob, the
  * other ranks import it.  Importing into a READY slot is a no-op (JM_OK); a blob
@@ -199,6 +215,13 @@ JM_API int jit_mat_set_stream(void *cuda_stream);
  * launching.  The analog of forcing an instantiation ahead of use. */
 JM_API int jit_mat_prepare(int n, int dtype, int addend, int kind);
 
+/* As jit_mat_prepare, but for the kernel a run with this `repeat` and `flags`
+ * (JM_FLAG_RESIDENT / JM_FLAG_STREAMING honoured) would launch — the resident
+ * or the streaming variant, see jit_mat_run; `*variant` (may be NULL)
+ * receives 0 (resident) or 1 (streaming). */
+JM_API int jit_mat_prepare_for(int n, int dtype, int addend, int kind, int64_t repeat, unsigned flags,
+                               int *variant);
+
 /* "float" -> JM_F32, "double" -> JM_F64; "long double" and anything else ->
  * JM_E_UNSUPPORTED (the GPU path supports two of Listing 4's three types). */
 JM_API int jit_mat_dtype_from_name(const char *name);
@@ -213,7 +236,7 @@ typedef struct {
   int64_t misses;            /* lookups that had to compile (or wait for a compile) */
   int64_t launches;          /* kernels launched by this library */
   double compile_ms_total;   /* wall time inside NVRTC + module load */
-  int32_t keys_ready;        /* cache slots in READY state */
+  int32_t keys_ready;        /* specialized cache slots (either variant) in READY state */
   int32_t keys_failed;       /* cache slots in FAILED state */
   int64_t imports;           /* keys installed by jit_mat_cache_import (no NVRTC) */
 } jm_stats;
@@ -229,7 +252,7 @@ typedef struct {
   int64_t cubin_bytes;
   double compile_ms;
   int32_t op;                /* 0 = update (jit_mat_run), 1 = multiply-accumulate (jit_mat_matmul) */
-  int32_t reserved;
+  int32_t variant;           /* update: 0 resident kernel, 1 streaming (low-repeat) kernel */
 } jm_key_info;
 
 /* tiling kinds reported in jm_key_info.tile */
@@ -272,6 +295,8 @@ JM_API const char *jit_mat_version(void);
  * the multiply-accumulate template instead.  cubin_bytes may be NULL. */
 #define JM_OP_MATMUL 2
 #define JM_OP_MASS 3     /* compile_check(dofs, quads, JM_OP_MASS, ...): k_mass<dofs, quads> */
+#define JM_OP_STREAM 4   /* the streaming variant of the update (addend Ones); JM_E_UNSUPPORTED
+                            for thread-per-matrix sizes (f64 n <= 7, f32 n <= 8) */
 JM_API int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes);
 
 /* Cache-hit cost of the key lookup (the paper calls the

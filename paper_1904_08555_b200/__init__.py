@@ -19,8 +19,8 @@ import os
 from ._lib import (  # noqa: F401  (re-exported C ABI)
     JM_ADDEND_IDENTITY, JM_ADDEND_ONES, JM_E_ALIGN, JM_E_ARCH, JM_E_COMPILE, JM_E_CUDA,
     JM_E_INVALID, JM_E_NOT_INITIALIZED, JM_E_UNSUPPORTED, JM_F32, JM_F64, JM_FLAG_HOST_BUFFERS,
-    JM_FLAG_SYNC, JM_KIND_AOT_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK, JM_OP_MATMUL,
-    JM_TILE_NAMES, JitMatError,
+    JM_FLAG_RESIDENT, JM_FLAG_STREAMING, JM_FLAG_SYNC, JM_KIND_AOT_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK, JM_OP_MATMUL,
+    JM_OP_STREAM, JM_TILE_NAMES, JitMatError,
     jm_key_info, jm_run_desc, jm_stats, lib, lib_path,
 )
 
@@ -28,7 +28,7 @@ __all__ = [
     "jit_mat_init", "jit_mat_run", "jit_mat_shutdown", "jit_mat_run_ex", "jit_mat_run_host",
     "jit_mat_run_many", "jit_mat_cache_export", "jit_mat_cache_import", "jit_mat_matmul",
     "jit_mat_time_lookup", "matmul", "jit_mat_mass", "mass",
-    "jit_mat_set_stream", "jit_mat_prepare", "jit_mat_dtype_from_name", "jit_mat_last_error",
+    "jit_mat_set_stream", "jit_mat_prepare", "jit_mat_prepare_for", "jit_mat_dtype_from_name", "jit_mat_last_error",
     "jit_mat_stats", "jit_mat_key_info", "jit_mat_reset_stats", "jit_mat_fill",
     "jit_mat_checksum", "jit_mat_device_info", "jit_mat_version", "jit_mat_compile_check",
     "run", "JitMatError",
@@ -181,6 +181,17 @@ def jit_mat_prepare(n: int, dtype, addend="ones", kind="specialized") -> None:
                                _KINDS.get(kind, kind)), "jit_mat_prepare")
 
 
+def jit_mat_prepare_for(n: int, dtype, repeat: int, addend="ones", kind="specialized",
+                        flags: int = 0) -> int:
+    """Prepare the kernel a run with this repeat count (and flags) launches;
+    returns its variant (0 resident, 1 streaming)."""
+    v = ctypes.c_int(-1)
+    _check(lib.jit_mat_prepare_for(int(n), _dt(dtype), _ADDENDS.get(addend, addend),
+                                   _KINDS.get(kind, kind), int(repeat), int(flags), ctypes.byref(v)),
+           "jit_mat_prepare_for")
+    return int(v.value)
+
+
 def jit_mat_dtype_from_name(name: str) -> int:
     return lib.jit_mat_dtype_from_name(name.encode())
 
@@ -239,24 +250,27 @@ def jit_mat_version() -> str:
 
 
 def jit_mat_compile_check(n: int, dtype, addend="ones") -> int:
-    """NVRTC-compile a key without a GPU; addend="matmul" selects k_matmul and
-    addend="mass" selects k_mass<n, dtype> (dtype = quads, an int)."""
+    """NVRTC-compile a key without a GPU; addend="matmul" selects k_matmul,
+    addend="stream" the streaming variant of k_update, and addend="mass"
+    selects k_mass<n, dtype> (dtype = quads, an int)."""
     cb = ctypes.c_longlong(0)
     if addend == "mass":
         _check(lib.jit_mat_compile_check(int(n), int(dtype), 3, ctypes.byref(cb)), "jit_mat_compile_check")
         return int(cb.value)
-    a = JM_OP_MATMUL if addend == "matmul" else _ADDENDS.get(addend, addend)
+    a = {"matmul": JM_OP_MATMUL, "stream": JM_OP_STREAM}.get(addend, _ADDENDS.get(addend, addend))
     _check(lib.jit_mat_compile_check(int(n), _dt(dtype), a, ctypes.byref(cb)), "jit_mat_compile_check")
     return int(cb.value)
 
 
 # ---------------------------------------------------------------- convenience
 def run(x, repeat: int, out=None, *, addend: str = "ones", kind: str = "specialized",
-        stream=None, sync: bool = False):
+        stream=None, sync: bool = False, variant: str | None = None):
     """Apply the update to a CUDA tensor ``x`` of shape (batch, n, n) (float32/float64).
 
     Marshals the tensor pointers into :func:`jit_mat_run_ex`; ``out`` may be ``x``
     (in place).  Runs on ``stream`` (default: torch's current stream).
+    ``variant`` = "resident" / "streaming" forces the kernel variant (default:
+    the library picks by repeat count, see jit_mat.h VARIANT).
     """
     import torch
 
@@ -271,8 +285,11 @@ def run(x, repeat: int, out=None, *, addend: str = "ones", kind: str = "speciali
     st = stream if stream is not None else torch.cuda.current_stream(x.device)
     jit_mat_run_ex(x.shape[1], str(x.dtype), x.shape[0], repeat, x.data_ptr(), out.data_ptr(),
                    addend=addend, kind=kind, stream=st.cuda_stream,
-                   flags=JM_FLAG_SYNC if sync else 0)
+                   flags=(JM_FLAG_SYNC if sync else 0) | _VARIANTS[variant])
     return out
+
+
+_VARIANTS = {None: 0, "auto": 0, "resident": JM_FLAG_RESIDENT, "streaming": JM_FLAG_STREAMING}
 
 
 def _selftest_loaded() -> str:

@@ -18,11 +18,12 @@ JM_KIND_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_AOT_SPECIALIZED = 0, 1, 2
 JM_OK = 0
 JM_E_INVALID, JM_E_UNSUPPORTED, JM_E_NOT_INITIALIZED = -1, -2, -3
 JM_E_ARCH, JM_E_COMPILE, JM_E_CUDA, JM_E_ALIGN = -4, -5, -6, -7
-JM_FLAG_SYNC, JM_FLAG_HOST_BUFFERS = 1, 2
+JM_FLAG_SYNC, JM_FLAG_HOST_BUFFERS, JM_FLAG_RESIDENT, JM_FLAG_STREAMING = 1, 2, 4, 8
 JM_TILE_NAMES = {0: "generic", 1: "tpm", 2: "warp_dmma", 3: "cta_dmma", 4: "warp_f32",
                  5: "cta_f32", 6: "rows", 7: "matmul"}
 JM_OP_MATMUL = 2
 JM_OP_MASS = 3
+JM_OP_STREAM = 4
 
 
 class JitMatError(RuntimeError):
@@ -51,7 +52,7 @@ class jm_key_info(ctypes.Structure):
                 ("local_bytes", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("tile", ctypes.c_int32),
                 ("cubin_bytes", ctypes.c_int64), ("compile_ms", ctypes.c_double),
-                ("op", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("op", ctypes.c_int32), ("variant", ctypes.c_int32)]
 
 
 _I, _I64, _P, _U64 = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_uint64
@@ -66,6 +67,7 @@ _SIGS = {
     "jit_mat_cache_import": (_I, [_P, ctypes.c_size_t]),
     "jit_mat_set_stream": (_I, [_P]),
     "jit_mat_prepare": (_I, [_I, _I, _I, _I]),
+    "jit_mat_prepare_for": (_I, [_I, _I, _I, _I, _I64, ctypes.c_uint, ctypes.POINTER(_I)]),
     "jit_mat_dtype_from_name": (_I, [ctypes.c_char_p]),
     "jit_mat_last_error": (ctypes.c_char_p, []),
     "jit_mat_stats": (_I, [ctypes.POINTER(jm_stats)]),

@@ -207,6 +207,72 @@ JM_HD constexpr bool use_mb1(int n, int dtype) {
   return tile_for(n, dtype) == Tile::Dmma && dmma_w(n) > 1;
 }
 
+// ---- streaming variant (low repeat: the HBM-bound side of the roofline) ----
+// At R(n+1) below the ridge (R(n+1) < 46 for both dtypes) the
+// update is bound by moving each matrix in and out once, and the resident
+// kinds above, which load -> compute -> store each chunk in turn, leave HBM
+// idle while they compute.  The streaming variant runs the SAME tiling kinds
+// (same compute code, same round of MPC matrices) behind a bulk-copy ring
+// (jm::Ring): chunks of K rounds, JM_RING_S stages deep, ~JM_RING_CHUNK bytes
+// each.  The host picks it per call from the repeat count (stream_rn); it is a
+// second cache key of the same (N, dtype, addend).
+// TPM (thread per matrix) keeps its resident kernel: its per-thread reads need
+// the odd-16-B staging stride, and it already streams at 0.89-0.99 of HBM.
+#ifndef JM_RING_S
+#define JM_RING_S 2
+#endif
+#ifndef JM_RING_CHUNK
+#define JM_RING_CHUNK 8192
+#endif
+JM_HD constexpr bool stream_ok(int n, int dtype) {
+  return tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::F32;
+}
+// The host's switch: stream iff repeat * (n + 1) < stream_rn(n, dtype).
+// Placed from the measured crossovers (profiles/r01_stream_sweep.jsonl, one
+// B200, R in {1..100}): the ring costs shared memory, hence residency, so it
+// wins while the load/store half of the roofline still matters and loses a
+// few % once the update is compute-bound.  f64 warp DMMA (n = 9..32) gains up
+// to R(n+1) ~ 600 (n = 32: 1.93x at R = 1, 1.17x at R = 8); n = 8 loses 8 % at
+// R = 1 (16 copies of 512 B per chunk) and gains <= 7 % elsewhere, so it stays
+// resident; CTA DMMA (n >= 33; n = 64 holds 131 KB of ring per CTA) to ~200;
+// f32 row panels to ~64; f32 tiles to ~140.
+JM_HD constexpr int stream_rn(int n, int dtype) {
+  return !stream_ok(n, dtype) ? 0
+         : dtype == 1        ? (dmma_w(n) == 1 ? (n >= 9 ? 600 : 0) : 200)
+         : f32p_use(n)       ? 64
+                             : 140;
+}
+// rounds per chunk: >= JM_RING_CHUNK bytes and a chunk a multiple of 16 B
+JM_HD constexpr int ring_k(int rb) {
+  return rup(cdiv(JM_RING_CHUNK, rb), (rb % 16 == 0) ? 1 : (rb % 8 == 0) ? 2 : 4);
+}
+// matrix stride in a ring stage: the odd-16-B stage stride when a matrix is a
+// multiple of 16 B (one bulk copy per matrix), else packed (one per chunk)
+JM_HD constexpr int ring_sbm(int n, int es) { return (n * n * es) % 16 == 0 ? stage_stride(n, es) : n * n * es; }
+JM_HD constexpr int ring_bytes(int n, int es, int rm) {
+  return JM_RING_S * ring_k(rm * n * n * es) * rm * ring_sbm(n, es) + rup(8 * JM_RING_S, 16);
+}
+// matrices per round of each kind (the resident plan's chunk)
+JM_HD constexpr int round_mpc(int n, int dtype) {
+  return tile_for(n, dtype) == Tile::Dmma ? (dmma_w(n) == 1 ? DMMA_WPC : 1)
+         : f32p_use(n)                   ? F32P_WPC * f32p_mpw(n)
+                                         : F32_WPC * f32_mpw(n);
+}
+// Plan of the streaming variant: mpc = matrices per ring chunk (the host sizes
+// the grid by it); smem = the ring + the kind's own work areas.
+JM_HD constexpr Plan plan_stream(int n, int dtype) {
+  const int es = dtype == 1 ? 8 : 4;
+  const int rm = round_mpc(n, dtype), rb = rm * n * n * es, chm = ring_k(rb) * rm;
+  if (!stream_ok(n, dtype)) return plan_specialized(n, dtype);
+  if (tile_for(n, dtype) == Tile::Dmma) {
+    const int w = dmma_w(n);
+    return w == 1 ? Plan{(int)Tile::Dmma, 32 * DMMA_WPC, chm, ring_bytes(n, es, rm) + DMMA_WPC * dmma_scr(n), 1}
+                  : Plan{(int)Tile::Dmma, 32 * w, chm, ring_bytes(n, es, rm) + 2 * dmma_scr(n), w};
+  }
+  if (f32p_use(n)) return Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
+  return Plan{(int)Tile::F32, 32 * F32_WPC, chm, ring_bytes(n, es, rm) + rm * f32_region(n), 1};
+}
+
 // Note: k_update passes only maxThreads to __launch_bounds__.  Registers are
 // granted per SMSP (16384 each), so a minBlocks cap only bites in steps of
 // warps-per-SMSP (2 -> 255, 3 -> 168 regs); 168 makes the FP32 row panels

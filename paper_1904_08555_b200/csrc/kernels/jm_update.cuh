@@ -148,6 +148,47 @@ __device__ __forceinline__ void stage_in_async(const char *__restrict__ g, char 
   }
 }
 
+// ------------------------------------------------ bulk-copy (TMA) primitives
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64 *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(u64 *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64 *bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// global -> shared, completion counted on `bar` (TMA 1-D bulk copy)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, u64 *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// shared -> global, tracked by bulk async-groups
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// make this thread's generic-proxy shared-memory writes visible to the async proxy
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // Chunk scheduler shared by the kernels: a persistent CTA walks chunks of MPC
 // matrices (chunk = blockIdx.x, += gridDim.x).  With PF (prefetch) the stage
 // area is double-buffered: while chunk i is computed, chunk i+gridDim.x is
@@ -200,7 +241,132 @@ struct Stager {
     ch += gridDim.x;
     ++it;
   }
+  __device__ __forceinline__ void finish() {}
+  static constexpr int SBM = SB;                                // matrix stride in a stage buffer
+  static constexpr int BYTES = (PF ? 2 : 1) * SZ;               // shared memory it occupies
 };
+
+// Streaming stager for the HBM-bound (low-repeat) variant, SURVEY.md §8(a)
+// a3/a5 "TMA-1D bulk": chunks of K rounds x MPC matrices move through an
+// S-stage shared-memory ring of 1-D bulk copies (cp.async.bulk, the TMA
+// engine) that complete on one mbarrier per stage; the updated chunk leaves by
+// bulk stores straight from the same buffer, so no register ever carries the
+// data.  When a matrix is a multiple of 16 B, each matrix is its own copy into
+// a slot at the odd-16-B stage stride (stage_stride: the kinds' per-matrix
+// shared-memory reads stay bank-conflict free, as in the resident kernel);
+// otherwise the chunk is one packed copy.  Warp 0 keeps the ring full: after
+// issuing chunk i's stores each of its lanes waits only until its own stores
+// have READ their slots, then refills them with chunk i + S, so S - 1 chunk
+// loads overlap the compute of chunk i.  A round (what the tiling kinds see
+// through buf()/cnt()) is MPC matrices.  The one ragged chunk at the end of
+// the batch is staged synchronously with element copies.
+template <int N, int ES, int NT, int MPC, int K, int S>
+struct Ring {
+  static constexpr int MB = N * N * ES;
+  static constexpr bool PER = (MB % 16) == 0;             // one copy per matrix
+  static constexpr int SBM = PER ? stage_stride(N, ES) : MB;
+  static constexpr int RB = MPC * SBM, CHM = K * MPC, CHB = K * RB, GB = CHM * MB;
+  static_assert(GB % 16 == 0 && CHB % 16 == 0, "bulk copies move multiples of 16 bytes");
+  static_assert(S >= 2, "ring of at least two stages");
+  static constexpr int BYTES = S * CHB + rup(8 * S, 16);
+  const char *in;
+  char *out;
+  char *base;
+  u64 *bar;
+  long long batch, nchunks, ch;
+  int sub, s, tid;
+  unsigned ph;
+  __device__ __forceinline__ Ring(const void *in_, void *out_, long long batch_, char *base_)
+      : in(reinterpret_cast<const char *>(in_)), out(reinterpret_cast<char *>(out_)), base(base_),
+        bar(reinterpret_cast<u64 *>(base_ + S * CHB)), batch(batch_), nchunks((batch_ + CHM - 1) / CHM),
+        ch(blockIdx.x), sub(0), s(0), tid(threadIdx.x), ph(0u) {}
+  __device__ __forceinline__ bool full(long long c) const { return (c + 1) * CHM <= batch; }
+  // warp 0: chunk c -> stage st (the mbarrier's tx count may run ahead of the
+  // expect_tx arrival: the phase cannot complete before that arrival)
+  __device__ __forceinline__ void issue(long long c, int st) {
+    const char *g = in + c * GB;
+    char *d = base + st * CHB;
+    if (tid == 0) mbar_expect_tx(bar + st, GB);
+    if constexpr (PER) {
+      for (int m = tid; m < CHM; m += 32) bulk_g2s(d + m * SBM, g + (size_t)m * MB, MB, bar + st);
+    } else {
+      if (tid == 0) bulk_g2s(d, g, GB, bar + st);
+    }
+  }
+  // warp 0: stage st -> chunk c, one bulk group per issuing lane
+  __device__ __forceinline__ void store(long long c, int st) {
+    char *g = out + c * GB;
+    const char *d = base + st * CHB;
+    if constexpr (PER) {
+      for (int m = tid; m < CHM; m += 32) bulk_s2g(g + (size_t)m * MB, d + m * SBM, MB);
+    } else {
+      if (tid == 0) bulk_s2g(g, d, GB);
+    }
+    bulk_commit();
+  }
+  __device__ __forceinline__ void start() {
+    if (tid == 0) {
+#pragma unroll
+      for (int k = 0; k < S; ++k) mbar_init(bar + k, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid < 32) {
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        const long long c = ch + (long long)k * gridDim.x;
+        if (c < nchunks && full(c)) issue(c, k);
+      }
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return ch < nchunks; }
+  __device__ __forceinline__ char *buf() const { return base + s * CHB + sub * RB; }
+  __device__ __forceinline__ int cnt() const {
+    const long long r = batch - (ch * CHM + (long long)sub * MPC);
+    return (int)(r <= 0 ? 0 : (r < MPC ? r : MPC));
+  }
+  __device__ __forceinline__ void acquire() {
+    if (sub != 0) return;
+    if (full(ch)) {
+      mbar_wait(bar + s, ph);
+    } else {   // the ragged last chunk: its stage may still be draining stores
+      if (tid < 32) bulk_wait_read_all();
+      __syncthreads();
+      stage_in<N, ES, SBM, NT, false>(in + ch * GB, base + s * CHB, (int)(batch - ch * CHM), tid);
+      __syncthreads();
+    }
+  }
+  __device__ __forceinline__ void release() {
+    fence_proxy_async();   // this thread's results -> visible to the bulk stores
+    __syncthreads();
+    if (sub != K - 1) return;
+    if (full(ch)) {
+      if (tid < 32) {
+        store(ch, s);
+        const long long nx = ch + (long long)S * gridDim.x;
+        if (nx < nchunks && full(nx)) {
+          bulk_wait_read_all();   // this lane's stores have read their slots: refill
+          issue(nx, s);
+        }
+      }
+    } else {
+      stage_out<N, ES, SBM, NT, false>(out + ch * GB, base + s * CHB, (int)(batch - ch * CHM), tid);
+    }
+  }
+  __device__ __forceinline__ void next() {
+    if (++sub == K) {
+      sub = 0;
+      ch += gridDim.x;
+      if (++s == S) { s = 0; ph ^= 1u; }
+    }
+  }
+  __device__ __forceinline__ void finish() {
+    if (tid < 32) bulk_wait_all();
+  }
+};
+
+template <bool B, class X, class Y> struct Pick { typedef X type; };
+template <class X, class Y> struct Pick<false, X, Y> { typedef Y type; };
 
 // ======================================================================
 // TPM: thread per matrix.  The whole matrix (and the product) lives in
@@ -365,7 +531,7 @@ __device__ __forceinline__ void dmma884_c(double &d0, double &d1, double a, doub
 //   (r * RSC + (cc ^ ((r & 6) ^ ((r & 1) << 2)))) * 16
 // (run_dmma precomputes this as lane constants + immediates: bofs / pofs).
 
-template <int N, Addend A, int W>
+template <int N, Addend A, int W, bool STRM>
 __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *__restrict__ out,
                                          long long batch, int repeat) {
   constexpr int T8 = dmma_t8(N), RT = dmma_rt(N), RSC = dmma_rsc(N), SCR = dmma_scr(N);
@@ -376,12 +542,14 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   static_assert(RT * W == T8, "row tiles must cover the matrix");
   constexpr bool PF = prefetch_for(N, 1);
+  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S>,
+                        Stager<N, ES, SB, NT, MPC, AL, PF>>::type Stg;
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int mi = (W == 1) ? warp : 0;        // matrix slot in the chunk
   const int wr = (W == 1) ? 0 : warp;        // this warp's rank within the matrix
-  char *scr = smem + (PF ? 2 : 1) * stage_bytes(MPC, N, 8) + ((W == 1) ? warp * SCR : 0);
+  char *scr = smem + Stg::BYTES + ((W == 1) ? warp * SCR : 0);
   const double c = 0.00005;
   // Swizzled-scratch offsets factored into a few lane constants plus
   // compile-time immediates (chunk c ^ f only touches c's low 3 bits, and the
@@ -399,13 +567,13 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
 #pragma unroll
   for (int j1 = 0; j1 < 2; ++j1) pofs[j1] = ((8 * wr * RT + g) * RSC + ((j1 * 4 + t) ^ fg)) * 16;
 
-  Stager<N, ES, SB, NT, MPC, AL, PF> sg(in, out, batch, smem);
+  Stg sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     char *stage = sg.buf();
     const int cnt = sg.cnt();
     if (mi < cnt) {
-      double *sm = reinterpret_cast<double *>(stage + mi * SB);
+      double *sm = reinterpret_cast<double *>(stage + mi * Stg::SBM);
       double acc[RT][T8][2];
 #pragma unroll
       for (int I = 0; I < RT; ++I)
@@ -474,6 +642,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
     }
     sg.release();
   }
+  sg.finish();
 }
 
 // ======================================================================
@@ -494,7 +663,7 @@ __device__ __forceinline__ int f32p_off(int row, int q) {
   return (row * NCS + (q ^ ((row >> 2) & (NCS - 1)))) * 16;
 }
 
-template <int N, Addend A>
+template <int N, Addend A, bool STRM>
 __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__restrict__ out,
                                          long long batch, int repeat) {
   constexpr int RP = f32p_rp(N), G = f32p_g(N), MPW = f32p_mpw(N), NCR = f32p_ncr(N);
@@ -507,15 +676,17 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   static_assert(G * RP >= N, "row panels must cover the matrix");
   constexpr bool PF = prefetch_for(N, 0);
+  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S>,
+                        Stager<N, ES, SB, NT, MPC, AL, PF>>::type Stg;
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int mw = lane / G, tg = lane - mw * G;
   const int mi = warp * MPW + mw;                      // matrix slot in the chunk
   const int r0 = tg * RP;
-  char *bufs = smem + (PF ? 2 : 1) * stage_bytes(MPC, N, 4) + mi * 2 * MBUF;
+  char *bufs = smem + Stg::BYTES + mi * 2 * MBUF;
   const float c = float(0.00005);
 
-  Stager<N, ES, SB, NT, MPC, AL, PF> sg(in, out, batch, smem);
+  Stg sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     char *stage = sg.buf();
@@ -523,7 +694,7 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
     // every lane runs the loop (a warp holds several matrices and syncs as one);
     // slots past the batch end compute on zeros and are never written back
     const bool live = mi < cnt;
-    float *sm = reinterpret_cast<float *>(stage + mi * SB);
+    float *sm = reinterpret_cast<float *>(stage + mi * Stg::SBM);
     float m[RP][NC];
 #pragma unroll
     for (int i = 0; i < RP; ++i)
@@ -628,6 +799,7 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
     }
     sg.release();
   }
+  sg.finish();
 }
 
 // ======================================================================
@@ -761,7 +933,7 @@ __device__ __forceinline__ void run_f64p(const double *__restrict__ in, double *
 // Steps k in [N, rup(N,4)) read zero padding (exact no-ops).  A warp holds
 // 32 / (RG*CG) whole matrices, so only __syncwarp is needed.
 // ======================================================================
-template <int N, Addend A>
+template <int N, Addend A, bool STRM>
 __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__restrict__ out,
                                         long long batch, int repeat) {
   constexpr int RG = f32_rg(N), RA = f32_ra(N), CG = f32_cg(N), CB = f32_cb(N);
@@ -782,11 +954,16 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
   auto row_of = [&](int i) { return i * RG + tr; };
   auto col_of = [&](int j) { return ((j >> 2) * CG + tc) * 4 + (j & 3); };
 
-  Stager<N, ES, REG, NT, MPC, AL, false> sg(in, out, batch, smem);
+  // resident: the staged matrix's region doubles as its work area (sM);
+  // streaming: packed ring stages, work areas of REG bytes after the ring
+  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S>,
+                        Stager<N, ES, REG, NT, MPC, AL, false>>::type Stg;
+  Stg sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     const bool live = (m < MPW) && (mi < sg.cnt());
-    float *sm = reinterpret_cast<float *>(sg.buf() + (m < MPW ? mi : 0) * REG);
+    float *src = reinterpret_cast<float *>(sg.buf() + (m < MPW ? mi : 0) * Stg::SBM);
+    float *sm = STRM ? reinterpret_cast<float *>(smem + Stg::BYTES + (m < MPW ? mi : 0) * REG) : src;
     float2 p[RA][CB / 2];
     if (live) {
 #pragma unroll
@@ -794,8 +971,8 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
 #pragma unroll
         for (int j = 0; j < CB; j += 2) {
           const int row = row_of(i), c0 = col_of(j), c1 = c0 + 1;
-          p[i][j / 2].x = (row < N && c0 < N) ? sm[row * N + c0] : 0.0f;
-          p[i][j / 2].y = (row < N && c1 < N) ? sm[row * N + c1] : 0.0f;
+          p[i][j / 2].x = (row < N && c0 < N) ? src[row * N + c0] : 0.0f;
+          p[i][j / 2].y = (row < N && c1 < N) ? src[row * N + c1] : 0.0f;
         }
     }
     __syncwarp();                        // staged matrix in registers: reuse the region as sM
@@ -869,32 +1046,34 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
 #pragma unroll
         for (int j = 0; j < CB; j += 2) {
           const int row = row_of(i), c0 = col_of(j), c1 = c0 + 1;
-          if (row < N && c0 < N) sm[row * N + c0] = p[i][j / 2].x;
-          if (row < N && c1 < N) sm[row * N + c1] = p[i][j / 2].y;
+          if (row < N && c0 < N) src[row * N + c0] = p[i][j / 2].x;
+          if (row < N && c1 < N) src[row * N + c1] = p[i][j / 2].y;
         }
     }
     sg.release();
   }
+  sg.finish();
 }
 
 // ------------------------------------------------------------------ entry
 // The NVRTC name expression is "jm::k_update<N, T, jm::Addend::X, jm::Tile::Y>"
 // with Y = tile_for(N, dtype); the host launches it with plan_specialized().
-template <int N, class T, Addend A, Tile K>
+template <int N, class T, Addend A, Tile K, bool STRM = false>
 __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restrict__ out,
                                             long long batch, int repeat) {
   static_assert(N >= 1 && N <= 64, "N in [1, 64]");
   static_assert(K == tile_for(N, sizeof(T) == 8 ? 1 : 0), "tile must match the plan");
+  static_assert(!STRM || stream_ok(N, sizeof(T) == 8 ? 1 : 0), "no streaming variant of this kind");
   if constexpr (K == Tile::TPM) {
     run_tpm<N, T, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Rows) {
     run_f64p<N, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Dmma) {
-    run_dmma<N, A, dmma_w(N)>(in, out, batch, repeat);
+    run_dmma<N, A, dmma_w(N), STRM>(in, out, batch, repeat);
   } else if constexpr (f32p_use(N)) {
-    run_f32p<N, A>(in, out, batch, repeat);
+    run_f32p<N, A, STRM>(in, out, batch, repeat);
   } else {
-    run_f32<N, A>(in, out, batch, repeat);
+    run_f32<N, A, STRM>(in, out, batch, repeat);
   }
 }
 
@@ -911,6 +1090,20 @@ template <int N, class T, Addend A, Tile K>
 __global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).threads, 1)
     k_update_mb1(const T *__restrict__ in, T *__restrict__ out, long long batch, int repeat) {
   update_body<N, T, A, K>(in, out, batch, repeat);
+}
+
+// The streaming (low-repeat) variant: same kinds behind the bulk-copy ring
+// (plan_stream); the host selects it when repeat * (n + 1) is below the
+// switch point.  Name expression "jm::k_update_stream[_mb1]<N, T, A, K>".
+template <int N, class T, Addend A, Tile K>
+__global__ void __launch_bounds__(plan_stream(N, sizeof(T) == 8 ? 1 : 0).threads)
+    k_update_stream(const T *__restrict__ in, T *__restrict__ out, long long batch, int repeat) {
+  update_body<N, T, A, K, true>(in, out, batch, repeat);
+}
+template <int N, class T, Addend A, Tile K>
+__global__ void __launch_bounds__(plan_stream(N, sizeof(T) == 8 ? 1 : 0).threads, 1)
+    k_update_stream_mb1(const T *__restrict__ in, T *__restrict__ out, long long batch, int repeat) {
+  update_body<N, T, A, K, true>(in, out, batch, repeat);
 }
 
 }  // namespace jm

@@ -186,6 +186,8 @@ constexpr int NKIND = 3, NADD = 2, NDT = 2, NMAX = JM_N_MAX;
 Slot g_slots[NKIND][NADD][NDT][NMAX + 1];
 Slot g_mm_slots[2][NDT][NMAX + 1];     // multiply-accumulate: [specialized|generic][dtype][n]
 Slot g_mass_slots[2][jm::MASS_MAX + 1][jm::MASS_MAX + 1];   // Laghos mass action: [kind][D][Q]
+// the streaming (low-repeat) variant of the specialized update: [addend][dtype][n]
+Slot g_stream_slots[NADD][NDT][NMAX + 1];
 
 struct State {
   std::mutex mu;
@@ -234,10 +236,10 @@ const char *tile_name(int t) {
   }
 }
 
-std::string name_expression(int n, int dtype, int addend) {
+std::string name_expression(int n, int dtype, int addend, bool stream = false) {
   char buf[160];
-  snprintf(buf, sizeof buf, "jm::%s<%d, %s, jm::Addend::%s, jm::Tile::%s>",
-           jm::use_mb1(n, dtype) ? "k_update_mb1" : "k_update", n,
+  snprintf(buf, sizeof buf, "jm::%s%s<%d, %s, jm::Addend::%s, jm::Tile::%s>",
+           stream ? "k_update_stream" : "k_update", jm::use_mb1(n, dtype) ? "_mb1" : "", n,
            dtype == JM_F64 ? "double" : "float", addend == JM_ADDEND_ONES ? "Ones" : "Identity",
            tile_name((int)jm::tile_for(n, dtype)));
   return buf;
@@ -306,13 +308,15 @@ int finish_function(Slot &s, CUfunction fn) {
 
 // ops: the Eigen-benchmark update (k_update) and the batched multiply-accumulate
 // of the RAJA benchmark (k_matmul, Listing 8)
-enum { OP_UPDATE = 0, OP_MATMUL = 1, OP_MASS = 2 };
+// and the streaming variant of k_update (k_update_stream, jm::plan_stream)
+enum { OP_UPDATE = 0, OP_MATMUL = 1, OP_MASS = 2, OP_UPDATE_STREAM = 3 };
 
 // (for OP_MASS: n = D = NUM_DOFS_1D, extra = Q = NUM_QUAD_1D)
 jm::Plan plan_for(int op, int n, int dtype, int extra) {
-  return op == OP_MATMUL ? jm::plan_matmul(n, dtype)
-         : op == OP_MASS ? jm::plan_mass(n, extra)
-                         : jm::plan_specialized(n, dtype);
+  return op == OP_MATMUL          ? jm::plan_matmul(n, dtype)
+         : op == OP_MASS          ? jm::plan_mass(n, extra)
+         : op == OP_UPDATE_STREAM ? jm::plan_stream(n, dtype)
+                                  : jm::plan_specialized(n, dtype);
 }
 
 std::string mass_name_expression(int d, int q) {
@@ -363,7 +367,7 @@ int compile_slot(Slot &s, int op, int n, int dtype, int addend) {
   std::string lowered, log;
   const std::string expr = op == OP_MATMUL ? mm_name_expression(n, dtype)
                            : op == OP_MASS ? mass_name_expression(n, addend)
-                                           : name_expression(n, dtype, addend);
+                                           : name_expression(n, dtype, addend, op == OP_UPDATE_STREAM);
   int rc = nvrtc_compile_expr(expr, cubin, lowered, log);
   if (rc != JM_OK) {
     s.err = log;
@@ -440,6 +444,42 @@ int acquire_slot(Slot &s, int op, int n, int dtype, int addend, int kind, Slot *
 
 int lookup(int n, int dtype, int addend, int kind, Slot **out) {
   return lookup_op(OP_UPDATE, n, dtype, addend, kind, out);
+}
+
+// Resident or streaming kernel for this call?  The roofline decides
+// (jm_plan.h, plan_stream): stream when repeat * (n + 1) is below the switch
+// point, i.e. when the call is bound by moving each matrix in and out once.
+// JIT_MAT_STREAM=0 / =1 force the resident / streaming kernel (where the
+// tiling kind has one); JIT_MAT_STREAM_RN moves the switch point.
+int stream_rn(int n, int dtype) {
+  static const int rn = [] {
+    const char *e = getenv("JIT_MAT_STREAM_RN");
+    return e && *e ? atoi(e) : -1;
+  }();
+  return rn >= 0 ? rn : jm::stream_rn(n, dtype);
+}
+bool want_stream(int n, int dtype, int kind, int64_t repeat, unsigned flags = 0) {
+  if (kind != JM_KIND_SPECIALIZED || !jm::stream_ok(n, dtype)) return false;
+  if (flags & JM_FLAG_RESIDENT) return false;
+  if (flags & JM_FLAG_STREAMING) return true;
+  static const int force = [] {
+    const char *e = getenv("JIT_MAT_STREAM");
+    return e && *e ? atoi(e) : -1;
+  }();
+  if (force >= 0) return force > 0;
+  return repeat * (int64_t)(n + 1) < (int64_t)stream_rn(n, dtype);
+}
+
+Slot &slot_of(int n, int dtype, int addend, int kind, bool stream) {
+  return stream ? g_stream_slots[addend][dtype][n] : g_slots[kind][addend][dtype][n];
+}
+
+// the kernel a run descriptor launches (key checked by the caller)
+int lookup_run(const jm_run_desc &d, Slot **out) {
+  if (!want_stream(d.n, d.dtype, d.kind, d.repeat, d.flags)) return lookup(d.n, d.dtype, d.addend, d.kind, out);
+  if (!G.inited.load(std::memory_order_acquire)) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
+  return acquire_slot(g_stream_slots[d.addend][d.dtype][d.n], OP_UPDATE_STREAM, d.n, d.dtype, d.addend,
+                      JM_KIND_SPECIALIZED, out);
 }
 
 int launch(Slot &s, int n, int64_t batch, int64_t repeat, const void *in, void *out, CUstream stream,
@@ -540,7 +580,7 @@ int run_impl(const jm_run_desc *d) {
   int rc = validate_run(d);
   if (rc != JM_OK || d->batch == 0) return rc;
   Slot *s = nullptr;
-  if ((rc = lookup(d->n, d->dtype, d->addend, d->kind, &s)) != JM_OK) return rc;
+  if ((rc = lookup_run(*d, &s)) != JM_OK) return rc;
   if ((rc = ensure_ctx()) != JM_OK) return rc;
   if (d->flags & JM_FLAG_HOST_BUFFERS) return run_host(d, *s);
   CUstream st = (CUstream)(d->stream ? d->stream : G.stream.load(std::memory_order_relaxed));
@@ -571,7 +611,7 @@ int run_many_impl(const jm_run_desc *d, int count, void *stream, unsigned flags)
   std::vector<int> todo;
   for (int i = 0; i < count; ++i) {
     if (d[i].batch == 0) continue;
-    Slot &s = g_slots[d[i].kind][d[i].addend][d[i].dtype][d[i].n];
+    Slot &s = slot_of(d[i].n, d[i].dtype, d[i].addend, d[i].kind, want_stream(d[i].n, d[i].dtype, d[i].kind, d[i].repeat, d[i].flags));
     if (s.state.load(std::memory_order_acquire) != S_READY) todo.push_back(i);
   }
   if (todo.size() > 1) {
@@ -582,7 +622,7 @@ int run_many_impl(const jm_run_desc *d, int count, void *stream, unsigned flags)
       th.emplace_back([&, t] {
         Slot *s = nullptr;
         const jm_run_desc &x = d[todo[t]];
-        rcs[t] = lookup(x.n, x.dtype, x.addend, x.kind, &s);
+        rcs[t] = lookup_run(x, &s);
         if (rcs[t] != JM_OK) errs[t] = t_err;
       });
     for (auto &t : th) t.join();
@@ -591,7 +631,7 @@ int run_many_impl(const jm_run_desc *d, int count, void *stream, unsigned flags)
   }
   for (int i = 0; i < count; ++i) {
     if (d[i].batch == 0) continue;
-    int rc = lookup(d[i].n, d[i].dtype, d[i].addend, d[i].kind, &slots[(size_t)i]);
+    int rc = lookup_run(d[i], &slots[(size_t)i]);
     if (rc != JM_OK) return rc;
   }
   int rc = ensure_ctx();
@@ -764,6 +804,9 @@ int jit_mat_shutdown(void) {
   for (int k = 0; k < 2; ++k)
     for (int d = 0; d <= jm::MASS_MAX; ++d)
       for (int q = 0; q <= jm::MASS_MAX; ++q) reset(g_mass_slots[k][d][q]);
+  for (int a = 0; a < NADD; ++a)
+    for (int t = 0; t < NDT; ++t)
+      for (int n = 0; n <= NMAX; ++n) reset(g_stream_slots[a][t][n]);
   {
     std::lock_guard<std::mutex> hl(G.host_mu);
     for (int i = 0; i < 3; ++i) {
@@ -818,57 +861,93 @@ int jit_mat_run_host(int n, int dtype, int64_t batch, int64_t repeat, const void
   return run_impl(&d);
 }
 
+// Blob "JMC2": magic, key {n, dtype, addend}, entry count, then per compiled
+// variant of the key (0 resident, 1 streaming): variant, symbol length,
+// symbol, cubin length, cubin.
 int jit_mat_cache_export(int n, int dtype, int addend, void *buf, size_t cap, size_t *len) {
   int rc = check_key(n, dtype, addend, JM_KIND_SPECIALIZED);
   if (rc != JM_OK) return rc;
   if (!len) return fail(JM_E_INVALID, "NULL len");
-  Slot &s = g_slots[JM_KIND_SPECIALIZED][addend][dtype][n];
-  if (s.state.load(std::memory_order_acquire) != S_READY || s.cubin.empty())
+  Slot *vs[2] = {&g_slots[JM_KIND_SPECIALIZED][addend][dtype][n], &g_stream_slots[addend][dtype][n]};
+  std::unique_lock<std::mutex> l0(vs[0]->mu), l1(vs[1]->mu);
+  bool have[2];
+  size_t total = 4 + 3 * 4 + 4;
+  int count = 0;
+  for (int v = 0; v < 2; ++v) {
+    have[v] = vs[v]->state.load(std::memory_order_acquire) == S_READY && !vs[v]->cubin.empty();
+    if (!have[v]) continue;
+    ++count;
+    total += 4 + 4 + vs[v]->lowered.size() + 8 + vs[v]->cubin.size();
+  }
+  if (!count)
     return fail(JM_E_INVALID, "key n=%d dtype=%d addend=%d is not compiled in this process", n, dtype, addend);
-  std::lock_guard<std::mutex> lk(s.mu);
-  const uint32_t nl = (uint32_t)s.lowered.size();
-  const uint64_t cl = (uint64_t)s.cubin.size();
-  const size_t total = 4 + 3 * 4 + 4 + nl + 8 + cl;
   *len = total;
   if (!buf) return JM_OK;
   if (cap < total) return fail(JM_E_INVALID, "buffer too small (%zu < %zu)", cap, total);
   char *p = (char *)buf;
   const int32_t key[3] = {n, dtype, addend};
-  memcpy(p, "JMC1", 4); p += 4;
+  const int32_t cnt = count;
+  memcpy(p, "JMC2", 4); p += 4;
   memcpy(p, key, sizeof key); p += sizeof key;
-  memcpy(p, &nl, 4); p += 4;
-  memcpy(p, s.lowered.data(), nl); p += nl;
-  memcpy(p, &cl, 8); p += 8;
-  memcpy(p, s.cubin.data(), cl);
+  memcpy(p, &cnt, 4); p += 4;
+  for (int v = 0; v < 2; ++v) {
+    if (!have[v]) continue;
+    const int32_t var = v;
+    const uint32_t nl = (uint32_t)vs[v]->lowered.size();
+    const uint64_t cl = (uint64_t)vs[v]->cubin.size();
+    memcpy(p, &var, 4); p += 4;
+    memcpy(p, &nl, 4); p += 4;
+    memcpy(p, vs[v]->lowered.data(), nl); p += nl;
+    memcpy(p, &cl, 8); p += 8;
+    memcpy(p, vs[v]->cubin.data(), cl); p += cl;
+  }
   return JM_OK;
 }
 
 int jit_mat_cache_import(const void *blob, size_t len) {
-  if (!blob || len < 4 + 12 + 4 + 8) return fail(JM_E_INVALID, "blob too short");
+  if (!blob || len < 4 + 12 + 4) return fail(JM_E_INVALID, "blob too short");
   if (!G.inited.load(std::memory_order_acquire)) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
   const char *p = (const char *)blob, *end = p + len;
-  if (memcmp(p, "JMC1", 4) != 0) return fail(JM_E_INVALID, "not a jitmat cubin blob");
+  if (memcmp(p, "JMC2", 4) != 0) return fail(JM_E_INVALID, "not a jitmat cubin blob");
   p += 4;
-  int32_t key[3];
+  int32_t key[3], cnt;
   memcpy(key, p, sizeof key); p += sizeof key;
+  memcpy(&cnt, p, 4); p += 4;
   int rc = check_key(key[0], key[1], key[2], JM_KIND_SPECIALIZED);
   if (rc != JM_OK) return rc;
-  uint32_t nl;
-  memcpy(&nl, p, 4); p += 4;
-  if ((size_t)(end - p) < (size_t)nl + 8) return fail(JM_E_INVALID, "truncated blob");
-  std::string lowered(p, nl); p += nl;
-  uint64_t cl;
-  memcpy(&cl, p, 8); p += 8;
-  if ((uint64_t)(end - p) != cl || cl == 0) return fail(JM_E_INVALID, "truncated blob");
-  if (lowered.find("k_update") == std::string::npos) return fail(JM_E_INVALID, "unexpected kernel symbol");
-  Slot &s = g_slots[JM_KIND_SPECIALIZED][key[2]][key[1]][key[0]];
-  std::lock_guard<std::mutex> lk(s.mu);
-  if (s.state.load(std::memory_order_acquire) == S_READY) return JM_OK;
-  std::vector<char> cubin(p, p + cl);
-  if ((rc = install_cubin(s, OP_UPDATE, key[0], key[1], key[2], std::move(cubin), lowered)) != JM_OK) return rc;
-  s.compile_ms = 0.0;
-  c_imports++;
-  s.state.store(S_READY, std::memory_order_release);
+  if (cnt < 1 || cnt > 2) return fail(JM_E_INVALID, "corrupt blob (entry count %d)", cnt);
+  // parse every entry before installing any
+  struct Entry { int32_t v; std::string sym; const char *cubin; uint64_t cl; };
+  std::vector<Entry> es;
+  for (int i = 0; i < cnt; ++i) {
+    Entry e{};
+    uint32_t nl;
+    if ((size_t)(end - p) < 8) return fail(JM_E_INVALID, "truncated blob");
+    memcpy(&e.v, p, 4); p += 4;
+    memcpy(&nl, p, 4); p += 4;
+    if (e.v < 0 || e.v > 1) return fail(JM_E_INVALID, "corrupt blob (variant %d)", e.v);
+    if ((size_t)(end - p) < (size_t)nl + 8) return fail(JM_E_INVALID, "truncated blob");
+    e.sym.assign(p, nl); p += nl;
+    memcpy(&e.cl, p, 8); p += 8;
+    if ((uint64_t)(end - p) < e.cl || e.cl == 0) return fail(JM_E_INVALID, "truncated blob");
+    e.cubin = p; p += e.cl;
+    if (e.sym.find(e.v ? "k_update_stream" : "k_update") == std::string::npos ||
+        (e.v == 0 && e.sym.find("k_update_stream") != std::string::npos))
+      return fail(JM_E_INVALID, "unexpected kernel symbol");
+    es.push_back(std::move(e));
+  }
+  if (p != end) return fail(JM_E_INVALID, "trailing bytes in blob");
+  for (const Entry &e : es) {
+    Slot &s = e.v ? g_stream_slots[key[2]][key[1]][key[0]] : g_slots[JM_KIND_SPECIALIZED][key[2]][key[1]][key[0]];
+    std::lock_guard<std::mutex> lk(s.mu);
+    if (s.state.load(std::memory_order_acquire) == S_READY) continue;
+    std::vector<char> cubin(e.cubin, e.cubin + e.cl);
+    if ((rc = install_cubin(s, e.v ? OP_UPDATE_STREAM : OP_UPDATE, key[0], key[1], key[2], std::move(cubin), e.sym)) != JM_OK)
+      return rc;
+    s.compile_ms = 0.0;
+    c_imports++;
+    s.state.store(S_READY, std::memory_order_release);
+  }
   return JM_OK;
 }
 
@@ -880,6 +959,17 @@ int jit_mat_set_stream(void *cuda_stream) {
 int jit_mat_prepare(int n, int dtype, int addend, int kind) {
   Slot *s = nullptr;
   return lookup(n, dtype, addend, kind, &s);
+}
+
+int jit_mat_prepare_for(int n, int dtype, int addend, int kind, int64_t repeat, unsigned flags, int *variant) {
+  int rc = check_key(n, dtype, addend, kind);
+  if (rc != JM_OK) return rc;
+  if (repeat < 0 || repeat > JM_REPEAT_MAX) return fail(JM_E_INVALID, "repeat must be in [0, 2^31)");
+  jm_run_desc d{n, dtype, addend, kind, 1, repeat, nullptr, nullptr, nullptr, flags};
+  Slot *s = nullptr;
+  if ((rc = lookup_run(d, &s)) != JM_OK) return rc;
+  if (variant) *variant = want_stream(n, dtype, kind, repeat, flags) ? 1 : 0;
+  return JM_OK;
 }
 
 int jit_mat_dtype_from_name(const char *name) {
@@ -903,9 +993,11 @@ int jit_mat_stats(jm_stats *out) {
   for (int a = 0; a < NADD; ++a)
     for (int t = 0; t < NDT; ++t)
       for (int n = 1; n <= NMAX; ++n) {
-        const int st = g_slots[JM_KIND_SPECIALIZED][a][t][n].state.load();
-        ready += st == S_READY;
-        failed += st == S_FAILED;
+        for (const Slot *sl : {&g_slots[JM_KIND_SPECIALIZED][a][t][n], &g_stream_slots[a][t][n]}) {
+          const int st = sl->state.load();
+          ready += st == S_READY;
+          failed += st == S_FAILED;
+        }
       }
   out->keys_ready = ready;
   out->keys_failed = failed;
@@ -934,9 +1026,30 @@ int jit_mat_key_info(jm_key_info *keys, int cap) {
             o.cubin_bytes = s.cubin_bytes;
             o.compile_ms = s.compile_ms;
             o.op = 0;
+            o.variant = 0;
           }
           ++cnt;
         }
+  for (int a = 0; a < NADD; ++a)
+    for (int t = 0; t < NDT; ++t)
+      for (int n = 1; n <= NMAX; ++n) {
+        Slot &s = g_stream_slots[a][t][n];
+        const int st = s.state.load(std::memory_order_acquire);
+        if (st == S_EMPTY) continue;
+        if (keys && cnt < cap) {
+          jm_key_info &o = keys[cnt];
+          o.n = n; o.dtype = t; o.addend = a; o.kind = JM_KIND_SPECIALIZED; o.state = st;
+          o.regs = s.regs; o.local_bytes = s.local_bytes; o.smem_bytes = s.plan.smem;
+          o.threads = s.plan.threads;
+          o.tile = s.plan.tile == (int)jm::Tile::Dmma ? (s.plan.w > 1 ? JM_TILE_CTA_DMMA : JM_TILE_WARP_DMMA)
+                                                      : JM_TILE_WARP_F32;
+          o.cubin_bytes = s.cubin_bytes;
+          o.compile_ms = s.compile_ms;
+          o.op = 0;
+          o.variant = 1;
+        }
+        ++cnt;
+      }
   for (int k = 0; k < 2; ++k)
     for (int t = 0; t < NDT; ++t)
       for (int n = 1; n <= NMAX; ++n) {
@@ -952,6 +1065,7 @@ int jit_mat_key_info(jm_key_info *keys, int cap) {
           o.cubin_bytes = s.cubin_bytes;
           o.compile_ms = s.compile_ms;
           o.op = 1;
+          o.variant = 0;
         }
         ++cnt;
       }
@@ -1040,9 +1154,15 @@ int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes) 
       return fail(JM_E_UNSUPPORTED, "dofs/quads must be in [1, %d]", jm::MASS_MAX);
     expr = mass_name_expression(n, dtype);
   } else {
-    rc = check_key(n, dtype, addend == JM_OP_MATMUL ? JM_ADDEND_ONES : addend, JM_KIND_SPECIALIZED);
+    const bool op = addend == JM_OP_MATMUL || addend == JM_OP_STREAM;
+    rc = check_key(n, dtype, op ? JM_ADDEND_ONES : addend, JM_KIND_SPECIALIZED);
     if (rc != JM_OK) return rc;
-    expr = addend == JM_OP_MATMUL ? mm_name_expression(n, dtype) : name_expression(n, dtype, addend);
+    if (addend == JM_OP_STREAM && !jm::stream_ok(n, dtype))
+      return fail(JM_E_UNSUPPORTED, "n=%d %s has no streaming variant (thread-per-matrix kind)", n,
+                  dtype == JM_F64 ? "double" : "float");
+    expr = addend == JM_OP_MATMUL   ? mm_name_expression(n, dtype)
+           : addend == JM_OP_STREAM ? name_expression(n, dtype, JM_ADDEND_ONES, true)
+                                    : name_expression(n, dtype, addend);
   }
   std::vector<char> cubin;
   std::string lowered, log;

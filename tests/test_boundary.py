@@ -48,6 +48,7 @@ def test_calls_fail_cleanly_without_init(jm):
     assert lib.jit_mat_run(4, 1, 1, 1, None, None) in (jm.JM_E_NOT_INITIALIZED, jm.JM_E_INVALID)
     assert lib.jit_mat_run(4, 1, 0, 1, None, None) == jm.JM_E_NOT_INITIALIZED
     assert lib.jit_mat_prepare(4, 1, 0, 0) == jm.JM_E_NOT_INITIALIZED
+    assert lib.jit_mat_prepare_for(16, 1, 0, 0, 1, 0, None) == jm.JM_E_NOT_INITIALIZED
     assert lib.jit_mat_shutdown() == jm.JM_E_NOT_INITIALIZED
     rc = lib.jit_mat_init(0)
     assert rc in (jm.JM_E_CUDA, jm.JM_E_ARCH)
@@ -81,6 +82,21 @@ def test_every_specialization_compiles_for_sm100a(jm, dtype):
     with cf.ThreadPoolExecutor(min(8, os.cpu_count() or 1)) as ex:
         sizes = list(ex.map(lambda n: jm.jit_mat_compile_check(n, dtype), range(1, 65)))
     assert all(s > 1000 for s in sizes)
+
+
+@pytest.mark.parametrize("dtype", ["double", "float"])
+def test_every_streaming_variant_compiles_for_sm100a(jm, dtype):
+    """The streaming (bulk-copy ring) variant k_update_stream<N, T, Ones> for
+    every N whose tiling kind has one; thread-per-matrix sizes have none."""
+    first = 8 if dtype == "double" else 9
+    with cf.ThreadPoolExecutor(min(8, os.cpu_count() or 1)) as ex:
+        sizes = list(ex.map(lambda n: jm.jit_mat_compile_check(n, dtype, "stream"), range(first, 65)))
+    assert all(s > 1000 for s in sizes)
+    from paper_1904_08555_b200 import JitMatError
+    for n in (1, first - 1):
+        with pytest.raises(JitMatError) as ei:
+            jm.jit_mat_compile_check(n, dtype, "stream")
+        assert ei.value.code == jm.JM_E_UNSUPPORTED
 
 
 @pytest.mark.parametrize("n", [1, 5, 8, 13, 33, 64])

@@ -195,16 +195,20 @@ def test_cache_export_import_skips_nvrtc(jm):
     _fresh(jm)
     x = torch.from_numpy(jm_synth.generate(13, "f64", "hard", 2, 0, 77)).cuda()
     ref = jm.run(x, 3, sync=True)
+    ref100 = jm.run(x, 100, sync=True)     # R = 3 runs the streaming variant, R = 100 the resident one
     blob = jm.jit_mat_cache_export(13, "double")
-    assert blob[:4] == b"JMC1" and len(blob) > 1000
+    assert blob[:4] == b"JMC2" and len(blob) > 2000
     _fresh(jm)
     jm.jit_mat_cache_import(blob)
     jm.jit_mat_cache_import(blob)          # second import: no-op
     got = jm.run(x, 3, sync=True)
+    got100 = jm.run(x, 100, sync=True)
     st = jm.jit_mat_stats()
-    assert st["compilations"] == 0 and st["imports"] == 1
-    assert torch.equal(got, ref)
+    assert st["compilations"] == 0 and st["imports"] == 2
+    assert torch.equal(got, ref) and torch.equal(got100, ref100)
     with pytest.raises(jm.JitMatError):
-        jm.jit_mat_cache_import(b"JMC1" + blob[4:40])
+        jm.jit_mat_cache_import(b"JMC2" + blob[4:40])
+    with pytest.raises(jm.JitMatError):
+        jm.jit_mat_cache_import(b"JMC1" + blob[4:])
     with pytest.raises(jm.JitMatError):
         jm.jit_mat_cache_export(14, "double")
