@@ -228,17 +228,17 @@ JM_HD constexpr bool stream_ok(int n, int dtype) {
   return tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::F32;
 }
 // The host's switch: stream iff repeat * (n + 1) < stream_rn(n, dtype).
-// Placed from the measured crossovers (profiles/r01_stream_sweep.jsonl, one
+// Placed from the measured crossovers (profiles/r01_stream_sweep*.jsonl, one
 // B200, R in {1..100}): the ring costs shared memory, hence residency, so it
 // wins while the load/store half of the roofline still matters and loses a
-// few % once the update is compute-bound.  f64 warp DMMA (n = 9..32) gains up
-// to R(n+1) ~ 600 (n = 32: 1.93x at R = 1, 1.17x at R = 8); n = 8 loses 8 % at
-// R = 1 (16 copies of 512 B per chunk) and gains <= 7 % elsewhere, so it stays
-// resident; CTA DMMA (n >= 33; n = 64 holds 131 KB of ring per CTA) to ~200;
-// f32 row panels to ~64; f32 tiles to ~140.
+// few % once the update is compute-bound.  f64 DMMA (n >= 9) gains up to
+// R(n+1) ~ 600 (n = 32: 1.96x at R = 1, 1.18x at R = 8; n = 64: 1.58x at
+// R = 1, 1.02x at R = 8); n = 8 loses 8 % at R = 1 (16 copies of 512 B per
+// chunk) and gains <= 7 % elsewhere, so it stays resident; f32 row panels
+// (n = 9..16) gain to ~64, f32 tiles (n >= 17) to ~140.
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype) ? 0
-         : dtype == 1        ? (dmma_w(n) == 1 ? (n >= 9 ? 600 : 0) : 200)
+         : dtype == 1        ? (n >= 9 ? 600 : 0)
          : f32p_use(n)       ? 64
                              : 140;
 }
@@ -252,6 +252,11 @@ JM_HD constexpr int ring_sbm(int n, int es) { return (n * n * es) % 16 == 0 ? st
 JM_HD constexpr int ring_bytes(int n, int es, int rm) {
   return JM_RING_S * ring_k(rm * n * n * es) * rm * ring_sbm(n, es) + rup(8 * JM_RING_S, 16);
 }
+// DMMA in the streaming variant: when the swizzled publish buffer fits in the
+// matrix's ring slot (n a multiple of 16), the slot is reused as that buffer
+// (W == 1) or as the first of the two (W > 1) once M sits in the accumulators:
+// n = 32 then holds 3 CTAs per SM instead of 2, n = 48 / 64 two instead of one
+JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8); }
 // matrices per round of each kind (the resident plan's chunk)
 JM_HD constexpr int round_mpc(int n, int dtype) {
   return tile_for(n, dtype) == Tile::Dmma ? (dmma_w(n) == 1 ? DMMA_WPC : 1)
@@ -266,8 +271,8 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   if (!stream_ok(n, dtype)) return plan_specialized(n, dtype);
   if (tile_for(n, dtype) == Tile::Dmma) {
     const int w = dmma_w(n);
-    return w == 1 ? Plan{(int)Tile::Dmma, 32 * DMMA_WPC, chm, ring_bytes(n, es, rm) + DMMA_WPC * dmma_scr(n), 1}
-                  : Plan{(int)Tile::Dmma, 32 * w, chm, ring_bytes(n, es, rm) + 2 * dmma_scr(n), w};
+    const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers
+    return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm) + own * dmma_scr(n), w};
   }
   if (f32p_use(n)) return Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
   return Plan{(int)Tile::F32, 32 * F32_WPC, chm, ring_bytes(n, es, rm) + rm * f32_region(n), 1};

@@ -544,12 +544,15 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   constexpr bool PF = prefetch_for(N, 1);
   typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S>,
                         Stager<N, ES, SB, NT, MPC, AL, PF>>::type Stg;
+  // streaming, n a multiple of 16: the matrix's ring slot doubles as its
+  // (first) publish buffer once M is in the accumulators (plan_stream)
+  constexpr bool INPL = STRM && dmma_inplace(N);
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int mi = (W == 1) ? warp : 0;        // matrix slot in the chunk
   const int wr = (W == 1) ? 0 : warp;        // this warp's rank within the matrix
-  char *scr = smem + Stg::BYTES + ((W == 1) ? warp * SCR : 0);
+  char *scr = smem + Stg::BYTES + ((W == 1 && !INPL) ? warp * SCR : 0);
   const double c = 0.00005;
   // Swizzled-scratch offsets factored into a few lane constants plus
   // compile-time immediates (chunk c ^ f only touches c's low 3 bits, and the
@@ -584,8 +587,12 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
             const int row = 8 * (wr * RT + I) + g, col = 8 * J + 2 * t + s;
             acc[I][J][s] = (row < N && col < N) ? sm[row * N + col] : 0.0;
           }
+      if constexpr (INPL) {                  // every warp has read M before the slot is reused
+        if constexpr (W == 1) __syncwarp(); else __syncthreads();
+      }
       for (int r = 0; r < repeat; ++r) {
-        char *sb = scr + ((W > 1) ? (r & 1) * SCR : 0);
+        char *sb = INPL ? ((W > 1 && (r & 1)) ? scr : reinterpret_cast<char *>(sm))
+                        : scr + ((W > 1) ? (r & 1) * SCR : 0);
         // publish M (own rows) for the B-fragment reads
 #pragma unroll
         for (int I = 0; I < RT; ++I)
@@ -630,6 +637,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
             }
         if constexpr (W == 1) __syncwarp();
       }
+      if constexpr (INPL && W > 1) __syncthreads();   // last B-fragment reads of the slot done
 #pragma unroll
       for (int I = 0; I < RT; ++I)
 #pragma unroll
