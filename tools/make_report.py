@@ -12,17 +12,21 @@ import sys
 def main(path: str) -> None:
     rows = [json.loads(ln) for ln in open(path) if ln.strip()]
     print(f"# Configuration sweep — `{path}` (tools/sweep.py, one B200)\n")
-    print("Roofline denominators: HBM 6458.1 GB/s (MEASURED_PEAKS.json); FP64 37.2 TF and FP32 74.4 TF "
+    import os
+    hbm = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                      "MEASURED_PEAKS.json")))["hbm_gbs"]
+    print(f"Roofline denominators: HBM {hbm} GB/s (MEASURED_PEAKS.json); FP64 37.2 TF and FP32 74.4 TF "
           "(148 SM x 64 / 128 FMA/clk x 2 x 1.965 GHz, DESIGN.md §6). Batch = 8 GB of input per config, "
           "`bench` inputs; generic = the AoT runtime-N kernel on the same inputs.\n")
     c3 = [d for d in rows if d["config"] == "C3"]
     if c3:
         print("## C3 — N sweep\n")
-        print("| n | dtype | R | tile | regs | spec ms | spec TF | frac HBM | frac pipe | generic ms | spec/generic |")
-        print("|---|---|---|---|---|---|---|---|---|---|---|")
+        print("| n | dtype | R | tile | variant | regs | spec ms | spec TF | frac HBM | frac pipe | generic ms | spec/generic |")
+        print("|---|---|---|---|---|---|---|---|---|---|---|---|")
         for d in c3:
             s, g = d["specialized"], d["generic"]
-            print(f"| {d['n']} | {d['dtype']} | {d['repeat']} | {d['tile']} | {d['regs']} | {s['ms']:.2f} | "
+            print(f"| {d['n']} | {d['dtype']} | {d['repeat']} | {d['tile']} | {d.get('variant', 'resident')} | "
+                  f"{d['regs']} | {s['ms']:.2f} | "
                   f"{s['tflops']:.2f} | {s['frac_hbm']:.3f} | {s['frac_pipe']:.3f} | {g['ms']:.2f} | {d['speedup']:.2f} |")
     for d in rows:
         if d["config"] == "C1":

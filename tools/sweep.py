@@ -97,14 +97,17 @@ def c3(fh, stream, sizes, dtypes, repeats, steps):
             y = torch.empty_like(x)
             jm.jit_mat_fill(n, dt, 1, SEED, 0, B, x.data_ptr())
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            jm.jit_mat_prepare(n, dt)
-            comp = (time.perf_counter() - t0) * 1e3
-            info = [k for k in jm.jit_mat_key_info() if k["n"] == n and k["dtype"] == (1 if dt == "f64" else 0)
-                    and k["kind"] == 0 and k["addend"] == 0][0]
             for R in repeats:
+                # the kernel this repeat count selects (resident or streaming variant)
+                t0 = time.perf_counter()
+                variant = jm.jit_mat_prepare_for(n, dt, R)
+                comp = (time.perf_counter() - t0) * 1e3
+                info = [k for k in jm.jit_mat_key_info() if k["op"] == 0 and k["n"] == n
+                        and k["dtype"] == (1 if dt == "f64" else 0)
+                        and k["kind"] == 0 and k["addend"] == 0 and k["variant"] == variant][0]
                 row = {"config": "C3", "n": n, "dtype": dt, "batch": B, "repeat": R,
-                       "tile": info["tile_name"], "regs": info["regs"], "smem": info["smem_bytes"],
+                       "tile": info["tile_name"], "variant": "streaming" if variant else "resident",
+                       "regs": info["regs"], "smem": info["smem_bytes"],
                        "nvrtc_ms": info["compile_ms"], "first_prepare_ms": comp}
                 t_hbm = 2 * B * n * n * es / (HBM * 1e9)
                 t_cmp = B * R * fpu(n) / (PEAK[dt] * 1e12)
