@@ -6,7 +6,7 @@
 // mapped onto the B200:
 //   TPM   thread-per-matrix, whole matrix in registers      f64 N<=6, f32 N<=8
 //   DMMA  FP64 tensor-core DMMA.8x8x4 (mma.sync m8n8k4.f64), N padded to 8k;
-//         W warps per matrix (W=1 for N<=32, else one CTA per matrix)
+//         W warps per matrix (W=1 up to N=40 resident / 32 streaming, else a CTA)
 //   F32   FP32 register-tiled outer products with FFMA2, W warps per matrix
 //   GENERIC the AoT runtime-N kernel (never NVRTC-compiled)
 #ifndef JM_PLAN_H
@@ -73,22 +73,36 @@ constexpr int TPM_THREADS = 128;
 
 // ---- DMMA (FP64) ----
 #ifndef JM_DMMA_WARP_MAX
-#define JM_DMMA_WARP_MAX 32  // whole matrix in one warp up to this n
+#define JM_DMMA_WARP_MAX 40          // resident kernel: whole matrix in one warp up to this n
+#endif
+#ifndef JM_DMMA_WARP_MAX_STREAM
+#define JM_DMMA_WARP_MAX_STREAM 32   // streaming variant: whole matrix in one warp up to this n
 #endif
 #ifndef JM_DMMA_RT_LARGE
-#define JM_DMMA_RT_LARGE 1   // row tiles per warp for n > 32 (one warp per 8-row tile)
+#define JM_DMMA_RT_LARGE 1   // row tiles per warp for other n > WARP_MAX (one warp per 8-row tile)
 #endif
 constexpr int DMMA_WPC = 4;                       // warps per CTA when W == 1
 JM_HD constexpr int dmma_t8(int n) { return cdiv(n, 8); }
-// row tiles per warp: whole matrix per warp up to n = 24; two warps of two
-// row tiles for 25..32 (keeps the accumulators + product under ~128 regs);
-// above 32 one CTA per matrix: 4 warps x 2 row tiles for 57..64, one row tile
-// per warp otherwise (r01 sweep: n=48 0.69 -> 0.72 of the FP64 pipe with one
-// tile per warp, n=64 0.92 with two vs 0.87 with one).
-JM_HD constexpr int dmma_rt(int n) {
-  return n <= JM_DMMA_WARP_MAX ? dmma_t8(n) : ((n <= 32 || dmma_t8(n) == 8) ? 2 : JM_DMMA_RT_LARGE);
+// Row tiles per warp (W = T8 / RT warps share a matrix), measured on B200
+// (profiles/r01_dmma_rt_sweep.jsonl, FP64 pipe fraction at R = 100):
+//  * whole matrix per warp (RT = T8) up to n = 40 in the resident kernel:
+//    n = 33..40 0.51-0.82 -> 0.60-0.93 over one warp per 8-row tile, the
+//    B fragment of a k-step now feeding 5 row tiles instead of 1 (210-226
+//    registers, 2 CTAs of 4 warps per SM, no spill);
+//  * 41..48 (T8 = 6): two warps of 3 row tiles (n = 48 0.84 -> 0.93, n = 44
+//    0.65 -> 0.70; up to 255 registers, no spill);
+//  * 57..64 (T8 = 8): four warps of 2 row tiles (n = 64 0.96);
+//  * 49..56 (T8 = 7, prime): one warp per row tile.
+// The streaming variant keeps one warp per row tile above n = 32: its ring
+// leaves too little shared memory for 4 whole-matrix warps per CTA, and at
+// its low repeat counts the wider CTAs stream better.
+JM_HD constexpr int dmma_rt(int n, bool strm = false) {
+  return n <= (strm ? JM_DMMA_WARP_MAX_STREAM : JM_DMMA_WARP_MAX) ? dmma_t8(n)
+         : dmma_t8(n) == 8                                         ? 2
+         : (!strm && dmma_t8(n) == 6)                              ? 3
+                                                                   : JM_DMMA_RT_LARGE;
 }
-JM_HD constexpr int dmma_w(int n) { return dmma_t8(n) / dmma_rt(n); }
+JM_HD constexpr int dmma_w(int n, bool strm = false) { return dmma_t8(n) / dmma_rt(n, strm); }
 JM_HD constexpr int dmma_rsc(int n) { return rup(4 * dmma_t8(n), 8); }     // scratch row stride, 16-B chunks
 JM_HD constexpr int dmma_scr(int n) { return 8 * dmma_t8(n) * dmma_rsc(n) * 16; }  // one scratch buffer
 
@@ -203,8 +217,8 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
 
 // Which entry point the specialization uses: k_update (maxThreads only) or
 // k_update_mb1 (maxThreads, minBlocks = 1) — the CTA-per-matrix DMMA kinds.
-JM_HD constexpr bool use_mb1(int n, int dtype) {
-  return tile_for(n, dtype) == Tile::Dmma && dmma_w(n) > 1;
+JM_HD constexpr bool use_mb1(int n, int dtype, bool strm = false) {
+  return tile_for(n, dtype) == Tile::Dmma && dmma_w(n, strm) > 1;
 }
 
 // ---- streaming variant (low repeat: the HBM-bound side of the roofline) ----
@@ -259,7 +273,7 @@ JM_HD constexpr int ring_bytes(int n, int es, int rm) {
 JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8); }
 // matrices per round of each kind (the resident plan's chunk)
 JM_HD constexpr int round_mpc(int n, int dtype) {
-  return tile_for(n, dtype) == Tile::Dmma ? (dmma_w(n) == 1 ? DMMA_WPC : 1)
+  return tile_for(n, dtype) == Tile::Dmma ? (dmma_w(n, true) == 1 ? DMMA_WPC : 1)
          : f32p_use(n)                   ? F32P_WPC * f32p_mpw(n)
                                          : F32_WPC * f32_mpw(n);
 }
@@ -270,7 +284,7 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   const int rm = round_mpc(n, dtype), rb = rm * n * n * es, chm = ring_k(rb) * rm;
   if (!stream_ok(n, dtype)) return plan_specialized(n, dtype);
   if (tile_for(n, dtype) == Tile::Dmma) {
-    const int w = dmma_w(n);
+    const int w = dmma_w(n, true);
     const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers
     return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm) + own * dmma_scr(n), w};
   }

@@ -534,7 +534,7 @@ __device__ __forceinline__ void dmma884_c(double &d0, double &d1, double a, doub
 template <int N, Addend A, int W, bool STRM>
 __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *__restrict__ out,
                                          long long batch, int repeat) {
-  constexpr int T8 = dmma_t8(N), RT = dmma_rt(N), RSC = dmma_rsc(N), SCR = dmma_scr(N);
+  constexpr int T8 = dmma_t8(N), RT = dmma_rt(N, STRM), RSC = dmma_rsc(N), SCR = dmma_scr(N);
   constexpr int ES = 8, MB = N * N * 8, SB = stage_stride(N, 8);
   constexpr int WPC = (W == 1) ? DMMA_WPC : W;
   constexpr int NT = 32 * WPC;
@@ -1077,7 +1077,7 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
   } else if constexpr (K == Tile::Rows) {
     run_f64p<N, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Dmma) {
-    run_dmma<N, A, dmma_w(N), STRM>(in, out, batch, repeat);
+    run_dmma<N, A, dmma_w(N, STRM), STRM>(in, out, batch, repeat);
   } else if constexpr (f32p_use(N)) {
     run_f32p<N, A, STRM>(in, out, batch, repeat);
   } else {

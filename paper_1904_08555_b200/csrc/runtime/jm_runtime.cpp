@@ -239,7 +239,7 @@ const char *tile_name(int t) {
 std::string name_expression(int n, int dtype, int addend, bool stream = false) {
   char buf[160];
   snprintf(buf, sizeof buf, "jm::%s%s<%d, %s, jm::Addend::%s, jm::Tile::%s>",
-           stream ? "k_update_stream" : "k_update", jm::use_mb1(n, dtype) ? "_mb1" : "", n,
+           stream ? "k_update_stream" : "k_update", jm::use_mb1(n, dtype, stream) ? "_mb1" : "", n,
            dtype == JM_F64 ? "double" : "float", addend == JM_ADDEND_ONES ? "Ones" : "Identity",
            tile_name((int)jm::tile_for(n, dtype)));
   return buf;
