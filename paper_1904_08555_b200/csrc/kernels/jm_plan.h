@@ -81,6 +81,9 @@ constexpr int TPM_THREADS = 128;
 #ifndef JM_DMMA_RT_LARGE
 #define JM_DMMA_RT_LARGE 1   // row tiles per warp for other n > WARP_MAX (one warp per 8-row tile)
 #endif
+#ifndef JM_DMMA_BORDER_MAX
+#define JM_DMMA_BORDER_MAX 2         // n = 8K + r, r <= this: border tiles by DFMA (run_dmma BORD)
+#endif
 constexpr int DMMA_WPC = 4;                       // warps per CTA when W == 1
 JM_HD constexpr int dmma_t8(int n) { return cdiv(n, 8); }
 // Row tiles per warp (W = T8 / RT warps share a matrix), measured on B200

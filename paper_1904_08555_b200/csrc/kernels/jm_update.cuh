@@ -547,6 +547,15 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   // streaming, n a multiple of 16: the matrix's ring slot doubles as its
   // (first) publish buffer once M is in the accumulators (plan_stream)
   constexpr bool INPL = STRM && dmma_inplace(N);
+  // thin border (n = 8K + BR, BR <= JM_DMMA_BORDER_MAX, whole matrix per warp):
+  // the last row / column tile holds only BR real rows / columns, so its
+  // 2K + 1 tiles are not sent through DMMA (7/8 of that work would be
+  // padding); their entries are dot products formed with DFMA from the lanes'
+  // own accumulators and the published M, reduced across the warp by shuffles
+  constexpr int BR = N - 8 * (T8 - 1);
+  constexpr bool BORD = (W == 1) && (N > 8) && (BR <= JM_DMMA_BORDER_MAX);
+  constexpr int KM = BORD ? T8 - 1 : RT;     // row tiles through DMMA
+  constexpr int KN = BORD ? T8 - 1 : T8;     // column tiles through DMMA
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -569,6 +578,14 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
       bofs[s][j1] = ((2 * t + s) * RSC + ((j1 * 4 + gh) ^ (2 * t ^ (s << 2)))) * 16 + 8 * gl;
 #pragma unroll
   for (int j1 = 0; j1 < 2; ++j1) pofs[j1] = ((8 * wr * RT + g) * RSC + ((j1 * 4 + t) ^ fg)) * 16;
+  // border (BORD): column pair (8K, 8K+1) of row 8J + 2t + s -> colofs[s] + 8J*RSC*16;
+  // element (8K + g', 8I + g) -> rowofs + (g'*RSC + 4*(I ^ (g' & 1)))*16
+  int colofs[2] = {0, 0}, rowofs = 0;
+  if constexpr (BORD) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) colofs[s] = ((2 * t + s) * RSC + ((4 * (T8 - 1)) ^ (2 * t ^ (s << 2)))) * 16;
+    rowofs = (8 * (T8 - 1) * RSC + gh) * 16 + 8 * gl;
+  }
 
   Stg sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
@@ -601,20 +618,93 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
             sts_f64x2(sb + pofs[J & 1] + (8 * I * RSC + 8 * (J >> 1)) * 16, acc[I][J][0], acc[I][J][1]);
         if constexpr (W == 1) __syncwarp(); else __syncthreads();
         double p[RT][T8][2];
+        if constexpr (BORD) {
+          constexpr int K = T8 - 1;
+          // column border P[8I+g][8K+c] (c < BR), every row tile I: lane (g,t)
+          // sums its own k = 8J+2t+s terms, then the 4 lanes of a row add up
+          double cs[T8][2];
+#pragma unroll
+          for (int I = 0; I < T8; ++I) cs[I][0] = cs[I][1] = 0.0;
+#pragma unroll
+          for (int J = 0; J < T8; ++J)
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              if (8 * J + s >= N) continue;
+              const char *q = sb + colofs[s] + 8 * J * RSC * 16;
+              double v0, v1 = 0.0;
+              if constexpr (BR == 2) {
+                const double2 v = *reinterpret_cast<const double2 *>(q);
+                v0 = v.x; v1 = v.y;
+              } else {
+                v0 = *reinterpret_cast<const double *>(q);
+              }
+#pragma unroll
+              for (int I = 0; I < T8; ++I) {
+                cs[I][0] = fmaT(acc[I][J][s], v0, cs[I][0]);
+                if constexpr (BR == 2) cs[I][1] = fmaT(acc[I][J][s], v1, cs[I][1]);
+              }
+            }
+#pragma unroll
+          for (int I = 0; I < T8; ++I)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+              double v = cs[I][cc];
+              if (cc < BR) {
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+              }
+              p[I][K][cc] = (cc < BR && t == 0) ? acc[I][K][cc] + v : 0.0;
+            }
+          // row border P[8K+g'][8J+2t+s] (g' < BR), column tiles J < K: lane
+          // (g,t) sums the k = 8I+g terms, then the 8 lanes of a column add up
+          double rs[BR][K > 0 ? K : 1][2];
+#pragma unroll
+          for (int q = 0; q < BR; ++q)
+#pragma unroll
+            for (int J = 0; J < K; ++J) rs[q][J][0] = rs[q][J][1] = 0.0;
+#pragma unroll
+          for (int I = 0; I < T8; ++I) {
+            double mr[BR];
+#pragma unroll
+            for (int q = 0; q < BR; ++q)
+              mr[q] = *reinterpret_cast<const double *>(sb + rowofs + (q * RSC + 4 * (I ^ (q & 1))) * 16);
+#pragma unroll
+            for (int q = 0; q < BR; ++q)
+#pragma unroll
+              for (int J = 0; J < K; ++J)
+#pragma unroll
+                for (int s = 0; s < 2; ++s) rs[q][J][s] = fmaT(mr[q], acc[I][J][s], rs[q][J][s]);
+          }
+#pragma unroll
+          for (int J = 0; J < K; ++J)
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              double mine = 0.0;
+#pragma unroll
+              for (int q = 0; q < BR; ++q) {
+                double v = rs[q][J][s];
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                if (g == q) mine = v;
+              }
+              p[K][J][s] = (g < BR) ? acc[K][J][s] + mine : 0.0;
+            }
+        }
 #pragma unroll
         for (int J = 0; J < T8; ++J) {
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             if (8 * J + s >= N) continue;   // every k of this k-step is padding: skip (compile time)
-            double b[T8];
+            double b[KN];
 #pragma unroll
-            for (int J2 = 0; J2 < T8; ++J2)
+            for (int J2 = 0; J2 < KN; ++J2)
               b[J2] = *reinterpret_cast<const double *>(sb + bofs[s][J2 & 1] +
                                                         (8 * J * RSC + 8 * (J2 >> 1)) * 16);
 #pragma unroll
-            for (int I = 0; I < RT; ++I)
+            for (int I = 0; I < KM; ++I)
 #pragma unroll
-              for (int J2 = 0; J2 < T8; ++J2) {
+              for (int J2 = 0; J2 < KN; ++J2) {
                 if (J == 0 && s == 0)   // P = M + (first k-step): accumulator init is M itself
                   dmma884_c(p[I][J2][0], p[I][J2][1], acc[I][J][s], b[J2], acc[I][J2][0], acc[I][J2][1]);
                 else
