@@ -551,9 +551,13 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   // the last row / column tile holds only BR real rows / columns, so its
   // 2K + 1 tiles are not sent through DMMA (7/8 of that work would be
   // padding); their entries are dot products formed with DFMA from the lanes'
-  // own accumulators and the published M, reduced across the warp by shuffles
+  // own accumulators and the published M, reduced across the warp by shuffles.
+  // Measured (r01_dmma_border_sweep): FP64 pipe at R = 100, n = 17 0.41 ->
+  // 0.54, 25 0.53 -> 0.67, 33 0.59 -> 0.73, 18 0.40 -> 0.43, 26 0.51 -> 0.56,
+  // 34 0.58 -> 0.64; at n = 9 / 10 (one main tile) the shuffles cost what the
+  // DMMAs save (0.23 -> 0.23 / 0.19), so those keep the padded tiles.
   constexpr int BR = N - 8 * (T8 - 1);
-  constexpr bool BORD = (W == 1) && (N > 8) && (BR <= JM_DMMA_BORDER_MAX);
+  constexpr bool BORD = (W == 1) && (N > 16) && (BR <= JM_DMMA_BORDER_MAX);
   constexpr int KM = BORD ? T8 - 1 : RT;     // row tiles through DMMA
   constexpr int KN = BORD ? T8 - 1 : T8;     // column tiles through DMMA
   extern __shared__ __align__(16) char smem[];
