@@ -5,7 +5,8 @@
     compute-sanitizer --tool racecheck python tools/sanitize_run.py
     compute-sanitizer --tool synccheck python tools/sanitize_run.py
 
-Covers TPM, warp/CTA DMMA, FP32 row panels and tiles, the generic kernels, the
+Covers TPM, warp/CTA DMMA (incl. the thin-border sizes), FP32 row panels and
+tiles, each in its resident and streaming (bulk-copy ring) variant, the generic kernels, the
 AoT specializations, the multiply-accumulate, fill, checksum, run_many and the
 host-buffer path, each on a ragged batch (several chunks + a partial one).
 Exits non-zero on any library error; the sanitizer reports the rest.
@@ -23,9 +24,9 @@ import torch  # noqa: E402
 
 import paper_1904_08555_b200 as jm  # noqa: E402
 
-CASES = [(2, "f64"), (3, "f64"), (5, "f64"), (7, "f64"), (16, "f64"), (13, "f64"), (32, "f64"),
-         (40, "f64"), (64, "f64"), (3, "f32"), (8, "f32"), (12, "f32"), (16, "f32"), (24, "f32"),
-         (33, "f32"), (64, "f32")]
+CASES = [(2, "f64"), (3, "f64"), (5, "f64"), (7, "f64"), (16, "f64"), (13, "f64"), (17, "f64"),
+         (26, "f64"), (32, "f64"), (33, "f64"), (40, "f64"), (44, "f64"), (48, "f64"), (64, "f64"),
+         (3, "f32"), (8, "f32"), (12, "f32"), (16, "f32"), (24, "f32"), (33, "f32"), (64, "f32")]
 
 
 def main():
@@ -39,6 +40,9 @@ def main():
         for kind in ("specialized", "generic"):
             for addend in ("ones", "identity"):
                 jm.run(x, 2, addend=addend, kind=kind, sync=True)
+        for variant in ("resident", "streaming"):      # both variants where the kind has two
+            jm.run(x, 2, variant=variant, sync=True)
+            jm.run(x.clone(), 1, variant=variant, sync=True)
         y = x.clone()
         jm.run(y, 2, y, sync=True)                       # in place
         jm.jit_mat_checksum(n, dt, 0, batch, y.data_ptr())
@@ -46,6 +50,12 @@ def main():
         jm.matmul(x, x, c, sync=True)
         jm.matmul(x, x, c, kind="generic", sync=True)
         print(f"ok n={n} {dt}", flush=True)
+    # streaming ring with several chunks per CTA (refills behind bulk stores)
+    for n, dt, b in ((16, "f64", 4741), (33, "f64", 700), (20, "f32", 3001)):
+        tdt = torch.float64 if dt == "f64" else torch.float32
+        x = torch.rand(b, n, n, dtype=tdt, device="cuda")
+        jm.run(x, 1, variant="streaming", sync=True)
+        print(f"ok ring n={n} {dt} batch={b}", flush=True)
     x = torch.rand(11, 16, 16, dtype=torch.float64, device="cuda")
     jm.run(x, 3, kind="aot_specialized", sync=True)
     groups = []
