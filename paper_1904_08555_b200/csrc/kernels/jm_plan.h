@@ -245,17 +245,22 @@ JM_HD constexpr bool stream_ok(int n, int dtype) {
   return tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::F32;
 }
 // The host's switch: stream iff repeat * (n + 1) < stream_rn(n, dtype).
-// Placed from the measured crossovers (profiles/r01_stream_sweep*.jsonl, one
-// B200, R in {1..100}): the ring costs shared memory, hence residency, so it
-// wins while the load/store half of the roofline still matters and loses a
-// few % once the update is compute-bound.  f64 DMMA (n >= 9) gains up to
-// R(n+1) ~ 600 (n = 32: 1.96x at R = 1, 1.18x at R = 8; n = 64: 1.58x at
-// R = 1, 1.02x at R = 8); n = 8 loses 8 % at R = 1 (16 copies of 512 B per
-// chunk) and gains <= 7 % elsewhere, so it stays resident; f32 row panels
+// Placed from the measured crossovers (profiles/r01_stream_sweep*.jsonl and
+// r01_stream_xover.jsonl, one B200): the ring costs shared memory, hence
+// residency, and above n = 32 the streaming variant also keeps the narrower
+// CTA mapping, so it wins while the load/store half of the roofline still
+// matters and loses once the update is compute-bound.  f64: n = 9..32 gains up
+// to R(n+1) ~ 600 (n = 32: 1.96x at R = 1, 1.18x at R = 8); n = 33 / 34 (the
+// resident kernel has the thin border there) only at R <= 2; 35..40 to ~300;
+// 41..48 to ~250; 49..56 to ~600; 57..64 to ~400; n = 8 loses 8 % at R = 1
+// (16 copies of 512 B per chunk) and stays resident.  f32 row panels
 // (n = 9..16) gain to ~64, f32 tiles (n >= 17) to ~140.
+JM_HD constexpr int stream_rn_f64(int n) {
+  return n <= 8 ? 0 : n <= 32 ? 600 : n <= 34 ? 100 : n <= 40 ? 300 : n <= 48 ? 250 : n <= 56 ? 600 : 400;
+}
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype) ? 0
-         : dtype == 1        ? (n >= 9 ? 600 : 0)
+         : dtype == 1        ? stream_rn_f64(n)
          : f32p_use(n)       ? 64
                              : 140;
 }

@@ -111,8 +111,10 @@ def test_variant_selection_and_key_info(jm):
     assert jm.jit_mat_prepare_for(16, "f64", 1) == 1
     assert jm.jit_mat_prepare_for(16, "f64", 35) == 1      # 595 < 600
     assert jm.jit_mat_prepare_for(16, "f64", 36) == 0      # 612
-    assert jm.jit_mat_prepare_for(64, "f64", 9) == 1       # 585 < 600
-    assert jm.jit_mat_prepare_for(64, "f64", 10) == 0
+    assert jm.jit_mat_prepare_for(64, "f64", 6) == 1       # 390 < 400
+    assert jm.jit_mat_prepare_for(64, "f64", 7) == 0
+    assert jm.jit_mat_prepare_for(33, "f64", 2) == 1       # 68 < 100: thin-border resident above
+    assert jm.jit_mat_prepare_for(33, "f64", 3) == 0
     assert jm.jit_mat_prepare_for(16, "f32", 3) == 1       # 51 < 64
     assert jm.jit_mat_prepare_for(16, "f32", 4) == 0
     assert jm.jit_mat_prepare_for(64, "f32", 2) == 1       # 130 < 140

@@ -1,4 +1,2 @@
-mkdir -p gpurun_out/san
-for tool in memcheck racecheck synccheck initcheck; do
-  timeout 1500 compute-sanitizer --tool $tool python tools/sanitize_run.py > gpurun_out/san/$tool.txt 2>&1; echo $tool rc=$?; tail -1 gpurun_out/san/$tool.txt
-done
+timeout 900 python -m pytest tests/test_gpu_stream.py -q -x 2>&1 | tail -2
+timeout 900 python tools/sweep.py --only c4 --out gpurun_out/c4b.jsonl > /dev/null 2>&1; echo rc=$?
