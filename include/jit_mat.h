@@ -122,7 +122,9 @@ JM_API int jit_mat_init(int device);
  * somewhat beyond) runs the STREAMING variant of the same
  * specialization — the same tile code behind a bulk-copy (TMA) ring — which is
  * a second cache key, compiled on its first such call.  Results agree with the
- * resident kernel bit for bit (same arithmetic in the same order).  Environment
+ * resident kernel bit for bit (same arithmetic in the same order), except f64
+ * n = 33, 34, where the resident kernel forms the thin border with DFMA (both
+ * within the parity bound).  Environment
  * JIT_MAT_STREAM=0/1 forces resident/streaming, JIT_MAT_STREAM_RN moves the
  * switch point (read once per process); per call, jm_run_desc.flags
  * JM_FLAG_RESIDENT / JM_FLAG_STREAMING force it. */

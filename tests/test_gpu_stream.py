@@ -6,8 +6,9 @@ the library picks it when repeat * (n + 1) is below the roofline switch point
 (include/jit_mat.h VARIANT).  Both variants are forced here for every n that
 has one, on parity-hard inputs, with batches that span
 several ring chunks and a ragged tail, and at sizes where every CTA walks the
-ring through several phase flips.  The two variants do the same arithmetic in
-the same order, so they must also agree bit for bit.
+ring through several phase flips.  Where the two variants use the same tile
+mapping they do the same arithmetic in the same order and must agree bit for
+bit (all sizes but f64 n = 33, 34).
 """
 from __future__ import annotations
 
@@ -44,6 +45,13 @@ def _batch_for(n):
     return 293 if n <= 12 else (77 if n <= 32 else 9)
 
 
+def _same_bits(n, dt):
+    # both variants form every entry in the same order, except f64 n = 33 / 34,
+    # where the resident kernel (whole matrix per warp) takes the thin-border
+    # DFMA path and the streaming one (one warp per row tile) does not
+    return not (dt == "f64" and n in (33, 34))
+
+
 def _run(jm, x, repeat, variant, addend="ones", inplace=False):
     xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
     out = xd if inplace else torch.empty_like(xd)
@@ -62,8 +70,11 @@ def test_stream_parity_all_n(jm, n, dt):
         got_s = _run(jm, x, r, "streaming")
         assert_parity(got_s, want, what=f"streaming n={n} {dt} R={r}")
         got_r = _run(jm, x, r, "resident")
-        assert np.array_equal(got_s.view(np.uint8), got_r.view(np.uint8)), \
-            f"streaming and resident differ bitwise at n={n} {dt} R={r}"
+        if _same_bits(n, dt):
+            assert np.array_equal(got_s.view(np.uint8), got_r.view(np.uint8)), \
+                f"streaming and resident differ bitwise at n={n} {dt} R={r}"
+        else:
+            assert_parity(got_r, want, what=f"resident n={n} {dt} R={r}")
 
 
 @pytest.mark.parametrize("dt", ["f64", "f32"])
@@ -88,7 +99,11 @@ def test_stream_ring_wraps(jm, n, dt):
     rng = np.random.default_rng(n)
     idx = np.unique(np.r_[0:96, batch - 96:batch, rng.integers(0, batch, 512)])
     assert_parity(got[idx], oracle.run(x[idx], 2), what=f"ring n={n} {dt} batch={batch}")
-    assert np.array_equal(got, _run(jm, x, 2, "resident"))
+    res = _run(jm, x, 2, "resident")
+    if _same_bits(n, dt):
+        assert np.array_equal(got, res)
+    else:
+        assert_parity(res[idx], oracle.run(x[idx], 2), what=f"ring resident n={n} {dt}")
 
 
 @pytest.mark.parametrize("n,dt", [(16, "f64"), (40, "f64"), (20, "f32"), (64, "f32")])
