@@ -78,6 +78,9 @@ constexpr int TPM_THREADS = 128;
 #ifndef JM_DMMA_WARP_MAX_STREAM
 #define JM_DMMA_WARP_MAX_STREAM 32   // streaming variant: whole matrix in one warp up to this n
 #endif
+#ifndef JM_DMMA_RT_T8_7
+#define JM_DMMA_RT_T8_7 1            // resident n = 49..56: row tiles per warp (4 = two warps of 4 + 3)
+#endif
 #ifndef JM_DMMA_RT_LARGE
 #define JM_DMMA_RT_LARGE 1   // row tiles per warp for other n > WARP_MAX (one warp per 8-row tile)
 #endif
@@ -95,7 +98,10 @@ JM_HD constexpr int dmma_t8(int n) { return cdiv(n, 8); }
 //  * 41..48 (T8 = 6): two warps of 3 row tiles (n = 48 0.84 -> 0.93, n = 44
 //    0.65 -> 0.70; up to 255 registers, no spill);
 //  * 57..64 (T8 = 8): four warps of 2 row tiles (n = 64 0.96);
-//  * 49..56 (T8 = 7, prime): one warp per row tile.
+//  * 49..56 (T8 = 7): one warp per row tile.  Two warps of 4 + 3 row tiles
+//    (JM_DMMA_RT_T8_7=4, RAG in run_dmma) measured worse: 255 registers,
+//    8 warps per SM, n = 49 0.61 -> 0.43, n = 56 0.82 -> 0.70
+//    (profiles/r01_dmma_rt_experiments.jsonl).
 // The streaming variant keeps one warp per row tile above n = 32: its ring
 // leaves too little shared memory for 4 whole-matrix warps per CTA, and at
 // its low repeat counts the wider CTAs stream better.
@@ -103,9 +109,10 @@ JM_HD constexpr int dmma_rt(int n, bool strm = false) {
   return n <= (strm ? JM_DMMA_WARP_MAX_STREAM : JM_DMMA_WARP_MAX) ? dmma_t8(n)
          : dmma_t8(n) == 8                                         ? 2
          : (!strm && dmma_t8(n) == 6)                              ? 3
+         : (!strm && dmma_t8(n) == 7)                              ? JM_DMMA_RT_T8_7
                                                                    : JM_DMMA_RT_LARGE;
 }
-JM_HD constexpr int dmma_w(int n, bool strm = false) { return dmma_t8(n) / dmma_rt(n, strm); }
+JM_HD constexpr int dmma_w(int n, bool strm = false) { return cdiv(dmma_t8(n), dmma_rt(n, strm)); }
 JM_HD constexpr int dmma_rsc(int n) { return rup(4 * dmma_t8(n), 8); }     // scratch row stride, 16-B chunks
 JM_HD constexpr int dmma_scr(int n) { return 8 * dmma_t8(n) * dmma_rsc(n) * 16; }  // one scratch buffer
 

@@ -540,7 +540,10 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   constexpr int NT = 32 * WPC;
   constexpr int MPC = (W == 1) ? DMMA_WPC : 1;
   constexpr bool AL = ((MPC * MB) % 16) == 0;
-  static_assert(RT * W == T8, "row tiles must cover the matrix");
+  static_assert(RT * W >= T8 && RT * (W - 1) < T8, "row tiles must cover the matrix");
+  // RAG: the last warp owns fewer row tiles (T8 = 7 as 4 + 3); its phantom
+  // tiles are skipped by warp-uniform branches
+  constexpr bool RAG = RT * W != T8;
   constexpr bool PF = prefetch_for(N, 1);
   typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S>,
                         Stager<N, ES, SB, NT, MPC, AL, PF>>::type Stg;
@@ -616,10 +619,12 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
                         : scr + ((W > 1) ? (r & 1) * SCR : 0);
         // publish M (own rows) for the B-fragment reads
 #pragma unroll
-        for (int I = 0; I < RT; ++I)
+        for (int I = 0; I < RT; ++I) {
+          if (RAG && wr * RT + I >= T8) continue;
 #pragma unroll
           for (int J = 0; J < T8; ++J)
             sts_f64x2(sb + pofs[J & 1] + (8 * I * RSC + 8 * (J >> 1)) * 16, acc[I][J][0], acc[I][J][1]);
+        }
         if constexpr (W == 1) __syncwarp(); else __syncthreads();
         double p[RT][T8][2];
         if constexpr (BORD) {
@@ -709,6 +714,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
             for (int I = 0; I < KM; ++I)
 #pragma unroll
               for (int J2 = 0; J2 < KN; ++J2) {
+                if (RAG && wr * RT + I >= T8) continue;
                 if (J == 0 && s == 0)   // P = M + (first k-step): accumulator init is M itself
                   dmma884_c(p[I][J2][0], p[I][J2][1], acc[I][J][s], b[J2], acc[I][J2][0], acc[I][J2][1]);
                 else
@@ -726,7 +732,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
               const int row = 8 * (wr * RT + I) + g, col = 8 * J + 2 * t + s;
               const double a = (A == Addend::Ones || row == col) ? 1.0 : 0.0;
               double v = fmaT(c, p[I][J][s], a);
-              if constexpr (N % 8 != 0) v = (row < N && col < N) ? v : 0.0;
+              if constexpr (N % 8 != 0 || RAG) v = (row < N && col < N) ? v : 0.0;
               acc[I][J][s] = v;
             }
         if constexpr (W == 1) __syncwarp();
