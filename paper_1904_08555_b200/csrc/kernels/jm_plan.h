@@ -277,9 +277,24 @@ JM_HD constexpr int ring_k(int rb) {
 }
 // matrix stride in a ring stage: the odd-16-B stage stride when a matrix is a
 // multiple of 16 B (one bulk copy per matrix), else packed (one per chunk)
-JM_HD constexpr int ring_sbm(int n, int es) { return (n * n * es) % 16 == 0 ? stage_stride(n, es) : n * n * es; }
-JM_HD constexpr int ring_bytes(int n, int es, int rm) {
-  return JM_RING_S * ring_k(rm * n * n * es) * rm * ring_sbm(n, es) + rup(8 * JM_RING_S, 16);
+// (slot: a larger per-matrix slot a kind wants to work in, see f32_ring_slot)
+JM_HD constexpr int ring_sbm(int n, int es, int slot = 0) {
+  return (n * n * es) % 16 == 0 ? (slot > stage_stride(n, es) ? slot : stage_stride(n, es)) : n * n * es;
+}
+JM_HD constexpr int ring_bytes(int n, int es, int rm, int slot = 0) {
+  return JM_RING_S * ring_k(rm * n * n * es) * rm * ring_sbm(n, es, slot) + rup(8 * JM_RING_S, 16);
+}
+// FP32 tiles, streaming: when matrices are bulk-copied one per slot (n even),
+// each slot can be a whole f32_region, so the kind works in place (publishes
+// its padded M over the staged matrix, as the resident kernel does) with no
+// separate work area (n = 32: 3 CTAs per SM instead of 2).  Off by default:
+// measured slower for n >= 28 (n = 32 at R = 1: 0.39 -> 0.31 of HBM), faster
+// only at n = 24 (0.46 -> 0.50) (profiles/r01_stream_f32_inplace.jsonl).
+#ifndef JM_F32_RING_INPLACE
+#define JM_F32_RING_INPLACE 0
+#endif
+JM_HD constexpr int f32_ring_slot(int n) {
+  return (JM_F32_RING_INPLACE && (n * n * 4) % 16 == 0) ? f32_region(n) : 0;
 }
 // DMMA in the streaming variant: when the swizzled publish buffer fits in the
 // matrix's ring slot (n a multiple of 16), the slot is reused as that buffer
@@ -304,7 +319,8 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
     return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm) + own * dmma_scr(n), w};
   }
   if (f32p_use(n)) return Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
-  return Plan{(int)Tile::F32, 32 * F32_WPC, chm, ring_bytes(n, es, rm) + rm * f32_region(n), 1};
+  return Plan{(int)Tile::F32, 32 * F32_WPC, chm,
+              ring_bytes(n, es, rm, f32_ring_slot(n)) + (f32_ring_slot(n) ? 0 : rm * f32_region(n)), 1};
 }
 
 // Note: k_update passes only maxThreads to __launch_bounds__.  Registers are

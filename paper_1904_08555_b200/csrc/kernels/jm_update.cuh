@@ -260,11 +260,11 @@ struct Stager {
 // loads overlap the compute of chunk i.  A round (what the tiling kinds see
 // through buf()/cnt()) is MPC matrices.  The one ragged chunk at the end of
 // the batch is staged synchronously with element copies.
-template <int N, int ES, int NT, int MPC, int K, int S>
+template <int N, int ES, int NT, int MPC, int K, int S, int SLOT = 0>
 struct Ring {
   static constexpr int MB = N * N * ES;
   static constexpr bool PER = (MB % 16) == 0;             // one copy per matrix
-  static constexpr int SBM = PER ? stage_stride(N, ES) : MB;
+  static constexpr int SBM = ring_sbm(N, ES, SLOT);       // matrix slot stride
   static constexpr int RB = MPC * SBM, CHM = K * MPC, CHB = K * RB, GB = CHM * MB;
   static_assert(GB % 16 == 0 && CHB % 16 == 0, "bulk copies move multiples of 16 bytes");
   static_assert(S >= 2, "ring of at least two stages");
@@ -1063,15 +1063,17 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
   auto col_of = [&](int j) { return ((j >> 2) * CG + tc) * 4 + (j & 3); };
 
   // resident: the staged matrix's region doubles as its work area (sM);
-  // streaming: packed ring stages, work areas of REG bytes after the ring
-  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S>,
+  // streaming: the same in REG-sized ring slots when each matrix is its own
+  // copy (f32_ring_slot), else work areas of REG bytes after the ring
+  constexpr int SLOT = f32_ring_slot(N);
+  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, SLOT>,
                         Stager<N, ES, REG, NT, MPC, AL, false>>::type Stg;
   Stg sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     const bool live = (m < MPW) && (mi < sg.cnt());
     float *src = reinterpret_cast<float *>(sg.buf() + (m < MPW ? mi : 0) * Stg::SBM);
-    float *sm = STRM ? reinterpret_cast<float *>(smem + Stg::BYTES + (m < MPW ? mi : 0) * REG) : src;
+    float *sm = (STRM && !SLOT) ? reinterpret_cast<float *>(smem + Stg::BYTES + (m < MPW ? mi : 0) * REG) : src;
     float2 p[RA][CB / 2];
     if (live) {
 #pragma unroll
