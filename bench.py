@@ -43,7 +43,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=16)
+    # (--size: the same option under torchrun, whose own parser takes --n for --nnodes)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=16)
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--batch", type=int, default=1 << 20, help="matrices per GPU")
     ap.add_argument("--global-batch", type=int, default=None,
@@ -234,10 +235,19 @@ def main():
     import paper_1904_08555_b200 as jm
     from paper_1904_08555_b200 import shard
 
+    # one process per GPU over NCCL; JM_BENCH_DIST_BACKEND=gloo (test hook)
+    # runs the same N > 1 path with ranks sharing the visible GPUs and the
+    # record gather on CPU, so the multi-rank logic can be exercised on a 1-GPU box
+    backend = os.environ.get("JM_BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if backend == "nccl" else torch.device("cpu")    # collective tensors
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     torch.cuda.init()
     jm.jit_mat_init(local)
     stream = torch.cuda.Stream(device=dev)
@@ -257,11 +267,25 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     with torch.cuda.stream(stream):
         jm.jit_mat_fill(n, dt, 1, 0x0019040855, gfirst, B, x.data_ptr())
     stream.synchronize()
+
+    # ---- multi-GPU: rank 0 specializes, the others import its cubins over
+    # NCCL instead of running NVRTC themselves
+    if world > 1 and a.kind == "specialized":
+        blob = None
+        if rank == 0:
+            jm.jit_mat_prepare_for(n, dt, R, a.addend, a.kind)
+            blob = jm.jit_mat_cache_export(n, dt, a.addend)
+        blob = shard.broadcast_blob(dist, blob, 0, cdev)
+        if rank != 0:
+            jm.jit_mat_cache_import(blob)
 
     # ---- first call: NVRTC specialization (reported separately, never timed)
     t0 = time.perf_counter()
@@ -305,7 +329,7 @@ def main():
     # max over ranks + checksum gather (NCCL, outside the data path)
     csum, _ = jm.jit_mat_checksum(n, dt, gfirst, B, y.data_ptr())
     if world > 1:
-        recs, cks = shard.gather_record(dist, [ms_step, float(B)], [csum], dev)
+        recs, cks = shard.gather_record(dist, [ms_step, float(B)], [csum], cdev)
     else:
         recs, cks = [[ms_step, float(B)]], [[csum]]
     ms_max = max(r[0] for r in recs)
@@ -360,6 +384,8 @@ def main():
         "clocks": clocks,
         "gpu_launches": launches,
         "nvrtc_first_call_ms": first_call_ms,
+        "specializations": ("rank 0 compiled, ranks 1..N-1 imported its cubins (NCCL broadcast)"
+                            if world > 1 and a.kind == "specialized" else "compiled in this process"),
         "kernel": {"tile": key["tile_name"], "variant": "streaming" if variant else "resident",
                    "regs": key["regs"], "local_bytes": key["local_bytes"],
                    "smem_bytes": key["smem_bytes"], "threads": key["threads"],
@@ -372,7 +398,7 @@ def main():
         gsteps = max(2, min(5, a.steps))
         g_ms, _ = timed("generic", gsteps, 1)
         g_ms_step = g_ms / gsteps
-        g_max = (max(r[0] for r in shard.gather_record(dist, [g_ms_step], [], dev)[0])
+        g_max = (max(r[0] for r in shard.gather_record(dist, [g_ms_step], [], cdev)[0])
                  if world > 1 else g_ms_step)
         gval = total_units / (g_max / 1e3)
         line["generic"] = {"value": gval, "unit": UNIT, "ms_per_step": g_max,
@@ -381,7 +407,7 @@ def main():
         # Fig. 3's third bar: the same template compiled ahead of time (n = 3, 7, 16 double)
         if dt == "f64" and n in (3, 7, 16):
             a_ms, _ = timed("aot_specialized", gsteps, 1)
-            a_max = (max(r[0] for r in shard.gather_record(dist, [a_ms / gsteps], [], dev)[0])
+            a_max = (max(r[0] for r in shard.gather_record(dist, [a_ms / gsteps], [], cdev)[0])
                      if world > 1 else a_ms / gsteps)
             aval = total_units / (a_max / 1e3)
             line["aot_specialized"] = {"value": aval, "unit": UNIT, "ms_per_step": a_max,
@@ -399,7 +425,7 @@ def main():
         for _ in range(e2e_steps):
             jm.jit_mat_run_host(n, dt, B, R, hx.data_ptr(), hy.data_ptr())
         el = time.perf_counter() - t0
-        e_max = (max(r[0] for r in shard.gather_record(dist, [el / e2e_steps], [], dev)[0])
+        e_max = (max(r[0] for r in shard.gather_record(dist, [el / e2e_steps], [], cdev)[0])
                  if world > 1 else el / e2e_steps)
         line["e2e"] = {"value": total_units / e_max, "unit": UNIT,
                        "h2d_bytes_per_step": B * n * n * es, "d2h_bytes_per_step": B * n * n * es,
@@ -414,7 +440,7 @@ def main():
     if rank == 0:
         emit(line, a)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
         dist.destroy_process_group()
 
 

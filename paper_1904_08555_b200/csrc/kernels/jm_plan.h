@@ -178,7 +178,10 @@ constexpr int F32P_RP_MAX = 4;
 constexpr int F32P_WPC = 2;                       // warps per CTA
 constexpr int F32P_KSTEP = 4;                     // k steps between scheduling fences
 // (n > 16 needs more than 4 x 16 resident floats next to the accumulators: spills)
-JM_HD constexpr bool f32p_use(int n) { return n >= 9 && n <= 16; }
+#ifndef JM_F32P_MAX
+#define JM_F32P_MAX 16
+#endif
+JM_HD constexpr bool f32p_use(int n) { return n >= 9 && n <= JM_F32P_MAX; }
 JM_HD constexpr int f32p_g(int n) { return n <= 16 ? 4 : 8; }                 // threads per matrix
 JM_HD constexpr int f32p_mpw(int n) { return 32 / f32p_g(n); }                // matrices per warp
 JM_HD constexpr int f32p_rp(int n) { return cdiv(n, f32p_g(n)); }             // rows per thread (<= 4)

@@ -66,3 +66,22 @@ def gather_record(dist, floats: list[float], u64s: list[int], device) -> tuple[l
     dist.all_gather(us, u)
     return ([t.cpu().tolist() for t in fs],
             [[x & MASK64 for x in t.cpu().tolist()] for t in us])
+
+
+def broadcast_blob(dist, blob: bytes | None, src: int, device) -> bytes:
+    """Broadcast a byte string (a jit_mat_cache_export blob) from rank ``src``.
+
+    SURVEY.md §8(f) f2: one rank runs NVRTC, the others install its cubins
+    with jit_mat_cache_import, so W ranks compile each key once instead of W
+    times (the paper's "maximal reuse of compiler state").  Two
+    collectives: the length, then the bytes (as uint8 on ``device``).
+    """
+    import torch
+
+    rank = dist.get_rank()
+    n = torch.tensor([len(blob) if rank == src else 0], dtype=torch.int64, device=device)
+    dist.broadcast(n, src)
+    buf = (torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(device) if rank == src
+           else torch.empty(int(n.item()), dtype=torch.uint8, device=device))
+    dist.broadcast(buf, src)
+    return bytes(buf.cpu().numpy().tobytes())

@@ -51,6 +51,34 @@ def _worker(rank, world, port, q, strong):
     dist.destroy_process_group()
 
 
+def _blob_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    blob = bytes(range(256)) * 37 + b"JMC2" if rank == 0 else None
+    got = shard.broadcast_blob(dist, blob, 0, "cpu")
+    q.put((rank, got))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_world2_gloo_broadcasts_cache_blob():
+    """f2: rank 0's compiled-kernel blob reaches every rank byte for byte."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_blob_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = bytes(range(256)) * 37 + b"JMC2"
+    assert got[0] == want and got[1] == want
+
+
 def _run_world(world, strong=True):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
