@@ -559,9 +559,19 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   // 0.54, 25 0.53 -> 0.67, 33 0.59 -> 0.73, 18 0.40 -> 0.43, 26 0.51 -> 0.56,
   // 34 0.58 -> 0.64; at n = 9 / 10 (one main tile) the shuffles cost what the
   // DMMAs save (0.23 -> 0.23 / 0.19), so those keep the padded tiles.
+  // The code also covers several warps per matrix (W > 1: each warp forms the
+  // column border of its own row tiles, the warp owning the border row tile
+  // forms the row border from the published M), but that measured slower
+  // (n = 41 0.63 -> 0.48, 57 0.68 -> 0.53 of the pipe: the owner warp's row
+  // border becomes the critical path at every __syncthreads;
+  // profiles/r01_dmma_border_multiwarp.jsonl), so it is enabled for W == 1
+  // only (JM_DMMA_BORDER_MULTIWARP=1 turns it on).
+#ifndef JM_DMMA_BORDER_MULTIWARP
+#define JM_DMMA_BORDER_MULTIWARP 0
+#endif
   constexpr int BR = N - 8 * (T8 - 1);
-  constexpr bool BORD = (W == 1) && (N > 16) && (BR <= JM_DMMA_BORDER_MAX);
-  constexpr int KM = BORD ? T8 - 1 : RT;     // row tiles through DMMA
+  constexpr bool BORD = (W == 1 || JM_DMMA_BORDER_MULTIWARP) && (N > 16) && (BR <= JM_DMMA_BORDER_MAX);
+  constexpr int KTOP = BORD ? T8 - 1 : T8;   // global row tiles through DMMA
   constexpr int KN = BORD ? T8 - 1 : T8;     // column tiles through DMMA
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -587,11 +597,14 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   for (int j1 = 0; j1 < 2; ++j1) pofs[j1] = ((8 * wr * RT + g) * RSC + ((j1 * 4 + t) ^ fg)) * 16;
   // border (BORD): column pair (8K, 8K+1) of row 8J + 2t + s -> colofs[s] + 8J*RSC*16;
   // element (8K + g', 8I + g) -> rowofs + (g'*RSC + 4*(I ^ (g' & 1)))*16
-  int colofs[2] = {0, 0}, rowofs = 0;
+  // and (W > 1) M's fragment of any tile (I', J) -> aofs[J&1] + (8I'*RSC + 8(J>>1))*16
+  int colofs[2] = {0, 0}, rowofs = 0, aofs[2] = {0, 0};
   if constexpr (BORD) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) colofs[s] = ((2 * t + s) * RSC + ((4 * (T8 - 1)) ^ (2 * t ^ (s << 2)))) * 16;
     rowofs = (8 * (T8 - 1) * RSC + gh) * 16 + 8 * gl;
+#pragma unroll
+    for (int j1 = 0; j1 < 2; ++j1) aofs[j1] = (g * RSC + ((j1 * 4 + t) ^ fg)) * 16;
   }
 
   Stg sg(in, out, batch, smem);
@@ -629,11 +642,11 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
         double p[RT][T8][2];
         if constexpr (BORD) {
           constexpr int K = T8 - 1;
-          // column border P[8I+g][8K+c] (c < BR), every row tile I: lane (g,t)
-          // sums its own k = 8J+2t+s terms, then the 4 lanes of a row add up
-          double cs[T8][2];
+          // column border P[8I+g][8K+c] (c < BR), this warp's row tiles: lane
+          // (g,t) sums its own k = 8J+2t+s terms, then the 4 lanes of a row add up
+          double cs[RT][2];
 #pragma unroll
-          for (int I = 0; I < T8; ++I) cs[I][0] = cs[I][1] = 0.0;
+          for (int I = 0; I < RT; ++I) cs[I][0] = cs[I][1] = 0.0;
 #pragma unroll
           for (int J = 0; J < T8; ++J)
 #pragma unroll
@@ -648,13 +661,13 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
                 v0 = *reinterpret_cast<const double *>(q);
               }
 #pragma unroll
-              for (int I = 0; I < T8; ++I) {
+              for (int I = 0; I < RT; ++I) {
                 cs[I][0] = fmaT(acc[I][J][s], v0, cs[I][0]);
                 if constexpr (BR == 2) cs[I][1] = fmaT(acc[I][J][s], v1, cs[I][1]);
               }
             }
 #pragma unroll
-          for (int I = 0; I < T8; ++I)
+          for (int I = 0; I < RT; ++I)
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc) {
               double v = cs[I][cc];
@@ -664,41 +677,79 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
               }
               p[I][K][cc] = (cc < BR && t == 0) ? acc[I][K][cc] + v : 0.0;
             }
-          // row border P[8K+g'][8J+2t+s] (g' < BR), column tiles J < K: lane
-          // (g,t) sums the k = 8I+g terms, then the 8 lanes of a column add up
-          double rs[BR][K > 0 ? K : 1][2];
+          // row border P[8K+g'][8J+2t+s] (g' < BR), column tiles J < K, by the
+          // warp owning row tile K: lane (g,t) sums the k = 8I+g terms (from its
+          // accumulators when it holds the whole matrix, else from the published
+          // M — the same values in the same order), then the 8 lanes of a
+          // column add up
+          constexpr int WK = K / RT, IK = K % RT;
+          auto finish_row = [&](int J, int s, const double (&rsv)[BR]) {
+            double mine = 0.0;
 #pragma unroll
-          for (int q = 0; q < BR; ++q)
-#pragma unroll
-            for (int J = 0; J < K; ++J) rs[q][J][0] = rs[q][J][1] = 0.0;
-#pragma unroll
-          for (int I = 0; I < T8; ++I) {
-            double mr[BR];
-#pragma unroll
-            for (int q = 0; q < BR; ++q)
-              mr[q] = *reinterpret_cast<const double *>(sb + rowofs + (q * RSC + 4 * (I ^ (q & 1))) * 16);
-#pragma unroll
-            for (int q = 0; q < BR; ++q)
-#pragma unroll
-              for (int J = 0; J < K; ++J)
-#pragma unroll
-                for (int s = 0; s < 2; ++s) rs[q][J][s] = fmaT(mr[q], acc[I][J][s], rs[q][J][s]);
-          }
-#pragma unroll
-          for (int J = 0; J < K; ++J)
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              double mine = 0.0;
-#pragma unroll
-              for (int q = 0; q < BR; ++q) {
-                double v = rs[q][J][s];
-                v += __shfl_xor_sync(0xffffffffu, v, 4);
-                v += __shfl_xor_sync(0xffffffffu, v, 8);
-                v += __shfl_xor_sync(0xffffffffu, v, 16);
-                if (g == q) mine = v;
-              }
-              p[K][J][s] = (g < BR) ? acc[K][J][s] + mine : 0.0;
+            for (int q = 0; q < BR; ++q) {
+              double v = rsv[q];
+              v += __shfl_xor_sync(0xffffffffu, v, 4);
+              v += __shfl_xor_sync(0xffffffffu, v, 8);
+              v += __shfl_xor_sync(0xffffffffu, v, 16);
+              if (g == q) mine = v;
             }
+            p[IK][J][s] = (g < BR) ? acc[IK][J][s] + mine : 0.0;
+          };
+          if constexpr (W == 1) {            // I outer: each border-row value loaded once
+            double rs[BR][K > 0 ? K : 1][2];
+#pragma unroll
+            for (int q = 0; q < BR; ++q)
+#pragma unroll
+              for (int J = 0; J < K; ++J) rs[q][J][0] = rs[q][J][1] = 0.0;
+#pragma unroll
+            for (int I = 0; I < T8; ++I) {
+              double mr[BR];
+#pragma unroll
+              for (int q = 0; q < BR; ++q)
+                mr[q] = *reinterpret_cast<const double *>(sb + rowofs + (q * RSC + 4 * (I ^ (q & 1))) * 16);
+#pragma unroll
+              for (int q = 0; q < BR; ++q)
+#pragma unroll
+                for (int J = 0; J < K; ++J)
+#pragma unroll
+                  for (int s = 0; s < 2; ++s) rs[q][J][s] = fmaT(mr[q], acc[I][J][s], rs[q][J][s]);
+            }
+#pragma unroll
+            for (int J = 0; J < K; ++J)
+#pragma unroll
+              for (int s = 0; s < 2; ++s) {
+                double rsv[BR];
+#pragma unroll
+                for (int q = 0; q < BR; ++q) rsv[q] = rs[q][J][s];
+                finish_row(J, s, rsv);
+              }
+          } else if (wr == WK) {             // J outer: few live registers next to the tiles
+#pragma unroll 1
+            for (int J = 0; J < K; ++J) {
+              double r0[BR], r1[BR];
+#pragma unroll
+              for (int q = 0; q < BR; ++q) r0[q] = r1[q] = 0.0;
+              const char *col = sb + aofs[J & 1] + 8 * (J >> 1) * 16;
+#pragma unroll
+              for (int I = 0; I < T8; ++I) {
+                const double2 v = *reinterpret_cast<const double2 *>(col + 8 * I * RSC * 16);
+#pragma unroll
+                for (int q = 0; q < BR; ++q) {
+                  const double mr =
+                      *reinterpret_cast<const double *>(sb + rowofs + (q * RSC + 4 * (I ^ (q & 1))) * 16);
+                  r0[q] = fmaT(mr, v.x, r0[q]);
+                  r1[q] = fmaT(mr, v.y, r1[q]);
+                }
+              }
+              // (J is a runtime loop index here: select the tile by unrolled compare)
+#pragma unroll
+              for (int J2 = 0; J2 < K; ++J2)
+                if (J2 == J) {
+                  finish_row(J2, 0, r0);
+                  finish_row(J2, 1, r1);
+                }
+            }
+          }
         }
 #pragma unroll
         for (int J = 0; J < T8; ++J) {
@@ -711,10 +762,10 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
               b[J2] = *reinterpret_cast<const double *>(sb + bofs[s][J2 & 1] +
                                                         (8 * J * RSC + 8 * (J2 >> 1)) * 16);
 #pragma unroll
-            for (int I = 0; I < KM; ++I)
+            for (int I = 0; I < RT; ++I)
 #pragma unroll
               for (int J2 = 0; J2 < KN; ++J2) {
-                if (RAG && wr * RT + I >= T8) continue;
+                if ((RAG || BORD) && wr * RT + I >= KTOP) continue;   // border / phantom row tile
                 if (J == 0 && s == 0)   // P = M + (first k-step): accumulator init is M itself
                   dmma884_c(p[I][J2][0], p[I][J2][1], acc[I][J][s], b[J2], acc[I][J2][0], acc[I][J2][1]);
                 else

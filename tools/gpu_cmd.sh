@@ -1,2 +1,2 @@
-JM_BENCH_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --steps 3 --warmup 3 --size 8 --repeat 1 --global-batch 8000000 --no-cpu --no-e2e > gpurun_out/b2s.json 2> gpurun_out/b2s.err; echo rc=$?
-timeout 600 python bench.py --gpus 1 --steps 3 --warmup 3 --size 8 --repeat 1 --global-batch 8000000 --no-cpu --no-e2e > gpurun_out/b1s.json 2> gpurun_out/b1s.err; echo rc=$?
+timeout 900 python -m pytest tests/test_gpu_stream.py tests/test_gpu_parity.py -q -x 2>&1 | tail -2
+python tools/stream_sweep.py --sizes 33,34,41,42,49,50,57,58 --dtypes f64 --repeats 1,4,100 --gb 1 --steps 3 > gpurun_out/bord2.jsonl 2>&1; echo rc=$?
