@@ -128,6 +128,17 @@ JM_HD constexpr int dmma_scr(int n) { return 8 * dmma_t8(n) * dmma_rsc(n) * 16; 
 // The tile is chosen per n by a small model: useful / padded FMAs x used lanes
 // x min(1, FMA clocks / LDS clocks), with an LDS.128 costing ~4.5 SM clocks
 // per warp in context and an FFMA2 0.5; accumulators + operands <= 200 regs.
+// Column-chunk mapping of the FP32 tiles (run_f32 chunk_of): blocked for
+// n = 21..36, where it removes the 2-way publish conflict (n = 24 0.49 -> 0.53,
+// n = 32 0.66 -> 0.67 of the FP32 pipe), interleaved elsewhere (n >= 40 lost
+// 1-5 % blocked; profiles/r01_f32_colmap_sweep.jsonl).  JM_F32_COL_BLOCKED=0/1
+// forces either.
+#ifndef JM_F32_COL_BLOCKED
+#define JM_F32_COL_BLOCKED -1
+#endif
+JM_HD constexpr bool f32_col_blocked(int n) {
+  return JM_F32_COL_BLOCKED >= 0 ? JM_F32_COL_BLOCKED == 1 : (n >= 21 && n <= 36);
+}
 struct F32Tile {
   int rg, ra, cg, cb;
 };

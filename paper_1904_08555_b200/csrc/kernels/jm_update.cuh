@@ -1111,7 +1111,13 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
   const int mi = warp * MPW + m;
   const float c = float(0.00005);
   auto row_of = [&](int i) { return i * RG + tr; };
-  auto col_of = [&](int j) { return ((j >> 2) * CG + tc) * 4 + (j & 3); };
+  // 16-B column chunk h of thread column tc: blocked (tc * CB/4 + h) or
+  // interleaved (h * CG + tc), per n (f32_col_blocked).  Blocked puts the
+  // thread columns of a quarter-warp CB/4 chunks apart, so the publish
+  // STS.128 of rows tr (LDM/4 odd chunks apart) hit distinct 16-B bank slots
+  // (interleaved: 2-way conflict at n = 32, ncu r01)
+  auto chunk_of = [&](int h) { return f32_col_blocked(N) ? tc * (CB / 4) + h : h * CG + tc; };
+  auto col_of = [&](int j) { return chunk_of(j >> 2) * 4 + (j & 3); };
 
   // resident: the staged matrix's region doubles as its work area (sM);
   // streaming: the same in REG-sized ring slots when each matrix is its own
@@ -1147,7 +1153,7 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
         for (int i = 0; i < RA; ++i)
 #pragma unroll
           for (int h = 0; h < CB / 4; ++h)
-            *reinterpret_cast<float4 *>(sm + row_of(i) * LDM + (h * CG + tc) * 4) =
+            *reinterpret_cast<float4 *>(sm + row_of(i) * LDM + chunk_of(h) * 4) =
                 make_float4(p[i][2 * h].x, p[i][2 * h].y, p[i][2 * h + 1].x, p[i][2 * h + 1].y);
       }
       __syncwarp();
@@ -1156,7 +1162,7 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
         auto load_b = [&](float (&dst)[CB], int k) {
 #pragma unroll
           for (int h = 0; h < CB / 4; ++h) {
-            const float4 v = *reinterpret_cast<const float4 *>(sm + k * LDM + (h * CG + tc) * 4);
+            const float4 v = *reinterpret_cast<const float4 *>(sm + k * LDM + chunk_of(h) * 4);
             dst[4 * h] = v.x; dst[4 * h + 1] = v.y; dst[4 * h + 2] = v.z; dst[4 * h + 3] = v.w;
           }
         };
