@@ -259,7 +259,8 @@ typedef struct {
 
 /* tiling kinds reported in jm_key_info.tile */
 enum { JM_TILE_GENERIC = 0, JM_TILE_TPM = 1, JM_TILE_WARP_DMMA = 2, JM_TILE_CTA_DMMA = 3,
-       JM_TILE_WARP_F32 = 4, JM_TILE_CTA_F32 = 5, JM_TILE_ROWS = 6, JM_TILE_MATMUL = 7 };
+       JM_TILE_WARP_F32 = 4, JM_TILE_CTA_F32 = 5, JM_TILE_ROWS = 6, JM_TILE_MATMUL = 7,
+       JM_TILE_TPM2 = 8 /* two threads per matrix (FP64 n = 8) */ };
 
 JM_API int jit_mat_stats(jm_stats *out);
 /* Copy up to `cap` non-empty slots into `keys`; returns the number of

@@ -4,7 +4,7 @@
 //
 // The plan picks, per (N, dtype), how a batch of independent N x N matrices is
 // mapped onto the B200:
-//   TPM   thread-per-matrix, whole matrix in registers      f64 N<=6, f32 N<=8
+//   TPM   thread-per-matrix, whole matrix in registers      f64 N<=7, f32 N<=8
 //   DMMA  FP64 tensor-core DMMA.8x8x4 (mma.sync m8n8k4.f64), N padded to 8k;
 //         W warps per matrix (W=1 up to N=40 resident / 32 streaming, else a CTA)
 //   F32   FP32 register-tiled outer products with FFMA2, W warps per matrix
@@ -21,7 +21,7 @@
 namespace jm {
 
 enum class Addend : int { Ones = 0, Identity = 1 };
-enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, F32 = 4, Rows = 6 };
+enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, Tpm2 = 3, F32 = 4, Rows = 6 };
 
 struct Plan {
   int tile;      // Tile
@@ -54,8 +54,20 @@ JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage
 #ifndef JM_F64_ROWS_MAX
 #define JM_F64_ROWS_MAX 0
 #endif
+// FP64 n = 8: the warp DMMA tile reaches 0.83 of the FP64 pipe, 0.90 of its
+// bare DMMA + DFMA mix (0.92, tools/microbench k_mix2_2; the rest is the
+// per-update publish / fragment loads / syncs).  A two-thread-per-matrix DFMA
+// kind (Tile::Tpm2, run_tpm2, JM_F64_TPM2=1; the DMMA tile then serves as its
+// low-repeat kernel) measured 0.71 at R = 100 (204 registers: 8 warps per SM,
+// the per-update shuffle exchange exposed; profiles/r01_tpm2_n8.jsonl), so it
+// is off.
+#ifndef JM_F64_TPM2
+#define JM_F64_TPM2 0
+#endif
 JM_HD constexpr Tile tile_for(int n, int dtype) {
-  return dtype == 1 ? (n <= 7 ? Tile::TPM : ((n >= 9 && n <= JM_F64_ROWS_MAX) ? Tile::Rows : Tile::Dmma))
+  return dtype == 1 ? (n <= 7 ? Tile::TPM
+                       : (n == 8 && JM_F64_TPM2) ? Tile::Tpm2
+                       : ((n >= 9 && n <= JM_F64_ROWS_MAX) ? Tile::Rows : Tile::Dmma))
                     : (n <= 8 ? Tile::TPM : Tile::F32);
 }
 
@@ -70,6 +82,10 @@ JM_HD constexpr int f64p_mbuf(int n) { return n * f64p_ncs(n) * 16 + 32; }
 
 // ---- TPM ----
 constexpr int TPM_THREADS = 128;
+// ---- TPM2: two threads per matrix (even n), 64 matrices per 128-thread CTA,
+// double-buffered (cp.async) staging: registers (~200 per thread) limit the SM
+// to 2 CTAs, so the next chunk streams in while this one iterates
+constexpr int TPM2_MPC = TPM_THREADS / 2;
 
 // ---- DMMA (FP64) ----
 #ifndef JM_DMMA_WARP_MAX
@@ -219,6 +235,9 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   if (t == Tile::TPM) {
     return Plan{(int)t, TPM_THREADS, TPM_THREADS, stage_bytes(TPM_THREADS, n, es), 1};
   }
+  if (t == Tile::Tpm2) {
+    return Plan{(int)t, TPM_THREADS, TPM2_MPC, 2 * stage_bytes(TPM2_MPC, n, es), 1};
+  }
   if (t == Tile::Rows) {
     const int mpc = F64P_WPC * (32 / F64P_G);
     return Plan{(int)t, 32 * F64P_WPC, mpc, stage_bytes(mpc, n, es) + 2 * mpc * f64p_mbuf(n), 1};
@@ -262,8 +281,11 @@ JM_HD constexpr bool use_mb1(int n, int dtype, bool strm = false) {
 #ifndef JM_RING_CHUNK
 #define JM_RING_CHUNK 8192
 #endif
+// (for Tile::Tpm2 the low-repeat kernel is the warp DMMA tile with its
+// resident staging: the two-thread kind's conflicted one-time loads lose at
+// R = 1, where the DMMA tile streams at 0.92 of HBM)
 JM_HD constexpr bool stream_ok(int n, int dtype) {
-  return tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::F32;
+  return tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::F32 || tile_for(n, dtype) == Tile::Tpm2;
 }
 // The host's switch: stream iff repeat * (n + 1) < stream_rn(n, dtype).
 // Placed from the measured crossovers (profiles/r01_stream_sweep*.jsonl and
@@ -276,8 +298,11 @@ JM_HD constexpr bool stream_ok(int n, int dtype) {
 // 41..48 to ~250; 49..56 to ~600; 57..64 to ~400; n = 8 loses 8 % at R = 1
 // (16 copies of 512 B per chunk) and stays resident.  f32 row panels
 // (n = 9..16) gain to ~64, f32 tiles (n >= 17) to ~140.
+#ifndef JM_TPM2_RN
+#define JM_TPM2_RN 20
+#endif
 JM_HD constexpr int stream_rn_f64(int n) {
-  return n <= 8 ? 0 : n <= 32 ? 600 : n <= 34 ? 100 : n <= 40 ? 300 : n <= 48 ? 250 : n <= 56 ? 600 : 400;
+  return n < 8 ? 0 : n == 8 ? (JM_F64_TPM2 ? JM_TPM2_RN : 0) : n <= 32 ? 600 : n <= 34 ? 100 : n <= 40 ? 300 : n <= 48 ? 250 : n <= 56 ? 600 : 400;
 }
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype) ? 0
@@ -327,6 +352,8 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   const int es = dtype == 1 ? 8 : 4;
   const int rm = round_mpc(n, dtype), rb = rm * n * n * es, chm = ring_k(rb) * rm;
   if (!stream_ok(n, dtype)) return plan_specialized(n, dtype);
+  if (tile_for(n, dtype) == Tile::Tpm2)   // low-repeat kernel: the resident warp DMMA tile
+    return Plan{(int)Tile::Dmma, 32 * DMMA_WPC, DMMA_WPC, stage_bytes(DMMA_WPC, n, es) + DMMA_WPC * dmma_scr(n), 1};
   if (tile_for(n, dtype) == Tile::Dmma) {
     const int w = dmma_w(n, true);
     const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers

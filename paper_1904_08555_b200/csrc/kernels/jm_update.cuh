@@ -500,6 +500,75 @@ __device__ __forceinline__ void run_tpm(const T *__restrict__ in, T *__restrict_
 }
 
 // ======================================================================
+// TPM2: two threads per matrix, DFMA only (FP64, even N; used for N = 8).
+// Each thread keeps the WHOLE matrix in registers and forms half of the rows
+// of P = M + M*M; the halves are exchanged with one shuffle per element.  The
+// thread of the odd lane works in a frame rotated by N/2 (rows and columns:
+// local (r, q) = global ((r + rot) % N, (q + rot) % N)), so that in BOTH
+// threads the own rows are local rows 0..N/2-1 and the partner's rows land in
+// local rows N/2.. with the columns rotated by N/2 — all compile-time register
+// indices.  The update commutes with this permutation similarity (the Ones
+// and Identity addends are invariant), so each thread computes exactly the
+// paper's update; only the k summation order of the odd-lane rows differs
+// (starts at k = N/2), within tolerance (reading R6).
+// ======================================================================
+template <int N, Addend A>
+__device__ __forceinline__ void run_tpm2(const double *__restrict__ in, double *__restrict__ out,
+                                         long long batch, int repeat) {
+  static_assert(N % 2 == 0, "two threads per matrix need an even N");
+  constexpr int H = N / 2;
+  constexpr int ES = 8, MB = N * N * 8, SB = stage_stride(N, 8);
+  constexpr int NT = TPM_THREADS, MPC = TPM2_MPC;
+  constexpr bool AL = ((MPC * MB) % 16) == 0;
+  extern __shared__ __align__(16) char smem[];
+  const int tid = threadIdx.x, mi = tid >> 1, rot = (tid & 1) * H;
+  const double c = 0.00005;
+  Stager<N, ES, SB, NT, MPC, AL, true> sg(in, out, batch, smem);
+  for (sg.start(); sg.valid(); sg.next()) {
+    sg.acquire();
+    const bool live = mi < sg.cnt();         // every lane runs the loop (shuffle partners)
+    double *sm = reinterpret_cast<double *>(sg.buf() + mi * SB);
+    double m[N][N];
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int q = 0; q < N; ++q) m[r][q] = live ? sm[((r + rot) % N) * N + (q + rot) % N] : 0.0;
+    for (int rep = 0; rep < repeat; ++rep) {
+      double p[H][N];
+      // P = M + M*M for the own rows: accumulators start at M; k outermost
+#pragma unroll
+      for (int i = 0; i < H; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j) p[i][j] = m[i][j];
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+#pragma unroll
+        for (int i = 0; i < H; ++i)
+#pragma unroll
+          for (int j = 0; j < N; ++j) p[i][j] = fmaT(m[i][k], m[k][j], p[i][j]);
+      // M' = A + c * P (own rows), then the partner's new rows
+#pragma unroll
+      for (int i = 0; i < H; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+          m[i][j] = (A == Addend::Ones || i == j) ? fmaT(c, p[i][j], 1.0) : c * p[i][j];
+#pragma unroll
+      for (int i = 0; i < H; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j) m[H + i][(j + H) % N] = __shfl_xor_sync(0xffffffffu, m[i][j], 1);
+    }
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < H; ++i)
+#pragma unroll
+        for (int q = 0; q < N; ++q) sm[((i + rot) % N) * N + (q + rot) % N] = m[i][q];
+    }
+    sg.release();
+  }
+  sg.finish();
+}
+
+// ======================================================================
 // DMMA: FP64 tensor cores (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4).
 //
 // M is padded to NP = 8*T8 and held in registers as DMMA accumulator
@@ -1233,6 +1302,9 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
   static_assert(!STRM || stream_ok(N, sizeof(T) == 8 ? 1 : 0), "no streaming variant of this kind");
   if constexpr (K == Tile::TPM) {
     run_tpm<N, T, A>(in, out, batch, repeat);
+  } else if constexpr (K == Tile::Tpm2) {
+    if constexpr (STRM) run_dmma<N, A, 1, false>(in, out, batch, repeat);   // its low-repeat kernel
+    else run_tpm2<N, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Rows) {
     run_f64p<N, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Dmma) {

@@ -115,14 +115,14 @@ def test_repeat_zero_is_bitwise_copy(jm, n, dt):
 
 
 @pytest.mark.parametrize("dt", ["f64", "f32"])
-@pytest.mark.parametrize("n", [2, 3, 5, 16, 31, 40])
+@pytest.mark.parametrize("n", [2, 3, 5, 8, 16, 31, 40])
 def test_in_place_alias(jm, n, dt):
     x = jm_synth.generate(n, dt, "hard", 7, 0, _batch_for(n))
     want = oracle.run(x, 2)
     assert_parity(_gpu_run(jm, x, 2, inplace=True), want, what=f"in-place n={n} {dt}")
 
 
-@pytest.mark.parametrize("n,dt", [(2, "f64"), (3, "f64"), (4, "f32"), (7, "f32"), (16, "f64"),
+@pytest.mark.parametrize("n,dt", [(2, "f64"), (3, "f64"), (4, "f32"), (7, "f32"), (8, "f64"), (16, "f64"),
                                   (13, "f64"), (20, "f32"), (64, "f64"), (45, "f32")])
 @pytest.mark.parametrize("batch", [1, 31, 32, 33, 1000, (1 << 16) + 7])
 def test_ragged_batches(jm, n, dt, batch):

@@ -95,6 +95,31 @@ __global__ void k_mix16_8(double *out, double av, double bv) {
   if (s == 12345.678) out[0] = s;
 }
 
+// The n = 8 kernel's mix per warp and update: 2 DMMA.8x8x4 into ONE
+// accumulator (dependent chain) + 2 DFMA (epilogue); DEP = false makes the two
+// DMMAs independent (two accumulators), to separate chain latency from the mix.
+template <bool DEP>
+__global__ void k_mix2_2(double *out, double av, double bv) {
+  double c[2][2], d[2];
+  c[0][0] = threadIdx.x; c[0][1] = 1; c[1][0] = 2; c[1][1] = 3;
+  d[0] = 0.5; d[1] = 0.25;
+  double a = av * threadIdx.x, b = bv;
+  for (int it = 0; it < ITER / 2; ++it) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0][0]), "+d"(c[0][1]) : "d"(a), "d"(b));
+    if (DEP)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[0][0]), "+d"(c[0][1]) : "d"(a), "d"(b));
+    else
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[1][0]), "+d"(c[1][1]) : "d"(a), "d"(b));
+    d[0] = fma(d[0], b, a);
+    d[1] = fma(d[1], b, a);
+  }
+  const double s = c[0][0] + c[0][1] + c[1][0] + c[1][1] + d[0] + d[1];
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void k_ffma(float *out, float b, float c) {
   float a[16];
 #pragma unroll
@@ -218,6 +243,12 @@ int main() {
   ms = timeit([&] { k_mix16_8<<<blocks, threads>>>(dd, 1e-3, 1e-3); });
   printf("  \"dmma16_dfma8_mix_tflops\": %.3f,\n",
          (nwarp * (ITER / 8) * 16 * 512.0 + nthr * (ITER / 8) * 8 * 2.0) / (ms * 1e-3) / 1e12);
+  ms = timeit([&] { k_mix2_2<true><<<blocks, threads>>>(dd, 1e-3, 1e-3); });
+  printf("  \"dmma2dep_dfma2_mix_tflops\": %.3f,\n",
+         (nwarp * (ITER / 2) * 2 * 512.0 + nthr * (ITER / 2) * 2 * 2.0) / (ms * 1e-3) / 1e12);
+  ms = timeit([&] { k_mix2_2<false><<<blocks, threads>>>(dd, 1e-3, 1e-3); });
+  printf("  \"dmma2ind_dfma2_mix_tflops\": %.3f,\n",
+         (nwarp * (ITER / 2) * 2 * 512.0 + nthr * (ITER / 2) * 2 * 2.0) / (ms * 1e-3) / 1e12);
   ms = timeit([&] { k_ffma<<<blocks, threads>>>(df, 1.0000001f, 1e-9f); });
   printf("  \"ffma_tflops\": %.3f,\n", nthr * ITER * 16 * 2 / (ms * 1e-3) / 1e12);
   ms = timeit([&] { k_ffma2<<<blocks, threads>>>(df, 1.0000001f, 1e-9f); });
