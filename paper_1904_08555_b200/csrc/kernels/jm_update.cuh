@@ -684,15 +684,37 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
     if (mi < cnt) {
       double *sm = reinterpret_cast<double *>(stage + mi * Stg::SBM);
       double acc[RT][T8][2];
+      if constexpr (N % 2 == 0) {
+        // even n: the lane's pair (8J+2t, 8J+2t+1) is one 16-B load; for n a
+        // multiple of 16 (rows 2^k * 128 B apart) the odd-g lanes take the
+        // column tiles of a pair in the other order, so a quarter-warp's two
+        // rows land in different bank slots (the element loads were 8-way
+        // conflicted: half the time of a streaming update at n = 64)
+        constexpr bool SWZ = (N % 16 == 0) && (T8 % 2 == 0);
+        const int odd = SWZ ? (g & 1) : 0;
 #pragma unroll
-      for (int I = 0; I < RT; ++I)
+        for (int I = 0; I < RT; ++I) {
+          const int row = 8 * (wr * RT + I) + g;
 #pragma unroll
-        for (int J = 0; J < T8; ++J)
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const int row = 8 * (wr * RT + I) + g, col = 8 * J + 2 * t + s;
-            acc[I][J][s] = (row < N && col < N) ? sm[row * N + col] : 0.0;
+          for (int J = 0; J < T8; ++J) {
+            const int Jr = J ^ odd;                 // the column tile this lane loads now
+            double2 v = make_double2(0.0, 0.0);
+            if (row < N && 8 * Jr + 2 * t < N) v = *reinterpret_cast<const double2 *>(sm + row * N + 8 * Jr + 2 * t);
+            if (SWZ && odd) { acc[I][J ^ 1][0] = v.x; acc[I][J ^ 1][1] = v.y; }
+            else { acc[I][J][0] = v.x; acc[I][J][1] = v.y; }
           }
+        }
+      } else {
+#pragma unroll
+        for (int I = 0; I < RT; ++I)
+#pragma unroll
+          for (int J = 0; J < T8; ++J)
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const int row = 8 * (wr * RT + I) + g, col = 8 * J + 2 * t + s;
+              acc[I][J][s] = (row < N && col < N) ? sm[row * N + col] : 0.0;
+            }
+      }
       if constexpr (INPL) {                  // every warp has read M before the slot is reused
         if constexpr (W == 1) __syncwarp(); else __syncthreads();
       }
@@ -858,15 +880,31 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
         if constexpr (W == 1) __syncwarp();
       }
       if constexpr (INPL && W > 1) __syncthreads();   // last B-fragment reads of the slot done
+      if constexpr (N % 2 == 0) {              // the same 16-B pattern back
+        constexpr bool SWZ = (N % 16 == 0) && (T8 % 2 == 0);
+        const int odd = SWZ ? (g & 1) : 0;
 #pragma unroll
-      for (int I = 0; I < RT; ++I)
+        for (int I = 0; I < RT; ++I) {
+          const int row = 8 * (wr * RT + I) + g;
 #pragma unroll
-        for (int J = 0; J < T8; ++J)
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const int row = 8 * (wr * RT + I) + g, col = 8 * J + 2 * t + s;
-            if (row < N && col < N) sm[row * N + col] = acc[I][J][s];
+          for (int J = 0; J < T8; ++J) {
+            const int Jr = J ^ odd;
+            const double2 v = (SWZ && odd) ? make_double2(acc[I][J ^ 1][0], acc[I][J ^ 1][1])
+                                           : make_double2(acc[I][J][0], acc[I][J][1]);
+            if (row < N && 8 * Jr + 2 * t < N) *reinterpret_cast<double2 *>(sm + row * N + 8 * Jr + 2 * t) = v;
           }
+        }
+      } else {
+#pragma unroll
+        for (int I = 0; I < RT; ++I)
+#pragma unroll
+          for (int J = 0; J < T8; ++J)
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const int row = 8 * (wr * RT + I) + g, col = 8 * J + 2 * t + s;
+              if (row < N && col < N) sm[row * N + col] = acc[I][J][s];
+            }
+      }
     }
     sg.release();
   }
