@@ -118,7 +118,7 @@ JM_API int jit_mat_init(int device);
  * DMMA and FP32-tile kinds: f64 n >= 8, f32 n >= 9), a call whose
  * repeat * (n + 1) is below the kind's measured switch point (jm_plan.h
  * stream_rn: 100..600 for f64 n >= 9 by tiling kind, 64 for f32 n = 9..16,
- * 140 for f32 n >= 17; the HBM-bound side of the roofline and
+ * 140 for f32 n >= 17, and not at f64 n = 16, R = 1; the HBM-bound side of the roofline and
  * somewhat beyond) runs the STREAMING variant of the same
  * specialization — the same tile code behind a bulk-copy (TMA) ring — which is
  * a second cache key, compiled on its first such call.  Results agree with the

@@ -304,6 +304,11 @@ JM_HD constexpr bool stream_ok(int n, int dtype) {
 JM_HD constexpr int stream_rn_f64(int n) {
   return n < 8 ? 0 : n == 8 ? (JM_F64_TPM2 ? JM_TPM2_RN : 0) : n <= 32 ? 600 : n <= 34 ? 100 : n <= 40 ? 300 : n <= 48 ? 250 : n <= 56 ? 600 : 400;
 }
+// ... and not below stream_lo(n, dtype): f64 n = 16 at R = 1, whose resident
+// kernel (16 KB, 48 registers: 40 warps per SM) streams at 0.95 of HBM once
+// its accumulator loads are conflict free, against 0.88 through the ring
+// (profiles/r01_ring_lowr_sweep.jsonl; from R = 2 the ring wins, 0.91 vs 0.80)
+JM_HD constexpr int stream_lo(int n, int dtype) { return (dtype == 1 && n == 16) ? 18 : 0; }
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype) ? 0
          : dtype == 1        ? stream_rn_f64(n)

@@ -468,7 +468,8 @@ bool want_stream(int n, int dtype, int kind, int64_t repeat, unsigned flags = 0)
     return e && *e ? atoi(e) : -1;
   }();
   if (force >= 0) return force > 0;
-  return repeat * (int64_t)(n + 1) < (int64_t)stream_rn(n, dtype);
+  const int64_t rn = repeat * (int64_t)(n + 1);
+  return rn < (int64_t)stream_rn(n, dtype) && rn >= (int64_t)jm::stream_lo(n, dtype);
 }
 
 Slot &slot_of(int n, int dtype, int addend, int kind, bool stream) {

@@ -123,7 +123,8 @@ def test_stream_tiny_batches(jm, batch):
 
 def test_variant_selection_and_key_info(jm):
     # the default switch: stream iff repeat * (n + 1) < stream_rn(n, dtype)
-    assert jm.jit_mat_prepare_for(16, "f64", 1) == 1
+    assert jm.jit_mat_prepare_for(16, "f64", 1) == 0       # below stream_lo: resident
+    assert jm.jit_mat_prepare_for(16, "f64", 2) == 1
     assert jm.jit_mat_prepare_for(16, "f64", 35) == 1      # 595 < 600
     assert jm.jit_mat_prepare_for(16, "f64", 36) == 0      # 612
     assert jm.jit_mat_prepare_for(64, "f64", 6) == 1       # 390 < 400
@@ -139,8 +140,10 @@ def test_variant_selection_and_key_info(jm):
     assert jm.jit_mat_prepare_for(8, "f32", 1) == 0        # TPM: resident only
     assert jm.jit_mat_prepare_for(16, "f64", 1, kind="generic") == 0
     assert jm.jit_mat_prepare_for(16, "f64", 100, flags=jm.JM_FLAG_STREAMING) == 1
+    assert jm.jit_mat_prepare_for(24, "f64", 1) == 1
     assert jm.jit_mat_prepare_for(8, "f64", 100, flags=jm.JM_FLAG_STREAMING) == 1
     assert jm.jit_mat_prepare_for(16, "f64", 1, flags=jm.JM_FLAG_RESIDENT) == 0
+    jm.jit_mat_prepare_for(16, "f64", 1)
     info = [k for k in jm.jit_mat_key_info() if k["op"] == 0 and k["n"] == 16 and k["dtype"] == 1
             and k["kind"] == 0 and k["addend"] == 0]
     assert sorted(k["variant"] for k in info) == [0, 1]
