@@ -114,13 +114,15 @@ JM_API int jit_mat_init(int device);
  * aligned) on the initialised device.  n in [1, 64]; batch >= 0 (0: no-op);
  * repeat in [0, 2^31) (0: out is a bitwise copy of in).  Asynchronous.
  *
- * VARIANT (every specialized entry point): where the tiling kind has one (the
- * DMMA and FP32-tile kinds: f64 n >= 8, f32 n >= 9), a call whose
+ * VARIANT (every specialized entry point): a call whose
  * repeat * (n + 1) is below the kind's measured switch point (jm_plan.h
  * stream_rn: 100..600 for f64 n >= 9 by tiling kind, 64 for f32 n = 9..16,
- * 140 for f32 n >= 17, and not at f64 n = 16, R = 1; the HBM-bound side of the roofline and
- * somewhat beyond) runs the STREAMING variant of the same
- * specialization — the same tile code behind a bulk-copy (TMA) ring — which is
+ * 140 for f32 n >= 17, 100 for the register-heavy thread-per-matrix sizes
+ * (f64 n = 5..7, f32 n = 8), never for the light ones, and not at f64 n = 16,
+ * R = 1; the HBM-bound side of the roofline and somewhat beyond)
+ * runs the STREAMING variant of the same specialization — the same tile code
+ * behind a bulk-copy (TMA) ring, or for thread-per-matrix sizes behind a
+ * double-buffered cp.async stage — which is
  * a second cache key, compiled on its first such call.  Results agree with the
  * resident kernel bit for bit (same arithmetic in the same order), except f64
  * n = 33, 34, where the resident kernel forms the thin border with DFMA (both
@@ -298,8 +300,7 @@ JM_API const char *jit_mat_version(void);
  * the multiply-accumulate template instead.  cubin_bytes may be NULL. */
 #define JM_OP_MATMUL 2
 #define JM_OP_MASS 3     /* compile_check(dofs, quads, JM_OP_MASS, ...): k_mass<dofs, quads> */
-#define JM_OP_STREAM 4   /* the streaming variant of the update (addend Ones); JM_E_UNSUPPORTED
-                            for thread-per-matrix sizes (f64 n <= 7, f32 n <= 8) */
+#define JM_OP_STREAM 4   /* the streaming (low-repeat) variant of the update (addend Ones) */
 JM_API int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes);
 
 /* Cache-hit cost of the key lookup (the paper calls the

@@ -284,8 +284,13 @@ JM_HD constexpr bool use_mb1(int n, int dtype, bool strm = false) {
 // (for Tile::Tpm2 the low-repeat kernel is the warp DMMA tile with its
 // resident staging: the two-thread kind's conflicted one-time loads lose at
 // R = 1, where the DMMA tile streams at 0.92 of HBM)
+// (for Tile::TPM the streaming variant is the same thread-per-matrix kernel
+// with the double-buffered cp.async stage: its per-thread reads need the
+// odd-16-B staging stride, which a bulk copy per matrix would make 1-D copies
+// of 32..512 B)
 JM_HD constexpr bool stream_ok(int n, int dtype) {
-  return tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::F32 || tile_for(n, dtype) == Tile::Tpm2;
+  return tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::F32 || tile_for(n, dtype) == Tile::Tpm2 ||
+         tile_for(n, dtype) == Tile::TPM;
 }
 // The host's switch: stream iff repeat * (n + 1) < stream_rn(n, dtype).
 // Placed from the measured crossovers (profiles/r01_stream_sweep*.jsonl and
@@ -309,8 +314,17 @@ JM_HD constexpr int stream_rn_f64(int n) {
 // its accumulator loads are conflict free, against 0.88 through the ring
 // (profiles/r01_ring_lowr_sweep.jsonl; from R = 2 the ring wins, 0.91 vs 0.80)
 JM_HD constexpr int stream_lo(int n, int dtype) { return (dtype == 1 && n == 16) ? 18 : 0; }
+// Thread per matrix (profiles/r01_tpm_stream_sweep.jsonl): the staged
+// variant wins where registers limit the resident kernel to few CTAs — f64
+// n = 5..7 (1.14-1.46x at R = 1..8; n = 6 R = 1: 0.66 -> 0.94 of HBM) and
+// f32 n = 8 (1.09-1.15x) — and loses up to 23 % on the small, light sizes
+// (f64 n = 2: 0.96 -> 0.74 of HBM), which keep the resident kernel.
+JM_HD constexpr int stream_rn_tpm(int n, int dtype) {
+  return dtype == 1 ? (n >= 5 ? 100 : 0) : (n == 8 ? 100 : 0);
+}
 JM_HD constexpr int stream_rn(int n, int dtype) {
-  return !stream_ok(n, dtype) ? 0
+  return !stream_ok(n, dtype)               ? 0
+         : tile_for(n, dtype) == Tile::TPM ? stream_rn_tpm(n, dtype)
          : dtype == 1        ? stream_rn_f64(n)
          : f32p_use(n)       ? 64
                              : 140;
@@ -357,6 +371,8 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   const int es = dtype == 1 ? 8 : 4;
   const int rm = round_mpc(n, dtype), rb = rm * n * n * es, chm = ring_k(rb) * rm;
   if (!stream_ok(n, dtype)) return plan_specialized(n, dtype);
+  if (tile_for(n, dtype) == Tile::TPM)
+    return Plan{(int)Tile::TPM, TPM_THREADS, TPM_THREADS, 2 * stage_bytes(TPM_THREADS, n, es), 1};
   if (tile_for(n, dtype) == Tile::Tpm2)   // low-repeat kernel: the resident warp DMMA tile
     return Plan{(int)Tile::Dmma, 32 * DMMA_WPC, DMMA_WPC, stage_bytes(DMMA_WPC, n, es) + DMMA_WPC * dmma_scr(n), 1};
   if (tile_for(n, dtype) == Tile::Dmma) {

@@ -446,22 +446,22 @@ __device__ __forceinline__ void tpm_iterate_f32x2(float (&m)[N * N], int repeat)
   }
 }
 
-template <int N, class T, Addend A>
+// STRM (the low-repeat variant): the same kernel with the double-buffered
+// cp.async Stager, so the next chunk streams in while this one is updated.
+template <int N, class T, Addend A, bool STRM = false>
 __device__ __forceinline__ void run_tpm(const T *__restrict__ in, T *__restrict__ out,
                                         long long batch, int repeat) {
   constexpr int ES = sizeof(T), MB = N * N * ES, SB = stage_stride(N, ES);
   constexpr int NT = TPM_THREADS, MPC = TPM_THREADS;
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x;
-  const long long nchunks = (batch + MPC - 1) / MPC;
-  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const long long b0 = ch * MPC;
-    const int cnt = (int)((batch - b0) < MPC ? (batch - b0) : MPC);
-    stage_in<N, ES, SB, NT, true>(reinterpret_cast<const char *>(in) + b0 * MB, smem, cnt, tid);
-    __syncthreads();
+  Stager<N, ES, SB, NT, MPC, true, STRM> sg(in, out, batch, smem);
+  for (sg.start(); sg.valid(); sg.next()) {
+    sg.acquire();
+    const int cnt = sg.cnt();
     if (tid < cnt) {
       T m[N * N];
-      char *mine = smem + tid * SB;
+      char *mine = sg.buf() + tid * SB;
       if constexpr (MB % 16 == 0) {  // 16-B pieces at an odd 16-B stride: conflict free
 #pragma unroll
         for (int q = 0; q < MB / 16; ++q) {
@@ -493,10 +493,9 @@ __device__ __forceinline__ void run_tpm(const T *__restrict__ in, T *__restrict_
         for (int e = 0; e < N * N; ++e) reinterpret_cast<T *>(mine)[e] = m[e];
       }
     }
-    __syncthreads();
-    stage_out<N, ES, SB, NT, true>(reinterpret_cast<char *>(out) + b0 * MB, smem, cnt, tid);
-    __syncthreads();
+    sg.release();
   }
+  sg.finish();
 }
 
 // ======================================================================
@@ -1339,7 +1338,7 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
   static_assert(K == tile_for(N, sizeof(T) == 8 ? 1 : 0), "tile must match the plan");
   static_assert(!STRM || stream_ok(N, sizeof(T) == 8 ? 1 : 0), "no streaming variant of this kind");
   if constexpr (K == Tile::TPM) {
-    run_tpm<N, T, A>(in, out, batch, repeat);
+    run_tpm<N, T, A, STRM>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Tpm2) {
     if constexpr (STRM) run_dmma<N, A, 1, false>(in, out, batch, repeat);   // its low-repeat kernel
     else run_tpm2<N, A>(in, out, batch, repeat);

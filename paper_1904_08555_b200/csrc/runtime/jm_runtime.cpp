@@ -1161,8 +1161,7 @@ int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes) 
     rc = check_key(n, dtype, op ? JM_ADDEND_ONES : addend, JM_KIND_SPECIALIZED);
     if (rc != JM_OK) return rc;
     if (addend == JM_OP_STREAM && !jm::stream_ok(n, dtype))
-      return fail(JM_E_UNSUPPORTED, "n=%d %s has no streaming variant (thread-per-matrix kind)", n,
-                  dtype == JM_F64 ? "double" : "float");
+      return fail(JM_E_UNSUPPORTED, "n=%d %s has no streaming variant", n, dtype == JM_F64 ? "double" : "float");
     expr = addend == JM_OP_MATMUL   ? mm_name_expression(n, dtype)
            : addend == JM_OP_STREAM ? name_expression(n, dtype, JM_ADDEND_ONES, true)
                                     : name_expression(n, dtype, addend);

@@ -24,9 +24,9 @@ pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
 
-# sizes with a streaming variant: the DMMA kinds (f64 n >= 8) and the FP32
-# row-panel / tile kinds (f32 n >= 9); thread-per-matrix sizes keep one kernel
-STREAM_N = {"f64": list(range(8, 65)), "f32": list(range(9, 65))}
+# every size has a low-repeat variant: the bulk-copy ring behind the DMMA /
+# FP32 kinds, the double-buffered stage behind thread-per-matrix (n <= 7 / 8)
+STREAM_N = {"f64": list(range(1, 65)), "f32": list(range(1, 65))}
 
 
 @pytest.fixture(scope="module")
@@ -86,7 +86,8 @@ def test_stream_identity_addend(jm, n, dt):
                       what=f"streaming identity n={n} {dt} R={r}")
 
 
-@pytest.mark.parametrize("n,dt", [(8, "f64"), (16, "f64"), (24, "f64"), (32, "f64"), (33, "f64"),
+@pytest.mark.parametrize("n,dt", [(3, "f64"), (4, "f64"), (7, "f64"), (3, "f32"), (8, "f32"),
+                                  (8, "f64"), (16, "f64"), (24, "f64"), (32, "f64"), (33, "f64"),
                                   (64, "f64"), (9, "f32"), (16, "f32"), (17, "f32"), (32, "f32"),
                                   (63, "f32"), (64, "f32")])
 def test_stream_ring_wraps(jm, n, dt):
@@ -136,8 +137,11 @@ def test_variant_selection_and_key_info(jm):
     assert jm.jit_mat_prepare_for(64, "f32", 2) == 1       # 130 < 140
     assert jm.jit_mat_prepare_for(64, "f32", 3) == 0
     assert jm.jit_mat_prepare_for(8, "f64", 1) == 0        # n = 8 DMMA: resident (measured)
-    assert jm.jit_mat_prepare_for(4, "f64", 1) == 0        # TPM: resident only
-    assert jm.jit_mat_prepare_for(8, "f32", 1) == 0        # TPM: resident only
+    assert jm.jit_mat_prepare_for(4, "f64", 1, flags=jm.JM_FLAG_STREAMING) == 1   # TPM: staged variant
+    assert jm.jit_mat_prepare_for(4, "f64", 1) == 0        # light TPM sizes stay resident
+    assert jm.jit_mat_prepare_for(6, "f64", 1) == 1        # register-heavy TPM: staged below R(n+1) = 100
+    assert jm.jit_mat_prepare_for(6, "f64", 15) == 0
+    assert jm.jit_mat_prepare_for(8, "f32", 2) == 1
     assert jm.jit_mat_prepare_for(16, "f64", 1, kind="generic") == 0
     assert jm.jit_mat_prepare_for(16, "f64", 100, flags=jm.JM_FLAG_STREAMING) == 1
     assert jm.jit_mat_prepare_for(24, "f64", 1) == 1
