@@ -224,16 +224,21 @@ JM_HD constexpr int f32p_mbuf(int n) { return n * f32p_ncs(n) * 16 + 32; }
 // Double-buffered (cp.async prefetch) staging.  Measured on B200 (r01 sweep):
 // it lifts DMMA n=16 at repeat 1 from 0.87 to 0.94 of HBM, but the doubled
 // stage area costs residency and the compute-bound repeat-100 configurations
-// lose 1-25 % (FP32 row panels most), so every kind currently runs the
-// single-buffered stage; the Stager keeps both paths.
-JM_HD constexpr bool prefetch_for(int, int) { return false; }
+// lose 1-25 % (FP32 row panels most), so those kinds run the single-buffered
+// stage (their low-repeat variant is the bulk-copy ring instead).  The
+// register-heavy thread-per-matrix sizes (f64 n = 5..7, f32 n = 8: 4-5
+// CTAs per SM) do take it: +2-3 % at R = 100, +10-46 % at R <= 16
+// (profiles/r01_tpm_stream_sweep.jsonl, r01_tpm_stream_hi.jsonl).
+JM_HD constexpr bool prefetch_for(int n, int dtype) {
+  return dtype == 1 ? (n >= 5 && n <= 7) : (n == 8);
+}
 
 JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   const int es = dtype == 1 ? 8 : 4;
   const Tile t = tile_for(n, dtype);
   const int nst = prefetch_for(n, dtype) ? 2 : 1;   // stage buffers
   if (t == Tile::TPM) {
-    return Plan{(int)t, TPM_THREADS, TPM_THREADS, stage_bytes(TPM_THREADS, n, es), 1};
+    return Plan{(int)t, TPM_THREADS, TPM_THREADS, nst * stage_bytes(TPM_THREADS, n, es), 1};
   }
   if (t == Tile::Tpm2) {
     return Plan{(int)t, TPM_THREADS, TPM2_MPC, 2 * stage_bytes(TPM2_MPC, n, es), 1};
@@ -317,11 +322,10 @@ JM_HD constexpr int stream_lo(int n, int dtype) { return (dtype == 1 && n == 16)
 // Thread per matrix (profiles/r01_tpm_stream_sweep.jsonl): the staged
 // variant wins where registers limit the resident kernel to few CTAs — f64
 // n = 5..7 (1.14-1.46x at R = 1..8; n = 6 R = 1: 0.66 -> 0.94 of HBM) and
-// f32 n = 8 (1.09-1.15x) — and loses up to 23 % on the small, light sizes
-// (f64 n = 2: 0.96 -> 0.74 of HBM), which keep the resident kernel.
-JM_HD constexpr int stream_rn_tpm(int n, int dtype) {
-  return dtype == 1 ? (n >= 5 ? 100 : 0) : (n == 8 ? 100 : 0);
-}
+// f32 n = 8 — at every R, so those sizes' resident kernel prefetches itself
+// (prefetch_for); it loses up to 23 % on the small, light sizes (f64 n = 2:
+// 0.96 -> 0.74 of HBM).  So the TPM streaming key is never picked by default.
+JM_HD constexpr int stream_rn_tpm(int, int) { return 0; }
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype)               ? 0
          : tile_for(n, dtype) == Tile::TPM ? stream_rn_tpm(n, dtype)

@@ -455,7 +455,7 @@ __device__ __forceinline__ void run_tpm(const T *__restrict__ in, T *__restrict_
   constexpr int NT = TPM_THREADS, MPC = TPM_THREADS;
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x;
-  Stager<N, ES, SB, NT, MPC, true, STRM> sg(in, out, batch, smem);
+  Stager<N, ES, SB, NT, MPC, true, STRM || prefetch_for(N, ES == 8 ? 1 : 0)> sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     const int cnt = sg.cnt();
