@@ -7,12 +7,15 @@ lines 319 and 347.
 """
 from __future__ import annotations
 
+import os
 import threading
 
 import numpy as np
 import pytest
 
 import jm_synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -212,3 +215,22 @@ def test_cache_export_import_skips_nvrtc(jm):
         jm.jit_mat_cache_import(b"JMC1" + blob[4:])
     with pytest.raises(jm.JitMatError):
         jm.jit_mat_cache_export(14, "double")
+
+
+def test_non_sm100_device_is_rejected_without_fallback():
+    """A device that is not compute capability 10.x (simulated with the
+    JIT_MAT_FAKE_CC_MAJOR test hook) gets JM_E_ARCH at init and every run then
+    fails with JM_E_NOT_INITIALIZED: there is no CPU fallback."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_1904_08555_b200 as jm\n"
+        "rc = jm.lib.jit_mat_init(0)\n"
+        "assert rc == jm.JM_E_ARCH, rc\n"
+        "assert 'compute capability 9' in jm.jit_mat_last_error()\n"
+        "assert jm.lib.jit_mat_run(4, 1, 0, 1, None, None) == jm.JM_E_NOT_INITIALIZED\n"
+        "print('ok')\n" % ROOT)
+    env = dict(os.environ, JIT_MAT_FAKE_CC_MAJOR="9")
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0 and p.stdout.strip() == "ok", p.stderr[-2000:]
