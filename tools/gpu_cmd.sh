@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_abi.py -q -x 2>&1 | tail -3
+timeout 1800 python tools/work_check.py --out gpurun_out/work_check2.jsonl > gpurun_out/work_check2.log 2>&1; echo rc=$?

@@ -52,7 +52,10 @@ def child(n, dt, batch, repeat, variant):
     tdt = torch.float64 if dt == "f64" else torch.float32
     x = torch.empty(batch, n, n, dtype=tdt, device="cuda")
     jm.jit_mat_fill(n, dt, 1, 0x0019040855, 0, batch, x.data_ptr())
-    jm.run(x, repeat, sync=True, variant=variant)
+    if variant == "generic":
+        jm.run(x, repeat, sync=True, kind="generic")
+    else:
+        jm.run(x, repeat, sync=True, variant=variant)
 
 
 def parse(csv_text):
@@ -70,6 +73,20 @@ def parse(csv_text):
         if m in tot:
             tot[m] += float(r[vi].replace(",", ""))
     return tot, sorted(kernels)
+
+
+def instructions(n, dt, kind, batch, repeat):
+    """Total warp instructions executed by the update kernel (specialized or generic)."""
+    cmd = ["ncu", "--csv", "--metrics", "smsp__inst_executed.sum", "-k", "regex:k_update|jm_generic",
+           sys.executable, os.path.abspath(__file__), "--child", str(n), dt, str(batch), str(repeat),
+           "generic" if kind == "generic" else "resident"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    rows = list(csv.reader(io.StringIO(p.stdout)))
+    hi = [i for i, r in enumerate(rows) if "Metric Name" in r][0]
+    h = rows[hi]
+    vi, ki = h.index("Metric Value"), h.index("Kernel Name")
+    return sum(float(r[vi].replace(",", "")) for r in rows[hi + 1:]
+               if len(r) > vi and ("k_update" in r[ki] or "jm_generic" in r[ki]))
 
 
 def main():
@@ -102,6 +119,19 @@ def main():
         row = {"n": n, "dtype": dt, "variant": variant, "batch": a.batch, "repeat": a.repeat,
                "kernels": kernels, "algorithmic_fma": alg, "executed_fma": done, "ratio": ratio,
                "exact_kind": exact, "ok": ok, "counts": tot}
+        s = json.dumps(row)
+        print(s, flush=True)
+        if fh:
+            fh.write(s + "\n")
+            fh.flush()
+    # SPEC.md:617/645 "specialized executes less": warp instructions of the
+    # specialized vs the generic runtime-N kernel on the same launch (Fig. 3 sizes)
+    for n, dt in ((3, "f64"), (7, "f64"), (16, "f64"), (16, "f32"), (64, "f64")):
+        spec = instructions(n, dt, "specialized", a.batch, a.repeat)
+        gen = instructions(n, dt, "generic", a.batch, a.repeat)
+        row = {"check": "instructions", "n": n, "dtype": dt, "batch": a.batch, "repeat": a.repeat,
+               "specialized_warp_inst": spec, "generic_warp_inst": gen, "generic_over_specialized": gen / spec}
+        bad += not (spec < gen)
         s = json.dumps(row)
         print(s, flush=True)
         if fh:
