@@ -120,6 +120,33 @@ __global__ void k_mix2_2(double *out, double av, double bv) {
   if (s == 12345.678) out[0] = s;
 }
 
+// The n = 4 thread-per-matrix update's exact DFMA stream (64 product DFMAs in
+// k-outer order + 16 epilogue DFMAs per update, whole matrix in registers, no
+// memory): the ceiling of the TPM kind's instruction mix.
+__global__ void k_tpm4(double *out, int iters) {
+  double m[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) m[e] = 1e-3 * (threadIdx.x + e);
+  const double c = 0.00005;
+  for (int it = 0; it < iters; ++it) {
+    double p[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) p[e] = m[e];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) p[i * 4 + j] = fma(m[i * 4 + k], m[k * 4 + j], p[i * 4 + j]);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) m[e] = fma(c, p[e], 1.0);
+  }
+  double s = 0;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) s += m[e];
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void k_ffma(float *out, float b, float c) {
   float a[16];
 #pragma unroll
@@ -249,6 +276,12 @@ int main() {
   ms = timeit([&] { k_mix2_2<false><<<blocks, threads>>>(dd, 1e-3, 1e-3); });
   printf("  \"dmma2ind_dfma2_mix_tflops\": %.3f,\n",
          (nwarp * (ITER / 2) * 2 * 512.0 + nthr * (ITER / 2) * 2 * 2.0) / (ms * 1e-3) / 1e12);
+  {
+    // 8 CTAs of 128 per SM, the TPM n = 4 kernel's occupancy
+    const int tb = sms * 8, tt = 128, it = ITER / 8;
+    ms = timeit([&] { k_tpm4<<<tb, tt>>>(dd, it); });
+    printf("  \"tpm4_dfma_stream_tflops\": %.3f,\n", (double)tb * tt * it * 80 * 2 / (ms * 1e-3) / 1e12);
+  }
   ms = timeit([&] { k_ffma<<<blocks, threads>>>(df, 1.0000001f, 1e-9f); });
   printf("  \"ffma_tflops\": %.3f,\n", nthr * ITER * 16 * 2 / (ms * 1e-3) / 1e12);
   ms = timeit([&] { k_ffma2<<<blocks, threads>>>(df, 1.0000001f, 1e-9f); });
