@@ -4,7 +4,7 @@
 //
 // The plan picks, per (N, dtype), how a batch of independent N x N matrices is
 // mapped onto the B200:
-//   TPM   thread-per-matrix, whole matrix in registers      f64 N<=7, f32 N<=8
+//   TPM   thread-per-matrix, whole matrix in registers      f64 N<=7, f32 N<=11
 //   DMMA  FP64 tensor-core DMMA.8x8x4 (mma.sync m8n8k4.f64), N padded to 8k;
 //         W warps per matrix (W=1 up to N=40 resident / 32 streaming, else a CTA)
 //   F32   FP32 register-tiled outer products with FFMA2, W warps per matrix
@@ -61,6 +61,14 @@ JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage
 // low-repeat kernel) measured 0.71 at R = 100 (204 registers: 8 warps per SM,
 // the per-update shuffle exchange exposed; profiles/r01_tpm2_n8.jsonl), so it
 // is off.
+// FP32: thread per matrix up to n = 11 (m and p: 242 floats, 216 registers,
+// no spill).  n = 9..11 ran on the row panels at 0.28-0.43 of the FP32 pipe
+// (R = 100; padding to 4-column chunks and 3-row panels); thread per matrix
+// with prefetching stage reaches 0.79-0.82, and 0.86-0.93 of HBM at R = 1
+// (profiles/r01_f32_tpm_n9_11.jsonl).  n = 12 (288 floats) would spill.
+#ifndef JM_F32_TPM_MAX
+#define JM_F32_TPM_MAX 11
+#endif
 #ifndef JM_F64_TPM2
 #define JM_F64_TPM2 0
 #endif
@@ -68,7 +76,7 @@ JM_HD constexpr Tile tile_for(int n, int dtype) {
   return dtype == 1 ? (n <= 7 ? Tile::TPM
                        : (n == 8 && JM_F64_TPM2) ? Tile::Tpm2
                        : ((n >= 9 && n <= JM_F64_ROWS_MAX) ? Tile::Rows : Tile::Dmma))
-                    : (n <= 8 ? Tile::TPM : Tile::F32);
+                    : (n <= JM_F32_TPM_MAX ? Tile::TPM : Tile::F32);
 }
 
 // ---- F64 row panels (9 <= n <= 12): DFMA, where DMMA padding wastes most ----
@@ -230,7 +238,7 @@ JM_HD constexpr int f32p_mbuf(int n) { return n * f32p_ncs(n) * 16 + 32; }
 // CTAs per SM) do take it: +2-3 % at R = 100, +10-46 % at R <= 16
 // (profiles/r01_tpm_stream_sweep.jsonl, r01_tpm_stream_hi.jsonl).
 JM_HD constexpr bool prefetch_for(int n, int dtype) {
-  return dtype == 1 ? (n >= 5 && n <= 7) : (n == 8);
+  return dtype == 1 ? (n >= 5 && n <= 7) : (n >= 8 && n <= JM_F32_TPM_MAX);
 }
 
 JM_HD constexpr Plan plan_specialized(int n, int dtype) {
