@@ -228,6 +228,19 @@ JM_HD constexpr int f32p_halves(int n) { return n <= 16 ? 1 : cdiv(f32p_ncr(n), 
 // multiple of 64 B, so the two matrices sharing a quarter-warp land in
 // opposite halves of the 128-B bank window
 JM_HD constexpr int f32p_mbuf(int n) { return n * f32p_ncs(n) * 16 + 32; }
+// resident kernel: the matrix's stage slot, widened to a row buffer, doubles as
+// the first row buffer (run_f32p INPL), one buffer less per matrix: n = 12
+// 0.52 -> 0.65 and n = 14 0.50 -> 0.60 of the FP32 pipe at R = 100; n = 16
+// (already register-limited to 5 CTAs per SM) measured 0.72 -> 0.69 and keeps
+// two own buffers (profiles/r01_f32p_inplace.jsonl).  JM_F32P_INPLACE=0 turns
+// it off.
+#ifndef JM_F32P_INPLACE
+#define JM_F32P_INPLACE 1
+#endif
+JM_HD constexpr bool f32p_inplace(int n) { return JM_F32P_INPLACE && (n * n * 4) % 16 == 0 && n < 16; }
+JM_HD constexpr int f32p_slot(int n) {
+  return rup(f32p_mbuf(n) > stage_stride(n, 4) ? f32p_mbuf(n) : stage_stride(n, 4), 16);
+}
 
 // Double-buffered (cp.async prefetch) staging.  Measured on B200 (r01 sweep):
 // it lifts DMMA n=16 at repeat 1 from 0.87 to 0.94 of HBM, but the doubled
@@ -264,6 +277,7 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   }
   if (f32p_use(n)) {
     const int mpc = F32P_WPC * f32p_mpw(n);
+    if (f32p_inplace(n)) return Plan{(int)t, 32 * F32P_WPC, mpc, nst * rup(mpc * f32p_slot(n), 16) + mpc * f32p_mbuf(n), 1};
     return Plan{(int)t, 32 * F32P_WPC, mpc, nst * stage_bytes(mpc, n, es) + 2 * mpc * f32p_mbuf(n), 1};
   }
   // F32 tiles: the stage area IS the per-matrix region (stride f32_region)

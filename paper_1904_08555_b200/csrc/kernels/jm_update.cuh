@@ -198,7 +198,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 template <int N, int ES, int SB, int NT, int MPC, bool AL, bool PF>
 struct Stager {
   static constexpr int MB = N * N * ES;
-  static constexpr int SZ = stage_bytes(MPC, N, ES);
+  static constexpr int SZ = rup(MPC * SB, 16);   // one stage buffer
   const char *in;
   char *out;
   char *base;
@@ -936,7 +936,12 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
   constexpr int NCS = f32p_ncs(N), HALVES = f32p_halves(N), MBUF = f32p_mbuf(N);
   constexpr int NC = 4 * NCR;                          // computed columns (16-B padded)
   constexpr int QH = cdiv(NCR, HALVES);                     // chunks per column group
-  constexpr int ES = 4, MB = N * N * 4, SB = stage_stride(N, 4);
+  constexpr int ES = 4, MB = N * N * 4;
+  // resident: the staged matrix's slot (f32p_slot bytes) doubles as the first
+  // of its two row buffers once the rows sit in registers, so only the second
+  // buffer needs its own area (f32p_inplace); streaming: two own buffers
+  constexpr bool INPL = !STRM && f32p_inplace(N);
+  constexpr int SB = INPL ? f32p_slot(N) : stage_stride(N, 4);
   constexpr int NT = 32 * F32P_WPC, MPC = F32P_WPC * MPW;
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   static_assert(G * RP >= N, "row panels must cover the matrix");
@@ -948,7 +953,7 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
   const int mw = lane / G, tg = lane - mw * G;
   const int mi = warp * MPW + mw;                      // matrix slot in the chunk
   const int r0 = tg * RP;
-  char *bufs = smem + Stg::BYTES + mi * 2 * MBUF;
+  char *bufs = smem + Stg::BYTES + mi * (INPL ? 1 : 2) * MBUF;
   const float c = float(0.00005);
 
   Stg sg(in, out, batch, smem);
@@ -960,6 +965,9 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
     // slots past the batch end compute on zeros and are never written back
     const bool live = mi < cnt;
     float *sm = reinterpret_cast<float *>(stage + mi * Stg::SBM);
+    // the two row buffers: b0 (the slot itself when INPL) and b1
+    char *b0 = INPL ? reinterpret_cast<char *>(sm) : bufs;
+    char *b1 = INPL ? bufs : bufs + MBUF;
     float m[RP][NC];
 #pragma unroll
     for (int i = 0; i < RP; ++i)
@@ -968,19 +976,20 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
         const int row = r0 + i;
         m[i][j] = (live && row < N && j < N) ? sm[row * N + j] : 0.0f;
       }
+    if constexpr (INPL) __syncwarp();         // the matrix's threads have read the slot
 #pragma unroll
     for (int i = 0; i < RP; ++i)
       if (r0 + i < N) {
 #pragma unroll
         for (int q = 0; q < NCR; ++q)
-          *reinterpret_cast<float4 *>(bufs + f32p_off<NCS>(r0 + i, q)) =
+          *reinterpret_cast<float4 *>(b0 + f32p_off<NCS>(r0 + i, q)) =
               make_float4(m[i][4 * q], m[i][4 * q + 1], m[i][4 * q + 2], m[i][4 * q + 3]);
       }
     __syncwarp();
 #pragma unroll 1
     for (int r = 0; r < repeat; ++r) {
-      const char *cur = bufs + (r & 1) * MBUF;
-      char *nxt = bufs + ((r & 1) ^ 1) * MBUF;
+      const char *cur = (r & 1) ? b1 : b0;
+      char *nxt = (r & 1) ? b0 : b1;
 #pragma unroll
       for (int h = 0; h < HALVES; ++h) {
         constexpr int QMAX = QH;
