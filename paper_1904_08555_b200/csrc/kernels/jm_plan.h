@@ -166,7 +166,15 @@ JM_HD constexpr bool f32_col_blocked(int n) {
 struct F32Tile {
   int rg, ra, cg, cb;
 };
+#ifndef JM_F32_TILE_RA                // tuning hook: force the register-tile shape
+#define JM_F32_TILE_RA 0
+#endif
+#ifndef JM_F32_TILE_CB
+#define JM_F32_TILE_CB 0
+#endif
 JM_HD constexpr F32Tile f32_tile(int n) {
+  if (JM_F32_TILE_RA > 0 && JM_F32_TILE_CB > 0)
+    return F32Tile{cdiv(n, JM_F32_TILE_RA), JM_F32_TILE_RA, cdiv(n, JM_F32_TILE_CB), JM_F32_TILE_CB};
   F32Tile best{cdiv(n, 8), cdiv(n, cdiv(n, 8)), cdiv(n, 16), rup(cdiv(n, cdiv(n, 16)), 4)};
   double bs = -1.0;
   for (int ra = 8; ra >= 2; --ra)
