@@ -126,8 +126,9 @@ JM_API int jit_mat_init(int device);
  * double-buffered cp.async stage — which is
  * a second cache key, compiled on its first such call.  Results agree with the
  * resident kernel bit for bit (same arithmetic in the same order), except f64
- * n = 33, 34, where the resident kernel forms the thin border with DFMA (both
- * within the parity bound).  Environment
+ * n = 33, 34, where the resident kernel forms the thin border with DFMA, and
+ * f64 n = 9, 10, where the resident kernel is thread-per-matrix DFMA and the
+ * low-repeat one the DMMA ring (both within the parity bound).  Environment
  * JIT_MAT_STREAM=0/1 forces resident/streaming, JIT_MAT_STREAM_RN moves the
  * switch point (read once per process); per call, jm_run_desc.flags
  * JM_FLAG_RESIDENT / JM_FLAG_STREAMING force it. */
@@ -263,7 +264,8 @@ typedef struct {
 /* tiling kinds reported in jm_key_info.tile */
 enum { JM_TILE_GENERIC = 0, JM_TILE_TPM = 1, JM_TILE_WARP_DMMA = 2, JM_TILE_CTA_DMMA = 3,
        JM_TILE_WARP_F32 = 4, JM_TILE_CTA_F32 = 5, JM_TILE_ROWS = 6, JM_TILE_MATMUL = 7,
-       JM_TILE_TPM2 = 8 /* two threads per matrix (FP64 n = 8) */ };
+       JM_TILE_TPM2 = 8 /* two threads per matrix (FP64 n = 8) */,
+       JM_TILE_TPMS = 9 /* thread per matrix, product staged in shared memory (FP64 n = 9, 10) */ };
 
 JM_API int jit_mat_stats(jm_stats *out);
 /* Copy up to `cap` non-empty slots into `keys`; returns the number of

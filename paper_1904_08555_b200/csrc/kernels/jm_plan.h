@@ -21,7 +21,7 @@
 namespace jm {
 
 enum class Addend : int { Ones = 0, Identity = 1 };
-enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, Tpm2 = 3, F32 = 4, Rows = 6 };
+enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, Tpm2 = 3, F32 = 4, Tpms = 5, Rows = 6 };
 
 struct Plan {
   int tile;      // Tile
@@ -72,9 +72,17 @@ JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage
 #ifndef JM_F64_TPM2
 #define JM_F64_TPM2 0
 #endif
+// FP64 n = 9, 10: thread per matrix with the product staged row by row in the
+// matrix's own shared-memory slot (Tile::Tpms, run_tpms): M stays in registers
+// (81 / 100 doubles), P (which needs the old M until its last row) waits in the
+// slot.  DMMA pads these sizes to 16 x 16 tiles (0.23 of the pipe).
+#ifndef JM_F64_TPMS_MAX
+#define JM_F64_TPMS_MAX 10
+#endif
 JM_HD constexpr Tile tile_for(int n, int dtype) {
   return dtype == 1 ? (n <= 7 ? Tile::TPM
                        : (n == 8 && JM_F64_TPM2) ? Tile::Tpm2
+                       : (n >= 9 && n <= JM_F64_TPMS_MAX) ? Tile::Tpms
                        : ((n >= 9 && n <= JM_F64_ROWS_MAX) ? Tile::Rows : Tile::Dmma))
                     : (n <= JM_F32_TPM_MAX ? Tile::TPM : Tile::F32);
 }
@@ -272,6 +280,9 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   if (t == Tile::Tpm2) {
     return Plan{(int)t, TPM_THREADS, TPM2_MPC, 2 * stage_bytes(TPM2_MPC, n, es), 1};
   }
+  if (t == Tile::Tpms) {
+    return Plan{(int)t, TPM_THREADS, TPM_THREADS, stage_bytes(TPM_THREADS, n, es), 1};
+  }
   if (t == Tile::Rows) {
     const int mpc = F64P_WPC * (32 / F64P_G);
     return Plan{(int)t, 32 * F64P_WPC, mpc, stage_bytes(mpc, n, es) + 2 * mpc * f64p_mbuf(n), 1};
@@ -325,6 +336,7 @@ JM_HD constexpr bool use_mb1(int n, int dtype, bool strm = false) {
 // of 32..512 B)
 JM_HD constexpr bool stream_ok(int n, int dtype) {
   return tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::F32 || tile_for(n, dtype) == Tile::Tpm2 ||
+         tile_for(n, dtype) == Tile::Tpms ||
          tile_for(n, dtype) == Tile::TPM;
 }
 // The host's switch: stream iff repeat * (n + 1) < stream_rn(n, dtype).
@@ -341,8 +353,14 @@ JM_HD constexpr bool stream_ok(int n, int dtype) {
 #ifndef JM_TPM2_RN
 #define JM_TPM2_RN 20
 #endif
+// n = 9, 10: the DMMA ring streams better only at R = 1 (0.68 vs 0.56 of HBM);
+// from R = 2 the staged-product kind wins (R = 100: 0.65 / 0.68 of the FP64
+// pipe vs 0.22 / 0.24 for the padded DMMA tile; profiles/r01_tpms_n9_10.jsonl)
+#ifndef JM_TPMS_RN
+#define JM_TPMS_RN 20
+#endif
 JM_HD constexpr int stream_rn_f64(int n) {
-  return n < 8 ? 0 : n == 8 ? (JM_F64_TPM2 ? JM_TPM2_RN : 0) : n <= 32 ? 600 : n <= 34 ? 100 : n <= 40 ? 300 : n <= 48 ? 250 : n <= 56 ? 600 : 400;
+  return (n >= 9 && n <= JM_F64_TPMS_MAX) ? JM_TPMS_RN : n < 8 ? 0 : n == 8 ? (JM_F64_TPM2 ? JM_TPM2_RN : 0) : n <= 32 ? 600 : n <= 34 ? 100 : n <= 40 ? 300 : n <= 48 ? 250 : n <= 56 ? 600 : 400;
 }
 // ... and not below stream_lo(n, dtype): f64 n = 16 at R = 1, whose resident
 // kernel (16 KB, 48 registers: 40 warps per SM) streams at 0.95 of HBM once
@@ -395,7 +413,7 @@ JM_HD constexpr int f32_ring_slot(int n) {
 JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8); }
 // matrices per round of each kind (the resident plan's chunk)
 JM_HD constexpr int round_mpc(int n, int dtype) {
-  return tile_for(n, dtype) == Tile::Dmma ? (dmma_w(n, true) == 1 ? DMMA_WPC : 1)
+  return (tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::Tpms) ? (dmma_w(n, true) == 1 ? DMMA_WPC : 1)
          : f32p_use(n)                   ? F32P_WPC * f32p_mpw(n)
                                          : F32_WPC * f32_mpw(n);
 }
@@ -409,7 +427,7 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
     return Plan{(int)Tile::TPM, TPM_THREADS, TPM_THREADS, 2 * stage_bytes(TPM_THREADS, n, es), 1};
   if (tile_for(n, dtype) == Tile::Tpm2)   // low-repeat kernel: the resident warp DMMA tile
     return Plan{(int)Tile::Dmma, 32 * DMMA_WPC, DMMA_WPC, stage_bytes(DMMA_WPC, n, es) + DMMA_WPC * dmma_scr(n), 1};
-  if (tile_for(n, dtype) == Tile::Dmma) {
+  if (tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::Tpms) {   // (Tpms: DMMA ring)
     const int w = dmma_w(n, true);
     const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers
     return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm) + own * dmma_scr(n), w};

@@ -499,6 +499,63 @@ __device__ __forceinline__ void run_tpm(const T *__restrict__ in, T *__restrict_
 }
 
 // ======================================================================
+// TPMS: thread per matrix with the product staged in shared memory (FP64,
+// N = 9, 10).  M lives in registers for all updates; P = M + M*M is formed
+// one row at a time (N independent accumulator chains, k ascending) and
+// parked in the matrix's own staging slot, which is idle between the chunk's
+// load and store; once every row of P exists the epilogue M = A + c*P reads
+// it back.  Slots of odd 8-B stride (packed, N*N odd) or odd 16-B stride keep
+// the lanes' 8-B accesses on distinct banks.
+// ======================================================================
+template <int N, Addend A>
+__device__ __forceinline__ void run_tpms(const double *__restrict__ in, double *__restrict__ out,
+                                         long long batch, int repeat) {
+  constexpr int ES = 8, SB = stage_stride(N, 8);
+  constexpr int NT = TPM_THREADS, MPC = TPM_THREADS;
+  extern __shared__ __align__(16) char smem[];
+  const int tid = threadIdx.x;
+  const double c = 0.00005;
+  Stager<N, ES, SB, NT, MPC, true, false> sg(in, out, batch, smem);
+  for (sg.start(); sg.valid(); sg.next()) {
+    sg.acquire();
+    if (tid < sg.cnt()) {
+      double *slot = reinterpret_cast<double *>(sg.buf() + tid * SB);
+      double m[N * N];
+#pragma unroll
+      for (int e = 0; e < N * N; ++e) m[e] = slot[e];
+#pragma unroll 1
+      for (int r = 0; r < repeat; ++r) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          // one row of P live at a time (ptxas would interleave rows: spills)
+          asm volatile("" ::: "memory");
+          double p[N];
+#pragma unroll
+          for (int j = 0; j < N; ++j) p[j] = m[i * N + j];      // accumulators start at M
+#pragma unroll
+          for (int k = 0; k < N; ++k)
+#pragma unroll
+            for (int j = 0; j < N; ++j) p[j] = fmaT(m[i * N + k], m[k * N + j], p[j]);
+#pragma unroll
+          for (int j = 0; j < N; ++j) slot[i * N + j] = p[j];
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            const double pv = slot[i * N + j];
+            m[i * N + j] = (A == Addend::Ones || i == j) ? fmaT(c, pv, 1.0) : c * pv;
+          }
+      }
+#pragma unroll
+      for (int e = 0; e < N * N; ++e) slot[e] = m[e];
+    }
+    sg.release();
+  }
+  sg.finish();
+}
+
+// ======================================================================
 // TPM2: two threads per matrix, DFMA only (FP64, even N; used for N = 8).
 // Each thread keeps the WHOLE matrix in registers and forms half of the rows
 // of P = M + M*M; the halves are exchanged with one shuffle per element.  The
@@ -1348,6 +1405,9 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
   static_assert(!STRM || stream_ok(N, sizeof(T) == 8 ? 1 : 0), "no streaming variant of this kind");
   if constexpr (K == Tile::TPM) {
     run_tpm<N, T, A, STRM>(in, out, batch, repeat);
+  } else if constexpr (K == Tile::Tpms) {
+    if constexpr (STRM) run_dmma<N, A, 1, true>(in, out, batch, repeat);   // low repeat: the DMMA ring
+    else run_tpms<N, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Tpm2) {
     if constexpr (STRM) run_dmma<N, A, 1, false>(in, out, batch, repeat);   // its low-repeat kernel
     else run_tpm2<N, A>(in, out, batch, repeat);

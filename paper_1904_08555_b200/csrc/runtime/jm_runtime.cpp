@@ -231,6 +231,7 @@ const char *tile_name(int t) {
     case jm::Tile::TPM: return "TPM";
     case jm::Tile::Dmma: return "Dmma";
     case jm::Tile::Tpm2: return "Tpm2";
+    case jm::Tile::Tpms: return "Tpms";
     case jm::Tile::F32: return "F32";
     case jm::Tile::Rows: return "Rows";
     default: return "Generic";
@@ -1023,6 +1024,7 @@ int jit_mat_key_info(jm_key_info *keys, int cap) {
             o.tile = k == JM_KIND_GENERIC ? JM_TILE_GENERIC
                      : (s.plan.tile == (int)jm::Tile::TPM ? JM_TILE_TPM
                         : s.plan.tile == (int)jm::Tile::Tpm2 ? JM_TILE_TPM2
+                        : s.plan.tile == (int)jm::Tile::Tpms ? JM_TILE_TPMS
                         : s.plan.tile == (int)jm::Tile::Rows ? JM_TILE_ROWS
                         : s.plan.tile == (int)jm::Tile::Dmma ? (s.plan.w > 1 ? JM_TILE_CTA_DMMA : JM_TILE_WARP_DMMA)
                         : (s.plan.w > 1 ? JM_TILE_CTA_F32 : JM_TILE_WARP_F32));

@@ -48,8 +48,10 @@ def _batch_for(n):
 def _same_bits(n, dt):
     # both variants form every entry in the same order, except f64 n = 33 / 34,
     # where the resident kernel (whole matrix per warp) takes the thin-border
-    # DFMA path and the streaming one (one warp per row tile) does not
-    return not (dt == "f64" and n in (33, 34))
+    # DFMA path and the streaming one (one warp per row tile) does not, and
+    # f64 n = 9 / 10, whose resident kernel is thread-per-matrix DFMA (TPMS)
+    # and whose low-repeat kernel is the DMMA ring
+    return not (dt == "f64" and n in (9, 10, 33, 34))
 
 
 def _run(jm, x, repeat, variant, addend="ones", inplace=False):
