@@ -38,8 +38,9 @@ CONFIGS = [(2, "f64", "resident", True), (4, "f64", "resident", True), (7, "f64"
            (8, "f64", "resident", True), (16, "f64", "resident", True), (16, "f64", "streaming", True),
            (32, "f64", "resident", True), (32, "f64", "streaming", True), (64, "f64", "resident", True),
            (12, "f64", "resident", False), (17, "f64", "resident", False), (25, "f64", "resident", False),
-           (41, "f64", "resident", False),
+           (41, "f64", "resident", False), (9, "f64", "resident", True), (10, "f64", "resident", True),
            (2, "f32", "resident", True), (3, "f32", "resident", True), (8, "f32", "resident", True),
+           (11, "f32", "resident", True), (12, "f32", "resident", True),
            (16, "f32", "resident", True), (32, "f32", "resident", False), (64, "f32", "resident", False)]
 
 
