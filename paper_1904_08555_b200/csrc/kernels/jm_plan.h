@@ -76,6 +76,9 @@ JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage
 // matrix's own shared-memory slot (Tile::Tpms, run_tpms): M stays in registers
 // (81 / 100 doubles), P (which needs the old M until its last row) waits in the
 // slot.  DMMA pads these sizes to 16 x 16 tiles (0.23 of the pipe).
+#ifndef JM_F32_TPMS_MAX
+#define JM_F32_TPMS_MAX 11           // FP32 staged-product thread per matrix up to this n (none by default)
+#endif
 #ifndef JM_F64_TPMS_MAX
 #define JM_F64_TPMS_MAX 10
 #endif
@@ -84,7 +87,8 @@ JM_HD constexpr Tile tile_for(int n, int dtype) {
                        : (n == 8 && JM_F64_TPM2) ? Tile::Tpm2
                        : (n >= 9 && n <= JM_F64_TPMS_MAX) ? Tile::Tpms
                        : ((n >= 9 && n <= JM_F64_ROWS_MAX) ? Tile::Rows : Tile::Dmma))
-                    : (n <= JM_F32_TPM_MAX ? Tile::TPM : Tile::F32);
+                    : (n <= JM_F32_TPM_MAX ? Tile::TPM
+                       : (n <= JM_F32_TPMS_MAX ? Tile::Tpms : Tile::F32));
 }
 
 // ---- F64 row panels (9 <= n <= 12): DFMA, where DMMA padding wastes most ----
@@ -413,7 +417,8 @@ JM_HD constexpr int f32_ring_slot(int n) {
 JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8); }
 // matrices per round of each kind (the resident plan's chunk)
 JM_HD constexpr int round_mpc(int n, int dtype) {
-  return (tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::Tpms) ? (dmma_w(n, true) == 1 ? DMMA_WPC : 1)
+  return (tile_for(n, dtype) == Tile::Dmma || (dtype == 1 && tile_for(n, dtype) == Tile::Tpms))
+             ? (dmma_w(n, true) == 1 ? DMMA_WPC : 1)
          : f32p_use(n)                   ? F32P_WPC * f32p_mpw(n)
                                          : F32_WPC * f32_mpw(n);
 }
@@ -427,7 +432,7 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
     return Plan{(int)Tile::TPM, TPM_THREADS, TPM_THREADS, 2 * stage_bytes(TPM_THREADS, n, es), 1};
   if (tile_for(n, dtype) == Tile::Tpm2)   // low-repeat kernel: the resident warp DMMA tile
     return Plan{(int)Tile::Dmma, 32 * DMMA_WPC, DMMA_WPC, stage_bytes(DMMA_WPC, n, es) + DMMA_WPC * dmma_scr(n), 1};
-  if (tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::Tpms) {   // (Tpms: DMMA ring)
+  if (tile_for(n, dtype) == Tile::Dmma || (dtype == 1 && tile_for(n, dtype) == Tile::Tpms)) {   // (Tpms: DMMA ring)
     const int w = dmma_w(n, true);
     const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers
     return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm) + own * dmma_scr(n), w};
@@ -435,6 +440,18 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   if (f32p_use(n)) return Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
   return Plan{(int)Tile::F32, 32 * F32_WPC, chm,
               ring_bytes(n, es, rm, f32_ring_slot(n)) + (f32_ring_slot(n) ? 0 : rm * f32_region(n)), 1};
+}
+
+// FP32: the ring's chunks must be multiples of 16 B, so for odd n >= 49 a
+// chunk holds 4 matrices (up to 63 KB) and the streaming plan needs up to
+// 162 KB of shared memory: one 2-warp CTA per SM, slower than the resident
+// kernel (n = 63 at R = 1: 0.18 vs 0.20 of HBM; profiles/r01_all_n_sweep.jsonl).
+// The host streams FP32 only when the plan leaves room for two CTAs.
+#ifndef JM_STREAM_F32_SMEM_MAX
+#define JM_STREAM_F32_SMEM_MAX (112 * 1024)
+#endif
+JM_HD constexpr bool stream_fits(int n, int dtype) {
+  return dtype == 1 || plan_stream(n, dtype).smem <= JM_STREAM_F32_SMEM_MAX;
 }
 
 // Note: k_update passes only maxThreads to __launch_bounds__.  Registers are

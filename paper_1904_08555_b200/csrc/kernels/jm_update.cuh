@@ -507,20 +507,20 @@ __device__ __forceinline__ void run_tpm(const T *__restrict__ in, T *__restrict_
 // it back.  Slots of odd 8-B stride (packed, N*N odd) or odd 16-B stride keep
 // the lanes' 8-B accesses on distinct banks.
 // ======================================================================
-template <int N, Addend A>
-__device__ __forceinline__ void run_tpms(const double *__restrict__ in, double *__restrict__ out,
+template <int N, class T, Addend A>
+__device__ __forceinline__ void run_tpms(const T *__restrict__ in, T *__restrict__ out,
                                          long long batch, int repeat) {
-  constexpr int ES = 8, SB = stage_stride(N, 8);
+  constexpr int ES = sizeof(T), SB = stage_stride(N, ES);
   constexpr int NT = TPM_THREADS, MPC = TPM_THREADS;
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x;
-  const double c = 0.00005;
+  const T c = T(0.00005);
   Stager<N, ES, SB, NT, MPC, true, false> sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     if (tid < sg.cnt()) {
-      double *slot = reinterpret_cast<double *>(sg.buf() + tid * SB);
-      double m[N * N];
+      T *slot = reinterpret_cast<T *>(sg.buf() + tid * SB);
+      T m[N * N];
 #pragma unroll
       for (int e = 0; e < N * N; ++e) m[e] = slot[e];
 #pragma unroll 1
@@ -529,22 +529,45 @@ __device__ __forceinline__ void run_tpms(const double *__restrict__ in, double *
         for (int i = 0; i < N; ++i) {
           // one row of P live at a time (ptxas would interleave rows: spills)
           asm volatile("" ::: "memory");
-          double p[N];
+          if constexpr (ES == 4) {     // FP32: column pairs through FFMA2
+            constexpr int NH = N / 2;
+            float2 p2[NH > 0 ? NH : 1];
+            float pl = 0.0f;
 #pragma unroll
-          for (int j = 0; j < N; ++j) p[j] = m[i * N + j];      // accumulators start at M
+            for (int jj = 0; jj < NH; ++jj) p2[jj] = make_float2(m[i * N + 2 * jj], m[i * N + 2 * jj + 1]);
+            if constexpr (N % 2) pl = m[i * N + N - 1];
 #pragma unroll
-          for (int k = 0; k < N; ++k)
+            for (int k = 0; k < N; ++k) {
+              const float a = m[i * N + k];
 #pragma unroll
-            for (int j = 0; j < N; ++j) p[j] = fmaT(m[i * N + k], m[k * N + j], p[j]);
+              for (int jj = 0; jj < NH; ++jj)
+                p2[jj] = __ffma2_rn(make_float2(a, a), make_float2(m[k * N + 2 * jj], m[k * N + 2 * jj + 1]), p2[jj]);
+              if constexpr (N % 2) pl = fmaT(a, m[k * N + N - 1], pl);
+            }
 #pragma unroll
-          for (int j = 0; j < N; ++j) slot[i * N + j] = p[j];
+            for (int jj = 0; jj < NH; ++jj) {
+              slot[i * N + 2 * jj] = p2[jj].x;
+              slot[i * N + 2 * jj + 1] = p2[jj].y;
+            }
+            if constexpr (N % 2) slot[i * N + N - 1] = pl;
+          } else {
+            T p[N];
+#pragma unroll
+            for (int j = 0; j < N; ++j) p[j] = m[i * N + j];      // accumulators start at M
+#pragma unroll
+            for (int k = 0; k < N; ++k)
+#pragma unroll
+              for (int j = 0; j < N; ++j) p[j] = fmaT(m[i * N + k], m[k * N + j], p[j]);
+#pragma unroll
+            for (int j = 0; j < N; ++j) slot[i * N + j] = p[j];
+          }
         }
 #pragma unroll
         for (int i = 0; i < N; ++i)
 #pragma unroll
           for (int j = 0; j < N; ++j) {
-            const double pv = slot[i * N + j];
-            m[i * N + j] = (A == Addend::Ones || i == j) ? fmaT(c, pv, 1.0) : c * pv;
+            const T pv = slot[i * N + j];
+            m[i * N + j] = (A == Addend::Ones || i == j) ? fmaT(c, pv, T(1)) : c * pv;
           }
       }
 #pragma unroll
@@ -1405,9 +1428,12 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
   static_assert(!STRM || stream_ok(N, sizeof(T) == 8 ? 1 : 0), "no streaming variant of this kind");
   if constexpr (K == Tile::TPM) {
     run_tpm<N, T, A, STRM>(in, out, batch, repeat);
+  } else if constexpr (K == Tile::Tpms && sizeof(T) == 4) {
+    if constexpr (STRM) run_f32p<N, A, true>(in, out, batch, repeat);      // low repeat: row panels + ring
+    else run_tpms<N, T, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Tpms) {
     if constexpr (STRM) run_dmma<N, A, 1, true>(in, out, batch, repeat);   // low repeat: the DMMA ring
-    else run_tpms<N, A>(in, out, batch, repeat);
+    else run_tpms<N, T, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Tpm2) {
     if constexpr (STRM) run_dmma<N, A, 1, false>(in, out, batch, repeat);   // its low-repeat kernel
     else run_tpm2<N, A>(in, out, batch, repeat);

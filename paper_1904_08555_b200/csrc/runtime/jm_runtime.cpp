@@ -470,7 +470,7 @@ bool want_stream(int n, int dtype, int kind, int64_t repeat, unsigned flags = 0)
   }();
   if (force >= 0) return force > 0;
   const int64_t rn = repeat * (int64_t)(n + 1);
-  return rn < (int64_t)stream_rn(n, dtype) && rn >= (int64_t)jm::stream_lo(n, dtype);
+  return rn < (int64_t)stream_rn(n, dtype) && rn >= (int64_t)jm::stream_lo(n, dtype) && jm::stream_fits(n, dtype);
 }
 
 Slot &slot_of(int n, int dtype, int addend, int kind, bool stream) {
