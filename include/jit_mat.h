@@ -127,8 +127,9 @@ JM_API int jit_mat_init(int device);
  * a second cache key, compiled on its first such call.  Results agree with the
  * resident kernel bit for bit (same arithmetic in the same order), except f64
  * n = 33, 34, where the resident kernel forms the thin border with DFMA, and
- * f64 n = 9, 10, where the resident kernel is thread-per-matrix DFMA and the
- * low-repeat one the DMMA ring (both within the parity bound).  Environment
+ * f64 n = 9, 10 and f32 n = 12..14, where the resident kernel is thread per
+ * matrix with a staged product and the low-repeat one the DMMA / row-panel
+ * ring (both within the parity bound).  Environment
  * JIT_MAT_STREAM=0/1 forces resident/streaming, JIT_MAT_STREAM_RN moves the
  * switch point (read once per process); per call, jm_run_desc.flags
  * JM_FLAG_RESIDENT / JM_FLAG_STREAMING force it. */

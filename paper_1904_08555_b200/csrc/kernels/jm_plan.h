@@ -76,8 +76,12 @@ JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage
 // matrix's own shared-memory slot (Tile::Tpms, run_tpms): M stays in registers
 // (81 / 100 doubles), P (which needs the old M until its last row) waits in the
 // slot.  DMMA pads these sizes to 16 x 16 tiles (0.23 of the pipe).
+// FP32 n = 12..14: thread per matrix with the product staged in the slot
+// (run_tpms, FFMA2 rows): 0.70 of the FP32 pipe at R = 100 against 0.48-0.60
+// for the row panels (n = 13: 0.44 -> 0.70); n = 15 (255 registers) is slower
+// than the row panels and keeps them (profiles/r01_f32_tpms.jsonl)
 #ifndef JM_F32_TPMS_MAX
-#define JM_F32_TPMS_MAX 11           // FP32 staged-product thread per matrix up to this n (none by default)
+#define JM_F32_TPMS_MAX 14
 #endif
 #ifndef JM_F64_TPMS_MAX
 #define JM_F64_TPMS_MAX 10
@@ -381,6 +385,7 @@ JM_HD constexpr int stream_rn_tpm(int, int) { return 0; }
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype)               ? 0
          : tile_for(n, dtype) == Tile::TPM ? stream_rn_tpm(n, dtype)
+         : (dtype == 0 && tile_for(n, dtype) == Tile::Tpms) ? (n == 12 ? 0 : 20)   // R = 1: row-panel ring
          : dtype == 1        ? stream_rn_f64(n)
          : f32p_use(n)       ? 64
                              : 140;

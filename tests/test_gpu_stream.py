@@ -49,9 +49,10 @@ def _same_bits(n, dt):
     # both variants form every entry in the same order, except f64 n = 33 / 34,
     # where the resident kernel (whole matrix per warp) takes the thin-border
     # DFMA path and the streaming one (one warp per row tile) does not, and
-    # f64 n = 9 / 10, whose resident kernel is thread-per-matrix DFMA (TPMS)
-    # and whose low-repeat kernel is the DMMA ring
-    return not (dt == "f64" and n in (9, 10, 33, 34))
+    # f64 n = 9 / 10 and f32 n = 12..14, whose resident kernel is thread per
+    # matrix with a staged product (TPMS) and whose low-repeat kernel is the
+    # DMMA ring / the row-panel ring
+    return not ((dt == "f64" and n in (9, 10, 33, 34)) or (dt == "f32" and n in (12, 13, 14)))
 
 
 def _run(jm, x, repeat, variant, addend="ones", inplace=False):
@@ -135,6 +136,8 @@ def test_variant_selection_and_key_info(jm):
     assert jm.jit_mat_prepare_for(33, "f64", 2) == 1       # 68 < 100: thin-border resident above
     assert jm.jit_mat_prepare_for(33, "f64", 3) == 0
     assert jm.jit_mat_prepare_for(16, "f32", 3) == 1       # 51 < 64
+    assert jm.jit_mat_prepare_for(12, "f32", 1) == 0       # TPMS beats the ring even at R = 1
+    assert jm.jit_mat_prepare_for(13, "f32", 1) == 1 and jm.jit_mat_prepare_for(13, "f32", 2) == 0
     assert jm.jit_mat_prepare_for(16, "f32", 4) == 0
     assert jm.jit_mat_prepare_for(64, "f32", 2) == 1       # 130 < 140
     assert jm.jit_mat_prepare_for(64, "f32", 3) == 0
