@@ -96,7 +96,10 @@ JM_HD constexpr Tile tile_for(int n, int dtype) {
 }
 
 // ---- F64 row panels (9 <= n <= 12): DFMA, where DMMA padding wastes most ----
-constexpr int F64P_G = 4;                          // threads per matrix
+#ifndef JM_F64P_G
+#define JM_F64P_G 4
+#endif
+constexpr int F64P_G = JM_F64P_G;                  // threads per matrix
 constexpr int F64P_WPC = 2;                        // warps per CTA
 JM_HD constexpr int f64p_rp(int n) { return cdiv(n, F64P_G); }             // rows per thread (3)
 JM_HD constexpr int f64p_ncr(int n) { return cdiv(n, 2); }                 // 16-B chunks per row
