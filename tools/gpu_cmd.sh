@@ -1,8 +1,5 @@
-for G in 2 4; do
-JM_BUILD_DEFINES="JM_F64_ROWS_MAX=15 JM_F64P_G=$G" python -m paper_1904_08555_b200._build --force > /dev/null 2>&1; echo build rc=$?
-python tools/stream_sweep.py --sizes 11,12,13,15 --dtypes f64 --repeats 1,100 --gb 1 --steps 3 2>/dev/null | python -c "
-import json,sys
-for l in sys.stdin:
-    d=json.loads(l); print('G=$G', d['n'], d['repeat'], 'pipe %.3f hbm %.2f'%(d['resident']['frac_pipe'], d['resident']['frac_hbm']), d['kernels']['0'])
-"
-done
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | grep -v "^\.\+ *\[" | tail -4
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 1800 python tools/sweep.py --out gpurun_out/sweep_v6.jsonl > gpurun_out/sweep_v6.log 2>&1; echo sweep rc=$?
+timeout 600 python bench.py > gpurun_out/bench_v6.json 2> gpurun_out/bench_v6.err; echo bench rc=$?
+python tools/stream_sweep.py --sizes $(seq -s, 2 64) --dtypes f64,f32 --repeats 1,100 --gb 0.5 --steps 3 > gpurun_out/all_n_v2.jsonl 2>&1; echo alln rc=$?
