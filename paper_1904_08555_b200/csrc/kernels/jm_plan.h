@@ -385,10 +385,12 @@ JM_HD constexpr int stream_lo(int n, int dtype) { return (dtype == 1 && n == 16)
 // (prefetch_for); it loses up to 23 % on the small, light sizes (f64 n = 2:
 // 0.96 -> 0.74 of HBM).  So the TPM streaming key is never picked by default.
 JM_HD constexpr int stream_rn_tpm(int, int) { return 0; }
+JM_HD constexpr bool f32_stream_pf(int n);   // below, with the ring sizes
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype)               ? 0
          : tile_for(n, dtype) == Tile::TPM ? stream_rn_tpm(n, dtype)
          : (dtype == 0 && tile_for(n, dtype) == Tile::Tpms) ? (n == 12 ? 0 : 20)   // R = 1: row-panel ring
+         : (dtype == 0 && f32_stream_pf(n)) ? n + 2   // the stage variant: R = 1 only (r01_f32_odd_stream)
          : dtype == 1        ? stream_rn_f64(n)
          : f32p_use(n)       ? 64
                              : 140;
@@ -415,6 +417,23 @@ JM_HD constexpr int ring_bytes(int n, int es, int rm, int slot = 0) {
 #ifndef JM_F32_RING_INPLACE
 #define JM_F32_RING_INPLACE 0
 #endif
+// FP32 tiles, low repeat: the bulk-copy ring, except where its plan would not
+// leave two CTAs per SM (odd n >= 49: the 16-B chunk rule makes 4-matrix
+// chunks, up to 162 KB); those use the resident layout with the double-
+// buffered cp.async stage instead (two REG regions per matrix): n = 63 at
+// R = 1 0.20 -> 0.23 of HBM, where the ring got 0.18 (r01_f32_stream_pf.jsonl;
+// elsewhere the ring is better, JM_F32_STREAM_PF=1 forces the stage for all)
+#ifndef JM_F32_STREAM_PF
+#define JM_F32_STREAM_PF 0
+#endif
+#ifndef JM_STREAM_F32_SMEM_MAX
+#define JM_STREAM_F32_SMEM_MAX (110 * 1024)   // two CTAs incl. the 1 KB per-CTA reserve
+#endif
+JM_HD constexpr int f32_rm(int n) { return F32_WPC * f32_mpw(n); }
+JM_HD constexpr bool f32_stream_pf(int n) {
+  return n >= 17 && !f32p_use(n) &&
+         (JM_F32_STREAM_PF || ring_bytes(n, 4, f32_rm(n)) + f32_rm(n) * f32_region(n) > JM_STREAM_F32_SMEM_MAX);
+}
 JM_HD constexpr int f32_ring_slot(int n) {
   return (JM_F32_RING_INPLACE && (n * n * 4) % 16 == 0) ? f32_region(n) : 0;
 }
@@ -446,18 +465,13 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
     return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm) + own * dmma_scr(n), w};
   }
   if (f32p_use(n)) return Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
+  if (f32_stream_pf(n)) return Plan{(int)Tile::F32, 32 * F32_WPC, rm, 2 * rup(rm * f32_region(n), 16), 1};
   return Plan{(int)Tile::F32, 32 * F32_WPC, chm,
               ring_bytes(n, es, rm, f32_ring_slot(n)) + (f32_ring_slot(n) ? 0 : rm * f32_region(n)), 1};
 }
 
-// FP32: the ring's chunks must be multiples of 16 B, so for odd n >= 49 a
-// chunk holds 4 matrices (up to 63 KB) and the streaming plan needs up to
-// 162 KB of shared memory: one 2-warp CTA per SM, slower than the resident
-// kernel (n = 63 at R = 1: 0.18 vs 0.20 of HBM; profiles/r01_all_n_sweep.jsonl).
-// The host streams FP32 only when the plan leaves room for two CTAs.
-#ifndef JM_STREAM_F32_SMEM_MAX
-#define JM_STREAM_F32_SMEM_MAX (112 * 1024)
-#endif
+// The host streams FP32 only when the plan leaves room for two CTAs per SM
+// (a single 2-warp CTA loses to the resident kernel; see f32_stream_pf).
 JM_HD constexpr bool stream_fits(int n, int dtype) {
   return dtype == 1 || plan_stream(n, dtype).smem <= JM_STREAM_F32_SMEM_MAX;
 }

@@ -1317,15 +1317,20 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
   // resident: the staged matrix's region doubles as its work area (sM);
   // streaming: the same in REG-sized ring slots when each matrix is its own
   // copy (f32_ring_slot), else work areas of REG bytes after the ring
-  constexpr int SLOT = f32_ring_slot(N);
-  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, SLOT>,
-                        Stager<N, ES, REG, NT, MPC, AL, false>>::type Stg;
+  // (f32_stream_pf: the low-repeat variant is instead the resident layout
+  // with the double-buffered cp.async stage — two REG regions per matrix
+  // rather than two ring slots plus a work area)
+  constexpr bool SPF = STRM && f32_stream_pf(N);
+  constexpr int SLOT = SPF ? 0 : f32_ring_slot(N);
+  typedef typename Pick<STRM && !SPF, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, SLOT>,
+                        Stager<N, ES, REG, NT, MPC, AL, SPF>>::type Stg;
   Stg sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     const bool live = (m < MPW) && (mi < sg.cnt());
     float *src = reinterpret_cast<float *>(sg.buf() + (m < MPW ? mi : 0) * Stg::SBM);
-    float *sm = (STRM && !SLOT) ? reinterpret_cast<float *>(smem + Stg::BYTES + (m < MPW ? mi : 0) * REG) : src;
+    float *sm = (STRM && !SPF && !SLOT) ? reinterpret_cast<float *>(smem + Stg::BYTES + (m < MPW ? mi : 0) * REG)
+                                        : src;
     float2 p[RA][CB / 2];
     if (live) {
 #pragma unroll

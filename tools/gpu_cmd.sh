@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_fullsize.py -q 2>&1 | tail -5
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | grep -v "^\.\+ *\[" | tail -4
+python tools/stream_sweep.py --sizes 49,51,53,55,57,59,61,63 --dtypes f32 --repeats 1,2,4 --gb 0.5 --steps 3 > gpurun_out/f32odd.jsonl 2>&1; echo rc=$?
