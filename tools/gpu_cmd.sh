@@ -1,3 +1,4 @@
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_update -s 2 -c 1 -o gpurun_out/prof_tpms10 python bench.py --n 10 --repeat 100 --batch 1048576 --steps 1 --warmup 3 --no-generic --no-e2e --no-cpu > /dev/null 2>&1; echo rc=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_update -s 2 -c 1 -o gpurun_out/prof_f32tpms13 python bench.py --n 13 --dtype f32 --repeat 100 --batch 1048576 --steps 1 --warmup 3 --no-generic --no-e2e --no-cpu > /dev/null 2>&1; echo rc=$?
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | grep -v "^\.\+ *\[" | tail -3
+mkdir -p gpurun_out/san
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 1800 compute-sanitizer --tool $tool python tools/sanitize_run.py > gpurun_out/san/$tool.txt 2>&1; echo $tool rc=$?; tail -1 gpurun_out/san/$tool.txt
+done

@@ -24,9 +24,11 @@ import torch  # noqa: E402
 
 import paper_1904_08555_b200 as jm  # noqa: E402
 
-CASES = [(2, "f64"), (3, "f64"), (5, "f64"), (7, "f64"), (16, "f64"), (13, "f64"), (17, "f64"),
-         (26, "f64"), (32, "f64"), (33, "f64"), (40, "f64"), (44, "f64"), (48, "f64"), (64, "f64"),
-         (3, "f32"), (8, "f32"), (12, "f32"), (16, "f32"), (24, "f32"), (33, "f32"), (64, "f32")]
+CASES = [(2, "f64"), (3, "f64"), (5, "f64"), (7, "f64"), (9, "f64"), (10, "f64"), (16, "f64"),
+         (13, "f64"), (17, "f64"), (26, "f64"), (32, "f64"), (33, "f64"), (40, "f64"), (44, "f64"),
+         (48, "f64"), (64, "f64"),
+         (3, "f32"), (8, "f32"), (10, "f32"), (12, "f32"), (13, "f32"), (16, "f32"), (24, "f32"),
+         (33, "f32"), (53, "f32"), (64, "f32")]
 
 
 def main():
