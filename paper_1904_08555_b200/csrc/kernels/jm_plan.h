@@ -441,7 +441,22 @@ JM_HD constexpr int f32_ring_slot(int n) {
 // matrix's ring slot (n a multiple of 16), the slot is reused as that buffer
 // (W == 1) or as the first of the two (W > 1) once M sits in the accumulators:
 // n = 32 then holds 3 CTAs per SM instead of 2, n = 48 / 64 two instead of one
-JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8); }
+// For other even n the slot can be widened to the publish buffer's size
+// (dmma_slot), one ring slot per matrix instead of a slot plus a separate
+// buffer.  Measured (profiles/r01_dmma_ring_slot.jsonl, R = 1): it pays where
+// it lifts the CTAs per SM — n = 26..30 (2 -> 3 CTAs: 0.65 -> 0.76 of HBM at
+// n = 28) and 58..62 (1 -> 2: 0.37 -> 0.45 at n = 62) — and is noise or a
+// loss elsewhere (n = 56: 0.54 -> 0.49), so it is applied there only
+// (JM_DMMA_RING_SLOT=0: never, =2: every even n).
+#ifndef JM_DMMA_RING_SLOT
+#define JM_DMMA_RING_SLOT 1
+#endif
+JM_HD constexpr int dmma_slot(int n) {
+  return (n % 2 == 0 && dmma_scr(n) > ring_sbm(n, 8) &&
+          (JM_DMMA_RING_SLOT == 2 || (JM_DMMA_RING_SLOT == 1 && ((n >= 26 && n <= 30) || n >= 58))))
+             ? dmma_scr(n) : 0;
+}
+JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8, dmma_slot(n)); }
 // matrices per round of each kind (the resident plan's chunk)
 JM_HD constexpr int round_mpc(int n, int dtype) {
   return (tile_for(n, dtype) == Tile::Dmma || (dtype == 1 && tile_for(n, dtype) == Tile::Tpms))
@@ -462,7 +477,7 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   if (tile_for(n, dtype) == Tile::Dmma || (dtype == 1 && tile_for(n, dtype) == Tile::Tpms)) {   // (Tpms: DMMA ring)
     const int w = dmma_w(n, true);
     const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers
-    return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm) + own * dmma_scr(n), w};
+    return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm, dmma_slot(n)) + own * dmma_scr(n), w};
   }
   if (f32p_use(n)) return Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
   if (f32_stream_pf(n)) return Plan{(int)Tile::F32, 32 * F32_WPC, rm, 2 * rup(rm * f32_region(n), 16), 1};

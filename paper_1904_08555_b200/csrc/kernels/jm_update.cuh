@@ -693,10 +693,11 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   // tiles are skipped by warp-uniform branches
   constexpr bool RAG = RT * W != T8;
   constexpr bool PF = prefetch_for(N, 1);
-  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S>,
+  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, dmma_slot(N)>,
                         Stager<N, ES, SB, NT, MPC, AL, PF>>::type Stg;
-  // streaming, n a multiple of 16: the matrix's ring slot doubles as its
-  // (first) publish buffer once M is in the accumulators (plan_stream)
+  // streaming, even n: the matrix's ring slot (widened to the publish buffer
+  // when needed, dmma_slot) doubles as its (first) publish buffer once M is in
+  // the accumulators (plan_stream)
   constexpr bool INPL = STRM && dmma_inplace(N);
   // thin border (n = 8K + BR, BR <= JM_DMMA_BORDER_MAX, whole matrix per warp):
   // the last row / column tile holds only BR real rows / columns, so its
