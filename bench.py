@@ -362,6 +362,15 @@ def main():
                                 % (64 if dt == "f64" else 128)),
                 "algorithmic_flops_per_launch": B * R * fpu,
                 "hbm_gbs_achieved": hbm_gbs}
+        # the same fraction against this pool's measured pipe peak (SURVEY.md §7
+        # hard part 3: nominal and measured side by side)
+        mb = os.path.join(ROOT, "profiles", "r01_microbench_peaks.json")
+        if os.path.exists(mb):
+            with open(mb) as f:
+                mpk = json.load(f).get("dmma_tflops" if dt == "f64" else "ffma2_tflops")
+            if mpk:
+                roof["peak_measured"] = mpk
+                roof["frac_of_measured"] = achieved_tf / mpk
     else:
         roof = {"bound": "hbm", "achieved": hbm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": hbm_gbs / peaks["hbm_gbs"], "traffic": traffic,
