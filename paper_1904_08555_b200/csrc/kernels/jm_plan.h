@@ -268,6 +268,13 @@ JM_HD constexpr bool f32p_inplace(int n) { return JM_F32P_INPLACE && (n * n * 4)
 JM_HD constexpr int f32p_slot(int n) {
   return rup(f32p_mbuf(n) > stage_stride(n, 4) ? f32p_mbuf(n) : stage_stride(n, 4), 16);
 }
+// the same in the streaming variant's ring (slots widened to a row buffer):
+// measured slower at R = 1 for n = 14 / 16 (0.69 -> 0.51, 0.54 -> 0.50 of
+// HBM; profiles/r01_f32p_ring_inplace.jsonl), so off
+#ifndef JM_F32P_RING_INPLACE
+#define JM_F32P_RING_INPLACE 0
+#endif
+JM_HD constexpr bool f32p_ring_inplace(int n) { return JM_F32P_RING_INPLACE && (n * n * 4) % 16 == 0; }
 
 // Double-buffered (cp.async prefetch) staging.  Measured on B200 (r01 sweep):
 // it lifts DMMA n=16 at repeat 1 from 0.87 to 0.94 of HBM, but the doubled
@@ -479,7 +486,10 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
     const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers
     return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm, dmma_slot(n)) + own * dmma_scr(n), w};
   }
-  if (f32p_use(n)) return Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
+  if (f32p_use(n))
+    return f32p_ring_inplace(n)
+               ? Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm, f32p_slot(n)) + rm * f32p_mbuf(n), 1}
+               : Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
   if (f32_stream_pf(n)) return Plan{(int)Tile::F32, 32 * F32_WPC, rm, 2 * rup(rm * f32_region(n), 16), 1};
   return Plan{(int)Tile::F32, 32 * F32_WPC, chm,
               ring_bytes(n, es, rm, f32_ring_slot(n)) + (f32_ring_slot(n) ? 0 : rm * f32_region(n)), 1};

@@ -1021,13 +1021,14 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
   // resident: the staged matrix's slot (f32p_slot bytes) doubles as the first
   // of its two row buffers once the rows sit in registers, so only the second
   // buffer needs its own area (f32p_inplace); streaming: two own buffers
-  constexpr bool INPL = !STRM && f32p_inplace(N);
+  // (streaming: the same with ring slots widened to a row buffer, f32p_ring_inplace)
+  constexpr bool INPL = STRM ? f32p_ring_inplace(N) : f32p_inplace(N);
   constexpr int SB = INPL ? f32p_slot(N) : stage_stride(N, 4);
   constexpr int NT = 32 * F32P_WPC, MPC = F32P_WPC * MPW;
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   static_assert(G * RP >= N, "row panels must cover the matrix");
   constexpr bool PF = prefetch_for(N, 0);
-  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S>,
+  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, INPL ? f32p_slot(N) : 0>,
                         Stager<N, ES, SB, NT, MPC, AL, PF>>::type Stg;
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
