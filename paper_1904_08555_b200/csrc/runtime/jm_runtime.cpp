@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <dlfcn.h>
 #include <nvrtc.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: no-ops unless a profiler injects itself
 
 #include <algorithm>
 #include <atomic>
@@ -362,7 +363,15 @@ int install_cubin(Slot &s, int op, int n, int dtype, int extra, std::vector<char
   return JM_OK;
 }
 
+// NVTX range for the duration of a scope (jm:compile / jm:run,
+// for ncu --nvtx filtering and timeline tools)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 int compile_slot(Slot &s, int op, int n, int dtype, int addend) {
+  NvtxRange nvtx("jm:compile");
   const auto t0 = std::chrono::steady_clock::now();
   c_compilations++;
   std::vector<char> cubin;
@@ -580,6 +589,7 @@ int run_host(const jm_run_desc *d, Slot &s) {
 }
 
 int run_impl(const jm_run_desc *d) {
+  NvtxRange nvtx("jm:run");
   int rc = validate_run(d);
   if (rc != JM_OK || d->batch == 0) return rc;
   Slot *s = nullptr;
