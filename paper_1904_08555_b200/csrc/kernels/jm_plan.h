@@ -191,9 +191,20 @@ struct F32Tile {
 #ifndef JM_F32_TILE_CB
 #define JM_F32_TILE_CB 0
 #endif
+// measured overrides of the model (profiles/r01_f32_tile_shape_search.txt,
+// FP32 pipe at R = 100): wider column blocks for the sizes just above 16 / 24
+JM_HD constexpr int f32_tile_ra_override(int n) {
+  return (n == 17 || n == 18) ? 6 : (n == 19 || n == 20 || n == 25) ? 5 : 0;
+}
+JM_HD constexpr int f32_tile_cb_override(int n) {
+  return (n == 17 || n == 18) ? 20 : (n == 19 || n == 25) ? 28 : n == 20 ? 12 : 0;
+}
 JM_HD constexpr F32Tile f32_tile(int n) {
   if (JM_F32_TILE_RA > 0 && JM_F32_TILE_CB > 0)
     return F32Tile{cdiv(n, JM_F32_TILE_RA), JM_F32_TILE_RA, cdiv(n, JM_F32_TILE_CB), JM_F32_TILE_CB};
+  if (f32_tile_ra_override(n) > 0)   // 17, 18: 0.31 / 0.36 -> 0.33 / 0.40; 19, 20, 25: +4..9 %
+    return F32Tile{cdiv(n, f32_tile_ra_override(n)), f32_tile_ra_override(n), cdiv(n, f32_tile_cb_override(n)),
+                   f32_tile_cb_override(n)};
   F32Tile best{cdiv(n, 8), cdiv(n, cdiv(n, 8)), cdiv(n, 16), rup(cdiv(n, cdiv(n, 16)), 4)};
   double bs = -1.0;
   for (int ra = 8; ra >= 2; --ra)
