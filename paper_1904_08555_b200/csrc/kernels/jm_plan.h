@@ -193,11 +193,16 @@ struct F32Tile {
 #endif
 // measured overrides of the model (profiles/r01_f32_tile_shape_search.txt,
 // FP32 pipe at R = 100): wider column blocks for the sizes just above 16 / 24
+// (and r01_f32_tile_shape_search_n21_64.txt: 21..24 as 6 x 12, +5..13 %;
+// 37..40 as 5 x 20, +24..28 %; elsewhere the model's shape was best or within
+// the ~5 % run-to-run noise)
 JM_HD constexpr int f32_tile_ra_override(int n) {
-  return (n == 17 || n == 18) ? 6 : (n == 19 || n == 20 || n == 25) ? 5 : 0;
+  return (n == 17 || n == 18) ? 6 : (n == 19 || n == 20 || n == 25) ? 5 : (n >= 21 && n <= 24) ? 6
+         : (n >= 37 && n <= 40) ? 5 : 0;
 }
 JM_HD constexpr int f32_tile_cb_override(int n) {
-  return (n == 17 || n == 18) ? 20 : (n == 19 || n == 25) ? 28 : n == 20 ? 12 : 0;
+  return (n == 17 || n == 18) ? 20 : (n == 19 || n == 25) ? 28 : n == 20 ? 12 : (n >= 21 && n <= 24) ? 12
+         : (n >= 37 && n <= 40) ? 20 : 0;
 }
 JM_HD constexpr F32Tile f32_tile(int n) {
   if (JM_F32_TILE_RA > 0 && JM_F32_TILE_CB > 0)
