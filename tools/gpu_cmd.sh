@@ -1,16 +1,7 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-SIZES=$(seq -s, 26 64)
-python tools/stream_sweep.py --sizes $SIZES --dtypes f32 --repeats 100 --gb 0.25 --steps 5 2>/dev/null | python -c "
-import json,sys
-for l in sys.stdin:
-    d=json.loads(l); print('default', d['n'], round(d['resident']['frac_pipe'],3), d['kernels']['0']['regs'], d['kernels']['0']['local'])
-"
-for shape in "7 12" "7 20" "6 24" "4 32" "8 8" "8 20" "3 16" "6 28"; do
-  set -- $shape
-  JM_BUILD_DEFINES="JM_F32_TILE_RA=$1 JM_F32_TILE_CB=$2" python -m paper_1904_08555_b200._build --force > /dev/null 2>&1
-  python tools/stream_sweep.py --sizes $SIZES --dtypes f32 --repeats 100 --gb 0.25 --steps 5 2>/dev/null | python -c "
-import json,sys
-for l in sys.stdin:
-    d=json.loads(l); print('ra=$1 cb=$2', d['n'], round(d['resident']['frac_pipe'],3), d['kernels']['0']['regs'], d['kernels']['0']['local'])
-"
-done
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | grep -v "^\.\+ *\[" | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 600 python bench.py > gpurun_out/bench_v9.json 2> gpurun_out/bench_v9.err; echo bench rc=$?
+timeout 1800 python tools/sweep.py --out gpurun_out/sweep_v9.jsonl > gpurun_out/sweep_v9.log 2>&1; echo sweep rc=$?
+python tools/stream_sweep.py --sizes $(seq -s, 2 64) --dtypes f64,f32 --repeats 1,100 --gb 0.5 --steps 3 > gpurun_out/all_n_v4.jsonl 2>&1; echo alln rc=$?
+timeout 1800 python tools/work_check.py --out gpurun_out/work_check4.jsonl > gpurun_out/work_check4.log 2>&1; echo wc rc=$?
