@@ -117,9 +117,9 @@ JM_API int jit_mat_init(int device);
  * VARIANT (every specialized entry point): a call whose
  * repeat * (n + 1) is below the kind's measured switch point (jm_plan.h
  * stream_rn: 100..600 for f64 n >= 9 by tiling kind, 64 for f32 n = 9..16,
- * 140 for f32 n >= 17, never for thread-per-matrix sizes (f64 n <= 7, f32
- * n <= 11; their staged variant is selectable with JM_FLAG_STREAMING) and not
- * at f64 n = 16, R = 1; the HBM-bound side of the roofline and somewhat
+ * 140 for f32 n >= 17, for thread-per-matrix sizes (f64 n <= 7, f32 n <= 11)
+ * only at f32 n = 3 with R >= 8 (their staged variant is selectable with
+ * JM_FLAG_STREAMING), and not at f64 n = 16, R = 1; the HBM-bound side of the roofline and somewhat
  * beyond)
  * runs the STREAMING variant of the same specialization — the same tile code
  * behind a bulk-copy (TMA) ring, or for thread-per-matrix sizes behind a

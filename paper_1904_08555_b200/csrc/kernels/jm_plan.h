@@ -400,14 +400,20 @@ JM_HD constexpr int stream_rn_f64(int n) {
 // kernel (16 KB, 48 registers: 40 warps per SM) streams at 0.95 of HBM once
 // its accumulator loads are conflict free, against 0.88 through the ring
 // (profiles/r01_ring_lowr_sweep.jsonl; from R = 2 the ring wins, 0.91 vs 0.80)
-JM_HD constexpr int stream_lo(int n, int dtype) { return (dtype == 1 && n == 16) ? 18 : 0; }
+JM_HD constexpr int stream_lo(int n, int dtype) {
+  return (dtype == 1 && n == 16) ? 18 : (dtype == 0 && n == 3) ? 32 : 0;
+}
 // Thread per matrix (profiles/r01_tpm_stream_sweep.jsonl): the staged
 // variant wins where registers limit the resident kernel to few CTAs — f64
 // n = 5..7 (1.14-1.46x at R = 1..8; n = 6 R = 1: 0.66 -> 0.94 of HBM) and
 // f32 n = 8 — at every R, so those sizes' resident kernel prefetches itself
 // (prefetch_for); it loses up to 23 % on the small, light sizes (f64 n = 2:
 // 0.96 -> 0.74 of HBM).  So the TPM streaming key is never picked by default.
-JM_HD constexpr int stream_rn_tpm(int, int) { return 0; }
+// One exception: f32 n = 3 gains from the staged variant once R >= 8
+// (1.13x at R = 8, 1.05x at R = 100) and loses below (0.89x at R = 1), so it
+// streams above the lower bound stream_lo (r01_all_n_sweep.jsonl,
+// r01_tpm_stream_sweep.jsonl).
+JM_HD constexpr int stream_rn_tpm(int n, int dtype) { return (dtype == 0 && n == 3) ? (1 << 30) : 0; }
 JM_HD constexpr bool f32_stream_pf(int n);   // below, with the ring sizes
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype)               ? 0

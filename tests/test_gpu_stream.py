@@ -144,6 +144,8 @@ def test_variant_selection_and_key_info(jm):
     assert jm.jit_mat_prepare_for(8, "f64", 1) == 0        # n = 8 DMMA: resident (measured)
     assert jm.jit_mat_prepare_for(4, "f64", 1, flags=jm.JM_FLAG_STREAMING) == 1   # TPM: staged variant
     assert jm.jit_mat_prepare_for(4, "f64", 1) == 0        # light TPM sizes stay resident
+    assert jm.jit_mat_prepare_for(3, "f32", 7) == 0        # ... except f32 n = 3 from R = 8 on
+    assert jm.jit_mat_prepare_for(3, "f32", 8) == 1 and jm.jit_mat_prepare_for(3, "f32", 100) == 1
     assert jm.jit_mat_prepare_for(6, "f64", 1) == 0        # register-heavy TPM: the resident kernel prefetches
     assert jm.jit_mat_prepare_for(16, "f64", 1, kind="generic") == 0
     assert jm.jit_mat_prepare_for(16, "f64", 100, flags=jm.JM_FLAG_STREAMING) == 1
