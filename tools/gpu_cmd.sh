@@ -1,3 +1,3 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | grep -v "^\.\+ *\[" | tail -3
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 1800 python tools/sweep.py --out gpurun_out/sweep_v10.jsonl > gpurun_out/sweep_v10.log 2>&1; echo sweep rc=$?
+timeout 600 python bench.py > gpurun_out/bench_v10.json 2> gpurun_out/bench_v10.err; echo bench rc=$?
