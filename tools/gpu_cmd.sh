@@ -1,3 +1,6 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-timeout 1800 python tools/sweep.py --out gpurun_out/sweep_v10.jsonl > gpurun_out/sweep_v10.log 2>&1; echo sweep rc=$?
-timeout 600 python bench.py > gpurun_out/bench_v10.json 2> gpurun_out/bench_v10.err; echo bench rc=$?
+for mb in 16 32 64 128 256; do
+  JIT_MAT_HOST_CHUNK_MB=$mb timeout 600 python bench.py --no-cpu --no-generic --steps 5 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('chunk_mb=$mb', d['e2e']['value'], d['e2e']['ms_per_step'])"
+done
