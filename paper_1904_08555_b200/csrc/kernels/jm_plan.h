@@ -382,8 +382,10 @@ JM_HD constexpr bool stream_ok(int n, int dtype) {
 // to R(n+1) ~ 600 (n = 32: 1.96x at R = 1, 1.18x at R = 8); n = 33 / 34 (the
 // resident kernel has the thin border there) only at R <= 2; 35..40 to ~300;
 // 41..48 to ~250; 49..56 to ~600; 57..64 to ~400; n = 8 loses 8 % at R = 1
-// (16 copies of 512 B per chunk) and stays resident.  f32 row panels
-// (n = 9..16) gain to ~64, f32 tiles (n >= 17) to ~140.
+// (16 copies of 512 B per chunk) and stays resident; n = 9, 10 see JM_TPMS_RN.
+// f32: row panels (n = 15, 16) gain to ~64, tiles (n >= 17) to ~140; the
+// staged-product sizes (12..14) and the thread-per-matrix sizes have their
+// own rules below.
 #ifndef JM_TPM2_RN
 #define JM_TPM2_RN 20
 #endif
@@ -406,9 +408,9 @@ JM_HD constexpr int stream_lo(int n, int dtype) {
 // Thread per matrix (profiles/r01_tpm_stream_sweep.jsonl): the staged
 // variant wins where registers limit the resident kernel to few CTAs — f64
 // n = 5..7 (1.14-1.46x at R = 1..8; n = 6 R = 1: 0.66 -> 0.94 of HBM) and
-// f32 n = 8 — at every R, so those sizes' resident kernel prefetches itself
-// (prefetch_for); it loses up to 23 % on the small, light sizes (f64 n = 2:
-// 0.96 -> 0.74 of HBM).  So the TPM streaming key is never picked by default.
+// f32 n = 8..11 — at every R, so those sizes' resident kernel prefetches
+// itself (prefetch_for); it loses up to 23 % on the small, light sizes (f64
+// n = 2: 0.96 -> 0.74 of HBM).  So the TPM streaming key is normally not picked.
 // One exception: f32 n = 3 gains from the staged variant once R >= 8
 // (1.13x at R = 8, 1.05x at R = 100) and loses below (0.89x at R = 1), so it
 // streams above the lower bound stream_lo (r01_all_n_sweep.jsonl,
