@@ -1,6 +1,5 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-for mb in 16 32 64 128 256; do
-  JIT_MAT_HOST_CHUNK_MB=$mb timeout 600 python bench.py --no-cpu --no-generic --steps 5 2>/dev/null | python -c "
-import json,sys
-d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('chunk_mb=$mb', d['e2e']['value'], d['e2e']['ms_per_step'])"
-done
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | grep -v "^\.\+ *\[" | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 600 python bench.py --steps 10 > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo bench rc=$?
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_final.json 2>&1; echo ref rc=$?
