@@ -83,6 +83,9 @@ JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage
 #ifndef JM_F32_TPMS_MAX
 #define JM_F32_TPMS_MAX 14
 #endif
+#ifndef JM_TPMS_ROWS
+#define JM_TPMS_ROWS 1               // rows of P formed between scheduling fences (run_tpms)
+#endif
 #ifndef JM_F64_TPMS_MAX
 #define JM_F64_TPMS_MAX 10
 #endif

@@ -527,8 +527,9 @@ __device__ __forceinline__ void run_tpms(const T *__restrict__ in, T *__restrict
       for (int r = 0; r < repeat; ++r) {
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          // one row of P live at a time (ptxas would interleave rows: spills)
-          asm volatile("" ::: "memory");
+          // JM_TPMS_ROWS rows of P live at a time (ptxas would interleave all
+          // rows: spills)
+          if (i % JM_TPMS_ROWS == 0) asm volatile("" ::: "memory");
           if constexpr (ES == 4) {     // FP32: column pairs through FFMA2
             constexpr int NH = N / 2;
             float2 p2[NH > 0 ? NH : 1];
