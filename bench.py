@@ -39,7 +39,9 @@ NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 TF
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs (one rank each); N > 1 without torchrun re-launches itself under "
+                         "torch.distributed.run (default: WORLD_SIZE, else 1)")
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -219,13 +221,45 @@ def emit(line: dict, a) -> None:
             f.write(s + "\n")
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(a) -> int:
+    """`bench.py --gpus N` (N > 1) started as a plain process: run the same
+    command as N ranks under torch.distributed.run (one process per GPU,
+    rendezvous on 127.0.0.1), so the driver's command line and torchrun's
+    give the same job."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def resolve_world(a) -> tuple[int, int, int]:
+    """(world, rank, local_rank) from the torchrun environment, checked against --gpus."""
+    env_world = os.environ.get("WORLD_SIZE")
+    world = int(env_world) if env_world is not None else 1
+    if a.gpus is None:
+        a.gpus = world
+    if env_world is not None and world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    return world, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
 # ------------------------------------------------------------------ GPU leg
 def main():
     a = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if a.impl == "reference":
+    if a.impl != "reference" and (a.gpus or 1) > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(a))
+    world, rank, local = resolve_world(a)
+    if os.environ.get("JM_BENCH_DRY_RUN"):    # test hook: the launch contract only, no GPU work
+        print(json.dumps({"rank": rank, "world": world, "gpus": a.gpus, "local_rank": local}), flush=True)
+        return
+    if a.impl == "reference":     # (rank 0 only; n_gpus = --gpus, as in the GPU arm)
         run_reference(a, rank)
         return
 
@@ -278,21 +312,26 @@ def main():
 
     # ---- multi-GPU: rank 0 specializes, the others import its cubins over
     # NCCL instead of running NVRTC themselves
+    # ---- first call: NVRTC specialization (reported separately, never timed);
+    # under N > 1 it is rank 0's compile, which the other ranks then import
+    first_call_ms = None
     if world > 1 and a.kind == "specialized":
         blob = None
         if rank == 0:
+            t0 = time.perf_counter()
             jm.jit_mat_prepare_for(n, dt, R, a.addend, a.kind)
+            first_call_ms = (time.perf_counter() - t0) * 1e3
             blob = jm.jit_mat_cache_export(n, dt, a.addend)
         blob = shard.broadcast_blob(dist, blob, 0, cdev)
         if rank != 0:
             jm.jit_mat_cache_import(blob)
 
-    # ---- first call: NVRTC specialization (reported separately, never timed)
     t0 = time.perf_counter()
     # the kernel this repeat count selects: resident, or the streaming variant
     # on the HBM-bound side (include/jit_mat.h VARIANT)
     variant = jm.jit_mat_prepare_for(n, dt, R, a.addend, a.kind)
-    first_call_ms = (time.perf_counter() - t0) * 1e3
+    if first_call_ms is None:
+        first_call_ms = (time.perf_counter() - t0) * 1e3
     key = [k for k in jm.jit_mat_key_info()
            if k["op"] == 0 and k["n"] == n and k["dtype"] == (1 if dt == "f64" else 0)
            and k["kind"] == {"specialized": 0, "generic": 1, "aot_specialized": 2}[a.kind]
@@ -338,14 +377,17 @@ def main():
     global_checksum = shard.combine_checksums(c[0] for c in cks)
 
     fpu = flops_per_update(n, a.addend)
-    achieved_tf = B * R * fpu / (ms_step / 1e3) / 1e12       # this rank's kernel
+    # the dominant kernel's rate per GPU: the largest slice over the slowest
+    # rank's launch time (max over ranks, as `value`)
+    b_max = max(r[1] for r in recs)
+    achieved_tf = b_max * R * fpu / (ms_max / 1e3) / 1e12
     peak_tf = NOMINAL_FP64_TFLOPS if dt == "f64" else NOMINAL_FP32_TFLOPS
-    alg_bytes = 2 * B * n * n * es
-    hbm_gbs = alg_bytes / (ms_step / 1e3) / 1e9
+    alg_bytes = 2 * int(b_max) * n * n * es
+    hbm_gbs = alg_bytes / (ms_max / 1e3) / 1e9
     # which roofline binds: compare ideal compute vs ideal HBM time
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         peaks = json.load(f)
-    t_comp = B * R * fpu / (peak_tf * 1e12)
+    t_comp = b_max * R * fpu / (peak_tf * 1e12)
     t_hbm = alg_bytes / (peaks["hbm_gbs"] * 1e9)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -360,7 +402,7 @@ def main():
                 "peak_source": ("derived: 148 SM x %d FMA/clk x 2 x 1.965 GHz (DESIGN.md); "
                                 "microbench measured DMMA 36.95 / DFMA 36.74 TF (profiles/r01_microbench_peaks.json)"
                                 % (64 if dt == "f64" else 128)),
-                "algorithmic_flops_per_launch": B * R * fpu,
+                "algorithmic_flops_per_launch": int(b_max) * R * fpu,
                 "hbm_gbs_achieved": hbm_gbs}
         # the same fraction against this pool's measured pipe peak (SURVEY.md §7
         # hard part 3: nominal and measured side by side)
@@ -378,7 +420,7 @@ def main():
                 "algorithmic_bytes_per_launch": alg_bytes, "tflops_achieved": achieved_tf}
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": max(3, a.warmup), "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "strong" if a.global_batch is not None else "weak",
         "vs_baseline": None, "dtype": dt, "data": "synthetic",
@@ -393,8 +435,9 @@ def main():
         "clocks": clocks,
         "gpu_launches": launches,
         "nvrtc_first_call_ms": first_call_ms,
-        "specializations": ("rank 0 compiled, ranks 1..N-1 imported its cubins (NCCL broadcast)"
+        "specializations": (f"rank 0 compiled, ranks 1..N-1 imported its cubins ({backend} broadcast)"
                             if world > 1 and a.kind == "specialized" else "compiled in this process"),
+        "collective_backend": backend if world > 1 else None,
         "kernel": {"tile": key["tile_name"], "variant": "streaming" if variant else "resident",
                    "regs": key["regs"], "local_bytes": key["local_bytes"],
                    "smem_bytes": key["smem_bytes"], "threads": key["threads"],

@@ -85,7 +85,9 @@ enum {
   JM_E_UNSUPPORTED = -2,      /* n > 64, dtype not f32/f64 ("long double"), unknown type name */
   JM_E_NOT_INITIALIZED = -3,  /* jit_mat_init not called, or after jit_mat_shutdown */
   JM_E_ARCH = -4,             /* device is not sm_100 (compute capability 10.x) */
-  JM_E_COMPILE = -5,          /* NVRTC or module load failed; log in jit_mat_last_error() */
+  JM_E_COMPILE = -5,          /* NVRTC or module load failed, or the compiled kernel's plan cannot
+                                  run on this device (shared memory, occupancy); log in
+                                  jit_mat_last_error(); the key is then FAILED (not retried) */
   JM_E_CUDA = -6,             /* CUDA driver error (message in jit_mat_last_error()) */
   JM_E_ALIGN = -7             /* in/out not 16-byte aligned */
 };
@@ -175,14 +177,17 @@ JM_API int jit_mat_run_many(const jm_run_desc *descs, int count, void *stream, u
 
 /* Share specializations between processes (the paper's
  * compile-time concern).  jit_mat_cache_export writes a
- * self-describing blob ("JMC2": key + per compiled variant — resident and/or
- * streaming — the kernel symbol and sm_100a cubin) of a specialized key into
+ * self-describing blob ("JMC3": the library's build digest, the key, and per
+ * compiled variant — resident and/or streaming — the name expression, kernel
+ * symbol and sm_100a cubin) of a specialized key into
  * `buf` (`cap` bytes); `*len` receives the blob size (pass buf = NULL to
  * query).  JM_E_INVALID if neither variant of the key has been compiled.
  * jit_mat_cache_import installs such a blob (from the same library build) for
  * its key without running NVRTC: one rank compiles, broadcasts the blob, the
- * other ranks import it.  Importing into a READY slot is a no-op (JM_OK); a blob
- * for another key or a corrupt blob is JM_E_INVALID. */
+ * other ranks import it.  Importing into a READY slot is a no-op (JM_OK); a
+ * blob from another build (digest mismatch), an entry whose name expression is
+ * not the one this build compiles for the key, or a corrupt blob is
+ * JM_E_INVALID. */
 JM_API int jit_mat_cache_export(int n, int dtype, int addend, void *buf, size_t cap, size_t *len);
 JM_API int jit_mat_cache_import(const void *blob, size_t len);
 
@@ -266,7 +271,8 @@ typedef struct {
 enum { JM_TILE_GENERIC = 0, JM_TILE_TPM = 1, JM_TILE_WARP_DMMA = 2, JM_TILE_CTA_DMMA = 3,
        JM_TILE_WARP_F32 = 4, JM_TILE_CTA_F32 = 5, JM_TILE_ROWS = 6, JM_TILE_MATMUL = 7,
        JM_TILE_TPM2 = 8 /* two threads per matrix (FP64 n = 8) */,
-       JM_TILE_TPMS = 9 /* thread per matrix, product staged in shared memory (FP64 n = 9, 10) */ };
+       JM_TILE_TPMS = 9 /* thread per matrix, product staged in shared memory (FP64 n = 9, 10, FP32 12..14) */,
+       JM_TILE_F32_ROWS = 10 /* FP32 row panels: 4 threads per matrix own full rows (n = 15, 16) */ };
 
 JM_API int jit_mat_stats(jm_stats *out);
 /* Copy up to `cap` non-empty slots into `keys`; returns the number of

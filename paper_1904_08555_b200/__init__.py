@@ -47,6 +47,23 @@ def _check(rc: int, what: str) -> int:
     return rc
 
 
+def _enum(table: dict, x, what: str) -> int:
+    """Name or integer -> the C enum value; an unknown name is an error, never 0."""
+    if isinstance(x, int):
+        return x
+    if x in table:
+        return table[x]
+    raise ValueError(f"unknown {what} {x!r} (one of {sorted(table)} or its integer value)")
+
+
+def _ad(addend) -> int:
+    return _enum(_ADDENDS, addend, "addend")
+
+
+def _kd(kind) -> int:
+    return _enum(_KINDS, kind, "kind")
+
+
 def _dt(dtype) -> int:
     if isinstance(dtype, int):
         return dtype
@@ -73,7 +90,7 @@ def jit_mat_run(n: int, dtype, batch: int, repeat: int, in_ptr: int, out_ptr: in
 def jit_mat_run_ex(n: int, dtype, batch: int, repeat: int, in_ptr: int, out_ptr: int, *,
                    addend="ones", kind="specialized", stream: int | None = None,
                    flags: int = 0) -> None:
-    d = jm_run_desc(int(n), _dt(dtype), _ADDENDS.get(addend, addend), _KINDS.get(kind, kind),
+    d = jm_run_desc(int(n), _dt(dtype), _ad(addend), _kd(kind),
                     int(batch), int(repeat), ctypes.c_void_p(in_ptr), ctypes.c_void_p(out_ptr),
                     ctypes.c_void_p(stream or 0), int(flags))
     _check(lib.jit_mat_run_ex(ctypes.byref(d)), "jit_mat_run_ex")
@@ -90,8 +107,8 @@ def jit_mat_run_many(groups, stream: int | None = None, sync: bool = False) -> N
     repeat, in_ptr, out_ptr and optional addend / kind (C: jit_mat_run_many)."""
     arr = (jm_run_desc * max(1, len(groups)))()
     for i, g in enumerate(groups):
-        arr[i] = jm_run_desc(int(g["n"]), _dt(g["dtype"]), _ADDENDS.get(g.get("addend", "ones"), 0),
-                             _KINDS.get(g.get("kind", "specialized"), 0), int(g["batch"]),
+        arr[i] = jm_run_desc(int(g["n"]), _dt(g["dtype"]), _ad(g.get("addend", "ones")),
+                             _kd(g.get("kind", "specialized")), int(g["batch"]),
                              int(g["repeat"]), ctypes.c_void_p(g["in_ptr"]),
                              ctypes.c_void_p(g["out_ptr"]), None, 0)
     _check(lib.jit_mat_run_many(arr, len(groups), ctypes.c_void_p(stream or 0),
@@ -101,7 +118,7 @@ def jit_mat_run_many(groups, stream: int | None = None, sync: bool = False) -> N
 def jit_mat_cache_export(n: int, dtype, addend="ones") -> bytes:
     """Blob (key + symbol + sm_100a cubin) of a compiled specialization."""
     ln = ctypes.c_size_t(0)
-    a = _ADDENDS.get(addend, addend)
+    a = _ad(addend)
     _check(lib.jit_mat_cache_export(int(n), _dt(dtype), a, None, 0, ctypes.byref(ln)),
            "jit_mat_cache_export")
     buf = ctypes.create_string_buffer(ln.value)
@@ -118,7 +135,7 @@ def jit_mat_cache_import(blob: bytes) -> None:
 def jit_mat_matmul(n: int, dtype, batch: int, a_ptr: int, b_ptr: int, c_ptr: int, *,
                    kind="specialized", stream: int | None = None) -> None:
     """c[b] += a[b] @ b[b] (Listing 8; C: jit_mat_matmul)."""
-    _check(lib.jit_mat_matmul(int(n), _dt(dtype), _KINDS.get(kind, kind), int(batch),
+    _check(lib.jit_mat_matmul(int(n), _dt(dtype), _kd(kind), int(batch),
                               ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), ctypes.c_void_p(c_ptr),
                               ctypes.c_void_p(stream or 0)), "jit_mat_matmul")
 
@@ -126,7 +143,7 @@ def jit_mat_matmul(n: int, dtype, batch: int, a_ptr: int, b_ptr: int, c_ptr: int
 def jit_mat_mass(dofs: int, quads: int, elements: int, B_ptr: int, op_ptr: int, x_ptr: int,
                  y_ptr: int, *, kind="specialized", stream: int | None = None) -> None:
     """Laghos 2D mass action y_e += B^T((B x_e B^T) .* op_e) B (C: jit_mat_mass)."""
-    _check(lib.jit_mat_mass(int(dofs), int(quads), _KINDS.get(kind, kind), int(elements),
+    _check(lib.jit_mat_mass(int(dofs), int(quads), _kd(kind), int(elements),
                             ctypes.c_void_p(B_ptr), ctypes.c_void_p(op_ptr), ctypes.c_void_p(x_ptr),
                             ctypes.c_void_p(y_ptr), ctypes.c_void_p(stream or 0)), "jit_mat_mass")
 
@@ -151,8 +168,8 @@ def mass(B, op, x, y, *, kind: str = "specialized", stream=None, sync: bool = Fa
 def jit_mat_time_lookup(n: int, dtype, addend="ones", kind="specialized", iters: int = 1_000_000) -> float:
     """Average ns per cache-hit lookup, timed inside the library (row a1)."""
     ns = ctypes.c_double(0.0)
-    _check(lib.jit_mat_time_lookup(int(n), _dt(dtype), _ADDENDS.get(addend, addend),
-                                   _KINDS.get(kind, kind), int(iters), ctypes.byref(ns)),
+    _check(lib.jit_mat_time_lookup(int(n), _dt(dtype), _ad(addend),
+                                   _kd(kind), int(iters), ctypes.byref(ns)),
            "jit_mat_time_lookup")
     return float(ns.value)
 
@@ -177,8 +194,8 @@ def jit_mat_set_stream(stream: int | None) -> None:
 
 
 def jit_mat_prepare(n: int, dtype, addend="ones", kind="specialized") -> None:
-    _check(lib.jit_mat_prepare(int(n), _dt(dtype), _ADDENDS.get(addend, addend),
-                               _KINDS.get(kind, kind)), "jit_mat_prepare")
+    _check(lib.jit_mat_prepare(int(n), _dt(dtype), _ad(addend),
+                               _kd(kind)), "jit_mat_prepare")
 
 
 def jit_mat_prepare_for(n: int, dtype, repeat: int, addend="ones", kind="specialized",
@@ -186,8 +203,8 @@ def jit_mat_prepare_for(n: int, dtype, repeat: int, addend="ones", kind="special
     """Prepare the kernel a run with this repeat count (and flags) launches;
     returns its variant (0 resident, 1 streaming)."""
     v = ctypes.c_int(-1)
-    _check(lib.jit_mat_prepare_for(int(n), _dt(dtype), _ADDENDS.get(addend, addend),
-                                   _KINDS.get(kind, kind), int(repeat), int(flags), ctypes.byref(v)),
+    _check(lib.jit_mat_prepare_for(int(n), _dt(dtype), _ad(addend),
+                                   _kd(kind), int(repeat), int(flags), ctypes.byref(v)),
            "jit_mat_prepare_for")
     return int(v.value)
 
@@ -257,7 +274,8 @@ def jit_mat_compile_check(n: int, dtype, addend="ones") -> int:
     if addend == "mass":
         _check(lib.jit_mat_compile_check(int(n), int(dtype), 3, ctypes.byref(cb)), "jit_mat_compile_check")
         return int(cb.value)
-    a = {"matmul": JM_OP_MATMUL, "stream": JM_OP_STREAM}.get(addend, _ADDENDS.get(addend, addend))
+    ops = {"matmul": JM_OP_MATMUL, "stream": JM_OP_STREAM}
+    a = ops[addend] if addend in ops else _ad(addend)
     _check(lib.jit_mat_compile_check(int(n), _dt(dtype), a, ctypes.byref(cb)), "jit_mat_compile_check")
     return int(cb.value)
 

@@ -21,7 +21,8 @@
 namespace jm {
 
 enum class Addend : int { Ones = 0, Identity = 1 };
-enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, Tpm2 = 3, F32 = 4, Tpms = 5, Rows = 6 };
+enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, Tpm2 = 3, F32 = 4, Tpms = 5, Rows = 6,
+                        F32Rows = 7 /* plan label only: the FP32 row panels of Tile::F32 */ };
 
 struct Plan {
   int tile;      // Tile
@@ -333,8 +334,8 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   }
   if (f32p_use(n)) {
     const int mpc = F32P_WPC * f32p_mpw(n);
-    if (f32p_inplace(n)) return Plan{(int)t, 32 * F32P_WPC, mpc, nst * rup(mpc * f32p_slot(n), 16) + mpc * f32p_mbuf(n), 1};
-    return Plan{(int)t, 32 * F32P_WPC, mpc, nst * stage_bytes(mpc, n, es) + 2 * mpc * f32p_mbuf(n), 1};
+    if (f32p_inplace(n)) return Plan{(int)Tile::F32Rows, 32 * F32P_WPC, mpc, nst * rup(mpc * f32p_slot(n), 16) + mpc * f32p_mbuf(n), 1};
+    return Plan{(int)Tile::F32Rows, 32 * F32P_WPC, mpc, nst * stage_bytes(mpc, n, es) + 2 * mpc * f32p_mbuf(n), 1};
   }
   // F32 tiles: the stage area IS the per-matrix region (stride f32_region)
   const int mpc = F32_WPC * f32_mpw(n);
@@ -515,8 +516,8 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   }
   if (f32p_use(n))
     return f32p_ring_inplace(n)
-               ? Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm, f32p_slot(n)) + rm * f32p_mbuf(n), 1}
-               : Plan{(int)Tile::F32, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
+               ? Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm, f32p_slot(n)) + rm * f32p_mbuf(n), 1}
+               : Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
   if (f32_stream_pf(n)) return Plan{(int)Tile::F32, 32 * F32_WPC, rm, 2 * rup(rm * f32_region(n), 16), 1};
   return Plan{(int)Tile::F32, 32 * F32_WPC, chm,
               ring_bytes(n, es, rm, f32_ring_slot(n)) + (f32_ring_slot(n) ? 0 : rm * f32_region(n)), 1};

@@ -43,6 +43,7 @@
 
 extern "C" {
 extern const unsigned char jm_embedded_kernel_src[];
+extern const char jm_build_digest[];   // sha256 hex of the build inputs (_build.py)
 extern const unsigned long long jm_embedded_kernel_src_len;
 extern const unsigned char jm_embedded_aot_cubin[];
 extern const unsigned long long jm_embedded_aot_cubin_len;
@@ -297,13 +298,21 @@ int finish_function(Slot &s, CUfunction fn) {
   s.regs = v;
   D.FuncGetAttribute(&v, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, fn);
   s.local_bytes = v;
-  if (s.plan.smem > 48 * 1024)
-    CU_TRY(D.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, s.plan.smem),
-           "cuFuncSetAttribute(max dynamic smem)");
+  // A failure here is a property of the compiled kernel and its plan on this
+  // device (shared memory above the limit, no CTA fits), not a transient driver
+  // state: JM_E_COMPILE, so the slot is marked FAILED and not recompiled per call.
+  CUresult cr = CUDA_SUCCESS;
+  if (s.plan.smem > 48 * 1024 &&
+      (cr = D.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, s.plan.smem)) != CUDA_SUCCESS) {
+    cu_fail(cr, "cuFuncSetAttribute(max dynamic smem)");
+    return fail(JM_E_COMPILE, "plan needs %d B of shared memory: %s", s.plan.smem, t_err.c_str());
+  }
   int nb = 0;
-  CU_TRY(D.OccupancyMaxActiveBlocks(&nb, fn, s.plan.threads, (size_t)s.plan.smem),
-         "cuOccupancyMaxActiveBlocksPerMultiprocessor");
-  if (nb < 1) return fail(JM_E_CUDA, "kernel cannot be resident (threads %d, smem %d)", s.plan.threads, s.plan.smem);
+  if ((cr = D.OccupancyMaxActiveBlocks(&nb, fn, s.plan.threads, (size_t)s.plan.smem)) != CUDA_SUCCESS) {
+    cu_fail(cr, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
+    return fail(JM_E_COMPILE, "%s", t_err.c_str());
+  }
+  if (nb < 1) return fail(JM_E_COMPILE, "kernel cannot be resident (threads %d, smem %d)", s.plan.threads, s.plan.smem);
   s.grid_cap = nb * G.sms;
   s.fn = fn;
   return JM_OK;
@@ -874,9 +883,15 @@ int jit_mat_run_host(int n, int dtype, int64_t batch, int64_t repeat, const void
   return run_impl(&d);
 }
 
-// Blob "JMC2": magic, key {n, dtype, addend}, entry count, then per compiled
-// variant of the key (0 resident, 1 streaming): variant, symbol length,
-// symbol, cubin length, cubin.
+// Blob "JMC3": magic, the build digest of the library that compiled it (64
+// hex chars: kernel source + planner + build defines, _build.py), key {n,
+// dtype, addend}, entry count, then per compiled variant of the key (0
+// resident, 1 streaming): variant, name expression, lowered symbol, cubin.
+// Import accepts a blob only from the same build and only if each entry's
+// name expression is the one this build would compile for the key, so the
+// cubin always matches the plan it is launched with.
+constexpr size_t DIGEST_LEN = 64;
+
 int jit_mat_cache_export(int n, int dtype, int addend, void *buf, size_t cap, size_t *len) {
   int rc = check_key(n, dtype, addend, JM_KIND_SPECIALIZED);
   if (rc != JM_OK) return rc;
@@ -884,13 +899,15 @@ int jit_mat_cache_export(int n, int dtype, int addend, void *buf, size_t cap, si
   Slot *vs[2] = {&g_slots[JM_KIND_SPECIALIZED][addend][dtype][n], &g_stream_slots[addend][dtype][n]};
   std::unique_lock<std::mutex> l0(vs[0]->mu), l1(vs[1]->mu);
   bool have[2];
-  size_t total = 4 + 3 * 4 + 4;
+  std::string expr[2];
+  size_t total = 4 + DIGEST_LEN + 3 * 4 + 4;
   int count = 0;
   for (int v = 0; v < 2; ++v) {
     have[v] = vs[v]->state.load(std::memory_order_acquire) == S_READY && !vs[v]->cubin.empty();
     if (!have[v]) continue;
     ++count;
-    total += 4 + 4 + vs[v]->lowered.size() + 8 + vs[v]->cubin.size();
+    expr[v] = name_expression(n, dtype, addend, v == 1);
+    total += 4 + 4 + expr[v].size() + 4 + vs[v]->lowered.size() + 8 + vs[v]->cubin.size();
   }
   if (!count)
     return fail(JM_E_INVALID, "key n=%d dtype=%d addend=%d is not compiled in this process", n, dtype, addend);
@@ -900,15 +917,19 @@ int jit_mat_cache_export(int n, int dtype, int addend, void *buf, size_t cap, si
   char *p = (char *)buf;
   const int32_t key[3] = {n, dtype, addend};
   const int32_t cnt = count;
-  memcpy(p, "JMC2", 4); p += 4;
+  memcpy(p, "JMC3", 4); p += 4;
+  memcpy(p, jm_build_digest, DIGEST_LEN); p += DIGEST_LEN;
   memcpy(p, key, sizeof key); p += sizeof key;
   memcpy(p, &cnt, 4); p += 4;
   for (int v = 0; v < 2; ++v) {
     if (!have[v]) continue;
     const int32_t var = v;
+    const uint32_t el = (uint32_t)expr[v].size();
     const uint32_t nl = (uint32_t)vs[v]->lowered.size();
     const uint64_t cl = (uint64_t)vs[v]->cubin.size();
     memcpy(p, &var, 4); p += 4;
+    memcpy(p, &el, 4); p += 4;
+    memcpy(p, expr[v].data(), el); p += el;
     memcpy(p, &nl, 4); p += 4;
     memcpy(p, vs[v]->lowered.data(), nl); p += nl;
     memcpy(p, &cl, 8); p += 8;
@@ -918,35 +939,45 @@ int jit_mat_cache_export(int n, int dtype, int addend, void *buf, size_t cap, si
 }
 
 int jit_mat_cache_import(const void *blob, size_t len) {
-  if (!blob || len < 4 + 12 + 4) return fail(JM_E_INVALID, "blob too short");
+  if (!blob || len < 4 + DIGEST_LEN + 12 + 4) return fail(JM_E_INVALID, "blob too short");
   if (!G.inited.load(std::memory_order_acquire)) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
   const char *p = (const char *)blob, *end = p + len;
-  if (memcmp(p, "JMC2", 4) != 0) return fail(JM_E_INVALID, "not a jitmat cubin blob");
+  if (memcmp(p, "JMC3", 4) != 0) return fail(JM_E_INVALID, "not a jitmat cubin blob");
   p += 4;
+  if (memcmp(p, jm_build_digest, DIGEST_LEN) != 0)
+    return fail(JM_E_INVALID, "blob from another library build (digest %.12s..., this build %.12s...)", p,
+                (const char *)jm_build_digest);
+  p += DIGEST_LEN;
   int32_t key[3], cnt;
   memcpy(key, p, sizeof key); p += sizeof key;
   memcpy(&cnt, p, 4); p += 4;
   int rc = check_key(key[0], key[1], key[2], JM_KIND_SPECIALIZED);
   if (rc != JM_OK) return rc;
   if (cnt < 1 || cnt > 2) return fail(JM_E_INVALID, "corrupt blob (entry count %d)", cnt);
-  // parse every entry before installing any
+  // parse and check every entry before installing any
   struct Entry { int32_t v; std::string sym; const char *cubin; uint64_t cl; };
   std::vector<Entry> es;
+  auto str = [&](std::string &out) -> bool {
+    uint32_t l;
+    if ((size_t)(end - p) < 4) return false;
+    memcpy(&l, p, 4); p += 4;
+    if ((size_t)(end - p) < l) return false;
+    out.assign(p, l); p += l;
+    return true;
+  };
   for (int i = 0; i < cnt; ++i) {
     Entry e{};
-    uint32_t nl;
-    if ((size_t)(end - p) < 8) return fail(JM_E_INVALID, "truncated blob");
+    std::string expr;
+    if ((size_t)(end - p) < 4) return fail(JM_E_INVALID, "truncated blob");
     memcpy(&e.v, p, 4); p += 4;
-    memcpy(&nl, p, 4); p += 4;
     if (e.v < 0 || e.v > 1) return fail(JM_E_INVALID, "corrupt blob (variant %d)", e.v);
-    if ((size_t)(end - p) < (size_t)nl + 8) return fail(JM_E_INVALID, "truncated blob");
-    e.sym.assign(p, nl); p += nl;
+    if (!str(expr) || !str(e.sym) || (size_t)(end - p) < 8) return fail(JM_E_INVALID, "truncated blob");
     memcpy(&e.cl, p, 8); p += 8;
     if ((uint64_t)(end - p) < e.cl || e.cl == 0) return fail(JM_E_INVALID, "truncated blob");
     e.cubin = p; p += e.cl;
-    if (e.sym.find(e.v ? "k_update_stream" : "k_update") == std::string::npos ||
-        (e.v == 0 && e.sym.find("k_update_stream") != std::string::npos))
-      return fail(JM_E_INVALID, "unexpected kernel symbol");
+    const std::string want = name_expression(key[0], key[1], key[2], e.v == 1);
+    if (expr != want)
+      return fail(JM_E_INVALID, "blob entry %s does not match the key's kernel %s", expr.c_str(), want.c_str());
     es.push_back(std::move(e));
   }
   if (p != end) return fail(JM_E_INVALID, "trailing bytes in blob");
@@ -1017,6 +1048,21 @@ int jit_mat_stats(jm_stats *out) {
   return JM_OK;
 }
 
+}  // extern "C"
+namespace {
+// the JM_TILE_* code of a slot's plan (resident and streaming slots alike)
+int tile_code(const jm::Plan &p) {
+  return p.tile == (int)jm::Tile::TPM    ? JM_TILE_TPM
+         : p.tile == (int)jm::Tile::Tpm2 ? JM_TILE_TPM2
+         : p.tile == (int)jm::Tile::Tpms ? JM_TILE_TPMS
+         : p.tile == (int)jm::Tile::Rows ? JM_TILE_ROWS
+         : p.tile == (int)jm::Tile::F32Rows ? JM_TILE_F32_ROWS
+         : p.tile == (int)jm::Tile::Dmma ? (p.w > 1 ? JM_TILE_CTA_DMMA : JM_TILE_WARP_DMMA)
+                                         : (p.w > 1 ? JM_TILE_CTA_F32 : JM_TILE_WARP_F32);
+}
+}  // namespace
+extern "C" {
+
 int jit_mat_key_info(jm_key_info *keys, int cap) {
   int cnt = 0;
   for (int k = 0; k < NKIND; ++k)
@@ -1031,13 +1077,7 @@ int jit_mat_key_info(jm_key_info *keys, int cap) {
             o.n = n; o.dtype = t; o.addend = a; o.kind = k; o.state = st;
             o.regs = s.regs; o.local_bytes = s.local_bytes; o.smem_bytes = s.plan.smem;
             o.threads = s.plan.threads;
-            o.tile = k == JM_KIND_GENERIC ? JM_TILE_GENERIC
-                     : (s.plan.tile == (int)jm::Tile::TPM ? JM_TILE_TPM
-                        : s.plan.tile == (int)jm::Tile::Tpm2 ? JM_TILE_TPM2
-                        : s.plan.tile == (int)jm::Tile::Tpms ? JM_TILE_TPMS
-                        : s.plan.tile == (int)jm::Tile::Rows ? JM_TILE_ROWS
-                        : s.plan.tile == (int)jm::Tile::Dmma ? (s.plan.w > 1 ? JM_TILE_CTA_DMMA : JM_TILE_WARP_DMMA)
-                        : (s.plan.w > 1 ? JM_TILE_CTA_F32 : JM_TILE_WARP_F32));
+            o.tile = k == JM_KIND_GENERIC ? JM_TILE_GENERIC : tile_code(s.plan);
             o.cubin_bytes = s.cubin_bytes;
             o.compile_ms = s.compile_ms;
             o.op = 0;
@@ -1056,8 +1096,7 @@ int jit_mat_key_info(jm_key_info *keys, int cap) {
           o.n = n; o.dtype = t; o.addend = a; o.kind = JM_KIND_SPECIALIZED; o.state = st;
           o.regs = s.regs; o.local_bytes = s.local_bytes; o.smem_bytes = s.plan.smem;
           o.threads = s.plan.threads;
-          o.tile = s.plan.tile == (int)jm::Tile::Dmma ? (s.plan.w > 1 ? JM_TILE_CTA_DMMA : JM_TILE_WARP_DMMA)
-                                                      : JM_TILE_WARP_F32;
+          o.tile = tile_code(s.plan);
           o.cubin_bytes = s.cubin_bytes;
           o.compile_ms = s.compile_ms;
           o.op = 0;

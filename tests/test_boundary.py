@@ -134,3 +134,18 @@ def test_oracle_is_not_linked_into_the_library(jm):
     import subprocess
     out = subprocess.run(["nm", "-D", jm.lib_path], capture_output=True, text=True).stdout
     assert "jm_oracle" not in out
+
+
+def test_binding_rejects_unknown_enum_names():
+    """a misspelled addend/kind name must raise, never become 0
+    (Ones / specialized); integers pass through unchanged."""
+    import paper_1904_08555_b200 as jm
+    assert jm._ad("identity") == jm.JM_ADDEND_IDENTITY and jm._ad(jm.JM_ADDEND_IDENTITY) == 1
+    assert jm._kd("generic") == jm.JM_KIND_GENERIC and jm._kd(jm.JM_KIND_GENERIC) == 1
+    with pytest.raises(ValueError):
+        jm._ad("Identity")
+    with pytest.raises(ValueError):
+        jm._kd("specialised")
+    with pytest.raises(ValueError):   # run_many marshals every group before calling the library
+        jm.jit_mat_run_many([{"n": 4, "dtype": "f64", "batch": 1, "repeat": 1, "in_ptr": 0, "out_ptr": 0,
+                              "addend": "Identity"}])

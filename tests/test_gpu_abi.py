@@ -109,7 +109,7 @@ def test_key_info_reports_registers(jm):
     assert k16["tile_name"] == "warp_dmma"
     assert info[(64, 1, 0)]["tile_name"] == "cta_dmma"
     assert info[(4, 1, 0)]["tile_name"] == "tpm"
-    assert info[(16, 0, 0)]["tile_name"] == "warp_f32"
+    assert info[(16, 0, 0)]["tile_name"] == "f32_rows"
     for k in info.values():
         assert k["local_bytes"] == 0, f"spill in {k}"
 
@@ -200,7 +200,7 @@ def test_cache_export_import_skips_nvrtc(jm):
     ref = jm.run(x, 3, sync=True)
     ref100 = jm.run(x, 100, sync=True)     # R = 3 runs the streaming variant, R = 100 the resident one
     blob = jm.jit_mat_cache_export(13, "double")
-    assert blob[:4] == b"JMC2" and len(blob) > 2000
+    assert blob[:4] == b"JMC3" and len(blob) > 2000
     _fresh(jm)
     jm.jit_mat_cache_import(blob)
     jm.jit_mat_cache_import(blob)          # second import: no-op
@@ -210,9 +210,20 @@ def test_cache_export_import_skips_nvrtc(jm):
     assert st["compilations"] == 0 and st["imports"] == 2
     assert torch.equal(got, ref) and torch.equal(got100, ref100)
     with pytest.raises(jm.JitMatError):
-        jm.jit_mat_cache_import(b"JMC2" + blob[4:40])
+        jm.jit_mat_cache_import(blob[:40])
     with pytest.raises(jm.JitMatError):
         jm.jit_mat_cache_import(b"JMC1" + blob[4:])
+    # another build: digest mismatch
+    bad = bytearray(blob)
+    bad[4] = ord("0") if bad[4] != ord("0") else ord("1")
+    with pytest.raises(jm.JitMatError, match="another library build"):
+        jm.jit_mat_cache_import(bytes(bad))
+    # the same cubins relabelled as another key: name expression mismatch
+    import struct
+    other = bytearray(blob)
+    struct.pack_into("<i", other, 4 + 64, 21)
+    with pytest.raises(jm.JitMatError, match="does not match"):
+        jm.jit_mat_cache_import(bytes(other))
     with pytest.raises(jm.JitMatError):
         jm.jit_mat_cache_export(14, "double")
 

@@ -1,14 +1,8 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-for C in 8192 4096; do
-  JM_BUILD_DEFINES="JM_RING_CHUNK=$C" python -m paper_1904_08555_b200._build --force > /dev/null 2>&1
-  python tools/stream_sweep.py --sizes 12,16,20,24,28 --dtypes f64 --repeats 1,2 --gb 0.5 --steps 5 2>/dev/null | python -c "
-import json,sys
-for l in sys.stdin:
-    d=json.loads(l); print('chunk=$C', d['dtype'], d['n'], d['repeat'], round(d['streaming']['frac_hbm'],3), d['kernels']['1']['smem'])
-"
-  python tools/stream_sweep.py --sizes 17,20,24,32 --dtypes f32 --repeats 1,2 --gb 0.5 --steps 5 2>/dev/null | python -c "
-import json,sys
-for l in sys.stdin:
-    d=json.loads(l); print('chunk=$C', d['dtype'], d['n'], d['repeat'], round(d['streaming']['frac_hbm'],3), d['kernels']['1']['smem'])
-"
-done
+set -x
+mkdir -p gpurun_out/ncu_r02
+CFG_A="2:f64:16777216:1:auto 4:f64:4194304:1:auto 4:f64:4194304:100:auto 4:f32:4194304:1:auto 10:f64:1048576:100:auto 16:f64:1048576:100:auto 17:f64:524288:100:auto 32:f64:131072:100:auto 48:f64:32768:100:auto 64:f64:16384:100:auto 32:f64:65536:1:auto 48:f64:32768:1:auto 64:f64:16384:1:auto"
+CFG_B="13:f32:1048576:100:auto 16:f32:1048576:100:auto 16:f32:524288:1:auto 17:f32:524288:100:auto 24:f32:262144:100:auto 32:f32:131072:100:auto 48:f32:65536:100:auto 64:f32:32768:100:auto 17:f32:524288:1:auto 24:f32:262144:1:auto 32:f32:131072:1:auto 48:f32:65536:1:auto 64:f32:32768:1:auto"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_update -o gpurun_out/ncu_r02/base_a python tools/ncu_configs.py $CFG_A > gpurun_out/ncu_r02/base_a.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_update -o gpurun_out/ncu_r02/base_b python tools/ncu_configs.py $CFG_B > gpurun_out/ncu_r02/base_b.log 2>&1
+tail -3 gpurun_out/ncu_r02/base_a.log gpurun_out/ncu_r02/base_b.log
