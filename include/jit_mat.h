@@ -101,6 +101,8 @@ enum {
                                     device buffers it owns, chunked and overlapped (see run_host) */
 #define JM_FLAG_RESIDENT 4u      /* use the resident kernel whatever the repeat count (see VARIANT) */
 #define JM_FLAG_STREAMING 8u     /* use the streaming kernel where the kind has one (see VARIANT) */
+#define JM_FLAG_BATCH_COMPILE 16u /* jit_mat_run_many: compile the cold keys as a few NVRTC programs
+                                    of several name expressions each (see jit_mat_run_many) */
 
 /* Initialise for `device` (-1 = the calling thread's current CUDA device, else
  * device 0).  Loads the CUDA driver, retains the device's primary context (the
@@ -134,7 +136,8 @@ JM_API int jit_mat_init(int device);
  * ring (both within the parity bound).  Environment
  * JIT_MAT_STREAM=0/1 forces resident/streaming, JIT_MAT_STREAM_RN moves the
  * switch point (read once per process); per call, jm_run_desc.flags
- * JM_FLAG_RESIDENT / JM_FLAG_STREAMING force it. */
+ * JM_FLAG_RESIDENT / JM_FLAG_STREAMING force it.  JIT_MAT_DUMP_CUBIN=<dir>
+ * (inspection only) writes each NVRTC cubin to <dir>/<symbol>.cubin. */
 JM_API int jit_mat_run(int n, int dtype, int64_t batch, int64_t repeat, const void *in, void *out);
 
 /* Unload every module, drop the cache and release the primary context.  Later
@@ -172,7 +175,11 @@ JM_API int jit_mat_run_host(int n, int dtype, int64_t batch, int64_t repeat, con
  * library streams forked from and joined back into `stream` (NULL = the set
  * stream), so small groups fill the GPU together.  Asynchronous w.r.t. the
  * host unless `flags` has JM_FLAG_SYNC.  Every descriptor is validated before
- * anything is compiled or launched. */
+ * anything is compiled or launched.  With JM_FLAG_BATCH_COMPILE the cold keys
+ * are instead split into G groups (environment JIT_MAT_COMPILE_GROUPS, default
+ * the host's hardware threads) and each group is ONE NVRTC program with a name
+ * expression per key, so the embedded template source is parsed G times rather
+ * than once per key. */
 JM_API int jit_mat_run_many(const jm_run_desc *descs, int count, void *stream, unsigned flags);
 
 /* Share specializations between processes (the paper's
@@ -251,6 +258,7 @@ typedef struct {
   int32_t keys_ready;        /* specialized cache slots (either variant) in READY state */
   int32_t keys_failed;       /* cache slots in FAILED state */
   int64_t imports;           /* keys installed by jit_mat_cache_import (no NVRTC) */
+  int64_t programs;          /* NVRTC programs of batched compiles (JM_FLAG_BATCH_COMPILE) */
 } jm_stats;
 
 typedef struct {
@@ -272,7 +280,8 @@ enum { JM_TILE_GENERIC = 0, JM_TILE_TPM = 1, JM_TILE_WARP_DMMA = 2, JM_TILE_CTA_
        JM_TILE_WARP_F32 = 4, JM_TILE_CTA_F32 = 5, JM_TILE_ROWS = 6, JM_TILE_MATMUL = 7,
        JM_TILE_TPM2 = 8 /* two threads per matrix (FP64 n = 8) */,
        JM_TILE_TPMS = 9 /* thread per matrix, product staged in shared memory (FP64 n = 9, 10, FP32 12..14) */,
-       JM_TILE_F32_ROWS = 10 /* FP32 row panels: 4 threads per matrix own full rows (n = 15, 16) */ };
+       JM_TILE_F32_ROWS = 10 /* FP32 row panels: 4 threads per matrix own full rows (n = 15, 16) */,
+       JM_TILE_F64_REG = 11 /* FP64 register tiles with DFMA (sizes DMMA pads badly) */ };
 
 JM_API int jit_mat_stats(jm_stats *out);
 /* Copy up to `cap` non-empty slots into `keys`; returns the number of
@@ -286,7 +295,7 @@ JM_API int jit_mat_reset_stats(void);
 /* Fill out[0 .. batch*n*n) on the device with the counter-hash input generator
  * keyed by the GLOBAL matrix index (global_first + b), so a batch split across
  * ranks equals the unsplit batch.  dist: 0 paper (iota), 1 bench (U[-1,1)),
- * 2 hard (U[0,1) * 2*4000/n).  The definition is written out in
+ * 2 hard (U[0,1) * 2*4000/n), 3 signed hard (U[-1,1) * 2*4000/n).  The definition is written out in
  * jm_synth/__init__.py (host side); this is an independent device
  * implementation of the same definition.  Asynchronous on the set stream. */
 JM_API int jit_mat_fill(int n, int dtype, int dist, uint64_t seed, int64_t global_first,

@@ -7,7 +7,7 @@ holds NONE of the method's arithmetic (no matrix product, no update): only
   keyed by the GLOBAL matrix index so that a batch sliced across W ranks is
   bit-identical to the unsliced batch ("a proxy for part of a
   larger computation"; SURVEY.md §8(e));
-* the three input distributions ``paper`` / ``bench`` / ``hard``;
+* the input distributions ``paper`` / ``bench`` / ``hard`` / ``shard``;
 * the order-independent u64 checksum used by the multi-GPU gather (plumbing,
   SURVEY.md §8(e)); the device re-implements both (csrc/kernels/jm_aux.cuh) —
   the two sides share no code, only this written definition:
@@ -20,6 +20,8 @@ holds NONE of the method's arithmetic (no matrix product, no update): only
                                       PAPER.md:374-377 Listing 4)
     bench : x = T(2u - 1)            (U[-1,1), throughput runs)
     hard  : x = T(u * 2*rho/n)       (rho = 4000: c*rho = 0.2, parity-hard)
+    shard : x = T((2u - 1) * 2*rho/n) (signed parity-hard: cancellation in M*M,
+                                      sign errors visible)
 
     checksum: S = sum_e mix64(bits(x_e) ^ (PHI * (g*n*n + e)))   (mod 2^64)
               with bits() the IEEE bit pattern zero-extended to 64 bits.
@@ -35,7 +37,8 @@ RHO_HARD = 4000.0
 DIST_PAPER = 0
 DIST_BENCH = 1
 DIST_HARD = 2
-DISTS = {"paper": DIST_PAPER, "bench": DIST_BENCH, "hard": DIST_HARD}
+DIST_SHARD = 3
+DISTS = {"paper": DIST_PAPER, "bench": DIST_BENCH, "hard": DIST_HARD, "shard": DIST_SHARD}
 
 SEED_BENCH = 0x0019040855
 SEED_HARD_BASE = 0x5EED0000
@@ -95,6 +98,8 @@ def generate(n: int, dtype, dist: str | int, seed: int, global_first: int = 0,
             x = 2.0 * u - 1.0
         elif d == DIST_HARD:
             x = u * (2.0 * RHO_HARD / n)
+        elif d == DIST_SHARD:
+            x = (2.0 * u - 1.0) * (2.0 * RHO_HARD / n)
         else:
             raise ValueError(f"unknown dist {dist!r}")
     return x.astype(dt).reshape(batch, n, n)

@@ -19,7 +19,7 @@ import os
 from ._lib import (  # noqa: F401  (re-exported C ABI)
     JM_ADDEND_IDENTITY, JM_ADDEND_ONES, JM_E_ALIGN, JM_E_ARCH, JM_E_COMPILE, JM_E_CUDA,
     JM_E_INVALID, JM_E_NOT_INITIALIZED, JM_E_UNSUPPORTED, JM_F32, JM_F64, JM_FLAG_HOST_BUFFERS,
-    JM_FLAG_RESIDENT, JM_FLAG_STREAMING, JM_FLAG_SYNC, JM_KIND_AOT_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK, JM_OP_MATMUL,
+    JM_FLAG_RESIDENT, JM_FLAG_STREAMING, JM_FLAG_SYNC, JM_FLAG_BATCH_COMPILE, JM_KIND_AOT_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK, JM_OP_MATMUL,
     JM_OP_STREAM, JM_TILE_NAMES, JitMatError,
     jm_key_info, jm_run_desc, jm_stats, lib, lib_path,
 )
@@ -102,9 +102,12 @@ def jit_mat_run_host(n: int, dtype, batch: int, repeat: int, in_ptr: int, out_pt
            "jit_mat_run_host")
 
 
-def jit_mat_run_many(groups, stream: int | None = None, sync: bool = False) -> None:
+def jit_mat_run_many(groups, stream: int | None = None, sync: bool = False,
+                     batch_compile: bool = False) -> None:
     """Mixed-N batch: ``groups`` is a sequence of dicts with keys n, dtype, batch,
-    repeat, in_ptr, out_ptr and optional addend / kind (C: jit_mat_run_many)."""
+    repeat, in_ptr, out_ptr and optional addend / kind (C: jit_mat_run_many);
+    ``batch_compile`` compiles the cold keys as a few multi-expression NVRTC
+    programs (JM_FLAG_BATCH_COMPILE)."""
     arr = (jm_run_desc * max(1, len(groups)))()
     for i, g in enumerate(groups):
         arr[i] = jm_run_desc(int(g["n"]), _dt(g["dtype"]), _ad(g.get("addend", "ones")),
@@ -112,7 +115,8 @@ def jit_mat_run_many(groups, stream: int | None = None, sync: bool = False) -> N
                              int(g["repeat"]), ctypes.c_void_p(g["in_ptr"]),
                              ctypes.c_void_p(g["out_ptr"]), None, 0)
     _check(lib.jit_mat_run_many(arr, len(groups), ctypes.c_void_p(stream or 0),
-                                JM_FLAG_SYNC if sync else 0), "jit_mat_run_many")
+                                (JM_FLAG_SYNC if sync else 0) | (JM_FLAG_BATCH_COMPILE if batch_compile else 0)),
+           "jit_mat_run_many")
 
 
 def jit_mat_cache_export(n: int, dtype, addend="ones") -> bytes:

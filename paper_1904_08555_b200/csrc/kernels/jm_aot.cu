@@ -163,7 +163,9 @@ __device__ __forceinline__ void fill_impl(T *__restrict__ out, int n, int dist, 
       const u64 ge = (u64)(gfirst * nn + e);
       const u64 z = splitmix64(seed ^ (0x9E3779B97F4A7C15ull * (ge + 1ull)));
       const double u = __dmul_rn((double)(z >> 11), 1.1102230246251565e-16);  // 2^-53
-      x = (dist == 1) ? __dsub_rn(__dmul_rn(2.0, u), 1.0) : __dmul_rn(u, scale);
+      x = (dist == 1)   ? __dsub_rn(__dmul_rn(2.0, u), 1.0)
+          : (dist == 2) ? __dmul_rn(u, scale)
+                        : __dmul_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0), scale);   // 3: signed hard
     }
     if constexpr (sizeof(T) == 8) out[e] = x;
     else out[e] = __double2float_rn(x);

@@ -21,8 +21,10 @@
 namespace jm {
 
 enum class Addend : int { Ones = 0, Identity = 1 };
-enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, Tpm2 = 3, F32 = 4, Tpms = 5, Rows = 6,
-                        F32Rows = 7 /* plan label only: the FP32 row panels of Tile::F32 */ };
+enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, Tpm2 = 3 /* r01, removed */, F32 = 4, Tpms = 5,
+                        Rows = 6 /* r01 FP64 row panels, removed */,
+                        F32Rows = 7 /* plan label only: the FP32 row panels of Tile::F32 */,
+                        Reg = 8 /* FP64 register tiles (DFMA; run_f64t) */ };
 
 struct Plan {
   int tile;      // Tile
@@ -48,20 +50,14 @@ JM_HD constexpr int stage_stride(int n, int es) {
 JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage_stride(n, es), 16); }
 
 // FP64: thread-per-matrix up to n = 7 (166 registers, no spill; DMMA would pad
-// 7 -> 8), FP64 tensor cores above.  The FP64 row panels (Tile::Rows) are kept
-// selectable through JM_F64_ROWS_MAX but off: measured on B200 they reach only
-// 0.26-0.35 of the FP64 pipe for n = 9..12 (shared-memory operand bound, three
-// FMAs per loaded double), not better than the padded DMMA tiles.
-#ifndef JM_F64_ROWS_MAX
-#define JM_F64_ROWS_MAX 0
-#endif
+// 7 -> 8), FP64 tensor cores above.  Measured and removed in r02 (the source
+// NVRTC parses for every key keeps only kinds that ship): FP64 DFMA row
+// panels for n = 9..12 (0.26-0.35 of the FP64 pipe, shared-memory operand
+// bound; profiles/r01_f64_rows_g2_g4.txt) and a two-thread-per-matrix DFMA
+// kind for n = 8 (0.71 vs the warp DMMA tile's 0.83; profiles/r01_tpm2_n8.jsonl).
 // FP64 n = 8: the warp DMMA tile reaches 0.83 of the FP64 pipe, 0.90 of its
 // bare DMMA + DFMA mix (0.92, tools/microbench k_mix2_2; the rest is the
-// per-update publish / fragment loads / syncs).  A two-thread-per-matrix DFMA
-// kind (Tile::Tpm2, run_tpm2, JM_F64_TPM2=1; the DMMA tile then serves as its
-// low-repeat kernel) measured 0.71 at R = 100 (204 registers: 8 warps per SM,
-// the per-update shuffle exchange exposed; profiles/r01_tpm2_n8.jsonl), so it
-// is off.
+// per-update publish / fragment loads / syncs).
 // FP32: thread per matrix up to n = 11 (m and p: 242 floats, 216 registers,
 // no spill).  n = 9..11 ran on the row panels at 0.28-0.43 of the FP32 pipe
 // (R = 100; padding to 4-column chunks and 3-row panels); thread per matrix
@@ -69,9 +65,6 @@ JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage
 // (profiles/r01_f32_tpm_n9_11.jsonl).  n = 12 (288 floats) would spill.
 #ifndef JM_F32_TPM_MAX
 #define JM_F32_TPM_MAX 11
-#endif
-#ifndef JM_F64_TPM2
-#define JM_F64_TPM2 0
 #endif
 // FP64 n = 9, 10: thread per matrix with the product staged row by row in the
 // matrix's own shared-memory slot (Tile::Tpms, run_tpms): M stays in registers
@@ -90,33 +83,18 @@ JM_HD constexpr int stage_bytes(int mpc, int n, int es) { return rup(mpc * stage
 #ifndef JM_F64_TPMS_MAX
 #define JM_F64_TPMS_MAX 10
 #endif
+JM_HD constexpr bool f64t_use(int n);
 JM_HD constexpr Tile tile_for(int n, int dtype) {
   return dtype == 1 ? (n <= 7 ? Tile::TPM
-                       : (n == 8 && JM_F64_TPM2) ? Tile::Tpm2
+                       : f64t_use(n) ? Tile::Reg
                        : (n >= 9 && n <= JM_F64_TPMS_MAX) ? Tile::Tpms
-                       : ((n >= 9 && n <= JM_F64_ROWS_MAX) ? Tile::Rows : Tile::Dmma))
+                       : Tile::Dmma)
                     : (n <= JM_F32_TPM_MAX ? Tile::TPM
                        : (n <= JM_F32_TPMS_MAX ? Tile::Tpms : Tile::F32));
 }
 
-// ---- F64 row panels (9 <= n <= 12): DFMA, where DMMA padding wastes most ----
-#ifndef JM_F64P_G
-#define JM_F64P_G 4
-#endif
-constexpr int F64P_G = JM_F64P_G;                  // threads per matrix
-constexpr int F64P_WPC = 2;                        // warps per CTA
-JM_HD constexpr int f64p_rp(int n) { return cdiv(n, F64P_G); }             // rows per thread (3)
-JM_HD constexpr int f64p_ncr(int n) { return cdiv(n, 2); }                 // 16-B chunks per row
-JM_HD constexpr int f64p_ncs(int n) { return f64p_ncr(n) <= 4 ? 4 : 8; }   // stored chunks (pow2)
-JM_HD constexpr int f64p_groups(int n) { return cdiv(f64p_ncr(n), 2); }    // 4-column groups
-JM_HD constexpr int f64p_mbuf(int n) { return n * f64p_ncs(n) * 16 + 32; }
-
 // ---- TPM ----
 constexpr int TPM_THREADS = 128;
-// ---- TPM2: two threads per matrix (even n), 64 matrices per 128-thread CTA,
-// double-buffered (cp.async) staging: registers (~200 per thread) limit the SM
-// to 2 CTAs, so the next chunk streams in while this one iterates
-constexpr int TPM2_MPC = TPM_THREADS / 2;
 
 // ---- DMMA (FP64) ----
 #ifndef JM_DMMA_WARP_MAX
@@ -163,93 +141,219 @@ JM_HD constexpr int dmma_w(int n, bool strm = false) { return cdiv(dmma_t8(n), d
 JM_HD constexpr int dmma_rsc(int n) { return rup(4 * dmma_t8(n), 8); }     // scratch row stride, 16-B chunks
 JM_HD constexpr int dmma_scr(int n) { return 8 * dmma_t8(n) * dmma_rsc(n) * 16; }  // one scratch buffer
 
-// ---- F32 tiles (17 <= n <= 64) ----
-// RG x CG threads per matrix, each owning an RA x CB block of P (RA <= 8,
-// CB <= 16, CB a multiple of 4) in registers; padding rows/columns are
-// computed and discarded.  Only M itself is published to shared memory
-// (row-major, row stride LDM): the A operand M[i][k..k+3] is one 16-B load per
-// owned row per four k steps, the B operand is row k (16-B pieces).  Shared
-// memory traffic per FFMA2 is what bounds these tiles (sm_100a: an LDS.128
-// costs 2.7-4 SM clocks, r01_microbench_lds_patterns.json), hence the large
-// 8 x 16 register tiles.  Whole matrices per warp: 32 / (RG*CG) of them.
-// The tile is chosen per n by a small model: useful / padded FMAs x used lanes
-// x min(1, FMA clocks / LDS clocks), with an LDS.128 costing ~4.5 SM clocks
-// per warp in context and an FFMA2 0.5; accumulators + operands <= 200 regs.
-// Column-chunk mapping of the FP32 tiles (run_f32 chunk_of): blocked for
-// n = 21..36, where it removes the 2-way publish conflict (n = 24 0.49 -> 0.53,
-// n = 32 0.66 -> 0.67 of the FP32 pipe), interleaved elsewhere (n >= 40 lost
-// 1-5 % blocked; profiles/r01_f32_colmap_sweep.jsonl).  JM_F32_COL_BLOCKED=0/1
-// forces either.
-#ifndef JM_F32_COL_BLOCKED
-#define JM_F32_COL_BLOCKED -1
-#endif
-JM_HD constexpr bool f32_col_blocked(int n) {
-  return JM_F32_COL_BLOCKED >= 0 ? JM_F32_COL_BLOCKED == 1 : (n >= 21 && n <= 36);
-}
-struct F32Tile {
-  int rg, ra, cg, cb;
+// ---- F32 tiles, r02 ("F32T", run_f32t) ----
+// r01's tiles (8 x 16 blocks, ~230-255 registers, 2-way conflicted shared
+// loads) kept the FMA pipe 55-73 % busy (profiles/r02_ncu_baseline.md).
+// run_f32t keeps the algorithm (thread-owned RA x CB blocks of P, the A
+// operand by LDS.128 of M[row][k..k+3], each row's block reloaded right after
+// its last use, the B operand by LDS.128 of row k one k ahead) and chooses,
+// per n, the register tile, the shared-memory layout, a register cap and the
+// unrolling of the k loop.  What bounds it (profiles/r02_f32_microbench.md):
+// * shared-memory wavefronts: an LDS.128 runs as two half-warps; a half costs
+//   one wavefront when its two quarter-warps touch disjoint 16-B bank slots
+//   (or one address), else the sum of the quarters (tools/microbench/
+//   lds_wavefronts.cu under ncu).  The layouts below are conflict free under
+//   that rule (tools/f32_layout.py; ncu: 0-2 % conflicts);
+// * the register-file return of shared loads: a pure FFMA2 stream runs at
+//   0.97 of the FP32 pipe, with one LDS.128 per 16 FFMA2 at 0.91, with two
+//   at 0.77-0.81 (tools/microbench/ffma2_lds_mix.cu) — so bigger register
+//   tiles (fewer loaded registers per FFMA2) win even at two warps per SMSP.
+struct F32T {
+  int ra, cb, rg, cg;   // RA x CB register tile; RG x CG threads per matrix
+  int ldm;              // row stride of the published M, floats (multiple of 4)
+  int pad;              // extra 16-B chunks per matrix region (bank-slot offset between matrices)
+  int colblk;           // 1: thread column tc owns chunks tc*CB/4 + h (blocked), 0: h*CG + tc
+  int trfast;           // 1: thread t of a matrix is (tr, tc) = (t % RG, t / RG), 0: (t / CG, t % CG)
+  int qmix;             // 1 (two matrices per warp): quarter-warp q holds matrix q % 2
+  int maxreg;           // register cap (__maxnreg__ of k_update_rc)
+  int kunroll;          // k blocks of four per iteration of the (rolled) k loop
+  int wpc;              // warps per CTA
 };
-#ifndef JM_F32_TILE_RA                // tuning hook: force the register-tile shape
-#define JM_F32_TILE_RA 0
+// Per-n choices, measured on B200 (tools/f32_search.py; the layout of each
+// shape from tools/f32_layout.py):
+// {n, RA, CB, row padding (16-B chunks), region padding (16-B chunks), colblk, trfast, qmix, maxreg, kunroll}
+struct F32TRow { int n, ra, cb, ldmpad, pad, colblk, trfast, qmix, maxreg, kunroll; };
+// FP64 register tiles (DFMA, run_f64t) for the sizes where DMMA's 8 x 8 x 4
+// granularity wastes most of the pipe; the same fields, CB a multiple of 2
+// (a 16-B chunk holds two doubles).  Only the sizes listed take this kind.
+constexpr F32TRow F64T_TABLE[] = {
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+};
+constexpr F32TRow F32T_TABLE[] = {
+    {17, 6, 12, 4, 6, 0, 0, 0, 168, 4},  // 0.433 of the pipe, 157 regs
+    {18, 6, 12, 4, 6, 0, 0, 0, 168, 4},  // 0.492 of the pipe, 155 regs
+    {19, 5, 12, 4, 1, 1, 1, 0, 168, 4},  // 0.535 of the pipe, 141 regs
+    {20, 5, 12, 4, 1, 1, 1, 0, 168, 5},  // 0.618 of the pipe, 146 regs
+    {21, 7, 12, 1, 5, 0, 0, 0, 168, 5},  // 0.563 of the pipe, 160 regs
+    {22, 6, 12, 4, 1, 1, 1, 0, 168, 5},  // 0.609 of the pipe, 150 regs
+    {23, 6, 12, 4, 1, 1, 1, 0, 168, 5},  // 0.654 of the pipe, 154 regs
+    {24, 6, 12, 4, 1, 1, 1, 0, 168, 6},  // 0.721 of the pipe, 158 regs
+    {25, 5, 16, 1, 1, 1, 0, 0, 168, 6},  // 0.543 of the pipe, 152 regs
+    {26, 7, 8, 1, 1, 1, 0, 1, 168, 6},  // 0.569 of the pipe, 148 regs
+    {27, 7, 8, 1, 1, 1, 0, 1, 168, 6},  // 0.599 of the pipe, 140 regs
+    {28, 7, 8, 1, 1, 1, 0, 1, 168, 7},  // 0.660 of the pipe, 148 regs
+    {29, 8, 8, 1, 3, 1, 0, 1, 168, 7},  // 0.615 of the pipe, 148 regs
+    {30, 8, 8, 1, 3, 1, 0, 1, 168, 7},  // 0.668 of the pipe, 152 regs
+    {31, 4, 16, 2, 3, 0, 0, 1, 168, 7},  // 0.700 of the pipe, 148 regs
+    {32, 4, 16, 2, 3, 0, 0, 1, 168, 8},  // 0.756 of the pipe, 142 regs
+    {33, 7, 12, 1, 1, 1, 0, 1, 168, 8},  // 0.575 of the pipe, 152 regs
+    {34, 7, 12, 1, 1, 1, 0, 1, 168, 8},  // 0.636 of the pipe, 161 regs
+    {35, 7, 12, 1, 1, 1, 0, 1, 168, 8},  // 0.662 of the pipe, 156 regs
+    {36, 8, 12, 1, 1, 1, 0, 1, 255, 9},  // 0.595 of the pipe, 200 regs
+    {37, 5, 12, 1, 0, 0, 1, 0, 168, 9},  // 0.551 of the pipe, 134 regs
+    {38, 5, 12, 1, 0, 0, 1, 0, 168, 9},  // 0.584 of the pipe, 144 regs
+    {39, 5, 12, 1, 0, 0, 1, 0, 168, 9},  // 0.613 of the pipe, 134 regs
+    {40, 5, 12, 1, 0, 0, 1, 0, 168, 10},  // 0.656 of the pipe, 142 regs
+    {41, 6, 12, 1, 0, 0, 0, 0, 168, 10},  // 0.554 of the pipe, 154 regs
+    {42, 6, 12, 1, 0, 0, 0, 0, 168, 10},  // 0.611 of the pipe, 153 regs
+    {43, 6, 12, 1, 0, 0, 1, 0, 168, 10},  // 0.604 of the pipe, 156 regs
+    {44, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.644 of the pipe, 160 regs
+    {45, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.662 of the pipe, 148 regs
+    {46, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.700 of the pipe, 154 regs
+    {47, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.718 of the pipe, 154 regs
+    {48, 6, 12, 1, 0, 0, 1, 0, 168, 12},  // 0.750 of the pipe, 154 regs
+    {49, 7, 16, 1, 0, 0, 0, 0, 255, 2},  // 0.491 of the pipe, 220 regs
+    {50, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.509 of the pipe, 214 regs
+    {51, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.530 of the pipe, 216 regs
+    {52, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.516 of the pipe, 244 regs
+    {53, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.554 of the pipe, 238 regs
+    {54, 7, 8, 1, 0, 0, 1, 0, 168, 2},  // 0.581 of the pipe, 160 regs
+    {55, 7, 8, 1, 0, 0, 1, 0, 168, 2},  // 0.584 of the pipe, 154 regs
+    {56, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.662 of the pipe, 204 regs
+    {57, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.587 of the pipe, 225 regs
+    {58, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.611 of the pipe, 221 regs
+    {59, 8, 8, 1, 0, 0, 0, 0, 255, 2},  // 0.640 of the pipe, 154 regs
+    {60, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.604 of the pipe, 233 regs
+    {61, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.679 of the pipe, 236 regs
+    {62, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.711 of the pipe, 244 regs
+    {63, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.730 of the pipe, 236 regs
+    {64, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.762 of the pipe, 217 regs
+};
+#ifndef JM_F32T_RA                // tuning hooks: force the register-tile shape / layout / knobs
+#define JM_F32T_RA 0
 #endif
-#ifndef JM_F32_TILE_CB
-#define JM_F32_TILE_CB 0
+#ifndef JM_F32T_CB
+#define JM_F32T_CB 0
 #endif
-// measured overrides of the model (profiles/r01_f32_tile_shape_search.txt,
-// FP32 pipe at R = 100): wider column blocks for the sizes just above 16 / 24
-// (and r01_f32_tile_shape_search_n21_64.txt: 21..24 as 6 x 12, +5..13 %;
-// 37..40 as 5 x 20, +24..28 %; elsewhere the model's shape was best or within
-// the ~5 % run-to-run noise)
-JM_HD constexpr int f32_tile_ra_override(int n) {
-  return (n == 17 || n == 18) ? 6 : (n == 19 || n == 20 || n == 25) ? 5 : (n >= 21 && n <= 24) ? 6
-         : (n >= 37 && n <= 40) ? 5 : 0;
-}
-JM_HD constexpr int f32_tile_cb_override(int n) {
-  return (n == 17 || n == 18) ? 20 : (n == 19 || n == 25) ? 28 : n == 20 ? 12 : (n >= 21 && n <= 24) ? 12
-         : (n >= 37 && n <= 40) ? 20 : 0;
-}
-JM_HD constexpr F32Tile f32_tile(int n) {
-  if (JM_F32_TILE_RA > 0 && JM_F32_TILE_CB > 0)
-    return F32Tile{cdiv(n, JM_F32_TILE_RA), JM_F32_TILE_RA, cdiv(n, JM_F32_TILE_CB), JM_F32_TILE_CB};
-  if (f32_tile_ra_override(n) > 0)   // 17, 18: 0.31 / 0.36 -> 0.33 / 0.40; 19, 20, 25: +4..9 %
-    return F32Tile{cdiv(n, f32_tile_ra_override(n)), f32_tile_ra_override(n), cdiv(n, f32_tile_cb_override(n)),
-                   f32_tile_cb_override(n)};
-  F32Tile best{cdiv(n, 8), cdiv(n, cdiv(n, 8)), cdiv(n, 16), rup(cdiv(n, cdiv(n, 16)), 4)};
+#ifndef JM_F32T_LDMPAD
+#define JM_F32T_LDMPAD -1
+#endif
+#ifndef JM_F32T_PAD
+#define JM_F32T_PAD -1
+#endif
+#ifndef JM_F32T_COLBLK
+#define JM_F32T_COLBLK -1
+#endif
+#ifndef JM_F32T_TRFAST
+#define JM_F32T_TRFAST -1
+#endif
+#ifndef JM_F32T_QMIX
+#define JM_F32T_QMIX -1
+#endif
+#ifndef JM_F32T_MAXREG
+#define JM_F32T_MAXREG 0
+#endif
+#ifndef JM_F32T_KUNROLL
+#define JM_F32T_KUNROLL 0
+#endif
+#ifndef JM_F32T_WPC
+#define JM_F32T_WPC 0
+#endif
+// the default shape when no table entry applies: the tile that covers the
+// matrix with <= 64 threads and wastes least (padding x idle lanes x loads per FFMA2)
+// (dt = 0 float, 1 double: VEC = 16 / element size elements per 16-B chunk)
+JM_HD constexpr int tt_vec(int dt) { return dt ? 2 : 4; }
+JM_HD constexpr F32T f32t_default(int n, int dt = 0) {
+  const int v = tt_vec(dt), w = dt ? 2 : 1;   // elements per chunk, 32-bit registers per element
+  F32T best{8, 8, cdiv(n, 8), cdiv(n, 8), 0, 0, 0, 1, 0, 168, 2, 4};
   double bs = -1.0;
   for (int ra = 8; ra >= 2; --ra)
-    for (int cb = 16; cb >= 4; cb -= 4) {
+    for (int cb = 16; cb >= v; cb -= v) {
       const int rg = cdiv(n, ra), cg = cdiv(n, cb), t = rg * cg;
-      if (t > 32 || ra * cb + 4 * ra + 2 * cb > 200) continue;
-      const double pad = (double)n * n * n / ((double)(rg * ra) * (cg * cb) * rup(n, 4));
-      const double lane = (double)((32 / t) * t) / 32.0;
-      double lsu = (double)(ra * cb) / (4.5 * (ra + cb));
-      if (lsu > 1.0) lsu = 1.0;
-      const double sc = pad * lane * lsu;
-      if (sc > bs + 1e-9) {
-        bs = sc;
-        best = F32Tile{rg, ra, cg, cb};
-      }
+      if (t > 64 || w * (ra * cb + v * ra + 2 * cb) > 200) continue;
+      const double pad = (double)n * n / ((double)(rg * ra) * (cg * cb));
+      const double lane = t > 32 ? (double)t / rup(t, 32) : (double)((32 / t) * t) / 32.0;
+      const double core = 1.0 / (1.0 + 0.3 * 4.0 * (ra + cb) / (ra * cb));
+      const double sc = pad * lane * core;
+      if (sc > bs + 1e-9) { bs = sc; best = F32T{ra, cb, rg, cg, 0, 0, 0, 1, 0, 168, 2, 4}; }
     }
+  best.ldm = best.cg * best.cb + v;
+  best.maxreg = w * (best.ra * best.cb + v * best.ra + 2 * best.cb) + 24 > 168 ? 255 : 168;
   return best;
 }
-JM_HD constexpr int f32_rg(int n) { return f32_tile(n).rg; }   // thread rows
-JM_HD constexpr int f32_ra(int n) { return f32_tile(n).ra; }   // rows per thread
-JM_HD constexpr int f32_cg(int n) { return f32_tile(n).cg; }   // thread cols
-JM_HD constexpr int f32_cb(int n) { return f32_tile(n).cb; }   // cols per thread
-JM_HD constexpr int f32_tpm(int n) { return f32_rg(n) * f32_cg(n); }      // threads per matrix
-JM_HD constexpr int f32_mpw(int n) { return 32 / f32_tpm(n); }            // matrices per warp
-constexpr int F32_WPC = 2;                                                // warps per CTA
-JM_HD constexpr int f32_rows(int n) { return f32_rg(n) * f32_ra(n); }     // padded rows
-JM_HD constexpr int f32_cols(int n) { return f32_cg(n) * f32_cb(n); }     // padded cols
-JM_HD constexpr int f32_kp(int n) { return rup(n, 4); }                   // k steps (blocks of 4)
-JM_HD constexpr int f32_srows(int n) { return f32_rows(n) > f32_kp(n) ? f32_rows(n) : f32_kp(n); }
-// row stride in floats: LDM / 4 odd, so eight consecutive rows' 16-B A loads
-// fall in eight different 16-B bank groups
-JM_HD constexpr int f32_ldm(int n) { return f32_cols(n) + (((f32_cols(n) / 4) % 2 == 0) ? 4 : 8); }
-// one matrix region: holds the staged matrix, then the published M
-JM_HD constexpr int f32_region(int n) {
-  return rup(f32_srows(n) * f32_ldm(n) * 4 > n * n * 4 ? f32_srows(n) * f32_ldm(n) * 4 : n * n * 4, 16);
+JM_HD constexpr F32T f32t_tile(int n, int dt = 0) {
+  F32T t = f32t_default(n, dt);
+  auto take = [&](const F32TRow &r) {
+    t = F32T{r.ra, r.cb, cdiv(n, r.ra), cdiv(n, r.cb), cdiv(n, r.cb) * r.cb + tt_vec(dt) * r.ldmpad, r.pad,
+             r.colblk, r.trfast, r.qmix, r.maxreg, r.kunroll, 4};
+  };
+  if (dt) {
+    for (const F32TRow &r : F64T_TABLE)
+      if (r.n == n && r.ra > 0) take(r);
+  } else {
+    for (const F32TRow &r : F32T_TABLE)
+      if (r.n == n && r.ra > 0) take(r);
+  }
+  if (dt) {   // (the JM_F32T_* tuning hooks below apply to the FP32 tiles)
+    if (t.rg * t.cg > 16 || t.rg * t.cg <= 8) t.qmix = 0;
+    return t;
+  }
+  if (JM_F32T_RA > 0 && JM_F32T_CB > 0) {
+    t.ra = JM_F32T_RA; t.cb = JM_F32T_CB; t.rg = cdiv(n, t.ra); t.cg = cdiv(n, t.cb);
+    t.ldm = t.cg * t.cb + 4;
+  }
+  if (JM_F32T_LDMPAD >= 0) t.ldm = t.cg * t.cb + 4 * JM_F32T_LDMPAD;
+  if (JM_F32T_PAD >= 0) t.pad = JM_F32T_PAD;
+  if (JM_F32T_COLBLK >= 0) t.colblk = JM_F32T_COLBLK;
+  if (JM_F32T_TRFAST >= 0) t.trfast = JM_F32T_TRFAST;
+  if (JM_F32T_QMIX >= 0) t.qmix = JM_F32T_QMIX;
+  if (JM_F32T_MAXREG > 0) t.maxreg = JM_F32T_MAXREG;
+  if (JM_F32T_KUNROLL > 0) t.kunroll = JM_F32T_KUNROLL;
+  if (JM_F32T_WPC > 0) t.wpc = JM_F32T_WPC;
+  if (t.rg * t.cg > 16 || t.rg * t.cg <= 8) t.qmix = 0;   // quarter mixing needs exactly two matrices per warp
+  return t;
 }
+JM_HD constexpr int f32t_tpmat(int n, int dt = 0) { return f32t_tile(n, dt).rg * f32t_tile(n, dt).cg; }   // threads per matrix
+// (a matrix of more than 32 threads takes whole warps; threads past RG*CG idle)
+JM_HD constexpr int f32t_wpm(int n, int dt = 0) {   // warps per matrix
+  return f32t_tpmat(n, dt) > 32 ? cdiv(f32t_tpmat(n, dt), 32) : 1;
+}
+JM_HD constexpr int f32t_mpw(int n, int dt = 0) {   // matrices per warp (1 for a multi-warp matrix; 2 under qmix)
+  return f32t_tpmat(n, dt) > 32 ? 1 : f32t_tile(n, dt).qmix ? 2 : 32 / f32t_tpmat(n, dt);
+}
+JM_HD constexpr int f32t_wpc(int n, int dt = 0) {
+  return f32t_tile(n, dt).wpc < f32t_wpm(n, dt) ? f32t_wpm(n, dt) : f32t_tile(n, dt).wpc;
+}
+JM_HD constexpr int f32t_mpc(int n, int dt = 0) {   // matrices per CTA
+  return f32t_wpc(n, dt) / f32t_wpm(n, dt) * f32t_mpw(n, dt);
+}
+JM_HD constexpr int f32t_nr(int n, int dt = 0) { return f32t_tile(n, dt).rg * f32t_tile(n, dt).ra; }   // padded rows
+JM_HD constexpr int f32t_kp(int n, int dt = 0) { return rup(n, tt_vec(dt)); }   // k blocks of one 16-B chunk
+// M rows in the work area: the A loads of M[row][kb-block] read rows up to rup(n, VEC) (zero beyond n)
+JM_HD constexpr int f32t_srows(int n, int dt = 0) {
+  return f32t_nr(n, dt) > f32t_kp(n, dt) ? f32t_nr(n, dt) : f32t_kp(n, dt);
+}
+// one matrix region: the staged matrix (packed, n*n), then the published M
+JM_HD constexpr int f32t_region(int n, int dt = 0) {
+  return rup(f32t_srows(n, dt) * f32t_tile(n, dt).ldm * (dt ? 8 : 4) > n * n * (dt ? 8 : 4)
+                 ? f32t_srows(n, dt) * f32t_tile(n, dt).ldm * (dt ? 8 : 4)
+                 : n * n * (dt ? 8 : 4),
+             16) +
+         16 * f32t_tile(n, dt).pad;
+}
+// register cap (__maxnreg__ of k_update_rc): at ~150-210 registers ptxas keeps
+// the next k step's B loads in flight; a lower cap forces earlier uses
+JM_HD constexpr int f32t_maxreg(int n, int dt = 0) { return f32t_tile(n, dt).maxreg; }
+JM_HD constexpr int f32t_kunroll(int n, int dt = 0) {
+  return f32t_tile(n, dt).kunroll < 1 ? 1 : f32t_tile(n, dt).kunroll;
+}
+// FP64 sizes that take the register tiles: those listed in F64T_TABLE
+JM_HD constexpr bool f64t_use(int n) {
+  for (const F32TRow &r : F64T_TABLE)
+    if (r.n == n && r.ra > 0) return true;
+  return false;
+}
+JM_HD constexpr bool f32t_use(int n) { return n >= 17; }
 
 // ---- F32 row panels (9 <= n <= 32) ----
 // A thread owns RP = 4 FULL rows of M (the A operand is local); row k of M
@@ -315,15 +419,10 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   if (t == Tile::TPM) {
     return Plan{(int)t, TPM_THREADS, TPM_THREADS, nst * stage_bytes(TPM_THREADS, n, es), 1};
   }
-  if (t == Tile::Tpm2) {
-    return Plan{(int)t, TPM_THREADS, TPM2_MPC, 2 * stage_bytes(TPM2_MPC, n, es), 1};
-  }
+  if (t == Tile::Reg)   // FP64 register tiles: the stage area IS the per-matrix region
+    return Plan{(int)t, 32 * f32t_wpc(n, 1), f32t_mpc(n, 1), f32t_mpc(n, 1) * f32t_region(n, 1), f32t_wpm(n, 1)};
   if (t == Tile::Tpms) {
     return Plan{(int)t, TPM_THREADS, TPM_THREADS, stage_bytes(TPM_THREADS, n, es), 1};
-  }
-  if (t == Tile::Rows) {
-    const int mpc = F64P_WPC * (32 / F64P_G);
-    return Plan{(int)t, 32 * F64P_WPC, mpc, stage_bytes(mpc, n, es) + 2 * mpc * f64p_mbuf(n), 1};
   }
   if (t == Tile::Dmma) {
     const int w = dmma_w(n);
@@ -337,15 +436,18 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
     if (f32p_inplace(n)) return Plan{(int)Tile::F32Rows, 32 * F32P_WPC, mpc, nst * rup(mpc * f32p_slot(n), 16) + mpc * f32p_mbuf(n), 1};
     return Plan{(int)Tile::F32Rows, 32 * F32P_WPC, mpc, nst * stage_bytes(mpc, n, es) + 2 * mpc * f32p_mbuf(n), 1};
   }
-  // F32 tiles: the stage area IS the per-matrix region (stride f32_region)
-  const int mpc = F32_WPC * f32_mpw(n);
-  return Plan{(int)t, 32 * F32_WPC, mpc, mpc * f32_region(n), 1};
+  // F32 tiles: the stage area IS the per-matrix region (stride f32t_region)
+  return Plan{(int)t, 32 * f32t_wpc(n), f32t_mpc(n), f32t_mpc(n) * f32t_region(n), f32t_wpm(n)};
 }
 
 // Which entry point the specialization uses: k_update (maxThreads only) or
 // k_update_mb1 (maxThreads, minBlocks = 1) — the CTA-per-matrix DMMA kinds.
 JM_HD constexpr bool use_mb1(int n, int dtype, bool strm = false) {
   return tile_for(n, dtype) == Tile::Dmma && dmma_w(n, strm) > 1;
+}
+// ... or k_update[_stream]_rc (a register cap, __maxnreg__): the F32T tiles
+JM_HD constexpr bool use_rc(int n, int dtype, bool strm = false) {
+  return (void)strm, (dtype == 0 && tile_for(n, dtype) == Tile::F32 && f32t_use(n)) || tile_for(n, dtype) == Tile::Reg;
 }
 
 // ---- streaming variant (low repeat: the HBM-bound side of the roofline) ----
@@ -365,15 +467,12 @@ JM_HD constexpr bool use_mb1(int n, int dtype, bool strm = false) {
 #ifndef JM_RING_CHUNK
 #define JM_RING_CHUNK 8192
 #endif
-// (for Tile::Tpm2 the low-repeat kernel is the warp DMMA tile with its
-// resident staging: the two-thread kind's conflicted one-time loads lose at
-// R = 1, where the DMMA tile streams at 0.92 of HBM)
 // (for Tile::TPM the streaming variant is the same thread-per-matrix kernel
 // with the double-buffered cp.async stage: its per-thread reads need the
 // odd-16-B staging stride, which a bulk copy per matrix would make 1-D copies
 // of 32..512 B)
 JM_HD constexpr bool stream_ok(int n, int dtype) {
-  return tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::F32 || tile_for(n, dtype) == Tile::Tpm2 ||
+  return tile_for(n, dtype) == Tile::Dmma || tile_for(n, dtype) == Tile::F32 || tile_for(n, dtype) == Tile::Reg ||
          tile_for(n, dtype) == Tile::Tpms ||
          tile_for(n, dtype) == Tile::TPM;
 }
@@ -387,12 +486,9 @@ JM_HD constexpr bool stream_ok(int n, int dtype) {
 // resident kernel has the thin border there) only at R <= 2; 35..40 to ~300;
 // 41..48 to ~250; 49..56 to ~600; 57..64 to ~400; n = 8 loses 8 % at R = 1
 // (16 copies of 512 B per chunk) and stays resident; n = 9, 10 see JM_TPMS_RN.
-// f32: row panels (n = 15, 16) gain to ~64, tiles (n >= 17) to ~140; the
-// staged-product sizes (12..14) and the thread-per-matrix sizes have their
-// own rules below.
-#ifndef JM_TPM2_RN
-#define JM_TPM2_RN 20
-#endif
+// f32: row panels (n = 15, 16) gain to ~64; the tiles (n >= 17) stream
+// through their prefetching stage below JM_F32T_RN; the staged-product sizes
+// (12..14) and the thread-per-matrix sizes have their own rules below.
 // n = 9, 10: the DMMA ring streams better only at R = 1 (0.68 vs 0.56 of HBM);
 // from R = 2 the staged-product kind wins (R = 100: 0.65 / 0.68 of the FP64
 // pipe vs 0.22 / 0.24 for the padded DMMA tile; profiles/r01_tpms_n9_10.jsonl)
@@ -400,7 +496,7 @@ JM_HD constexpr bool stream_ok(int n, int dtype) {
 #define JM_TPMS_RN 20
 #endif
 JM_HD constexpr int stream_rn_f64(int n) {
-  return (n >= 9 && n <= JM_F64_TPMS_MAX) ? JM_TPMS_RN : n < 8 ? 0 : n == 8 ? (JM_F64_TPM2 ? JM_TPM2_RN : 0) : n <= 32 ? 600 : n <= 34 ? 100 : n <= 40 ? 300 : n <= 48 ? 250 : n <= 56 ? 600 : 400;
+  return (n >= 9 && n <= JM_F64_TPMS_MAX) ? JM_TPMS_RN : n <= 8 ? 0 : n <= 32 ? 600 : n <= 34 ? 100 : n <= 40 ? 300 : n <= 48 ? 250 : n <= 56 ? 600 : 400;
 }
 // ... and not below stream_lo(n, dtype): f64 n = 16 at R = 1, whose resident
 // kernel (16 KB, 48 registers: 40 warps per SM) streams at 0.95 of HBM once
@@ -419,16 +515,23 @@ JM_HD constexpr int stream_lo(int n, int dtype) {
 // (1.13x at R = 8, 1.05x at R = 100) and loses below (0.89x at R = 1), so it
 // streams above the lower bound stream_lo (r01_all_n_sweep.jsonl,
 // r01_tpm_stream_sweep.jsonl).
+// FP64 / FP32 register tiles: the prefetching stage (twice the shared
+// memory per matrix) wins below this R(n+1)
+#ifndef JM_F64T_RN
+#define JM_F64T_RN 60
+#endif
+#ifndef JM_F32T_RN
+#define JM_F32T_RN 140
+#endif
 JM_HD constexpr int stream_rn_tpm(int n, int dtype) { return (dtype == 0 && n == 3) ? (1 << 30) : 0; }
-JM_HD constexpr bool f32_stream_pf(int n);   // below, with the ring sizes
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype)               ? 0
          : tile_for(n, dtype) == Tile::TPM ? stream_rn_tpm(n, dtype)
+         : tile_for(n, dtype) == Tile::Reg ? JM_F64T_RN
          : (dtype == 0 && tile_for(n, dtype) == Tile::Tpms) ? (n == 12 ? 0 : 20)   // R = 1: row-panel ring
-         : (dtype == 0 && f32_stream_pf(n)) ? n + 2   // the stage variant: R = 1 only (r01_f32_odd_stream)
          : dtype == 1        ? stream_rn_f64(n)
          : f32p_use(n)       ? 64
-                             : 140;
+                             : JM_F32T_RN;
 }
 // rounds per chunk: >= JM_RING_CHUNK bytes and a chunk a multiple of 16 B
 JM_HD constexpr int ring_k(int rb) {
@@ -436,41 +539,12 @@ JM_HD constexpr int ring_k(int rb) {
 }
 // matrix stride in a ring stage: the odd-16-B stage stride when a matrix is a
 // multiple of 16 B (one bulk copy per matrix), else packed (one per chunk)
-// (slot: a larger per-matrix slot a kind wants to work in, see f32_ring_slot)
+// (slot: a larger per-matrix slot a kind wants to work in, see dmma_slot)
 JM_HD constexpr int ring_sbm(int n, int es, int slot = 0) {
   return (n * n * es) % 16 == 0 ? (slot > stage_stride(n, es) ? slot : stage_stride(n, es)) : n * n * es;
 }
 JM_HD constexpr int ring_bytes(int n, int es, int rm, int slot = 0) {
   return JM_RING_S * ring_k(rm * n * n * es) * rm * ring_sbm(n, es, slot) + rup(8 * JM_RING_S, 16);
-}
-// FP32 tiles, streaming: when matrices are bulk-copied one per slot (n even),
-// each slot can be a whole f32_region, so the kind works in place (publishes
-// its padded M over the staged matrix, as the resident kernel does) with no
-// separate work area (n = 32: 3 CTAs per SM instead of 2).  Off by default:
-// measured slower for n >= 28 (n = 32 at R = 1: 0.39 -> 0.31 of HBM), faster
-// only at n = 24 (0.46 -> 0.50) (profiles/r01_stream_f32_inplace.jsonl).
-#ifndef JM_F32_RING_INPLACE
-#define JM_F32_RING_INPLACE 0
-#endif
-// FP32 tiles, low repeat: the bulk-copy ring, except where its plan would not
-// leave two CTAs per SM (odd n >= 49: the 16-B chunk rule makes 4-matrix
-// chunks, up to 162 KB); those use the resident layout with the double-
-// buffered cp.async stage instead (two REG regions per matrix): n = 63 at
-// R = 1 0.20 -> 0.23 of HBM, where the ring got 0.18 (r01_f32_stream_pf.jsonl;
-// elsewhere the ring is better, JM_F32_STREAM_PF=1 forces the stage for all)
-#ifndef JM_F32_STREAM_PF
-#define JM_F32_STREAM_PF 0
-#endif
-#ifndef JM_STREAM_F32_SMEM_MAX
-#define JM_STREAM_F32_SMEM_MAX (110 * 1024)   // two CTAs incl. the 1 KB per-CTA reserve
-#endif
-JM_HD constexpr int f32_rm(int n) { return F32_WPC * f32_mpw(n); }
-JM_HD constexpr bool f32_stream_pf(int n) {
-  return n >= 17 && !f32p_use(n) &&
-         (JM_F32_STREAM_PF || ring_bytes(n, 4, f32_rm(n)) + f32_rm(n) * f32_region(n) > JM_STREAM_F32_SMEM_MAX);
-}
-JM_HD constexpr int f32_ring_slot(int n) {
-  return (JM_F32_RING_INPLACE && (n * n * 4) % 16 == 0) ? f32_region(n) : 0;
 }
 // DMMA in the streaming variant: when the swizzled publish buffer fits in the
 // matrix's ring slot (n a multiple of 16), the slot is reused as that buffer
@@ -497,7 +571,7 @@ JM_HD constexpr int round_mpc(int n, int dtype) {
   return (tile_for(n, dtype) == Tile::Dmma || (dtype == 1 && tile_for(n, dtype) == Tile::Tpms))
              ? (dmma_w(n, true) == 1 ? DMMA_WPC : 1)
          : f32p_use(n)                   ? F32P_WPC * f32p_mpw(n)
-                                         : F32_WPC * f32_mpw(n);
+                                         : f32t_mpc(n);
 }
 // Plan of the streaming variant: mpc = matrices per ring chunk (the host sizes
 // the grid by it); smem = the ring + the kind's own work areas.
@@ -507,8 +581,9 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   if (!stream_ok(n, dtype)) return plan_specialized(n, dtype);
   if (tile_for(n, dtype) == Tile::TPM)
     return Plan{(int)Tile::TPM, TPM_THREADS, TPM_THREADS, 2 * stage_bytes(TPM_THREADS, n, es), 1};
-  if (tile_for(n, dtype) == Tile::Tpm2)   // low-repeat kernel: the resident warp DMMA tile
-    return Plan{(int)Tile::Dmma, 32 * DMMA_WPC, DMMA_WPC, stage_bytes(DMMA_WPC, n, es) + DMMA_WPC * dmma_scr(n), 1};
+  if (tile_for(n, dtype) == Tile::Reg)
+    return Plan{(int)Tile::Reg, 32 * f32t_wpc(n, 1), f32t_mpc(n, 1), 2 * rup(f32t_mpc(n, 1) * f32t_region(n, 1), 16),
+                f32t_wpm(n, 1)};
   if (tile_for(n, dtype) == Tile::Dmma || (dtype == 1 && tile_for(n, dtype) == Tile::Tpms)) {   // (Tpms: DMMA ring)
     const int w = dmma_w(n, true);
     const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers
@@ -518,15 +593,9 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
     return f32p_ring_inplace(n)
                ? Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm, f32p_slot(n)) + rm * f32p_mbuf(n), 1}
                : Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
-  if (f32_stream_pf(n)) return Plan{(int)Tile::F32, 32 * F32_WPC, rm, 2 * rup(rm * f32_region(n), 16), 1};
-  return Plan{(int)Tile::F32, 32 * F32_WPC, chm,
-              ring_bytes(n, es, rm, f32_ring_slot(n)) + (f32_ring_slot(n) ? 0 : rm * f32_region(n)), 1};
-}
-
-// The host streams FP32 only when the plan leaves room for two CTAs per SM
-// (a single 2-warp CTA loses to the resident kernel; see f32_stream_pf).
-JM_HD constexpr bool stream_fits(int n, int dtype) {
-  return dtype == 1 || plan_stream(n, dtype).smem <= JM_STREAM_F32_SMEM_MAX;
+  // F32T: the resident layout with the double-buffered cp.async stage (the
+  // next chunk streams in while this one is updated)
+  return Plan{(int)Tile::F32, 32 * f32t_wpc(n), f32t_mpc(n), 2 * rup(f32t_mpc(n) * f32t_region(n), 16), f32t_wpm(n)};
 }
 
 // Note: k_update passes only maxThreads to __launch_bounds__.  Registers are

@@ -580,75 +580,6 @@ __device__ __forceinline__ void run_tpms(const T *__restrict__ in, T *__restrict
 }
 
 // ======================================================================
-// TPM2: two threads per matrix, DFMA only (FP64, even N; used for N = 8).
-// Each thread keeps the WHOLE matrix in registers and forms half of the rows
-// of P = M + M*M; the halves are exchanged with one shuffle per element.  The
-// thread of the odd lane works in a frame rotated by N/2 (rows and columns:
-// local (r, q) = global ((r + rot) % N, (q + rot) % N)), so that in BOTH
-// threads the own rows are local rows 0..N/2-1 and the partner's rows land in
-// local rows N/2.. with the columns rotated by N/2 — all compile-time register
-// indices.  The update commutes with this permutation similarity (the Ones
-// and Identity addends are invariant), so each thread computes exactly the
-// paper's update; only the k summation order of the odd-lane rows differs
-// (starts at k = N/2), within tolerance (reading R6).
-// ======================================================================
-template <int N, Addend A>
-__device__ __forceinline__ void run_tpm2(const double *__restrict__ in, double *__restrict__ out,
-                                         long long batch, int repeat) {
-  static_assert(N % 2 == 0, "two threads per matrix need an even N");
-  constexpr int H = N / 2;
-  constexpr int ES = 8, MB = N * N * 8, SB = stage_stride(N, 8);
-  constexpr int NT = TPM_THREADS, MPC = TPM2_MPC;
-  constexpr bool AL = ((MPC * MB) % 16) == 0;
-  extern __shared__ __align__(16) char smem[];
-  const int tid = threadIdx.x, mi = tid >> 1, rot = (tid & 1) * H;
-  const double c = 0.00005;
-  Stager<N, ES, SB, NT, MPC, AL, true> sg(in, out, batch, smem);
-  for (sg.start(); sg.valid(); sg.next()) {
-    sg.acquire();
-    const bool live = mi < sg.cnt();         // every lane runs the loop (shuffle partners)
-    double *sm = reinterpret_cast<double *>(sg.buf() + mi * SB);
-    double m[N][N];
-#pragma unroll
-    for (int r = 0; r < N; ++r)
-#pragma unroll
-      for (int q = 0; q < N; ++q) m[r][q] = live ? sm[((r + rot) % N) * N + (q + rot) % N] : 0.0;
-    for (int rep = 0; rep < repeat; ++rep) {
-      double p[H][N];
-      // P = M + M*M for the own rows: accumulators start at M; k outermost
-#pragma unroll
-      for (int i = 0; i < H; ++i)
-#pragma unroll
-        for (int j = 0; j < N; ++j) p[i][j] = m[i][j];
-#pragma unroll
-      for (int k = 0; k < N; ++k)
-#pragma unroll
-        for (int i = 0; i < H; ++i)
-#pragma unroll
-          for (int j = 0; j < N; ++j) p[i][j] = fmaT(m[i][k], m[k][j], p[i][j]);
-      // M' = A + c * P (own rows), then the partner's new rows
-#pragma unroll
-      for (int i = 0; i < H; ++i)
-#pragma unroll
-        for (int j = 0; j < N; ++j)
-          m[i][j] = (A == Addend::Ones || i == j) ? fmaT(c, p[i][j], 1.0) : c * p[i][j];
-#pragma unroll
-      for (int i = 0; i < H; ++i)
-#pragma unroll
-        for (int j = 0; j < N; ++j) m[H + i][(j + H) % N] = __shfl_xor_sync(0xffffffffu, m[i][j], 1);
-    }
-    if (live) {
-#pragma unroll
-      for (int i = 0; i < H; ++i)
-#pragma unroll
-        for (int q = 0; q < N; ++q) sm[((i + rot) % N) * N + (q + rot) % N] = m[i][q];
-    }
-    sg.release();
-  }
-  sg.finish();
-}
-
-// ======================================================================
 // DMMA: FP64 tensor cores (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4).
 //
 // M is padded to NP = 8*T8 and held in registers as DMMA accumulator
@@ -709,18 +640,12 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   // 0.54, 25 0.53 -> 0.67, 33 0.59 -> 0.73, 18 0.40 -> 0.43, 26 0.51 -> 0.56,
   // 34 0.58 -> 0.64; at n = 9 / 10 (one main tile) the shuffles cost what the
   // DMMAs save (0.23 -> 0.23 / 0.19), so those keep the padded tiles.
-  // The code also covers several warps per matrix (W > 1: each warp forms the
-  // column border of its own row tiles, the warp owning the border row tile
-  // forms the row border from the published M), but that measured slower
-  // (n = 41 0.63 -> 0.48, 57 0.68 -> 0.53 of the pipe: the owner warp's row
-  // border becomes the critical path at every __syncthreads;
-  // profiles/r01_dmma_border_multiwarp.jsonl), so it is enabled for W == 1
-  // only (JM_DMMA_BORDER_MULTIWARP=1 turns it on).
-#ifndef JM_DMMA_BORDER_MULTIWARP
-#define JM_DMMA_BORDER_MULTIWARP 0
-#endif
+  // (Only for whole-matrix warps: a several-warp version, where the warp
+  // owning the border row tile forms the row border, measured slower — n = 41
+  // 0.63 -> 0.48, 57 0.68 -> 0.53 of the pipe, profiles/r01_dmma_border_multiwarp.jsonl —
+  // and was removed in r02.)
   constexpr int BR = N - 8 * (T8 - 1);
-  constexpr bool BORD = (W == 1 || JM_DMMA_BORDER_MULTIWARP) && (N > 16) && (BR <= JM_DMMA_BORDER_MAX);
+  constexpr bool BORD = (W == 1) && (N > 16) && (BR <= JM_DMMA_BORDER_MAX);
   constexpr int KTOP = BORD ? T8 - 1 : T8;   // global row tiles through DMMA
   constexpr int KN = BORD ? T8 - 1 : T8;     // column tiles through DMMA
   extern __shared__ __align__(16) char smem[];
@@ -747,14 +672,11 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   for (int j1 = 0; j1 < 2; ++j1) pofs[j1] = ((8 * wr * RT + g) * RSC + ((j1 * 4 + t) ^ fg)) * 16;
   // border (BORD): column pair (8K, 8K+1) of row 8J + 2t + s -> colofs[s] + 8J*RSC*16;
   // element (8K + g', 8I + g) -> rowofs + (g'*RSC + 4*(I ^ (g' & 1)))*16
-  // and (W > 1) M's fragment of any tile (I', J) -> aofs[J&1] + (8I'*RSC + 8(J>>1))*16
-  int colofs[2] = {0, 0}, rowofs = 0, aofs[2] = {0, 0};
+  int colofs[2] = {0, 0}, rowofs = 0;
   if constexpr (BORD) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) colofs[s] = ((2 * t + s) * RSC + ((4 * (T8 - 1)) ^ (2 * t ^ (s << 2)))) * 16;
     rowofs = (8 * (T8 - 1) * RSC + gh) * 16 + 8 * gl;
-#pragma unroll
-    for (int j1 = 0; j1 < 2; ++j1) aofs[j1] = (g * RSC + ((j1 * 4 + t) ^ fg)) * 16;
   }
 
   Stg sg(in, out, batch, smem);
@@ -849,12 +771,10 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
               }
               p[I][K][cc] = (cc < BR && t == 0) ? acc[I][K][cc] + v : 0.0;
             }
-          // row border P[8K+g'][8J+2t+s] (g' < BR), column tiles J < K, by the
-          // warp owning row tile K: lane (g,t) sums the k = 8I+g terms (from its
-          // accumulators when it holds the whole matrix, else from the published
-          // M — the same values in the same order), then the 8 lanes of a
-          // column add up
-          constexpr int WK = K / RT, IK = K % RT;
+          // row border P[8K+g'][8J+2t+s] (g' < BR), column tiles J < K: lane
+          // (g,t) sums the k = 8I+g terms from its accumulators, then the 8
+          // lanes of a column add up
+          constexpr int IK = K;              // (whole matrix per warp: RT = T8)
           auto finish_row = [&](int J, int s, const double (&rsv)[BR]) {
             double mine = 0.0;
 #pragma unroll
@@ -867,7 +787,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
             }
             p[IK][J][s] = (g < BR) ? acc[IK][J][s] + mine : 0.0;
           };
-          if constexpr (W == 1) {            // I outer: each border-row value loaded once
+          {                                  // I outer: each border-row value loaded once
             double rs[BR][K > 0 ? K : 1][2];
 #pragma unroll
             for (int q = 0; q < BR; ++q)
@@ -895,32 +815,6 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
                 for (int q = 0; q < BR; ++q) rsv[q] = rs[q][J][s];
                 finish_row(J, s, rsv);
               }
-          } else if (wr == WK) {             // J outer: few live registers next to the tiles
-#pragma unroll 1
-            for (int J = 0; J < K; ++J) {
-              double r0[BR], r1[BR];
-#pragma unroll
-              for (int q = 0; q < BR; ++q) r0[q] = r1[q] = 0.0;
-              const char *col = sb + aofs[J & 1] + 8 * (J >> 1) * 16;
-#pragma unroll
-              for (int I = 0; I < T8; ++I) {
-                const double2 v = *reinterpret_cast<const double2 *>(col + 8 * I * RSC * 16);
-#pragma unroll
-                for (int q = 0; q < BR; ++q) {
-                  const double mr =
-                      *reinterpret_cast<const double *>(sb + rowofs + (q * RSC + 4 * (I ^ (q & 1))) * 16);
-                  r0[q] = fmaT(mr, v.x, r0[q]);
-                  r1[q] = fmaT(mr, v.y, r1[q]);
-                }
-              }
-              // (J is a runtime loop index here: select the tile by unrolled compare)
-#pragma unroll
-              for (int J2 = 0; J2 < K; ++J2)
-                if (J2 == J) {
-                  finish_row(J2, 0, r0);
-                  finish_row(J2, 1, r1);
-                }
-            }
           }
         }
 #pragma unroll
@@ -1160,253 +1054,303 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
 }
 
 // ======================================================================
-// F64P: FP64 row panels (9 <= N <= 12), the DFMA counterpart of F32P for the
-// sizes where DMMA's 8x8x4 granularity wastes most of the pipe (n = 9 pads to
-// 16: 24 % useful).  G = 4 threads per matrix, RP = 3 full rows each (A operand
-// local), row k of M broadcast from a double-buffered, chunk-swizzled shared
-// copy (16-B chunk = 2 doubles); accumulators in column groups of 2 chunks.
+// F32T (r02; 17 <= n <= 64): FP32 register-tiled outer products with FFMA2,
+// sized for occupancy (jm_plan.h F32T).  The RG x CG threads of a matrix each
+// own an RA x CB block of P = M + M*M (rows i*RG + tr, 16-B column chunks
+// f32t_chunk(h, tc)); accumulators start at M, so P is the only state.  Per
+// update: publish M (row stride LDM) over the matrix's region, sync, then for
+// every k: P[i][:] += M[i][k] * M[k][:] with the A operand from a per-row
+// LDS.128 of M[i][kb..kb+3] (reloaded right after its last use at kk = 3) and
+// the B operand, row k, loaded one k ahead; k steps in [N, rup(N, 4)) are not
+// computed (their A values are zero padding).  Epilogue M' = A + c*P in FFMA2
+// pairs.  Matrices of <= 32 threads share a warp (__syncwarp); 64-thread
+// matrices sync their two warps with a named barrier.
 // ======================================================================
-template <int N, Addend A>
-__device__ __forceinline__ void run_f64p(const double *__restrict__ in, double *__restrict__ out,
-                                         long long batch, int repeat) {
-  constexpr int RP = f64p_rp(N), G = F64P_G, MPW = 32 / F64P_G, NCR = f64p_ncr(N);
-  constexpr int NCS = f64p_ncs(N), GROUPS = f64p_groups(N), MBUF = f64p_mbuf(N);
-  constexpr int NC = 2 * NCR;                          // computed columns (16-B padded)
-  constexpr int QH = cdiv(NCR, GROUPS);                // chunks per column group
-  constexpr int ES = 8, MB = N * N * 8, SB = stage_stride(N, 8);
-  constexpr int NT = 32 * F64P_WPC, MPC = F64P_WPC * MPW;
-  constexpr bool AL = ((MPC * MB) % 16) == 0;
-  static_assert(G * RP >= N, "row panels must cover the matrix");
-  extern __shared__ __align__(16) char smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int mw = lane / G, tg = lane - mw * G;
-  const int mi = warp * MPW + mw;
-  const int r0 = tg * RP;
-  char *bufs = smem + stage_bytes(MPC, N, 8) + mi * 2 * MBUF;
-  const double c = 0.00005;
+__device__ __forceinline__ void bar_named(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// 32-bit shared-window addresses throughout: NVRTC otherwise keeps the
+// work-area pointers as 64-bit generic addresses (r02: 166 vs 132 registers
+// for the same n = 32 kernel built by nvcc, which infers the shared space)
+__device__ __forceinline__ float4 lds128(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(unsigned a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
 
-  Stager<N, ES, SB, NT, MPC, AL, false> sg(in, out, batch, smem);
+template <int N, Addend A, bool STRM>
+__device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__restrict__ out,
+                                         long long batch, int repeat) {
+  constexpr F32T TL = f32t_tile(N);
+  constexpr int RA = TL.ra, CB = TL.cb, RG = TL.rg, CG = TL.cg, NH = CB / 4, LDM = TL.ldm;
+  constexpr int TPMAT = RG * CG, WPM = f32t_wpm(N), MPW = f32t_mpw(N), WPC = f32t_wpc(N);
+  constexpr int MPC = f32t_mpc(N), NR = f32t_nr(N), NC = CG * CB, SROWS = f32t_srows(N);
+  constexpr int REG = f32t_region(N), ES = 4, MB = N * N * 4, NT = 32 * WPC;
+  constexpr bool AL = ((MPC * MB) % 16) == 0;
+  constexpr bool PAD = (NR != N) || (NC != N);
+  static_assert(CB % 4 == 0 && NC >= f32t_kp(N), "tile shape");
+  static_assert(WPC % WPM == 0, "whole matrices per CTA");
+  extern __shared__ __align__(16) char smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // matrix slot in the chunk (mi) and thread index within the matrix (t)
+  // (qmix: the two matrices of a warp alternate by quarter-warp, so the two
+  // quarters of a half-warp always read different matrices: disjoint
+  // addresses, one wavefront per half for both the A and the B loads)
+  const int m = WPM == 1 ? (TL.qmix ? (lane >> 3) & 1 : lane / TPMAT) : 0;
+  const int t = WPM == 1 ? (TL.qmix ? ((lane >> 4) << 3) + (lane & 7) : lane - m * TPMAT) : (warp % WPM) * 32 + lane;
+  const int mi = WPM == 1 ? warp * MPW + m : warp / WPM;
+  // lanes past the last whole matrix of a warp, or past RG*CG in a multi-warp
+  // matrix, idle (but take part in the syncs)
+  const bool lane_ok = WPM > 1 ? t < TPMAT : (m < MPW && t < TPMAT);
+  const int tr = TL.trfast ? t % RG : t / CG, tc = TL.trfast ? t / RG : t % CG;
+  const float c = float(0.00005);
+  auto sync = [&]() {
+    if constexpr (WPM == 1) __syncwarp();
+    else if constexpr (WPM == WPC) __syncthreads();
+    else bar_named(1 + mi, 32 * WPM);
+  };
+  auto row_of = [&](int i) { return i * RG + tr; };
+  auto chunk_of = [&](int h) { return TL.colblk ? tc * NH + h : h * CG + tc; };
+  // STRM (the low-repeat variant): the same kernel with the double-buffered
+  // cp.async stage (the next chunk streams in while this one is updated)
+  Stager<N, ES, REG, NT, MPC, AL, STRM> sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
-    char *stage = sg.buf();
-    const int cnt = sg.cnt();
-    const bool live = mi < cnt;      // all lanes run the loop; dead slots are never stored
-    double *sm = reinterpret_cast<double *>(stage + mi * SB);
-    double m[RP][NC];
+    const bool live = lane_ok && mi < sg.cnt();
+    float *sm = reinterpret_cast<float *>(sg.buf() + (lane_ok ? mi : 0) * REG);
+    const unsigned sbase = smem_u32(sm);
+    float2 p[RA][CB / 2];
+    // own block of the staged matrix (packed, row stride N)
 #pragma unroll
-    for (int i = 0; i < RP; ++i)
+    for (int i = 0; i < RA; ++i)
 #pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        const int row = r0 + i;
-        m[i][j] = (live && row < N && j < N) ? sm[row * N + j] : 0.0;
-      }
+      for (int h = 0; h < NH; ++h)
 #pragma unroll
-    for (int i = 0; i < RP; ++i)
-      if (r0 + i < N) {
-#pragma unroll
-        for (int q = 0; q < NCR; ++q)
-          sts_f64x2(bufs + f32p_off<NCS>(r0 + i, q), m[i][2 * q], m[i][2 * q + 1]);
-      }
-    __syncwarp();
-#pragma unroll 1
-    for (int r = 0; r < repeat; ++r) {
-      const char *cur = bufs + (r & 1) * MBUF;
-      char *nxt = bufs + ((r & 1) ^ 1) * MBUF;
-#pragma unroll
-      for (int h = 0; h < GROUPS; ++h) {
-        const int qlo = h * QH;
-        const int qn = (NCR - qlo) < QH ? (NCR - qlo) : QH;
-        double p[RP][2 * QH];
-#pragma unroll
-        for (int i = 0; i < RP; ++i)
-#pragma unroll
-          for (int j = 0; j < 2 * QH; ++j)
-            if (j < 2 * qn) p[i][j] = m[i][2 * qlo + j];
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double b[2 * QH];
-#pragma unroll
-          for (int q = 0; q < QH; ++q)
-            if (q < qn) {
-              const double2 v = *reinterpret_cast<const double2 *>(cur + f32p_off<NCS>(k, qlo + q));
-              b[2 * q] = v.x; b[2 * q + 1] = v.y;
-            }
-#pragma unroll
-          for (int i = 0; i < RP; ++i)
-#pragma unroll
-            for (int j = 0; j < 2 * QH; ++j)
-              if (j < 2 * qn) p[i][j] = fmaT(m[i][k], b[j], p[i][j]);
+        for (int e = 0; e < 4; e += 2) {
+          const int row = row_of(i), c0 = chunk_of(h) * 4 + e;
+          p[i][2 * h + e / 2].x = (live && row < N && c0 < N) ? sm[row * N + c0] : 0.0f;
+          p[i][2 * h + e / 2].y = (live && row < N && c0 + 1 < N) ? sm[row * N + c0 + 1] : 0.0f;
         }
-#pragma unroll
-        for (int i = 0; i < RP; ++i) {
-          const int row = r0 + i;
-#pragma unroll
-          for (int q = 0; q < QH; ++q)
-            if (q < qn) {
-              double v[2];
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int col = 2 * (qlo + q) + e;
-                const double a = (A == Addend::Ones || col == row) ? 1.0 : 0.0;
-                v[e] = (row < N && col < N) ? fmaT(c, p[i][2 * q + e], a) : 0.0;
-              }
-              if (row < N) sts_f64x2(nxt + f32p_off<NCS>(row, qlo + q), v[0], v[1]);
-            }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < RP; ++i)   // own rows back from the next buffer (written by this thread)
-        if (r0 + i < N) {
-#pragma unroll
-          for (int q = 0; q < NCR; ++q) {
-            const double2 v = *reinterpret_cast<const double2 *>(nxt + f32p_off<NCS>(r0 + i, q));
-            m[i][2 * q] = v.x; m[i][2 * q + 1] = v.y;
-          }
-        }
-      __syncwarp();
+    sync();                            // staged matrix read: the region becomes the work area
+    if constexpr (SROWS > NR) {        // rows read as k padding (k in [NR, KP)) are zero
+      if (live)
+        for (int e = t; e < (SROWS - NR) * LDM; e += TPMAT) sm[NR * LDM + e] = 0.0f;
     }
-    if (live) {
+    for (int r = 0; r < repeat; ++r) {
+      if (live) {                      // publish M
 #pragma unroll
-      for (int i = 0; i < RP; ++i)
+        for (int i = 0; i < RA; ++i)
 #pragma unroll
-        for (int j = 0; j < NC; ++j) {
-          const int row = r0 + i;
-          if (row < N && j < N) sm[row * N + j] = m[i][j];
+          for (int h = 0; h < NH; ++h)
+            sts128(sbase + (row_of(i) * LDM + chunk_of(h) * 4) * 4, p[i][2 * h].x, p[i][2 * h].y,
+                   p[i][2 * h + 1].x, p[i][2 * h + 1].y);
+      }
+      sync();
+      if (live) {
+        const unsigned bcol = sbase + chunk_of(0) * 16;   // B: row k at bcol + k*LDM*4
+        float4 bq[NH], bn[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) bq[h] = lds128(bcol + (chunk_of(h) - chunk_of(0)) * 16);
+        // A: row i*RG + tr at arow + i*RG*LDM*4, four k values per LDS.128,
+        // each row's block reloaded right after its last use
+        const unsigned arow = sbase + tr * LDM * 4;
+        float4 av[RA];
+#pragma unroll
+        for (int i = 0; i < RA; ++i) av[i] = lds128(arow + i * RG * LDM * 4);
+        // full blocks of four k steps (rolled above n ~ 48: the fully
+        // unrolled update overflows the instruction cache), then N % 4
+        constexpr int KF = N / 4, KT = N % 4;
+        auto kstep = [&](int k, int kk, bool more, bool reload_a) {
+          if (more) {
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+              bn[h] = lds128(bcol + (k + 1) * LDM * 4 + (chunk_of(h) - chunk_of(0)) * 16);
+          }
+#pragma unroll
+          for (int i = 0; i < RA; ++i) {
+            const float a = kk == 0 ? av[i].x : kk == 1 ? av[i].y : kk == 2 ? av[i].z : av[i].w;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+              p[i][2 * h] = __ffma2_rn(make_float2(a, a), make_float2(bq[h].x, bq[h].y), p[i][2 * h]);
+              p[i][2 * h + 1] = __ffma2_rn(make_float2(a, a), make_float2(bq[h].z, bq[h].w), p[i][2 * h + 1]);
+            }
+            if (reload_a) av[i] = lds128(arow + i * RG * LDM * 4 + (k + 1) * 4);
+          }
+#pragma unroll
+          for (int h = 0; h < NH; ++h) bq[h] = bn[h];
+        };
+        constexpr int KU = f32t_kunroll(N);
+#pragma unroll KU
+        for (int kb = 0; kb < KF; ++kb) {
+          const bool last = kb == KF - 1;
+          kstep(4 * kb + 0, 0, true, false);
+          kstep(4 * kb + 1, 1, true, false);
+          kstep(4 * kb + 2, 2, true, false);
+          kstep(4 * kb + 3, 3, !last || KT > 0, !last || KT > 0);
         }
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk) kstep(4 * KF + kk, kk, kk + 1 < KT, false);
+      }
+      sync();                          // every read of this update's M done before the next publish
+      if (live) {
+        const float2 c2 = make_float2(c, c);
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+#pragma unroll
+          for (int j = 0; j < CB / 2; ++j) {
+            const int row = row_of(i), c0 = chunk_of(j / 2) * 4 + 2 * (j & 1);
+            float2 a2 = make_float2(1.0f, 1.0f);
+            if constexpr (A == Addend::Identity) a2 = make_float2(row == c0 ? 1.0f : 0.0f, row == c0 + 1 ? 1.0f : 0.0f);
+            float2 q = __ffma2_rn(c2, p[i][j], a2);
+            if constexpr (PAD) {         // padding stays exactly zero
+              if (row >= N || c0 >= N) q.x = 0.0f;
+              if (row >= N || c0 + 1 >= N) q.y = 0.0f;
+            }
+            p[i][j] = q;
+          }
+      }
+    }
+    if (live) {                        // back to the packed layout for the store
+#pragma unroll
+      for (int i = 0; i < RA; ++i)
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+#pragma unroll
+          for (int e = 0; e < 4; e += 2) {
+            const int row = row_of(i), c0 = chunk_of(h) * 4 + e;
+            if (row < N && c0 < N) sm[row * N + c0] = p[i][2 * h + e / 2].x;
+            if (row < N && c0 + 1 < N) sm[row * N + c0 + 1] = p[i][2 * h + e / 2].y;
+          }
     }
     sg.release();
   }
+  sg.finish();
 }
 
 // ======================================================================
-// F32 (17 <= n <= 64): FP32 register-tiled outer products with FFMA2.  The
-// RG x CG threads of a matrix each own an RA x CB block of P = M + M*M in
-// registers (the accumulators start at M, so P is the only state); thread
-// (tr, tc) owns rows i*RG + tr and columns in 16-B pieces (h*CG + tc)*4.
-// Every update republishes M row-major into the matrix's shared-memory region
-// (the region the chunk was staged into); then per block of four k steps a
-// thread loads M[row][k..k+3] for its RA rows (one LDS.128 each) and, one k
-// ahead of the math, row k's CB/4 pieces, and issues RA*CB/2 FFMA2 per k.
-// Steps k in [N, rup(N,4)) read zero padding (exact no-ops).  A warp holds
-// 32 / (RG*CG) whole matrices, so only __syncwarp is needed.
+// F64T (r02): FP64 register tiles with DFMA, for the sizes where DMMA's
+// 8 x 8 x 4 granularity wastes most of the FP64 pipe (jm_plan.h F64T_TABLE).
+// The same scheme as run_f32t with a 16-B chunk holding two doubles: thread
+// (tr, tc) owns an RA x CB block of P; per k, A = M[i][k] from a per-row
+// LDS.128 of M[i][2kb..2kb+1] (reloaded after its last use at kk = 1) and B =
+// row k one k ahead; DFMA and DMMA share the FP64 pipe (64 FMA/clk/SM), so
+// padding only to multiples of the register tile (not of 8) is the gain.
 // ======================================================================
+__device__ __forceinline__ double2 lds128d(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128d(unsigned a, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1,%2};" ::"r"(a), "d"(x), "d"(y) : "memory");
+}
+
 template <int N, Addend A, bool STRM>
-__device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__restrict__ out,
-                                        long long batch, int repeat) {
-  constexpr int RG = f32_rg(N), RA = f32_ra(N), CG = f32_cg(N), CB = f32_cb(N);
-  constexpr int TPMAT = RG * CG, MPW = f32_mpw(N);
-  constexpr int ROWS = f32_rows(N), COLS = f32_cols(N), KP = f32_kp(N), SROWS = f32_srows(N);
-  constexpr int LDM = f32_ldm(N), REG = f32_region(N);
-  constexpr int ES = 4, MB = N * N * 4;
-  constexpr int NT = 32 * F32_WPC, MPC = F32_WPC * MPW;
+__device__ __forceinline__ void run_f64t(const double *__restrict__ in, double *__restrict__ out,
+                                         long long batch, int repeat) {
+  constexpr F32T TL = f32t_tile(N, 1);
+  constexpr int RA = TL.ra, CB = TL.cb, RG = TL.rg, CG = TL.cg, NH = CB / 2, LDM = TL.ldm;
+  constexpr int TPMAT = RG * CG, WPM = f32t_wpm(N, 1), MPW = f32t_mpw(N, 1), WPC = f32t_wpc(N, 1);
+  constexpr int MPC = f32t_mpc(N, 1), NR = f32t_nr(N, 1), NC = CG * CB, SROWS = f32t_srows(N, 1);
+  constexpr int REG = f32t_region(N, 1), ES = 8, MB = N * N * 8, NT = 32 * WPC;
   constexpr bool AL = ((MPC * MB) % 16) == 0;
-  constexpr bool PAD = (ROWS != N) || (COLS != N);
-  static_assert(CB % 4 == 0 && MPW >= 1, "tile shape");
+  constexpr bool PAD = (NR != N) || (NC != N);
+  static_assert(CB % 2 == 0 && NC >= f32t_kp(N, 1), "tile shape");
+  static_assert(WPC % WPM == 0, "whole matrices per CTA");
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int m = lane / TPMAT, t = lane - m * TPMAT;
-  const int tr = t % RG, tc = t / RG;
-  const int mi = warp * MPW + m;
-  const float c = float(0.00005);
+  const int m = WPM == 1 ? (TL.qmix ? (lane >> 3) & 1 : lane / TPMAT) : 0;
+  const int t = WPM == 1 ? (TL.qmix ? ((lane >> 4) << 3) + (lane & 7) : lane - m * TPMAT) : (warp % WPM) * 32 + lane;
+  const int mi = WPM == 1 ? warp * MPW + m : warp / WPM;
+  const bool lane_ok = WPM > 1 ? t < TPMAT : (m < MPW && t < TPMAT);
+  const int tr = TL.trfast ? t % RG : t / CG, tc = TL.trfast ? t / RG : t % CG;
+  const double c = 0.00005;
+  auto sync = [&]() {
+    if constexpr (WPM == 1) __syncwarp();
+    else if constexpr (WPM == WPC) __syncthreads();
+    else bar_named(1 + mi, 32 * WPM);
+  };
   auto row_of = [&](int i) { return i * RG + tr; };
-  // 16-B column chunk h of thread column tc: blocked (tc * CB/4 + h) or
-  // interleaved (h * CG + tc), per n (f32_col_blocked).  Blocked puts the
-  // thread columns of a quarter-warp CB/4 chunks apart, so the publish
-  // STS.128 of rows tr (LDM/4 odd chunks apart) hit distinct 16-B bank slots
-  // (interleaved: 2-way conflict at n = 32, ncu r01)
-  auto chunk_of = [&](int h) { return f32_col_blocked(N) ? tc * (CB / 4) + h : h * CG + tc; };
-  auto col_of = [&](int j) { return chunk_of(j >> 2) * 4 + (j & 3); };
-
-  // resident: the staged matrix's region doubles as its work area (sM);
-  // streaming: the same in REG-sized ring slots when each matrix is its own
-  // copy (f32_ring_slot), else work areas of REG bytes after the ring
-  // (f32_stream_pf: the low-repeat variant is instead the resident layout
-  // with the double-buffered cp.async stage — two REG regions per matrix
-  // rather than two ring slots plus a work area)
-  constexpr bool SPF = STRM && f32_stream_pf(N);
-  constexpr int SLOT = SPF ? 0 : f32_ring_slot(N);
-  typedef typename Pick<STRM && !SPF, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, SLOT>,
-                        Stager<N, ES, REG, NT, MPC, AL, SPF>>::type Stg;
-  Stg sg(in, out, batch, smem);
+  auto chunk_of = [&](int h) { return TL.colblk ? tc * NH + h : h * CG + tc; };
+  Stager<N, ES, REG, NT, MPC, AL, STRM> sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
-    const bool live = (m < MPW) && (mi < sg.cnt());
-    float *src = reinterpret_cast<float *>(sg.buf() + (m < MPW ? mi : 0) * Stg::SBM);
-    float *sm = (STRM && !SPF && !SLOT) ? reinterpret_cast<float *>(smem + Stg::BYTES + (m < MPW ? mi : 0) * REG)
-                                        : src;
-    float2 p[RA][CB / 2];
-    if (live) {
+    const bool live = lane_ok && mi < sg.cnt();
+    double *sm = reinterpret_cast<double *>(sg.buf() + (lane_ok ? mi : 0) * REG);
+    const unsigned sbase = smem_u32(sm);
+    double p[RA][CB];
 #pragma unroll
-      for (int i = 0; i < RA; ++i)
+    for (int i = 0; i < RA; ++i)
 #pragma unroll
-        for (int j = 0; j < CB; j += 2) {
-          const int row = row_of(i), c0 = col_of(j), c1 = c0 + 1;
-          p[i][j / 2].x = (row < N && c0 < N) ? src[row * N + c0] : 0.0f;
-          p[i][j / 2].y = (row < N && c1 < N) ? src[row * N + c1] : 0.0f;
-        }
-    }
-    __syncwarp();                        // staged matrix in registers: reuse the region as sM
-    if constexpr (SROWS > ROWS) {        // rows read as padding by k in [ROWS, KP): zero once
+      for (int j = 0; j < CB; ++j) {
+        const int row = row_of(i), col = chunk_of(j / 2) * 2 + (j & 1);
+        p[i][j] = (live && row < N && col < N) ? sm[row * N + col] : 0.0;
+      }
+    sync();
+    if constexpr (SROWS > NR) {
       if (live)
-        for (int e = t; e < (SROWS - ROWS) * LDM; e += TPMAT) sm[ROWS * LDM + e] = 0.0f;
+        for (int e = t; e < (SROWS - NR) * LDM; e += TPMAT) sm[NR * LDM + e] = 0.0;
     }
     for (int r = 0; r < repeat; ++r) {
       if (live) {
 #pragma unroll
         for (int i = 0; i < RA; ++i)
 #pragma unroll
-          for (int h = 0; h < CB / 4; ++h)
-            *reinterpret_cast<float4 *>(sm + row_of(i) * LDM + chunk_of(h) * 4) =
-                make_float4(p[i][2 * h].x, p[i][2 * h].y, p[i][2 * h + 1].x, p[i][2 * h + 1].y);
+          for (int h = 0; h < NH; ++h) sts128d(sbase + (row_of(i) * LDM + chunk_of(h) * 2) * 8, p[i][2 * h], p[i][2 * h + 1]);
       }
-      __syncwarp();
+      sync();
       if (live) {
-        float b[CB], bn[CB];
-        auto load_b = [&](float (&dst)[CB], int k) {
+        const unsigned bcol = sbase + chunk_of(0) * 16;
+        double2 bq[NH], bn[NH];
 #pragma unroll
-          for (int h = 0; h < CB / 4; ++h) {
-            const float4 v = *reinterpret_cast<const float4 *>(sm + k * LDM + chunk_of(h) * 4);
-            dst[4 * h] = v.x; dst[4 * h + 1] = v.y; dst[4 * h + 2] = v.z; dst[4 * h + 3] = v.w;
+        for (int h = 0; h < NH; ++h) bq[h] = lds128d(bcol + (chunk_of(h) - chunk_of(0)) * 16);
+        const unsigned arow = sbase + tr * LDM * 8;
+        double2 av[RA];
+#pragma unroll
+        for (int i = 0; i < RA; ++i) av[i] = lds128d(arow + i * RG * LDM * 8);
+        constexpr int KF = N / 2, KT = N % 2;
+        auto kstep = [&](int k, int kk, bool more, bool reload_a) {
+          if (more) {
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+              bn[h] = lds128d(bcol + (k + 1) * LDM * 8 + (chunk_of(h) - chunk_of(0)) * 16);
           }
-        };
-        load_b(b, 0);
-#pragma unroll 1
-        for (int kb = 0; kb < KP; kb += 4) {
-          float4 av[RA];
 #pragma unroll
-          for (int i = 0; i < RA; ++i) av[i] = *reinterpret_cast<const float4 *>(sm + row_of(i) * LDM + kb);
+          for (int i = 0; i < RA; ++i) {
+            const double a = kk == 0 ? av[i].x : av[i].y;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const int kn = kb + kk + 1 < KP ? kb + kk + 1 : kb + kk;
-            load_b(bn, kn);              // next step's B row ahead of this step's math
-#pragma unroll
-            for (int i = 0; i < RA; ++i) {
-              const float a = kk == 0 ? av[i].x : kk == 1 ? av[i].y : kk == 2 ? av[i].z : av[i].w;
-#pragma unroll
-              for (int j = 0; j < CB / 2; ++j)
-                p[i][j] = __ffma2_rn(make_float2(a, a), make_float2(b[2 * j], b[2 * j + 1]), p[i][j]);
+            for (int h = 0; h < NH; ++h) {
+              p[i][2 * h] = fmaT(a, bq[h].x, p[i][2 * h]);
+              p[i][2 * h + 1] = fmaT(a, bq[h].y, p[i][2 * h + 1]);
             }
-#pragma unroll
-            for (int j = 0; j < CB; ++j) b[j] = bn[j];
+            if (reload_a) av[i] = lds128d(arow + i * RG * LDM * 8 + (k + 1) * 8);
           }
+#pragma unroll
+          for (int h = 0; h < NH; ++h) bq[h] = bn[h];
+        };
+        constexpr int KU = f32t_kunroll(N, 1);
+#pragma unroll KU
+        for (int kb = 0; kb < KF; ++kb) {
+          const bool last = kb == KF - 1;
+          kstep(2 * kb + 0, 0, true, false);
+          kstep(2 * kb + 1, 1, !last || KT > 0, !last || KT > 0);
         }
+        if constexpr (KT > 0) kstep(2 * KF, 0, false, false);
       }
-      __syncwarp();                      // all reads of this update done before the next publish
+      sync();
       if (live) {
 #pragma unroll
         for (int i = 0; i < RA; ++i)
 #pragma unroll
-          for (int j = 0; j < CB; j += 2) {
-            const int row = row_of(i), c0 = col_of(j), c1 = c0 + 1;
-            float2 &q = p[i][j / 2];
-            const float a0 = (A == Addend::Ones || row == c0) ? 1.0f : 0.0f;
-            const float a1 = (A == Addend::Ones || row == c1) ? 1.0f : 0.0f;
-            q.x = fmaT(c, q.x, a0);
-            q.y = fmaT(c, q.y, a1);
-            if constexpr (PAD) {         // padding stays exactly zero
-              if (row >= N || c0 >= N) q.x = 0.0f;
-              if (row >= N || c1 >= N) q.y = 0.0f;
-            }
+          for (int j = 0; j < CB; ++j) {
+            const int row = row_of(i), col = chunk_of(j / 2) * 2 + (j & 1);
+            const double a = (A == Addend::Ones || row == col) ? 1.0 : 0.0;
+            double v = fmaT(c, p[i][j], a);
+            if constexpr (PAD) v = (row < N && col < N) ? v : 0.0;
+            p[i][j] = v;
           }
       }
     }
@@ -1414,10 +1358,9 @@ __device__ __forceinline__ void run_f32(const float *__restrict__ in, float *__r
 #pragma unroll
       for (int i = 0; i < RA; ++i)
 #pragma unroll
-        for (int j = 0; j < CB; j += 2) {
-          const int row = row_of(i), c0 = col_of(j), c1 = c0 + 1;
-          if (row < N && c0 < N) src[row * N + c0] = p[i][j / 2].x;
-          if (row < N && c1 < N) src[row * N + c1] = p[i][j / 2].y;
+        for (int j = 0; j < CB; ++j) {
+          const int row = row_of(i), col = chunk_of(j / 2) * 2 + (j & 1);
+          if (row < N && col < N) sm[row * N + col] = p[i][j];
         }
     }
     sg.release();
@@ -1442,17 +1385,14 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
   } else if constexpr (K == Tile::Tpms) {
     if constexpr (STRM) run_dmma<N, A, 1, true>(in, out, batch, repeat);   // low repeat: the DMMA ring
     else run_tpms<N, T, A>(in, out, batch, repeat);
-  } else if constexpr (K == Tile::Tpm2) {
-    if constexpr (STRM) run_dmma<N, A, 1, false>(in, out, batch, repeat);   // its low-repeat kernel
-    else run_tpm2<N, A>(in, out, batch, repeat);
-  } else if constexpr (K == Tile::Rows) {
-    run_f64p<N, A>(in, out, batch, repeat);
+  } else if constexpr (K == Tile::Reg) {
+    run_f64t<N, A, STRM>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Dmma) {
     run_dmma<N, A, dmma_w(N, STRM), STRM>(in, out, batch, repeat);
   } else if constexpr (f32p_use(N)) {
     run_f32p<N, A, STRM>(in, out, batch, repeat);
   } else {
-    run_f32<N, A, STRM>(in, out, batch, repeat);
+    run_f32t<N, A, STRM>(in, out, batch, repeat);
   }
 }
 
@@ -1469,6 +1409,20 @@ template <int N, class T, Addend A, Tile K>
 __global__ void __launch_bounds__(plan_specialized(N, sizeof(T) == 8 ? 1 : 0).threads, 1)
     k_update_mb1(const T *__restrict__ in, T *__restrict__ out, long long batch, int repeat) {
   update_body<N, T, A, K>(in, out, batch, repeat);
+}
+
+// Same body under a register cap instead of launch bounds (CUDA forbids both
+// on one kernel): the F32T tiles (jm_plan.h f32t_maxreg).
+template <int N, class T, Addend A, Tile K>
+__global__ void __maxnreg__(f32t_maxreg(N, sizeof(T) == 8)) k_update_rc(const T *__restrict__ in, T *__restrict__ out,
+                                                        long long batch, int repeat) {
+  update_body<N, T, A, K>(in, out, batch, repeat);
+}
+
+template <int N, class T, Addend A, Tile K>
+__global__ void __maxnreg__(f32t_maxreg(N, sizeof(T) == 8)) k_update_stream_rc(const T *__restrict__ in, T *__restrict__ out,
+                                                               long long batch, int repeat) {
+  update_body<N, T, A, K, true>(in, out, batch, repeat);
 }
 
 // The streaming (low-repeat) variant: same kinds behind the bulk-copy ring

@@ -214,6 +214,7 @@ struct State {
 State G;
 
 std::atomic<long long> c_compilations{0}, c_hits{0}, c_misses{0}, c_launches{0}, c_imports{0};
+std::atomic<long long> c_programs{0};   // NVRTC programs of the batched compile (JM_FLAG_BATCH_COMPILE)
 std::atomic<long long> c_compile_us{0};
 
 bool env_flag(const char *name) {
@@ -236,6 +237,7 @@ const char *tile_name(int t) {
     case jm::Tile::Tpms: return "Tpms";
     case jm::Tile::F32: return "F32";
     case jm::Tile::Rows: return "Rows";
+    case jm::Tile::Reg: return "Reg";
     default: return "Generic";
   }
 }
@@ -243,7 +245,8 @@ const char *tile_name(int t) {
 std::string name_expression(int n, int dtype, int addend, bool stream = false) {
   char buf[160];
   snprintf(buf, sizeof buf, "jm::%s%s<%d, %s, jm::Addend::%s, jm::Tile::%s>",
-           stream ? "k_update_stream" : "k_update", jm::use_mb1(n, dtype, stream) ? "_mb1" : "", n,
+           stream ? "k_update_stream" : "k_update",
+           jm::use_mb1(n, dtype, stream) ? "_mb1" : jm::use_rc(n, dtype, stream) ? "_rc" : "", n,
            dtype == JM_F64 ? "double" : "float", addend == JM_ADDEND_ONES ? "Ones" : "Identity",
            tile_name((int)jm::tile_for(n, dtype)));
   return buf;
@@ -255,10 +258,14 @@ std::string mm_name_expression(int n, int dtype) {
   return buf;
 }
 
-// NVRTC: instantiate one name expression of the embedded template source ->
-// sm_100a cubin (+ the lowered, i.e. mangled, symbol).
-int nvrtc_compile_expr(const std::string &expr, std::vector<char> &cubin, std::string &lowered,
-                       std::string &log) {
+// NVRTC: instantiate name expressions of the embedded template source in ONE
+// program -> one sm_100a cubin holding every instantiation (+ the lowered,
+// i.e. mangled, symbol of each).  One expression per call is the per-key
+// miss path; several are the batched compile of jit_mat_run_many (the
+// template source is parsed once for all of them — the paper's "maximal,
+// incremental reuse of the state of the compiler").
+int nvrtc_compile_exprs(const std::vector<std::string> &exprs, std::vector<char> &cubin,
+                        std::vector<std::string> &lowered, std::string &log) {
   const std::string src((const char *)jm_embedded_kernel_src, (size_t)jm_embedded_kernel_src_len);
   nvrtcProgram prog;
   nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "jm_update.cu", 0, nullptr, nullptr);
@@ -266,7 +273,7 @@ int nvrtc_compile_expr(const std::string &expr, std::vector<char> &cubin, std::s
     log = nvrtcGetErrorString(r);
     return JM_E_COMPILE;
   }
-  nvrtcAddNameExpression(prog, expr.c_str());
+  for (const std::string &e : exprs) nvrtcAddNameExpression(prog, e.c_str());
   const char *opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=true", "-lineinfo",
                         "--ftz=false", "--prec-div=true", "--prec-sqrt=true"};
   r = nvrtcCompileProgram(prog, (int)(sizeof opts / sizeof opts[0]), opts);
@@ -277,19 +284,38 @@ int nvrtc_compile_expr(const std::string &expr, std::vector<char> &cubin, std::s
     nvrtcGetProgramLog(prog, &log[0]);
   }
   if (r != NVRTC_SUCCESS) {
-    log = std::string("NVRTC failed for ") + expr + ": " + nvrtcGetErrorString(r) + "\n" + log;
+    log = std::string("NVRTC failed for ") + exprs[0] + (exprs.size() > 1 ? " (+ others)" : "") + ": " +
+          nvrtcGetErrorString(r) + "\n" + log;
     nvrtcDestroyProgram(&prog);
     return JM_E_COMPILE;
   }
-  const char *low = nullptr;
-  nvrtcGetLoweredName(prog, expr.c_str(), &low);
-  lowered = low ? low : "";
+  lowered.clear();
+  for (const std::string &e : exprs) {
+    const char *low = nullptr;
+    nvrtcGetLoweredName(prog, e.c_str(), &low);
+    lowered.emplace_back(low ? low : "");
+  }
   size_t csz = 0;
   nvrtcGetCUBINSize(prog, &csz);
   cubin.resize(csz);
   nvrtcGetCUBIN(prog, cubin.data());
   nvrtcDestroyProgram(&prog);
+  if (const char *dir = getenv("JIT_MAT_DUMP_CUBIN")) {   // inspection hook: cuobjdump -sass the real cubin
+    std::string fn = std::string(dir) + "/" + lowered[0] + (exprs.size() > 1 ? ".multi" : "") + ".cubin";
+    if (FILE *f = fopen(fn.c_str(), "wb")) {
+      fwrite(cubin.data(), 1, cubin.size(), f);
+      fclose(f);
+    }
+  }
   return JM_OK;
+}
+
+int nvrtc_compile_expr(const std::string &expr, std::vector<char> &cubin, std::string &lowered,
+                       std::string &log) {
+  std::vector<std::string> low;
+  const int rc = nvrtc_compile_exprs({expr}, cubin, low, log);
+  if (rc == JM_OK) lowered = low[0];
+  return rc;
 }
 
 int finish_function(Slot &s, CUfunction fn) {
@@ -488,7 +514,7 @@ bool want_stream(int n, int dtype, int kind, int64_t repeat, unsigned flags = 0)
   }();
   if (force >= 0) return force > 0;
   const int64_t rn = repeat * (int64_t)(n + 1);
-  return rn < (int64_t)stream_rn(n, dtype) && rn >= (int64_t)jm::stream_lo(n, dtype) && jm::stream_fits(n, dtype);
+  return rn < (int64_t)stream_rn(n, dtype) && rn >= (int64_t)jm::stream_lo(n, dtype);
 }
 
 Slot &slot_of(int n, int dtype, int addend, int kind, bool stream) {
@@ -610,6 +636,89 @@ int run_impl(const jm_run_desc *d) {
   return sync_if(d->flags, st);
 }
 
+// Batched specialization (jit_mat_run_many with JM_FLAG_BATCH_COMPILE): the
+// distinct cold specialized keys of the descriptors are split into G groups
+// (G = JIT_MAT_COMPILE_GROUPS, default the hardware threads, at most the key
+// count), each group is ONE NVRTC program with one name expression per key,
+// and the groups compile on G host threads.  The resulting cubin (all of a
+// group's kernels) is then loaded into each key's slot under that slot's own
+// lock; a slot another thread made READY meanwhile is left alone, so there
+// is no lock ordering to get wrong (at worst a key is compiled twice).
+struct ColdKey {
+  int op, n, dtype, addend;
+  Slot *slot;
+};
+int batch_compile(const jm_run_desc *d, const std::vector<int> &todo) {
+  std::vector<ColdKey> keys;
+  for (int i : todo) {
+    const bool st = want_stream(d[i].n, d[i].dtype, d[i].kind, d[i].repeat, d[i].flags);
+    if (d[i].kind != JM_KIND_SPECIALIZED) continue;   // generic / AoT slots are seeded, never compiled
+    Slot *s = &slot_of(d[i].n, d[i].dtype, d[i].addend, d[i].kind, st);
+    bool dup = false;
+    for (const ColdKey &k : keys) dup |= (k.slot == s);
+    if (!dup) keys.push_back({st ? OP_UPDATE_STREAM : OP_UPDATE, d[i].n, d[i].dtype, d[i].addend, s});
+  }
+  if (keys.empty()) return JM_OK;
+  int groups = (int)std::thread::hardware_concurrency();
+  if (const char *e = getenv("JIT_MAT_COMPILE_GROUPS")) groups = atoi(e);
+  if (groups < 1) groups = 1;
+  if (groups > (int)keys.size()) groups = (int)keys.size();
+  // balance the groups by expected compile cost (larger n: bigger kernels)
+  std::vector<int> order(keys.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return keys[a].n > keys[b].n; });
+  std::vector<std::vector<int>> part((size_t)groups);
+  std::vector<long long> load((size_t)groups, 0);
+  for (int i : order) {
+    const size_t g = (size_t)(std::min_element(load.begin(), load.end()) - load.begin());
+    part[g].push_back(i);
+    load[g] += 64 + (long long)keys[(size_t)i].n * keys[(size_t)i].n;
+  }
+  std::vector<int> rcs((size_t)groups, JM_OK);
+  std::vector<std::string> errs((size_t)groups);
+  std::vector<std::thread> th;
+  for (int g = 0; g < groups; ++g)
+    th.emplace_back([&, g] {
+      NvtxRange nvtx("jm:compile");
+      const auto t0 = std::chrono::steady_clock::now();
+      std::vector<std::string> exprs, lowered;
+      for (int i : part[(size_t)g]) {
+        const ColdKey &k = keys[(size_t)i];
+        exprs.push_back(name_expression(k.n, k.dtype, k.addend, k.op == OP_UPDATE_STREAM));
+      }
+      std::vector<char> cubin;
+      std::string log;
+      int rc = nvrtc_compile_exprs(exprs, cubin, lowered, log);
+      if (rc != JM_OK) { rcs[(size_t)g] = rc; errs[(size_t)g] = log; return; }
+      const double ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      for (size_t j = 0; j < exprs.size(); ++j) {
+        const ColdKey &k = keys[(size_t)part[(size_t)g][j]];
+        Slot &s = *k.slot;
+        std::lock_guard<std::mutex> lk(s.mu);
+        if (s.state.load(std::memory_order_acquire) == S_READY) continue;
+        std::vector<char> copy(cubin);
+        rc = install_cubin(s, k.op, k.n, k.dtype, k.addend, std::move(copy), lowered[j]);
+        if (rc != JM_OK) {
+          s.err = t_err;
+          if (rc == JM_E_COMPILE) s.state.store(S_FAILED, std::memory_order_release);
+          rcs[(size_t)g] = rc;
+          errs[(size_t)g] = t_err;
+          continue;
+        }
+        s.compile_ms = ms / (double)exprs.size();   // the program's time, shared by its keys
+        c_compilations++;
+        c_compile_us += (long long)(s.compile_ms * 1000.0);
+        s.state.store(S_READY, std::memory_order_release);
+      }
+      c_programs++;
+    });
+  for (auto &t : th) t.join();
+  for (int g = 0; g < groups; ++g)
+    if (rcs[(size_t)g] != JM_OK) return fail(rcs[(size_t)g], "batched compile: %s", errs[(size_t)g].c_str());
+  return JM_OK;
+}
+
 // Mixed-N: resolve every key (cold keys compile concurrently), then fork the
 // groups over a pool of streams and join them back into the caller's stream.
 constexpr int POOL = 8;
@@ -628,7 +737,9 @@ int run_many_impl(const jm_run_desc *d, int count, void *stream, unsigned flags)
       return rc;
     }
   }
-  // 1. specialize: distinct cold keys in parallel (one host thread per key)
+  // 1. specialize: distinct cold keys in parallel (one host thread per key),
+  // or (JM_FLAG_BATCH_COMPILE) as a few NVRTC programs of several name
+  // expressions each, compiled in parallel
   std::vector<Slot *> slots((size_t)count, nullptr);
   std::vector<int> todo;
   for (int i = 0; i < count; ++i) {
@@ -636,7 +747,10 @@ int run_many_impl(const jm_run_desc *d, int count, void *stream, unsigned flags)
     Slot &s = slot_of(d[i].n, d[i].dtype, d[i].addend, d[i].kind, want_stream(d[i].n, d[i].dtype, d[i].kind, d[i].repeat, d[i].flags));
     if (s.state.load(std::memory_order_acquire) != S_READY) todo.push_back(i);
   }
-  if (todo.size() > 1) {
+  if ((flags & JM_FLAG_BATCH_COMPILE) && todo.size() > 1) {
+    int rc = batch_compile(d, todo);
+    if (rc != JM_OK) return rc;
+  } else if (todo.size() > 1) {
     std::vector<std::thread> th;
     std::vector<int> rcs(todo.size(), JM_OK);
     std::vector<std::string> errs(todo.size());
@@ -1032,6 +1146,7 @@ int jit_mat_stats(jm_stats *out) {
   out->misses = c_misses.load();
   out->launches = c_launches.load();
   out->imports = c_imports.load();
+  out->programs = c_programs.load();
   out->compile_ms_total = c_compile_us.load() / 1000.0;
   int ready = 0, failed = 0;
   for (int a = 0; a < NADD; ++a)
@@ -1057,6 +1172,7 @@ int tile_code(const jm::Plan &p) {
          : p.tile == (int)jm::Tile::Tpms ? JM_TILE_TPMS
          : p.tile == (int)jm::Tile::Rows ? JM_TILE_ROWS
          : p.tile == (int)jm::Tile::F32Rows ? JM_TILE_F32_ROWS
+         : p.tile == (int)jm::Tile::Reg ? JM_TILE_F64_REG
          : p.tile == (int)jm::Tile::Dmma ? (p.w > 1 ? JM_TILE_CTA_DMMA : JM_TILE_WARP_DMMA)
                                          : (p.w > 1 ? JM_TILE_CTA_F32 : JM_TILE_WARP_F32);
 }
@@ -1127,14 +1243,14 @@ int jit_mat_key_info(jm_key_info *keys, int cap) {
 }
 
 int jit_mat_reset_stats(void) {
-  c_compilations = 0; c_hits = 0; c_misses = 0; c_launches = 0; c_compile_us = 0; c_imports = 0;
+  c_compilations = 0; c_hits = 0; c_misses = 0; c_launches = 0; c_compile_us = 0; c_imports = 0; c_programs = 0;
   return JM_OK;
 }
 
 int jit_mat_fill(int n, int dtype, int dist, uint64_t seed, int64_t global_first, int64_t batch, void *out) {
   int rc = check_key(n, dtype, JM_ADDEND_ONES, JM_KIND_SPECIALIZED);
   if (rc != JM_OK) return rc;
-  if (dist < 0 || dist > 2) return fail(JM_E_INVALID, "dist %d invalid", dist);
+  if (dist < 0 || dist > 3) return fail(JM_E_INVALID, "dist %d invalid", dist);
   if (batch < 0 || global_first < 0) return fail(JM_E_INVALID, "negative batch/global_first");
   if (!G.inited.load()) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
   if (batch == 0) return JM_OK;

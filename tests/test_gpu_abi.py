@@ -245,3 +245,24 @@ def test_non_sm100_device_is_rejected_without_fallback():
     env = dict(os.environ, JIT_MAT_FAKE_CC_MAJOR="9")
     p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert p.returncode == 0 and p.stdout.strip() == "ok", p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("groups", ["1", "3"])
+def test_run_many_batched_compile(jm, groups, monkeypatch):
+    """f2: the cold keys of a mixed-N call compiled as multi-expression NVRTC
+    programs (JM_FLAG_BATCH_COMPILE) give the same bits as the per-key path."""
+    monkeypatch.setenv("JIT_MAT_COMPILE_GROUPS", groups)
+    cases = [(5, "f64", 3), (12, "f64", 1), (17, "f64", 100), (24, "f32", 2), (33, "f32", 100), (40, "f64", 3)]
+    xs = [torch.from_numpy(jm_synth.generate(n, dt, "shard", 77 + n, 0, 41)).cuda() for n, dt, _ in cases]
+    _fresh(jm)
+    want = [jm.run(x, r, sync=True) for x, (n, dt, r) in zip(xs, cases)]
+    _fresh(jm)
+    outs = [torch.empty_like(x) for x in xs]
+    jm.jit_mat_run_many([dict(n=n, dtype=dt, batch=41, repeat=r, in_ptr=x.data_ptr(), out_ptr=y.data_ptr())
+                         for x, y, (n, dt, r) in zip(xs, outs, cases)], sync=True, batch_compile=True)
+    st = jm.jit_mat_stats()
+    assert st["compilations"] == len(cases) and st["programs"] == min(int(groups), len(cases))
+    for w, g, c in zip(want, outs, cases):
+        assert torch.equal(w, g), f"batched compile differs at {c}"
+    info = [k for k in jm.jit_mat_key_info() if k["kind"] == 0]
+    assert len(info) == len(cases) and all(k["state"] == 2 and k["regs"] > 0 for k in info)

@@ -136,7 +136,7 @@ def c4(fh, stream):
         jm.jit_mat_set_stream(stream.cuda_stream)
         jm.jit_mat_reset_stats()
         tdt = torch.float64 if dt == "f64" else torch.float32
-        groups = []
+        groups = groups_ = []
         for n in range(2, 65):
             if counts[n]:
                 x = torch.empty(int(counts[n]), n, n, dtype=tdt, device="cuda")
@@ -168,6 +168,23 @@ def c4(fh, stream):
         one_pass("specialized")
         stream.synchronize()
         par_s = time.perf_counter() - t0
+        # cold again, the cold keys compiled as a few multi-expression NVRTC
+        # programs (JM_FLAG_BATCH_COMPILE), for several group counts
+        batched = {}
+        for groups in ("1", "4", str(os.cpu_count() or 8), "16"):
+            os.environ["JIT_MAT_COMPILE_GROUPS"] = groups
+            jm.jit_mat_shutdown()
+            jm.jit_mat_init(0)
+            jm.jit_mat_set_stream(stream.cuda_stream)
+            jm.jit_mat_reset_stats()
+            t0 = time.perf_counter()
+            jm.jit_mat_run_many([dict(n=n, dtype=dt, batch=b, repeat=R, in_ptr=x.data_ptr(),
+                                      out_ptr=y.data_ptr()) for n, b, x, y in groups_],
+                                stream=stream.cuda_stream, batch_compile=True)
+            stream.synchronize()
+            batched[groups] = {"cold_pass_s": time.perf_counter() - t0, "programs": jm.jit_mat_stats()["programs"],
+                               "compilations": jm.jit_mat_stats()["compilations"]}
+        os.environ.pop("JIT_MAT_COMPILE_GROUPS", None)
         res = {}
         for kind, many in (("specialized", True), ("generic", True), ("specialized_serial", False)):
             kind_ = kind.split("_")[0]
@@ -189,6 +206,7 @@ def c4(fh, stream):
               "compile_ms_per_key_median": float(np.median([k["compile_ms"] for k in keys])),
               "compile_ms_per_key_max": float(np.max([k["compile_ms"] for k in keys])),
               "cold_pass_s_run_many_parallel_compiles": par_s,
+              "cold_pass_run_many_batched_programs": batched, "host_cpus": os.cpu_count(),
               "warm": res, "specialized_speedup": res["specialized"]["updates_per_s"] / res["generic"]["updates_per_s"]},
              fh)
         del groups
