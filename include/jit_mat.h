@@ -101,6 +101,7 @@ enum {
                                     device buffers it owns, chunked and overlapped (see run_host) */
 #define JM_FLAG_RESIDENT 4u      /* use the resident kernel whatever the repeat count (see VARIANT) */
 #define JM_FLAG_STREAMING 8u     /* use the streaming kernel where the kind has one (see VARIANT) */
+#define JM_FLAG_LATENCY 32u      /* use the latency kernel (a warp per matrix; n*n <= 32; see VARIANT) */
 #define JM_FLAG_BATCH_COMPILE 16u /* jit_mat_run_many: compile the cold keys as a few NVRTC programs
                                     of several name expressions each (see jit_mat_run_many) */
 
@@ -136,8 +137,14 @@ JM_API int jit_mat_init(int device);
  * ring (both within the parity bound).  Environment
  * JIT_MAT_STREAM=0/1 forces resident/streaming, JIT_MAT_STREAM_RN moves the
  * switch point (read once per process); per call, jm_run_desc.flags
- * JM_FLAG_RESIDENT / JM_FLAG_STREAMING force it.  JIT_MAT_DUMP_CUBIN=<dir>
- * (inspection only) writes each NVRTC cubin to <dir>/<symbol>.cubin. */
+ * JM_FLAG_RESIDENT / JM_FLAG_STREAMING force it.  A third, LATENCY variant
+ * (a third cache key) serves tiny batches of n*n <= 32 matrices: when the batch
+ * is at most 4 matrices per SM (or with JM_FLAG_LATENCY) each matrix gets a warp,
+ * one element per lane, and the update's critical path is one n-long FMA chain
+ * instead of a thread's n^2(n+1) FMAs (BASELINE.json configs[0], C1); it sums
+ * in the thread-per-matrix kernel's order, so results agree bit for bit;
+ * JIT_MAT_LATENCY=0 turns it off.  JIT_MAT_DUMP_CUBIN=<dir> (inspection only)
+ * writes each NVRTC cubin to <dir>/<symbol>.cubin. */
 JM_API int jit_mat_run(int n, int dtype, int64_t batch, int64_t repeat, const void *in, void *out);
 
 /* Unload every module, drop the cache and release the primary context.  Later
@@ -281,7 +288,8 @@ enum { JM_TILE_GENERIC = 0, JM_TILE_TPM = 1, JM_TILE_WARP_DMMA = 2, JM_TILE_CTA_
        JM_TILE_TPM2 = 8 /* two threads per matrix (FP64 n = 8) */,
        JM_TILE_TPMS = 9 /* thread per matrix, product staged in shared memory (FP64 n = 9, 10, FP32 12..14) */,
        JM_TILE_F32_ROWS = 10 /* FP32 row panels: 4 threads per matrix own full rows (n = 15, 16) */,
-       JM_TILE_F64_REG = 11 /* FP64 register tiles with DFMA (sizes DMMA pads badly) */ };
+       JM_TILE_F64_REG = 11 /* FP64 register tiles with DFMA (sizes DMMA pads badly) */,
+       JM_TILE_LAT = 12 /* latency kernel: a warp per matrix, an element per lane (tiny batches) */ };
 
 JM_API int jit_mat_stats(jm_stats *out);
 /* Copy up to `cap` non-empty slots into `keys`; returns the number of
@@ -320,6 +328,7 @@ JM_API const char *jit_mat_version(void);
 #define JM_OP_MATMUL 2
 #define JM_OP_MASS 3     /* compile_check(dofs, quads, JM_OP_MASS, ...): k_mass<dofs, quads> */
 #define JM_OP_STREAM 4   /* the streaming (low-repeat) variant of the update (addend Ones) */
+#define JM_OP_LAT 5      /* the latency variant of the update (addend Ones; n*n <= 32) */
 JM_API int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes);
 
 /* Cache-hit cost of the key lookup (the paper calls the

@@ -19,8 +19,8 @@ import os
 from ._lib import (  # noqa: F401  (re-exported C ABI)
     JM_ADDEND_IDENTITY, JM_ADDEND_ONES, JM_E_ALIGN, JM_E_ARCH, JM_E_COMPILE, JM_E_CUDA,
     JM_E_INVALID, JM_E_NOT_INITIALIZED, JM_E_UNSUPPORTED, JM_F32, JM_F64, JM_FLAG_HOST_BUFFERS,
-    JM_FLAG_RESIDENT, JM_FLAG_STREAMING, JM_FLAG_SYNC, JM_FLAG_BATCH_COMPILE, JM_KIND_AOT_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK, JM_OP_MATMUL,
-    JM_OP_STREAM, JM_TILE_NAMES, JitMatError,
+    JM_FLAG_RESIDENT, JM_FLAG_STREAMING, JM_FLAG_SYNC, JM_FLAG_BATCH_COMPILE, JM_FLAG_LATENCY, JM_KIND_AOT_SPECIALIZED, JM_KIND_GENERIC, JM_KIND_SPECIALIZED, JM_OK, JM_OP_MATMUL,
+    JM_OP_LAT, JM_OP_STREAM, JM_TILE_NAMES, JitMatError,
     jm_key_info, jm_run_desc, jm_stats, lib, lib_path,
 )
 
@@ -278,7 +278,7 @@ def jit_mat_compile_check(n: int, dtype, addend="ones") -> int:
     if addend == "mass":
         _check(lib.jit_mat_compile_check(int(n), int(dtype), 3, ctypes.byref(cb)), "jit_mat_compile_check")
         return int(cb.value)
-    ops = {"matmul": JM_OP_MATMUL, "stream": JM_OP_STREAM}
+    ops = {"matmul": JM_OP_MATMUL, "stream": JM_OP_STREAM, "lat": JM_OP_LAT}
     a = ops[addend] if addend in ops else _ad(addend)
     _check(lib.jit_mat_compile_check(int(n), _dt(dtype), a, ctypes.byref(cb)), "jit_mat_compile_check")
     return int(cb.value)
@@ -291,8 +291,8 @@ def run(x, repeat: int, out=None, *, addend: str = "ones", kind: str = "speciali
 
     Marshals the tensor pointers into :func:`jit_mat_run_ex`; ``out`` may be ``x``
     (in place).  Runs on ``stream`` (default: torch's current stream).
-    ``variant`` = "resident" / "streaming" forces the kernel variant (default:
-    the library picks by repeat count, see jit_mat.h VARIANT).
+    ``variant`` = "resident" / "streaming" / "latency" forces the kernel variant
+    (default: the library picks by repeat count and batch, see jit_mat.h VARIANT).
     """
     import torch
 
@@ -311,7 +311,8 @@ def run(x, repeat: int, out=None, *, addend: str = "ones", kind: str = "speciali
     return out
 
 
-_VARIANTS = {None: 0, "auto": 0, "resident": JM_FLAG_RESIDENT, "streaming": JM_FLAG_STREAMING}
+_VARIANTS = {None: 0, "auto": 0, "resident": JM_FLAG_RESIDENT, "streaming": JM_FLAG_STREAMING,
+             "latency": JM_FLAG_LATENCY}
 
 
 def _selftest_loaded() -> str:

@@ -20,11 +20,13 @@ JM_E_INVALID, JM_E_UNSUPPORTED, JM_E_NOT_INITIALIZED = -1, -2, -3
 JM_E_ARCH, JM_E_COMPILE, JM_E_CUDA, JM_E_ALIGN = -4, -5, -6, -7
 JM_FLAG_SYNC, JM_FLAG_HOST_BUFFERS, JM_FLAG_RESIDENT, JM_FLAG_STREAMING = 1, 2, 4, 8
 JM_FLAG_BATCH_COMPILE = 16
+JM_FLAG_LATENCY = 32
 JM_TILE_NAMES = {0: "generic", 1: "tpm", 2: "warp_dmma", 3: "cta_dmma", 4: "warp_f32",
-                 5: "cta_f32", 6: "rows", 7: "matmul", 8: "tpm2", 9: "tpms", 10: "f32_rows", 11: "f64_reg"}
+                 5: "cta_f32", 6: "rows", 7: "matmul", 8: "tpm2", 9: "tpms", 10: "f32_rows", 11: "f64_reg", 12: "lat"}
 JM_OP_MATMUL = 2
 JM_OP_MASS = 3
 JM_OP_STREAM = 4
+JM_OP_LAT = 5
 
 
 class JitMatError(RuntimeError):

@@ -24,7 +24,8 @@ enum class Addend : int { Ones = 0, Identity = 1 };
 enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, Tpm2 = 3 /* r01, removed */, F32 = 4, Tpms = 5,
                         Rows = 6 /* r01 FP64 row panels, removed */,
                         F32Rows = 7 /* plan label only: the FP32 row panels of Tile::F32 */,
-                        Reg = 8 /* FP64 register tiles (DFMA; run_f64t) */ };
+                        Reg = 8 /* FP64 register tiles (DFMA; run_f64t) */,
+                        Lat = 9 /* latency path: a warp per matrix, an element per lane (k_update_lat) */ };
 
 struct Plan {
   int tile;      // Tile
@@ -603,6 +604,21 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
 // warps-per-SMSP (2 -> 255, 3 -> 168 regs); 168 makes the FP32 row panels
 // spill, and an explicit minBlocks = 1 changes ptxas' heuristics (r01: TPM
 // f32 n=2 went 32 -> 45 registers and lost 18 % of HBM throughput).
+
+// ---- latency path (tiny batches; BASELINE.json configs[0] "C1") ----
+// A thread-per-matrix kernel runs each matrix's N^2 (N+1) FMAs per update on
+// ONE thread; with few matrices the GPU idles and one update costs ~200 SM
+// clocks (r01 C1: 1 x 4x4 x 1000 updates in 109 us, slower than a CPU core).
+// k_update_lat gives each matrix a warp, lane i*N+j owning M[i][j], and forms
+// P[i][j] with N shuffled pairs: the per-update critical path is one N-long
+// FMA chain.  For N*N <= 32; chosen when the batch is at most LAT_BATCH_PER_SM
+// matrices per SM (each matrix then has its own warp) or by JM_FLAG_LATENCY.
+constexpr int LAT_THREADS = 128;                   // 4 matrices (warps) per CTA
+constexpr int LAT_BATCH_PER_SM = 4;
+JM_HD constexpr bool lat_ok(int n) { return n * n <= 32; }
+JM_HD constexpr Plan plan_lat(int n, int dtype) {
+  return Plan{(int)Tile::Lat, LAT_THREADS, LAT_THREADS / 32, 0, (n + dtype) > 0 ? 1 : 1};
+}
 
 // ---- AoT specializations (nvcc-compiled at build time; Fig. 3's sizes) ----
 JM_HD constexpr bool aot_spec_available(int n, int dtype) {

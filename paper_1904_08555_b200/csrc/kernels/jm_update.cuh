@@ -1425,6 +1425,35 @@ __global__ void __maxnreg__(f32t_maxreg(N, sizeof(T) == 8)) k_update_stream_rc(c
   update_body<N, T, A, K, true>(in, out, batch, repeat);
 }
 
+// Latency path (jm_plan.h plan_lat): one warp per matrix, lane e = i*N + j
+// holds M[i][j]; P[i][j] = M[i][j] + sum_k M[i][k] M[k][j] with the k terms
+// shuffled in, k ascending with FMA — the thread-per-matrix kernel's order, so
+// the two agree bit for bit.  Grid-stride over matrices; the warp index is
+// warp-uniform, so whole warps leave together and every shuffle is full-warp.
+template <int N, class T, Addend A>
+__global__ void __launch_bounds__(LAT_THREADS) k_update_lat(const T *__restrict__ in, T *__restrict__ out,
+                                                            long long batch, int repeat) {
+  static_assert(N * N <= 32, "one matrix per warp");
+  const int lane = threadIdx.x & 31;
+  const int e = lane < N * N ? lane : 0, i = e / N, j = e - (e / N) * N;
+  const T c = T(0.00005);
+  const long long nw = (long long)gridDim.x * (LAT_THREADS / 32);
+  for (long long b = (long long)blockIdx.x * (LAT_THREADS / 32) + (threadIdx.x >> 5); b < batch; b += nw) {
+    T m = lane < N * N ? in[b * N * N + e] : T(0);
+    for (int r = 0; r < repeat; ++r) {
+      T p = m;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const T a = __shfl_sync(0xffffffffu, m, i * N + k);
+        const T bk = __shfl_sync(0xffffffffu, m, k * N + j);
+        p = fmaT(a, bk, p);
+      }
+      m = (A == Addend::Ones || i == j) ? fmaT(c, p, T(1)) : c * p;
+    }
+    if (lane < N * N) out[b * N * N + e] = m;
+  }
+}
+
 // The streaming (low-repeat) variant: same kinds behind the bulk-copy ring
 // (plan_stream); the host selects it when repeat * (n + 1) is below the
 // switch point.  Name expression "jm::k_update_stream[_mb1]<N, T, A, K>".

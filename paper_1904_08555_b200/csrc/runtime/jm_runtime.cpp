@@ -190,6 +190,9 @@ Slot g_mm_slots[2][NDT][NMAX + 1];     // multiply-accumulate: [specialized|gene
 Slot g_mass_slots[2][jm::MASS_MAX + 1][jm::MASS_MAX + 1];   // Laghos mass action: [kind][D][Q]
 // the streaming (low-repeat) variant of the specialized update: [addend][dtype][n]
 Slot g_stream_slots[NADD][NDT][NMAX + 1];
+// the latency variant (a warp per matrix, tiny batches; n*n <= 32): [addend][dtype][n]
+constexpr int NLAT = 5;
+Slot g_lat_slots[NADD][NDT][NLAT + 1];
 
 struct State {
   std::mutex mu;
@@ -251,6 +254,16 @@ std::string name_expression(int n, int dtype, int addend, bool stream = false) {
            tile_name((int)jm::tile_for(n, dtype)));
   return buf;
 }
+
+std::string lat_name_expression(int n, int dtype, int addend) {
+  char buf[96];
+  snprintf(buf, sizeof buf, "jm::k_update_lat<%d, %s, jm::Addend::%s>", n, dtype == JM_F64 ? "double" : "float",
+           addend == JM_ADDEND_ONES ? "Ones" : "Identity");
+  return buf;
+}
+
+// the name expression of an update-op slot (resident / streaming / latency)
+std::string update_expression(int op, int n, int dtype, int addend);
 
 std::string mm_name_expression(int n, int dtype) {
   char buf[96];
@@ -347,14 +360,20 @@ int finish_function(Slot &s, CUfunction fn) {
 // ops: the Eigen-benchmark update (k_update) and the batched multiply-accumulate
 // of the RAJA benchmark (k_matmul, Listing 8)
 // and the streaming variant of k_update (k_update_stream, jm::plan_stream)
-enum { OP_UPDATE = 0, OP_MATMUL = 1, OP_MASS = 2, OP_UPDATE_STREAM = 3 };
+enum { OP_UPDATE = 0, OP_MATMUL = 1, OP_MASS = 2, OP_UPDATE_STREAM = 3, OP_UPDATE_LAT = 4 };
 
 // (for OP_MASS: n = D = NUM_DOFS_1D, extra = Q = NUM_QUAD_1D)
 jm::Plan plan_for(int op, int n, int dtype, int extra) {
   return op == OP_MATMUL          ? jm::plan_matmul(n, dtype)
          : op == OP_MASS          ? jm::plan_mass(n, extra)
          : op == OP_UPDATE_STREAM ? jm::plan_stream(n, dtype)
+         : op == OP_UPDATE_LAT    ? jm::plan_lat(n, dtype)
                                   : jm::plan_specialized(n, dtype);
+}
+
+std::string update_expression(int op, int n, int dtype, int addend) {
+  return op == OP_UPDATE_LAT ? lat_name_expression(n, dtype, addend)
+                             : name_expression(n, dtype, addend, op == OP_UPDATE_STREAM);
 }
 
 std::string mass_name_expression(int d, int q) {
@@ -413,7 +432,7 @@ int compile_slot(Slot &s, int op, int n, int dtype, int addend) {
   std::string lowered, log;
   const std::string expr = op == OP_MATMUL ? mm_name_expression(n, dtype)
                            : op == OP_MASS ? mass_name_expression(n, addend)
-                                           : name_expression(n, dtype, addend, op == OP_UPDATE_STREAM);
+                                           : update_expression(op, n, dtype, addend);
   int rc = nvrtc_compile_expr(expr, cubin, lowered, log);
   if (rc != JM_OK) {
     s.err = log;
@@ -517,16 +536,42 @@ bool want_stream(int n, int dtype, int kind, int64_t repeat, unsigned flags = 0)
   return rn < (int64_t)stream_rn(n, dtype) && rn >= (int64_t)jm::stream_lo(n, dtype);
 }
 
-Slot &slot_of(int n, int dtype, int addend, int kind, bool stream) {
-  return stream ? g_stream_slots[addend][dtype][n] : g_slots[kind][addend][dtype][n];
+// The latency variant: a warp per matrix for tiny batches (every matrix gets
+// its own warp: batch <= LAT_BATCH_PER_SM x SMs), n*n <= 32, or forced by
+// JM_FLAG_LATENCY; JM_FLAG_RESIDENT / JM_FLAG_STREAMING and
+// JIT_MAT_LATENCY=0 keep it off.
+bool want_lat(int n, int dtype, int kind, int64_t batch, unsigned flags) {
+  (void)dtype;
+  if (kind != JM_KIND_SPECIALIZED || !jm::lat_ok(n)) return false;
+  if (flags & JM_FLAG_LATENCY) return true;
+  if (flags & (JM_FLAG_RESIDENT | JM_FLAG_STREAMING)) return false;
+  static const bool off = [] {
+    const char *e = getenv("JIT_MAT_LATENCY");
+    return e && *e && strcmp(e, "0") == 0;
+  }();
+  return !off && batch > 0 && batch <= (int64_t)jm::LAT_BATCH_PER_SM * G.sms;
 }
+
+// variant of a run: 0 resident, 1 streaming, 2 latency
+int variant_of(const jm_run_desc &d) {
+  if (want_lat(d.n, d.dtype, d.kind, d.batch, d.flags)) return 2;
+  return want_stream(d.n, d.dtype, d.kind, d.repeat, d.flags) ? 1 : 0;
+}
+
+Slot &slot_of(int n, int dtype, int addend, int kind, int variant) {
+  return variant == 2 ? g_lat_slots[addend][dtype][n]
+         : variant == 1 ? g_stream_slots[addend][dtype][n] : g_slots[kind][addend][dtype][n];
+}
+
+int op_of_variant(int variant) { return variant == 2 ? OP_UPDATE_LAT : variant == 1 ? OP_UPDATE_STREAM : OP_UPDATE; }
 
 // the kernel a run descriptor launches (key checked by the caller)
 int lookup_run(const jm_run_desc &d, Slot **out) {
-  if (!want_stream(d.n, d.dtype, d.kind, d.repeat, d.flags)) return lookup(d.n, d.dtype, d.addend, d.kind, out);
+  const int v = variant_of(d);
+  if (v == 0) return lookup(d.n, d.dtype, d.addend, d.kind, out);
   if (!G.inited.load(std::memory_order_acquire)) return fail(JM_E_NOT_INITIALIZED, "jit_mat_init has not been called");
-  return acquire_slot(g_stream_slots[d.addend][d.dtype][d.n], OP_UPDATE_STREAM, d.n, d.dtype, d.addend,
-                      JM_KIND_SPECIALIZED, out);
+  return acquire_slot(slot_of(d.n, d.dtype, d.addend, JM_KIND_SPECIALIZED, v), op_of_variant(v), d.n, d.dtype,
+                      d.addend, JM_KIND_SPECIALIZED, out);
 }
 
 int launch(Slot &s, int n, int64_t batch, int64_t repeat, const void *in, void *out, CUstream stream,
@@ -651,12 +696,12 @@ struct ColdKey {
 int batch_compile(const jm_run_desc *d, const std::vector<int> &todo) {
   std::vector<ColdKey> keys;
   for (int i : todo) {
-    const bool st = want_stream(d[i].n, d[i].dtype, d[i].kind, d[i].repeat, d[i].flags);
+    const int v = variant_of(d[i]);
     if (d[i].kind != JM_KIND_SPECIALIZED) continue;   // generic / AoT slots are seeded, never compiled
-    Slot *s = &slot_of(d[i].n, d[i].dtype, d[i].addend, d[i].kind, st);
+    Slot *s = &slot_of(d[i].n, d[i].dtype, d[i].addend, d[i].kind, v);
     bool dup = false;
     for (const ColdKey &k : keys) dup |= (k.slot == s);
-    if (!dup) keys.push_back({st ? OP_UPDATE_STREAM : OP_UPDATE, d[i].n, d[i].dtype, d[i].addend, s});
+    if (!dup) keys.push_back({op_of_variant(v), d[i].n, d[i].dtype, d[i].addend, s});
   }
   if (keys.empty()) return JM_OK;
   int groups = (int)std::thread::hardware_concurrency();
@@ -684,7 +729,7 @@ int batch_compile(const jm_run_desc *d, const std::vector<int> &todo) {
       std::vector<std::string> exprs, lowered;
       for (int i : part[(size_t)g]) {
         const ColdKey &k = keys[(size_t)i];
-        exprs.push_back(name_expression(k.n, k.dtype, k.addend, k.op == OP_UPDATE_STREAM));
+        exprs.push_back(update_expression(k.op, k.n, k.dtype, k.addend));
       }
       std::vector<char> cubin;
       std::string log;
@@ -744,7 +789,7 @@ int run_many_impl(const jm_run_desc *d, int count, void *stream, unsigned flags)
   std::vector<int> todo;
   for (int i = 0; i < count; ++i) {
     if (d[i].batch == 0) continue;
-    Slot &s = slot_of(d[i].n, d[i].dtype, d[i].addend, d[i].kind, want_stream(d[i].n, d[i].dtype, d[i].kind, d[i].repeat, d[i].flags));
+    Slot &s = slot_of(d[i].n, d[i].dtype, d[i].addend, d[i].kind, variant_of(d[i]));
     if (s.state.load(std::memory_order_acquire) != S_READY) todo.push_back(i);
   }
   if ((flags & JM_FLAG_BATCH_COMPILE) && todo.size() > 1) {
@@ -941,8 +986,10 @@ int jit_mat_shutdown(void) {
     for (int d = 0; d <= jm::MASS_MAX; ++d)
       for (int q = 0; q <= jm::MASS_MAX; ++q) reset(g_mass_slots[k][d][q]);
   for (int a = 0; a < NADD; ++a)
-    for (int t = 0; t < NDT; ++t)
+    for (int t = 0; t < NDT; ++t) {
       for (int n = 0; n <= NMAX; ++n) reset(g_stream_slots[a][t][n]);
+      for (int n = 0; n <= NLAT; ++n) reset(g_lat_slots[a][t][n]);
+    }
   {
     std::lock_guard<std::mutex> hl(G.host_mu);
     for (int i = 0; i < 3; ++i) {
@@ -1123,10 +1170,11 @@ int jit_mat_prepare_for(int n, int dtype, int addend, int kind, int64_t repeat, 
   int rc = check_key(n, dtype, addend, kind);
   if (rc != JM_OK) return rc;
   if (repeat < 0 || repeat > JM_REPEAT_MAX) return fail(JM_E_INVALID, "repeat must be in [0, 2^31)");
-  jm_run_desc d{n, dtype, addend, kind, 1, repeat, nullptr, nullptr, nullptr, flags};
+  // (the latency variant depends on the batch: prepared only when forced by JM_FLAG_LATENCY)
+  jm_run_desc d{n, dtype, addend, kind, (int64_t)1 << 40, repeat, nullptr, nullptr, nullptr, flags};
   Slot *s = nullptr;
   if ((rc = lookup_run(d, &s)) != JM_OK) return rc;
-  if (variant) *variant = want_stream(n, dtype, kind, repeat, flags) ? 1 : 0;
+  if (variant) *variant = variant_of(d);
   return JM_OK;
 }
 
@@ -1217,6 +1265,25 @@ int jit_mat_key_info(jm_key_info *keys, int cap) {
           o.compile_ms = s.compile_ms;
           o.op = 0;
           o.variant = 1;
+        }
+        ++cnt;
+      }
+  for (int a = 0; a < NADD; ++a)
+    for (int t = 0; t < NDT; ++t)
+      for (int n = 1; n <= NLAT; ++n) {
+        Slot &s = g_lat_slots[a][t][n];
+        const int st = s.state.load(std::memory_order_acquire);
+        if (st == S_EMPTY) continue;
+        if (keys && cnt < cap) {
+          jm_key_info &o = keys[cnt];
+          o.n = n; o.dtype = t; o.addend = a; o.kind = JM_KIND_SPECIALIZED; o.state = st;
+          o.regs = s.regs; o.local_bytes = s.local_bytes; o.smem_bytes = s.plan.smem;
+          o.threads = s.plan.threads;
+          o.tile = JM_TILE_LAT;
+          o.cubin_bytes = s.cubin_bytes;
+          o.compile_ms = s.compile_ms;
+          o.op = 0;
+          o.variant = 2;
         }
         ++cnt;
       }
@@ -1324,13 +1391,16 @@ int jit_mat_compile_check(int n, int dtype, int addend, long long *cubin_bytes) 
       return fail(JM_E_UNSUPPORTED, "dofs/quads must be in [1, %d]", jm::MASS_MAX);
     expr = mass_name_expression(n, dtype);
   } else {
-    const bool op = addend == JM_OP_MATMUL || addend == JM_OP_STREAM;
+    const bool op = addend == JM_OP_MATMUL || addend == JM_OP_STREAM || addend == JM_OP_LAT;
     rc = check_key(n, dtype, op ? JM_ADDEND_ONES : addend, JM_KIND_SPECIALIZED);
     if (rc != JM_OK) return rc;
     if (addend == JM_OP_STREAM && !jm::stream_ok(n, dtype))
       return fail(JM_E_UNSUPPORTED, "n=%d %s has no streaming variant", n, dtype == JM_F64 ? "double" : "float");
+    if (addend == JM_OP_LAT && !jm::lat_ok(n))
+      return fail(JM_E_UNSUPPORTED, "n=%d has no latency variant (n*n <= 32)", n);
     expr = addend == JM_OP_MATMUL   ? mm_name_expression(n, dtype)
            : addend == JM_OP_STREAM ? name_expression(n, dtype, JM_ADDEND_ONES, true)
+           : addend == JM_OP_LAT    ? lat_name_expression(n, dtype, JM_ADDEND_ONES)
                                     : name_expression(n, dtype, addend);
   }
   std::vector<char> cubin;

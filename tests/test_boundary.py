@@ -94,6 +94,15 @@ def test_every_streaming_variant_compiles_for_sm100a(jm, dtype):
     assert all(s > 1000 for s in sizes)
 
 
+@pytest.mark.parametrize("dtype", ["double", "float"])
+def test_every_latency_variant_compiles_for_sm100a(jm, dtype):
+    """k_update_lat<N, T, Ones> (a warp per matrix) for every N with N*N <= 32;
+    larger N has no latency variant."""
+    assert all(jm.jit_mat_compile_check(n, dtype, "lat") > 1000 for n in range(1, 6))
+    with pytest.raises(jm.JitMatError):
+        jm.jit_mat_compile_check(6, dtype, "lat")
+
+
 @pytest.mark.parametrize("n", [1, 5, 8, 13, 33, 64])
 def test_identity_specializations_compile(jm, n):
     assert jm.jit_mat_compile_check(n, "double", "identity") > 0

@@ -252,3 +252,27 @@ def test_run_many_rejects_bad_descriptor_before_launch(jm):
         jm.jit_mat_run_many(bad, sync=True)
     torch.cuda.synchronize()
     assert torch.all(y == 7.0)
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_latency_variant(jm, n, dt):
+    """Tiny batches run a warp per matrix (k_update_lat, C1's kernel): parity
+    with the oracle, bit-identical to the thread-per-matrix kernel (same
+    summation order), picked automatically for batch <= 4 x SMs."""
+    for batch, dist in ((1, "paper"), (7, "shard"), (600, "hard")):
+        x = jm_synth.generate(n, dt, dist, 40 + n, 0, batch)
+        xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        for r in (1, 3, 1000 if batch == 1 else 25):
+            got = jm.run(xd, r, sync=True, variant="latency").cpu().numpy()
+            tpm = jm.run(xd, r, sync=True, variant="resident").cpu().numpy()
+            assert np.array_equal(got.view(np.uint8), tpm.view(np.uint8)), f"lat != tpm n={n} {dt} b={batch} R={r}"
+            assert_parity(got, oracle.run(x, r), what=f"latency n={n} {dt} batch={batch} R={r}")
+            auto = jm.run(xd, r, sync=True).cpu().numpy()
+            assert np.array_equal(auto.view(np.uint8), got.view(np.uint8))
+    x = jm_synth.generate(n, dt, "shard", 9, 0, 5)
+    xd = torch.from_numpy(x).cuda()
+    got_i = jm.run(xd, 3, addend="identity", sync=True, variant="latency").cpu().numpy()
+    assert_parity(got_i, oracle.run(x, 3, "identity"), what=f"latency identity n={n} {dt}")
+    lat = [k for k in jm.jit_mat_key_info() if k["variant"] == 2 and k["n"] == n]
+    assert lat and lat[0]["tile_name"] == "lat"
