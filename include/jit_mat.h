@@ -262,7 +262,7 @@ typedef struct {
   int64_t misses;            /* lookups that had to compile (or wait for a compile) */
   int64_t launches;          /* kernels launched by this library */
   double compile_ms_total;   /* wall time inside NVRTC + module load */
-  int32_t keys_ready;        /* specialized cache slots (either variant) in READY state */
+  int32_t keys_ready;        /* specialized update cache slots (resident, streaming or latency variant) in READY state */
   int32_t keys_failed;       /* cache slots in FAILED state */
   int64_t imports;           /* keys installed by jit_mat_cache_import (no NVRTC) */
   int64_t programs;          /* NVRTC programs of batched compiles (JM_FLAG_BATCH_COMPILE) */

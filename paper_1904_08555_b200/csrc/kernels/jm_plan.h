@@ -111,7 +111,16 @@ constexpr int TPM_THREADS = 128;
 #define JM_DMMA_RT_LARGE 1   // row tiles per warp for other n > WARP_MAX (one warp per 8-row tile)
 #endif
 #ifndef JM_DMMA_BORDER_MAX
-#define JM_DMMA_BORDER_MAX 2         // n = 8K + r, r <= this: border tiles by DFMA (run_dmma BORD)
+#define JM_DMMA_BORDER_MAX 4         // n = 8K + r, r <= this: border tiles by DFMA (run_dmma BORD)
+#endif
+#ifndef JM_DMMA_BORDER_MIN
+#define JM_DMMA_BORDER_MIN 16        // ... and n above this
+#endif
+// k-compaction (run_dmma CMP): n = 8K + r with 2 <= r <= 4 puts the last k
+// tile's r real k into ONE k-step (k = 8K + t) instead of the two half-padding
+// k-steps of the k-permutation; its A fragment takes two shuffles per row tile
+#ifndef JM_DMMA_KCOMPACT
+#define JM_DMMA_KCOMPACT 1
 #endif
 constexpr int DMMA_WPC = 4;                       // warps per CTA when W == 1
 JM_HD constexpr int dmma_t8(int n) { return cdiv(n, 8); }
@@ -177,8 +186,22 @@ struct F32TRow { int n, ra, cb, ldmpad, pad, colblk, trfast, qmix, maxreg, kunro
 // FP64 register tiles (DFMA, run_f64t) for the sizes where DMMA's 8 x 8 x 4
 // granularity wastes most of the pipe; the same fields, CB a multiple of 2
 // (a 16-B chunk holds two doubles).  Only the sizes listed take this kind.
+// Candidates from the r02 search (tools/f64_candidates.json, profiles/r02_f64_search.jsonl;
+// FP64 pipe at R = 100, "was" = the DMMA / TPMS kinds before k-compaction and
+// the BR <= 4 border), kept behind JM_F64T_ON until measured against those.
+#ifndef JM_F64T_ON
+#define JM_F64T_ON 0
+#endif
 constexpr F32TRow F64T_TABLE[] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+#if JM_F64T_ON
+    {11, 3, 12, 4, 1, 0, 1, 0, 255, 2},   // 0.512 of the pipe (was 0.304), 208 regs
+    {12, 3, 12, 4, 1, 0, 1, 0, 168, 6},   // 0.630 of the pipe (was 0.398), 146 regs
+    {18, 6, 10, 4, 6, 0, 0, 0, 255, 9},   // 0.558 of the pipe (was 0.426), 224 regs
+    {19, 5, 10, 4, 1, 1, 1, 0, 255, 9},   // 0.612 of the pipe (was 0.470), 206 regs
+    {20, 5, 10, 4, 1, 1, 1, 0, 255, 10},  // 0.683 of the pipe (was 0.546), 200 regs
+    {35, 7, 6, 4, 0, 0, 0, 0, 168, 17},   // 0.650 of the pipe (was 0.611), 152 regs
+#endif
 };
 constexpr F32TRow F32T_TABLE[] = {
     {17, 6, 12, 4, 6, 0, 0, 0, 168, 4},  // 0.433 of the pipe, 157 regs
@@ -567,6 +590,19 @@ JM_HD constexpr int dmma_slot(int n) {
              ? dmma_scr(n) : 0;
 }
 JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8, dmma_slot(n)); }
+// FP32 tiles' low-repeat variant: the bulk-copy ring with slots widened to the
+// work region when a matrix is a multiple of 16 B (even n: one bulk copy per
+// matrix); odd n keep the double-buffered cp.async stage.  JM_F32T_RING=0: off.
+#ifndef JM_F32T_RING
+#define JM_F32T_RING 1
+#endif
+#ifndef JM_F32T_RING_MAXB
+#define JM_F32T_RING_MAXB (113 * 1024)   // ... while two CTAs still fit on an SM
+#endif
+JM_HD constexpr bool f32t_ring(int n) {
+  return JM_F32T_RING && (n * n * 4) % 16 == 0 &&
+         ring_bytes(n, 4, f32t_mpc(n), f32t_region(n)) <= JM_F32T_RING_MAXB;
+}
 // matrices per round of each kind (the resident plan's chunk)
 JM_HD constexpr int round_mpc(int n, int dtype) {
   return (tile_for(n, dtype) == Tile::Dmma || (dtype == 1 && tile_for(n, dtype) == Tile::Tpms))
@@ -594,8 +630,13 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
     return f32p_ring_inplace(n)
                ? Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm, f32p_slot(n)) + rm * f32p_mbuf(n), 1}
                : Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
-  // F32T: the resident layout with the double-buffered cp.async stage (the
-  // next chunk streams in while this one is updated)
+  // F32T, even n: the bulk-copy ring, each matrix's slot widened to its work
+  // region (the staged matrix is read into the accumulators, then the slot is
+  // the work area; the result goes back packed and leaves by a bulk store)
+  if (f32t_ring(n))
+    return Plan{(int)Tile::F32, 32 * f32t_wpc(n), chm, ring_bytes(n, es, rm, f32t_region(n)), f32t_wpm(n)};
+  // F32T, odd n: the resident layout with the double-buffered cp.async stage
+  // (the next chunk streams in while this one is updated)
   return Plan{(int)Tile::F32, 32 * f32t_wpc(n), f32t_mpc(n), 2 * rup(f32t_mpc(n) * f32t_region(n), 16), f32t_wpm(n)};
 }
 

@@ -645,9 +645,14 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   // 0.63 -> 0.48, 57 0.68 -> 0.53 of the pipe, profiles/r01_dmma_border_multiwarp.jsonl —
   // and was removed in r02.)
   constexpr int BR = N - 8 * (T8 - 1);
-  constexpr bool BORD = (W == 1) && (N > 16) && (BR <= JM_DMMA_BORDER_MAX);
+  constexpr bool BORD = (W == 1) && (N > JM_DMMA_BORDER_MIN) && (BR <= JM_DMMA_BORDER_MAX);
   constexpr int KTOP = BORD ? T8 - 1 : T8;   // global row tiles through DMMA
   constexpr int KN = BORD ? T8 - 1 : T8;     // column tiles through DMMA
+  // k-compaction (jm_plan.h JM_DMMA_KCOMPACT): the last k tile's BR <= 4 real
+  // k go through ONE k-step, k_t = 8(T8-1) + t.  Its A fragment M[8I+g][8K+t]
+  // sits in slot t&1 of lane (g, t>>1): two shuffles per row tile.  Its B
+  // fragment is the plain read of row 8K+t of the published M.
+  constexpr bool CMP = JM_DMMA_KCOMPACT && T8 >= 2 && BR >= 2 && BR <= 4;
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -670,13 +675,22 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
       bofs[s][j1] = ((2 * t + s) * RSC + ((j1 * 4 + gh) ^ (2 * t ^ (s << 2)))) * 16 + 8 * gl;
 #pragma unroll
   for (int j1 = 0; j1 < 2; ++j1) pofs[j1] = ((8 * wr * RT + g) * RSC + ((j1 * 4 + t) ^ fg)) * 16;
-  // border (BORD): column pair (8K, 8K+1) of row 8J + 2t + s -> colofs[s] + 8J*RSC*16;
-  // element (8K + g', 8I + g) -> rowofs + (g'*RSC + 4*(I ^ (g' & 1)))*16
+  // border (BORD): column pair (8K, 8K+1) of row 8J + 2t + s -> colofs[s] + 8J*RSC*16
+  // (the pair (8K+2, 8K+3) 16 B further);
+  // element (8K + g', 8I + g) -> rowofs + (g'*RSC + 4*(I ^ (g' & 1)) + (g' & 2))*16
   int colofs[2] = {0, 0}, rowofs = 0;
   if constexpr (BORD) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) colofs[s] = ((2 * t + s) * RSC + ((4 * (T8 - 1)) ^ (2 * t ^ (s << 2)))) * 16;
     rowofs = (8 * (T8 - 1) * RSC + gh) * 16 + 8 * gl;
+  }
+  // compacted k-step (CMP): B fragment M[8K + t][8J2 + g] -> cofs[J2&1] + (8K*RSC + 8(J2>>1))*16
+  // (row 8K + t has swizzle (t & 2) ^ ((t & 1) << 2)); A fragment source lane (g, t >> 1)
+  int cofs[2] = {0, 0};
+  const int csrc = (lane & ~3) | (t >> 1);
+  if constexpr (CMP) {
+#pragma unroll
+    for (int j1 = 0; j1 < 2; ++j1) cofs[j1] = (t * RSC + ((j1 * 4 + gh) ^ ((t & 2) ^ ((t & 1) << 2)))) * 16 + 8 * gl;
   }
 
   Stg sg(in, out, batch, smem);
@@ -738,56 +752,92 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
           constexpr int K = T8 - 1;
           // column border P[8I+g][8K+c] (c < BR), this warp's row tiles: lane
           // (g,t) sums its own k = 8J+2t+s terms, then the 4 lanes of a row add up
-          double cs[RT][2];
+          constexpr int NCC = BR <= 2 ? 2 : 4;   // border columns formed (the rest of a chunk is padding)
+          double cs[RT][NCC];
 #pragma unroll
-          for (int I = 0; I < RT; ++I) cs[I][0] = cs[I][1] = 0.0;
+          for (int I = 0; I < RT; ++I)
+#pragma unroll
+            for (int cc = 0; cc < NCC; ++cc) cs[I][cc] = 0.0;
 #pragma unroll
           for (int J = 0; J < T8; ++J)
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
               if (8 * J + s >= N) continue;
               const char *q = sb + colofs[s] + 8 * J * RSC * 16;
-              double v0, v1 = 0.0;
-              if constexpr (BR == 2) {
-                const double2 v = *reinterpret_cast<const double2 *>(q);
-                v0 = v.x; v1 = v.y;
+              double v[NCC];
+              if constexpr (BR == 1) {
+                v[0] = *reinterpret_cast<const double *>(q);
+                v[1] = 0.0;
               } else {
-                v0 = *reinterpret_cast<const double *>(q);
+#pragma unroll
+                for (int h = 0; h < NCC / 2; ++h) {   // chunk 4K + h sits 16 B after chunk 4K (XOR touches bits 1, 2)
+                  const double2 w = *reinterpret_cast<const double2 *>(q + 16 * h);
+                  v[2 * h] = w.x; v[2 * h + 1] = w.y;
+                }
               }
 #pragma unroll
-              for (int I = 0; I < RT; ++I) {
-                cs[I][0] = fmaT(acc[I][J][s], v0, cs[I][0]);
-                if constexpr (BR == 2) cs[I][1] = fmaT(acc[I][J][s], v1, cs[I][1]);
-              }
+              for (int I = 0; I < RT; ++I)
+#pragma unroll
+                for (int cc = 0; cc < NCC; ++cc)
+                  if (cc < BR) cs[I][cc] = fmaT(acc[I][J][s], v[cc], cs[I][cc]);
             }
 #pragma unroll
-          for (int I = 0; I < RT; ++I)
+          for (int I = 0; I < RT; ++I) {
+            if constexpr (NCC == 2) {
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-              double v = cs[I][cc];
-              if (cc < BR) {
-                v += __shfl_xor_sync(0xffffffffu, v, 1);
-                v += __shfl_xor_sync(0xffffffffu, v, 2);
+              for (int cc = 0; cc < 2; ++cc) {
+                double v = cs[I][cc];
+                if (cc < BR) {
+                  v += __shfl_xor_sync(0xffffffffu, v, 1);
+                  v += __shfl_xor_sync(0xffffffffu, v, 2);
+                }
+                p[I][K][cc] = (cc < BR && t == 0) ? acc[I][K][cc] + v : 0.0;
               }
-              p[I][K][cc] = (cc < BR && t == 0) ? acc[I][K][cc] + v : 0.0;
+            } else {
+              // reduce-scatter over the 4 lanes of a row: even t keeps columns
+              // (0, 1), odd t (2, 3); then the pair adds across t ^ 2
+              const bool od = t & 1;
+              const double r0 = __shfl_xor_sync(0xffffffffu, od ? cs[I][0] : cs[I][2], 1);
+              const double r1 = __shfl_xor_sync(0xffffffffu, od ? cs[I][1] : cs[I][3], 1);
+              double k0 = (od ? cs[I][2] : cs[I][0]) + r0, k1 = (od ? cs[I][3] : cs[I][1]) + r1;
+              k0 += __shfl_xor_sync(0xffffffffu, k0, 2);
+              k1 += __shfl_xor_sync(0xffffffffu, k1, 2);
+              p[I][K][0] = (t < 2 && 2 * t < BR) ? acc[I][K][0] + k0 : 0.0;
+              p[I][K][1] = (t < 2 && 2 * t + 1 < BR) ? acc[I][K][1] + k1 : 0.0;
             }
+          }
           // row border P[8K+g'][8J+2t+s] (g' < BR), column tiles J < K: lane
           // (g,t) sums the k = 8I+g terms from its accumulators, then the 8
           // lanes of a column add up
           constexpr int IK = K;              // (whole matrix per warp: RT = T8)
           auto finish_row = [&](int J, int s, const double (&rsv)[BR]) {
             double mine = 0.0;
-#pragma unroll
-            for (int q = 0; q < BR; ++q) {
-              double v = rsv[q];
+            if constexpr (BR == 1) {
+              double v = rsv[0];
               v += __shfl_xor_sync(0xffffffffu, v, 4);
               v += __shfl_xor_sync(0xffffffffu, v, 8);
               v += __shfl_xor_sync(0xffffffffu, v, 16);
-              if (g == q) mine = v;
+              mine = v;
+            } else {
+              // reduce-scatter over the 8 lanes of a column (g): g bit 0 picks
+              // rows {0, 2} / {1, 3}, g bit 1 the row of the pair, g bit 2 adds
+              const bool g0 = g & 1, g1 = (g >> 1) & 1;
+              const double v2 = BR > 2 ? rsv[BR > 2 ? 2 : 0] : 0.0, v3 = BR > 3 ? rsv[BR > 3 ? 3 : 0] : 0.0;
+              const double r0 = __shfl_xor_sync(0xffffffffu, g0 ? rsv[0] : rsv[1], 4);
+              double w0 = (g0 ? rsv[1] : rsv[0]) + r0, w1 = 0.0;
+              if constexpr (BR > 2) {
+                const double r1 = __shfl_xor_sync(0xffffffffu, g0 ? v2 : v3, 4);
+                w1 = (g0 ? v3 : v2) + r1;
+                const double r = __shfl_xor_sync(0xffffffffu, g1 ? w0 : w1, 8);
+                mine = (g1 ? w1 : w0) + r;
+              } else {
+                mine = w0 + __shfl_xor_sync(0xffffffffu, w0, 8);   // (g1 = 1 lanes hold rows >= 2: unused)
+              }
+              mine += __shfl_xor_sync(0xffffffffu, mine, 16);
             }
             p[IK][J][s] = (g < BR) ? acc[IK][J][s] + mine : 0.0;
           };
-          {                                  // I outer: each border-row value loaded once
+          if constexpr (BR * K <= 8) {       // I outer: each border-row value loaded once
             double rs[BR][K > 0 ? K : 1][2];
 #pragma unroll
             for (int q = 0; q < BR; ++q)
@@ -798,7 +848,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
               double mr[BR];
 #pragma unroll
               for (int q = 0; q < BR; ++q)
-                mr[q] = *reinterpret_cast<const double *>(sb + rowofs + (q * RSC + 4 * (I ^ (q & 1))) * 16);
+                mr[q] = *reinterpret_cast<const double *>(sb + rowofs + (q * RSC + 4 * (I ^ (q & 1)) + (q & 2)) * 16);
 #pragma unroll
               for (int q = 0; q < BR; ++q)
 #pragma unroll
@@ -815,6 +865,24 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
                 for (int q = 0; q < BR; ++q) rsv[q] = rs[q][J][s];
                 finish_row(J, s, rsv);
               }
+          } else {                           // J outer (fewer live sums; the row values are reloaded per J)
+#pragma unroll
+            for (int J = 0; J < K; ++J) {
+              double rs[2][BR];
+#pragma unroll
+              for (int q = 0; q < BR; ++q) rs[0][q] = rs[1][q] = 0.0;
+#pragma unroll
+              for (int I = 0; I < T8; ++I)
+#pragma unroll
+                for (int q = 0; q < BR; ++q) {
+                  const double mr =
+                      *reinterpret_cast<const double *>(sb + rowofs + (q * RSC + 4 * (I ^ (q & 1)) + (q & 2)) * 16);
+                  rs[0][q] = fmaT(mr, acc[I][J][0], rs[0][q]);
+                  rs[1][q] = fmaT(mr, acc[I][J][1], rs[1][q]);
+                }
+              finish_row(J, 0, rs[0]);
+              finish_row(J, 1, rs[1]);
+            }
           }
         }
 #pragma unroll
@@ -822,21 +890,30 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             if (8 * J + s >= N) continue;   // every k of this k-step is padding: skip (compile time)
+            const bool cmp = CMP && J == T8 - 1;   // the compacted last k-step (compile time)
+            if (cmp && s == 1) continue;
             double b[KN];
 #pragma unroll
             for (int J2 = 0; J2 < KN; ++J2)
-              b[J2] = *reinterpret_cast<const double *>(sb + bofs[s][J2 & 1] +
+              b[J2] = *reinterpret_cast<const double *>(sb + (cmp ? cofs[J2 & 1] : bofs[s][J2 & 1]) +
                                                         (8 * J * RSC + 8 * (J2 >> 1)) * 16);
 #pragma unroll
-            for (int I = 0; I < RT; ++I)
+            for (int I = 0; I < RT; ++I) {
+              if ((RAG || BORD) && wr * RT + I >= KTOP) continue;   // border / phantom row tile
+              double a = acc[I][J][s];
+              if (cmp) {
+                const double a0 = __shfl_sync(0xffffffffu, acc[I][J][0], csrc);
+                const double a1 = __shfl_sync(0xffffffffu, acc[I][J][1], csrc);
+                a = (t & 1) ? a1 : a0;
+              }
 #pragma unroll
               for (int J2 = 0; J2 < KN; ++J2) {
-                if ((RAG || BORD) && wr * RT + I >= KTOP) continue;   // border / phantom row tile
                 if (J == 0 && s == 0)   // P = M + (first k-step): accumulator init is M itself
-                  dmma884_c(p[I][J2][0], p[I][J2][1], acc[I][J][s], b[J2], acc[I][J2][0], acc[I][J2][1]);
+                  dmma884_c(p[I][J2][0], p[I][J2][1], a, b[J2], acc[I][J2][0], acc[I][J2][1]);
                 else
-                  dmma884(p[I][J2][0], p[I][J2][1], acc[I][J][s], b[J2]);
+                  dmma884(p[I][J2][0], p[I][J2][1], a, b[J2]);
               }
+            }
           }
         }
         // M' = A + c * P  (padding stays exactly zero)
@@ -1114,13 +1191,18 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
   };
   auto row_of = [&](int i) { return i * RG + tr; };
   auto chunk_of = [&](int h) { return TL.colblk ? tc * NH + h : h * CG + tc; };
-  // STRM (the low-repeat variant): the same kernel with the double-buffered
-  // cp.async stage (the next chunk streams in while this one is updated)
-  Stager<N, ES, REG, NT, MPC, AL, STRM> sg(in, out, batch, smem);
+  // STRM (the low-repeat variant): even n run behind the bulk-copy ring with
+  // each slot widened to the work region (f32t_ring); odd n keep the
+  // double-buffered cp.async stage (the next chunk streams in while this one
+  // is updated)
+  typedef typename Pick<STRM && f32t_ring(N), Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, REG>,
+                        Stager<N, ES, REG, NT, MPC, AL, STRM>>::type Stg;
+  static_assert(Stg::SBM >= REG, "a slot holds the work region");
+  Stg sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     const bool live = lane_ok && mi < sg.cnt();
-    float *sm = reinterpret_cast<float *>(sg.buf() + (lane_ok ? mi : 0) * REG);
+    float *sm = reinterpret_cast<float *>(sg.buf() + (lane_ok ? mi : 0) * Stg::SBM);
     const unsigned sbase = smem_u32(sm);
     float2 p[RA][CB / 2];
     // own block of the staged matrix (packed, row stride N)

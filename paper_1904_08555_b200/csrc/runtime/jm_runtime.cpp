@@ -1205,6 +1205,11 @@ int jit_mat_stats(jm_stats *out) {
           ready += st == S_READY;
           failed += st == S_FAILED;
         }
+        if (n <= NLAT) {   // the latency variant's keys (tiny batches)
+          const int st = g_lat_slots[a][t][n].state.load();
+          ready += st == S_READY;
+          failed += st == S_FAILED;
+        }
       }
   out->keys_ready = ready;
   out->keys_failed = failed;
