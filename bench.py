@@ -233,9 +233,12 @@ def relaunch(a) -> int:
     command as N ranks under torch.distributed.run (one process per GPU,
     rendezvous on 127.0.0.1), so the driver's command line and torchrun's
     give the same job."""
+    # torch.distributed.run's own parser takes "--n" as an abbreviation of its
+    # --nnodes / --nproc-per-node even after the script: pass it as --size
+    args = ["--size" + x[3:] if x == "--n" or x.startswith("--n=") else x for x in sys.argv[1:]]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={free_port()}",
-           os.path.abspath(__file__), *sys.argv[1:]]
+           os.path.abspath(__file__), *args]
     return subprocess.call(cmd)
 
 

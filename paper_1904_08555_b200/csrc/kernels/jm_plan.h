@@ -110,8 +110,12 @@ constexpr int TPM_THREADS = 128;
 #ifndef JM_DMMA_RT_LARGE
 #define JM_DMMA_RT_LARGE 1   // row tiles per warp for other n > WARP_MAX (one warp per 8-row tile)
 #endif
+// (r02: the border generalised to BR = 3, 4 — two-chunk column loads,
+// reduce-scatter shuffles — measured slower than the padded tiles with
+// k-compaction: n = 19 0.54 -> 0.45, 20 0.64 -> 0.49, 28 0.72 -> 0.60,
+// 36 0.76 -> 0.69 of the FP64 pipe at R = 100; profiles/r02_ab_dmma.md)
 #ifndef JM_DMMA_BORDER_MAX
-#define JM_DMMA_BORDER_MAX 4         // n = 8K + r, r <= this: border tiles by DFMA (run_dmma BORD)
+#define JM_DMMA_BORDER_MAX 2         // n = 8K + r, r <= this: border tiles by DFMA (run_dmma BORD)
 #endif
 #ifndef JM_DMMA_BORDER_MIN
 #define JM_DMMA_BORDER_MIN 16        // ... and n above this
@@ -186,21 +190,23 @@ struct F32TRow { int n, ra, cb, ldmpad, pad, colblk, trfast, qmix, maxreg, kunro
 // FP64 register tiles (DFMA, run_f64t) for the sizes where DMMA's 8 x 8 x 4
 // granularity wastes most of the pipe; the same fields, CB a multiple of 2
 // (a 16-B chunk holds two doubles).  Only the sizes listed take this kind.
-// Candidates from the r02 search (tools/f64_candidates.json, profiles/r02_f64_search.jsonl;
-// FP64 pipe at R = 100, "was" = the DMMA / TPMS kinds before k-compaction and
-// the BR <= 4 border), kept behind JM_F64T_ON until measured against those.
+// Picked from the r02 search (tools/f64_candidates.json, profiles/r02_f64_search.jsonl)
+// and kept where they beat the DMMA tile WITH k-compaction (profiles/r02_ab_dmma.md,
+// FP64 pipe at R = 100, DMMA in brackets): n = 11 0.512 (0.375), 12 0.636 (0.496),
+// 18 0.560 (0.480), 19 0.613 (0.542), 20 0.704 (0.636); n = 35 (0.656 vs 0.689)
+// stays DMMA.  Their low-repeat kernel is the DMMA ring (plan_stream).
+// JM_F64T_ON=0: none.
 #ifndef JM_F64T_ON
-#define JM_F64T_ON 0
+#define JM_F64T_ON 1
 #endif
 constexpr F32TRow F64T_TABLE[] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
 #if JM_F64T_ON
-    {11, 3, 12, 4, 1, 0, 1, 0, 255, 2},   // 0.512 of the pipe (was 0.304), 208 regs
-    {12, 3, 12, 4, 1, 0, 1, 0, 168, 6},   // 0.630 of the pipe (was 0.398), 146 regs
-    {18, 6, 10, 4, 6, 0, 0, 0, 255, 9},   // 0.558 of the pipe (was 0.426), 224 regs
-    {19, 5, 10, 4, 1, 1, 1, 0, 255, 9},   // 0.612 of the pipe (was 0.470), 206 regs
-    {20, 5, 10, 4, 1, 1, 1, 0, 255, 10},  // 0.683 of the pipe (was 0.546), 200 regs
-    {35, 7, 6, 4, 0, 0, 0, 0, 168, 17},   // 0.650 of the pipe (was 0.611), 152 regs
+    {11, 3, 12, 4, 1, 0, 1, 0, 255, 2},
+    {12, 3, 12, 4, 1, 0, 1, 0, 168, 6},
+    {18, 6, 10, 4, 6, 0, 0, 0, 255, 9},
+    {19, 5, 10, 4, 1, 1, 1, 0, 255, 9},
+    {20, 5, 10, 4, 1, 1, 1, 0, 255, 10},
 #endif
 };
 constexpr F32TRow F32T_TABLE[] = {
@@ -539,11 +545,15 @@ JM_HD constexpr int stream_lo(int n, int dtype) {
 // (1.13x at R = 8, 1.05x at R = 100) and loses below (0.89x at R = 1), so it
 // streams above the lower bound stream_lo (r01_all_n_sweep.jsonl,
 // r01_tpm_stream_sweep.jsonl).
-// FP64 / FP32 register tiles: the prefetching stage (twice the shared
-// memory per matrix) wins below this R(n+1)
+// FP64 register tiles: the DMMA ring wins below this R(n+1) (R = 1: 0.69-0.90
+// of HBM against 0.31-0.47 for the register tiles; crossovers measured at
+// R = 1..16, profiles/r02_f64t_xover.jsonl: n = 11, 12 ~ 100-140, 18 ~ 150,
+// 19, 20 ~ 300)
 #ifndef JM_F64T_RN
-#define JM_F64T_RN 60
+#define JM_F64T_RN 0     // > 0: one switch point for every register-tile size
 #endif
+JM_HD constexpr int f64t_rn(int n) { return JM_F64T_RN > 0 ? JM_F64T_RN : n <= 12 ? 120 : n <= 18 ? 160 : 330; }
+// FP32 register tiles: the streaming kernel (ring / prefetching stage) below this R(n+1)
 #ifndef JM_F32T_RN
 #define JM_F32T_RN 140
 #endif
@@ -551,7 +561,7 @@ JM_HD constexpr int stream_rn_tpm(int n, int dtype) { return (dtype == 0 && n ==
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype)               ? 0
          : tile_for(n, dtype) == Tile::TPM ? stream_rn_tpm(n, dtype)
-         : tile_for(n, dtype) == Tile::Reg ? JM_F64T_RN
+         : tile_for(n, dtype) == Tile::Reg ? f64t_rn(n)
          : (dtype == 0 && tile_for(n, dtype) == Tile::Tpms) ? (n == 12 ? 0 : 20)   // R = 1: row-panel ring
          : dtype == 1        ? stream_rn_f64(n)
          : f32p_use(n)       ? 64
@@ -605,7 +615,8 @@ JM_HD constexpr bool f32t_ring(int n) {
 }
 // matrices per round of each kind (the resident plan's chunk)
 JM_HD constexpr int round_mpc(int n, int dtype) {
-  return (tile_for(n, dtype) == Tile::Dmma || (dtype == 1 && tile_for(n, dtype) == Tile::Tpms))
+  return (tile_for(n, dtype) == Tile::Dmma ||
+          (dtype == 1 && (tile_for(n, dtype) == Tile::Tpms || tile_for(n, dtype) == Tile::Reg)))
              ? (dmma_w(n, true) == 1 ? DMMA_WPC : 1)
          : f32p_use(n)                   ? F32P_WPC * f32p_mpw(n)
                                          : f32t_mpc(n);
@@ -618,10 +629,8 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   if (!stream_ok(n, dtype)) return plan_specialized(n, dtype);
   if (tile_for(n, dtype) == Tile::TPM)
     return Plan{(int)Tile::TPM, TPM_THREADS, TPM_THREADS, 2 * stage_bytes(TPM_THREADS, n, es), 1};
-  if (tile_for(n, dtype) == Tile::Reg)
-    return Plan{(int)Tile::Reg, 32 * f32t_wpc(n, 1), f32t_mpc(n, 1), 2 * rup(f32t_mpc(n, 1) * f32t_region(n, 1), 16),
-                f32t_wpm(n, 1)};
-  if (tile_for(n, dtype) == Tile::Dmma || (dtype == 1 && tile_for(n, dtype) == Tile::Tpms)) {   // (Tpms: DMMA ring)
+  if (tile_for(n, dtype) == Tile::Dmma ||
+      (dtype == 1 && (tile_for(n, dtype) == Tile::Tpms || tile_for(n, dtype) == Tile::Reg))) {   // (Tpms, Reg: DMMA ring)
     const int w = dmma_w(n, true);
     const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers
     return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm, dmma_slot(n)) + own * dmma_scr(n), w};

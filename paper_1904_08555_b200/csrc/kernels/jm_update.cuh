@@ -1468,7 +1468,8 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
     if constexpr (STRM) run_dmma<N, A, 1, true>(in, out, batch, repeat);   // low repeat: the DMMA ring
     else run_tpms<N, T, A>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Reg) {
-    run_f64t<N, A, STRM>(in, out, batch, repeat);
+    if constexpr (STRM) run_dmma<N, A, 1, true>(in, out, batch, repeat);   // low repeat: the DMMA ring
+    else run_f64t<N, A, false>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Dmma) {
     run_dmma<N, A, dmma_w(N, STRM), STRM>(in, out, batch, repeat);
   } else if constexpr (f32p_use(N)) {

@@ -21,7 +21,8 @@ def _env(**kw):
 
 
 def test_gpus_n_relaunches_n_ranks():
-    p = subprocess.run([sys.executable, BENCH, "--gpus", "2", "--steps", "1", "--warmup", "3"],
+    # (--n: torch.distributed.run's parser would take it for --nnodes; relaunch passes --size)
+    p = subprocess.run([sys.executable, BENCH, "--gpus", "2", "--steps", "1", "--warmup", "3", "--n", "8"],
                        env=_env(JM_BENCH_DRY_RUN="1"), capture_output=True, text=True, timeout=300)
     assert p.returncode == 0, p.stderr[-2000:]
     recs = [json.loads(ln) for ln in p.stdout.splitlines() if ln.startswith("{")]

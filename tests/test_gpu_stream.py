@@ -45,14 +45,31 @@ def _batch_for(n):
     return 293 if n <= 12 else (77 if n <= 32 else 9)
 
 
+# f64 sizes whose resident kernel is the DFMA register tile (jm_plan.h F64T_TABLE)
+# and whose low-repeat kernel is the DMMA ring
+F64_REG_N = (11, 12, 18, 19, 20)
+
+
 def _same_bits(n, dt):
     # both variants form every entry in the same order, except f64 n = 33 / 34,
     # where the resident kernel (whole matrix per warp) takes the thin-border
     # DFMA path and the streaming one (one warp per row tile) does not, and
     # f64 n = 9 / 10 and f32 n = 12..14, whose resident kernel is thread per
     # matrix with a staged product (TPMS) and whose low-repeat kernel is the
-    # DMMA ring / the row-panel ring
-    return not ((dt == "f64" and n in (9, 10, 33, 34)) or (dt == "f32" and n in (12, 13, 14)))
+    # DMMA ring / the row-panel ring, and the DFMA register-tile sizes
+    return not ((dt == "f64" and n in (9, 10, 33, 34) + F64_REG_N) or (dt == "f32" and n in (12, 13, 14)))
+
+
+def test_f64_reg_sizes_match_the_plan(jm):
+    """F64_REG_N above is the set of sizes the planner gives the DFMA register tiles."""
+    got = []
+    for n in range(1, 65):
+        jm.jit_mat_prepare(n, "double")
+    for k in jm.jit_mat_key_info():
+        if k["op"] == 0 and k["dtype"] == 1 and k["kind"] == 0 and k["addend"] == 0 and k["variant"] == 0 \
+                and k["tile_name"] == "f64_reg":
+            got.append(k["n"])
+    assert sorted(got) == list(F64_REG_N)
 
 
 def _run(jm, x, repeat, variant, addend="ones", inplace=False):

@@ -187,10 +187,13 @@ class Cand:
                 "wf": (wa, wb, ws), "region": self.region}
 
 
+RA_MAX, CB_MAX = 8, 16   # r02 extended search: tools/f32_search.py --wide sets 13 / 24
+
+
 def candidates(n, maxreg=128, es=4):
     vec = 16 // es
-    for ra in range(2, 9):
-        for cb in range(vec, 17, vec):
+    for ra in range(2, RA_MAX + 1):
+        for cb in range(vec, CB_MAX + 1, vec):
             rg, cg = cdiv(n, ra), cdiv(n, cb)
             t = rg * cg
             if t > 64 or (es // 4) * (ra * cb + vec * ra + 2 * cb) + 14 > 240:

@@ -41,10 +41,12 @@ def write_table(rows: list[str], dt: str = "f32") -> None:
     open(PLAN, "w").write(s)
 
 
-def candidates(ns, top, es=4):
+def candidates(ns, top, es=4, wide=False):
     import f32_layout as L
+    if wide:   # r02: register tiles up to 12 (FP64) / 13 (FP32) rows and 12 / 24 columns
+        L.RA_MAX, L.CB_MAX = (12, 12) if es == 8 else (13, 24)
     from multiprocessing import Pool
-    with Pool() as pool:
+    with Pool(initializer=_widen, initargs=(L.RA_MAX, L.CB_MAX)) as pool:
         res = pool.starmap(L.best_for, [(n, top, 128, es) for n in ns])
     out = {}
     for n, lst in zip(ns, res):
@@ -58,6 +60,11 @@ def candidates(ns, top, es=4):
             cs.append(dict(base, maxreg=255, kunroll=2))
         out[n] = cs
     return out
+
+
+def _widen(ra_max, cb_max):
+    import f32_layout as L
+    L.RA_MAX, L.CB_MAX = ra_max, cb_max
 
 
 def run(cands: dict, out: str, steps: int, dt: str = "f32", baseline: bool = False) -> None:
@@ -121,13 +128,14 @@ def main():
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--baseline", action="store_true", help="also time the sizes with the table empty")
     ap.add_argument("--margin", type=float, default=0.0)
+    ap.add_argument("--wide", action="store_true", help="larger register tiles (see candidates())")
     a = ap.parse_args()
     if a.candidates:
         ns = []
         for part in a.candidates.split(","):
             lo, _, hi = part.partition("..")
             ns += list(range(int(lo), int(hi or lo) + 1))
-        print(json.dumps(candidates(ns, a.top, 8 if a.dtype == "f64" else 4), indent=0))
+        print(json.dumps(candidates(ns, a.top, 8 if a.dtype == "f64" else 4, a.wide), indent=0))
     elif a.run:
         run(json.load(open(a.run)), a.out, a.steps, a.dtype, a.baseline)
     elif a.pick:

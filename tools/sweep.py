@@ -145,7 +145,7 @@ def c4(fh, stream):
         jm.jit_mat_set_stream(stream.cuda_stream)
         jm.jit_mat_reset_stats()
         tdt = torch.float64 if dt == "f64" else torch.float32
-        groups = groups_ = []
+        groups = []
         for n in range(2, 65):
             if counts[n]:
                 x = torch.empty(int(counts[n]), n, n, dtype=tdt, device="cuda")
@@ -180,18 +180,18 @@ def c4(fh, stream):
         # cold again, the cold keys compiled as a few multi-expression NVRTC
         # programs (JM_FLAG_BATCH_COMPILE), for several group counts
         batched = {}
-        for groups in ("1", "4", str(os.cpu_count() or 8), "16"):
-            os.environ["JIT_MAT_COMPILE_GROUPS"] = groups
+        for ng in ("1", "4", str(os.cpu_count() or 8), "16"):
+            os.environ["JIT_MAT_COMPILE_GROUPS"] = ng
             jm.jit_mat_shutdown()
             jm.jit_mat_init(0)
             jm.jit_mat_set_stream(stream.cuda_stream)
             jm.jit_mat_reset_stats()
             t0 = time.perf_counter()
             jm.jit_mat_run_many([dict(n=n, dtype=dt, batch=b, repeat=R, in_ptr=x.data_ptr(),
-                                      out_ptr=y.data_ptr()) for n, b, x, y in groups_],
+                                      out_ptr=y.data_ptr()) for n, b, x, y in groups],
                                 stream=stream.cuda_stream, batch_compile=True)
             stream.synchronize()
-            batched[groups] = {"cold_pass_s": time.perf_counter() - t0, "programs": jm.jit_mat_stats()["programs"],
+            batched[ng] = {"cold_pass_s": time.perf_counter() - t0, "programs": jm.jit_mat_stats()["programs"],
                                "compilations": jm.jit_mat_stats()["compilations"]}
         os.environ.pop("JIT_MAT_COMPILE_GROUPS", None)
         res = {}
