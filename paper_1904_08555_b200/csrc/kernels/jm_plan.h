@@ -193,7 +193,9 @@ struct F32TRow { int n, ra, cb, ldmpad, pad, colblk, trfast, qmix, maxreg, kunro
 // Picked from the r02 search (tools/f64_candidates.json, profiles/r02_f64_search.jsonl)
 // and kept where they beat the DMMA tile WITH k-compaction (profiles/r02_ab_dmma.md,
 // FP64 pipe at R = 100, DMMA in brackets): n = 11 0.512 (0.375), 12 0.636 (0.496),
-// 18 0.560 (0.480), 19 0.613 (0.542), 20 0.704 (0.636); n = 35 (0.656 vs 0.689)
+// 17 0.553 (0.536), 18 0.628 (0.480), 19 0.613 (0.542), 20 0.704 (0.636) — 17
+// and 18 as 9 x 6 tiles from the wider search (profiles/r02_f64_wide_search.jsonl);
+// n = 35 (0.656 vs 0.689)
 // stays DMMA.  Their low-repeat kernel is the DMMA ring (plan_stream).
 // JM_F64T_ON=0: none.
 #ifndef JM_F64T_ON
@@ -204,15 +206,16 @@ constexpr F32TRow F64T_TABLE[] = {
 #if JM_F64T_ON
     {11, 3, 12, 4, 1, 0, 1, 0, 255, 2},
     {12, 3, 12, 4, 1, 0, 1, 0, 168, 6},
-    {18, 6, 10, 4, 6, 0, 0, 0, 255, 9},
+    {17, 9, 6, 3, 1, 1, 1, 0, 255, 8},    // (r02 wide search: 0.553 vs the border DMMA's 0.536)
+    {18, 9, 6, 3, 1, 1, 1, 0, 255, 9},    // (r02 wide search: 0.628; 6 x 10 0.560)
     {19, 5, 10, 4, 1, 1, 1, 0, 255, 9},
     {20, 5, 10, 4, 1, 1, 1, 0, 255, 10},
 #endif
 };
 constexpr F32TRow F32T_TABLE[] = {
-    {17, 6, 12, 4, 6, 0, 0, 0, 168, 4},  // 0.433 of the pipe, 157 regs
-    {18, 6, 12, 4, 6, 0, 0, 0, 168, 4},  // 0.492 of the pipe, 155 regs
-    {19, 5, 12, 4, 1, 1, 1, 0, 168, 4},  // 0.535 of the pipe, 141 regs
+    {17, 6, 20, 2, 1, 0, 1, 0, 255, 4},  // 0.515 of the pipe, 200 regs (r02 wide search; was 0.434)
+    {18, 6, 20, 2, 1, 0, 1, 0, 255, 4},  // 0.586 of the pipe, 247 regs (r02 wide search; was 0.491)
+    {19, 5, 20, 1, 1, 0, 1, 0, 255, 4},  // 0.638 of the pipe, 205 regs (r02 wide search; was 0.487)
     {20, 5, 12, 4, 1, 1, 1, 0, 168, 5},  // 0.618 of the pipe, 146 regs
     {21, 7, 12, 1, 5, 0, 0, 0, 168, 5},  // 0.563 of the pipe, 160 regs
     {22, 6, 12, 4, 1, 1, 1, 0, 168, 5},  // 0.609 of the pipe, 150 regs
@@ -242,10 +245,10 @@ constexpr F32TRow F32T_TABLE[] = {
     {46, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.700 of the pipe, 154 regs
     {47, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.718 of the pipe, 154 regs
     {48, 6, 12, 1, 0, 0, 1, 0, 168, 12},  // 0.750 of the pipe, 154 regs
-    {49, 7, 16, 1, 0, 0, 0, 0, 255, 2},  // 0.491 of the pipe, 220 regs
-    {50, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.509 of the pipe, 214 regs
-    {51, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.530 of the pipe, 216 regs
-    {52, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.516 of the pipe, 244 regs
+    {49, 13, 8, 4, 0, 0, 1, 0, 255, 2},  // 0.518 of the pipe, 227 regs (r02 wide search; was 0.492)
+    {50, 13, 8, 4, 0, 0, 1, 0, 255, 2},  // 0.534 of the pipe, 229 regs (r02 wide search; was 0.509)
+    {51, 13, 8, 4, 0, 0, 1, 0, 255, 2},  // 0.560 of the pipe, 227 regs (r02 wide search; was 0.508)
+    {52, 13, 8, 1, 0, 0, 1, 0, 255, 2},  // 0.533 of the pipe, 230 regs (r02 wide search; was 0.516)
     {53, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.554 of the pipe, 238 regs
     {54, 7, 8, 1, 0, 0, 1, 0, 168, 2},  // 0.581 of the pipe, 160 regs
     {55, 7, 8, 1, 0, 0, 1, 0, 168, 2},  // 0.584 of the pipe, 154 regs
@@ -258,6 +261,12 @@ constexpr F32TRow F32T_TABLE[] = {
     {62, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.711 of the pipe, 244 regs
     {63, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.730 of the pipe, 236 regs
     {64, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.762 of the pipe, 217 regs
+};
+// The low-repeat (streaming) kernel's own shapes, where they differ from the
+// resident kernel's (R = 1 is bound by moving the matrices, so a smaller work
+// region -- more warps per SM -- can beat the faster k loop); same fields.
+constexpr F32TRow F32TS_TABLE[] = {
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
 };
 #ifndef JM_F32T_RA                // tuning hooks: force the register-tile shape / layout / knobs
 #define JM_F32T_RA 0
@@ -291,10 +300,13 @@ constexpr F32TRow F32T_TABLE[] = {
 #endif
 // the default shape when no table entry applies: the tile that covers the
 // matrix with <= 64 threads and wastes least (padding x idle lanes x loads per FFMA2)
-// (dt = 0 float, 1 double: VEC = 16 / element size elements per 16-B chunk)
-JM_HD constexpr int tt_vec(int dt) { return dt ? 2 : 4; }
+// (dt = 0 float, 1 double, 2 float in the low-repeat (streaming) kernel, which
+// may take its own shape from F32TS_TABLE; VEC = 16 / element size elements
+// per 16-B chunk)
+JM_HD constexpr int tt_vec(int dt) { return dt == 1 ? 2 : 4; }
+JM_HD constexpr int tt_es(int dt) { return dt == 1 ? 8 : 4; }
 JM_HD constexpr F32T f32t_default(int n, int dt = 0) {
-  const int v = tt_vec(dt), w = dt ? 2 : 1;   // elements per chunk, 32-bit registers per element
+  const int v = tt_vec(dt), w = dt == 1 ? 2 : 1;   // elements per chunk, 32-bit registers per element
   F32T best{8, 8, cdiv(n, 8), cdiv(n, 8), 0, 0, 0, 1, 0, 168, 2, 4};
   double bs = -1.0;
   for (int ra = 8; ra >= 2; --ra)
@@ -317,14 +329,17 @@ JM_HD constexpr F32T f32t_tile(int n, int dt = 0) {
     t = F32T{r.ra, r.cb, cdiv(n, r.ra), cdiv(n, r.cb), cdiv(n, r.cb) * r.cb + tt_vec(dt) * r.ldmpad, r.pad,
              r.colblk, r.trfast, r.qmix, r.maxreg, r.kunroll, 4};
   };
-  if (dt) {
+  if (dt == 1) {
     for (const F32TRow &r : F64T_TABLE)
       if (r.n == n && r.ra > 0) take(r);
   } else {
     for (const F32TRow &r : F32T_TABLE)
       if (r.n == n && r.ra > 0) take(r);
+    if (dt == 2)
+      for (const F32TRow &r : F32TS_TABLE)
+        if (r.n == n && r.ra > 0) take(r);
   }
-  if (dt) {   // (the JM_F32T_* tuning hooks below apply to the FP32 tiles)
+  if (dt == 1) {   // (the JM_F32T_* tuning hooks below apply to the FP32 tiles)
     if (t.rg * t.cg > 16 || t.rg * t.cg <= 8) t.qmix = 0;
     return t;
   }
@@ -365,9 +380,9 @@ JM_HD constexpr int f32t_srows(int n, int dt = 0) {
 }
 // one matrix region: the staged matrix (packed, n*n), then the published M
 JM_HD constexpr int f32t_region(int n, int dt = 0) {
-  return rup(f32t_srows(n, dt) * f32t_tile(n, dt).ldm * (dt ? 8 : 4) > n * n * (dt ? 8 : 4)
-                 ? f32t_srows(n, dt) * f32t_tile(n, dt).ldm * (dt ? 8 : 4)
-                 : n * n * (dt ? 8 : 4),
+  return rup(f32t_srows(n, dt) * f32t_tile(n, dt).ldm * tt_es(dt) > n * n * tt_es(dt)
+                 ? f32t_srows(n, dt) * f32t_tile(n, dt).ldm * tt_es(dt)
+                 : n * n * tt_es(dt),
              16) +
          16 * f32t_tile(n, dt).pad;
 }
@@ -606,12 +621,15 @@ JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8, 
 #ifndef JM_F32T_RING
 #define JM_F32T_RING 1
 #endif
+#ifndef JM_F32T_RING_ROWS
+#define JM_F32T_RING_ROWS 1   // n % 4 == 0: row-pitched copies straight into the work layout (run_f32t RROWS)
+#endif
 #ifndef JM_F32T_RING_MAXB
 #define JM_F32T_RING_MAXB (113 * 1024)   // ... while two CTAs still fit on an SM
 #endif
 JM_HD constexpr bool f32t_ring(int n) {
   return JM_F32T_RING && (n * n * 4) % 16 == 0 &&
-         ring_bytes(n, 4, f32t_mpc(n), f32t_region(n)) <= JM_F32T_RING_MAXB;
+         ring_bytes(n, 4, f32t_mpc(n, 2), f32t_region(n, 2)) <= JM_F32T_RING_MAXB;
 }
 // matrices per round of each kind (the resident plan's chunk)
 JM_HD constexpr int round_mpc(int n, int dtype) {
@@ -619,7 +637,7 @@ JM_HD constexpr int round_mpc(int n, int dtype) {
           (dtype == 1 && (tile_for(n, dtype) == Tile::Tpms || tile_for(n, dtype) == Tile::Reg)))
              ? (dmma_w(n, true) == 1 ? DMMA_WPC : 1)
          : f32p_use(n)                   ? F32P_WPC * f32p_mpw(n)
-                                         : f32t_mpc(n);
+                                         : f32t_mpc(n, 2);
 }
 // Plan of the streaming variant: mpc = matrices per ring chunk (the host sizes
 // the grid by it); smem = the ring + the kind's own work areas.
@@ -643,10 +661,11 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   // region (the staged matrix is read into the accumulators, then the slot is
   // the work area; the result goes back packed and leaves by a bulk store)
   if (f32t_ring(n))
-    return Plan{(int)Tile::F32, 32 * f32t_wpc(n), chm, ring_bytes(n, es, rm, f32t_region(n)), f32t_wpm(n)};
+    return Plan{(int)Tile::F32, 32 * f32t_wpc(n, 2), chm, ring_bytes(n, es, rm, f32t_region(n, 2)), f32t_wpm(n, 2)};
   // F32T, odd n: the resident layout with the double-buffered cp.async stage
   // (the next chunk streams in while this one is updated)
-  return Plan{(int)Tile::F32, 32 * f32t_wpc(n), f32t_mpc(n), 2 * rup(f32t_mpc(n) * f32t_region(n), 16), f32t_wpm(n)};
+  return Plan{(int)Tile::F32, 32 * f32t_wpc(n, 2), f32t_mpc(n, 2), 2 * rup(f32t_mpc(n, 2) * f32t_region(n, 2), 16),
+              f32t_wpm(n, 2)};
 }
 
 // Note: k_update passes only maxThreads to __launch_bounds__.  Registers are

@@ -260,9 +260,15 @@ struct Stager {
 // loads overlap the compute of chunk i.  A round (what the tiling kinds see
 // through buf()/cnt()) is MPC matrices.  The one ragged chunk at the end of
 // the batch is staged synchronously with element copies.
-template <int N, int ES, int NT, int MPC, int K, int S, int SLOT = 0>
+// RPB > 0 (row-pitched): each ROW of a matrix is its own bulk copy into the
+// slot at a row pitch of RPB bytes, i.e. straight into a kind's padded work
+// layout (the rows must be multiples of 16 B); results leave row by row too.
+template <int N, int ES, int NT, int MPC, int K, int S, int SLOT = 0, int RPB = 0>
 struct Ring {
   static constexpr int MB = N * N * ES;
+  static constexpr int ROWB = N * ES;
+  static constexpr bool ROWS = RPB > 0;                   // one copy per row
+  static_assert(!ROWS || (ROWB % 16 == 0 && RPB % 16 == 0 && RPB >= ROWB), "row-pitched copies of 16-B rows");
   static constexpr bool PER = (MB % 16) == 0;             // one copy per matrix
   static constexpr int SBM = ring_sbm(N, ES, SLOT);       // matrix slot stride
   static constexpr int RB = MPC * SBM, CHM = K * MPC, CHB = K * RB, GB = CHM * MB;
@@ -287,7 +293,12 @@ struct Ring {
     const char *g = in + c * GB;
     char *d = base + st * CHB;
     if (tid == 0) mbar_expect_tx(bar + st, GB);
-    if constexpr (PER) {
+    if constexpr (ROWS) {
+      for (int e = tid; e < CHM * N; e += 32) {
+        const int m = e / N, r = e - m * N;
+        bulk_g2s(d + m * SBM + r * RPB, g + (size_t)e * ROWB, ROWB, bar + st);
+      }
+    } else if constexpr (PER) {
       for (int m = tid; m < CHM; m += 32) bulk_g2s(d + m * SBM, g + (size_t)m * MB, MB, bar + st);
     } else {
       if (tid == 0) bulk_g2s(d, g, GB, bar + st);
@@ -297,7 +308,12 @@ struct Ring {
   __device__ __forceinline__ void store(long long c, int st) {
     char *g = out + c * GB;
     const char *d = base + st * CHB;
-    if constexpr (PER) {
+    if constexpr (ROWS) {
+      for (int e = tid; e < CHM * N; e += 32) {
+        const int m = e / N, r = e - m * N;
+        bulk_s2g(g + (size_t)e * ROWB, d + m * SBM + r * RPB, ROWB);
+      }
+    } else if constexpr (PER) {
       for (int m = tid; m < CHM; m += 32) bulk_s2g(g + (size_t)m * MB, d + m * SBM, MB);
     } else {
       if (tid == 0) bulk_s2g(g, d, GB);
@@ -332,7 +348,8 @@ struct Ring {
     } else {   // the ragged last chunk: its stage may still be draining stores
       if (tid < 32) bulk_wait_read_all();
       __syncthreads();
-      stage_in<N, ES, SBM, NT, false>(in + ch * GB, base + s * CHB, (int)(batch - ch * CHM), tid);
+      if constexpr (ROWS) rows_io<true>(const_cast<char *>(in) + ch * GB, base + s * CHB, (int)(batch - ch * CHM));
+      else stage_in<N, ES, SBM, NT, false>(in + ch * GB, base + s * CHB, (int)(batch - ch * CHM), tid);
       __syncthreads();
     }
   }
@@ -350,7 +367,24 @@ struct Ring {
         }
       }
     } else {
-      stage_out<N, ES, SBM, NT, false>(out + ch * GB, base + s * CHB, (int)(batch - ch * CHM), tid);
+      if constexpr (ROWS) rows_io<false>(out + ch * GB, base + s * CHB, (int)(batch - ch * CHM));
+      else stage_out<N, ES, SBM, NT, false>(out + ch * GB, base + s * CHB, (int)(batch - ch * CHM), tid);
+    }
+  }
+  // the ragged chunk, row-pitched: element copies global <-> slot rows
+  template <bool IN>
+  __device__ __forceinline__ void rows_io(char *g, char *d, int cnt) {
+    for (int e = tid; e < cnt * N * N; e += NT) {
+      const int m = e / (N * N), q = e - m * (N * N), r = q / N, c = q - r * N;
+      char *sp = d + m * SBM + r * RPB + c * ES;
+      char *gp = g + (size_t)e * ES;
+      if constexpr (ES == 8) {
+        if (IN) *reinterpret_cast<u64 *>(sp) = *reinterpret_cast<const u64 *>(gp);
+        else *reinterpret_cast<u64 *>(gp) = *reinterpret_cast<const u64 *>(sp);
+      } else {
+        if (IN) *reinterpret_cast<unsigned *>(sp) = *reinterpret_cast<const unsigned *>(gp);
+        else *reinterpret_cast<unsigned *>(gp) = *reinterpret_cast<const unsigned *>(sp);
+      }
     }
   }
   __device__ __forceinline__ void next() {
@@ -1023,23 +1057,55 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
     char *b0 = INPL ? reinterpret_cast<char *>(sm) : bufs;
     char *b1 = INPL ? bufs : bufs + MBUF;
     float m[RP][NC];
-#pragma unroll
-    for (int i = 0; i < RP; ++i)
-#pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        const int row = r0 + i;
-        m[i][j] = (live && row < N && j < N) ? sm[row * N + j] : 0.0f;
+    // VCP (own row buffers, rows of whole 16-B chunks): the warp copies its
+    // matrices' packed slots into their first row buffers chunk by chunk (lane
+    // = consecutive chunks: both sides bank-conflict free), then each thread
+    // reads its rows back with LDS.128 in the publish pattern.  r02: the
+    // per-element reads of the packed slot put a matrix's 4 threads (rows
+    // 256 B apart) on one bank (60 % of the ring kernel's wavefronts conflicted
+    // at n = 16, R = 1; profiles/r02_ncu_baseline_f32.md)
+    constexpr bool VCP = !INPL && (N % 4 == 0);
+    constexpr int CPM = N * NCR;                  // 16-B chunks per matrix
+    if constexpr (VCP) {
+#pragma unroll 4
+      for (int e = lane; e < MPW * CPM; e += 32) {
+        const int ml = e / CPM, cc = e - ml * CPM, row = cc / NCR, q = cc - row * NCR, ms = warp * MPW + ml;
+        const float4 v = ms < cnt ? *reinterpret_cast<const float4 *>(stage + ms * Stg::SBM + cc * 16)
+                                  : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        *reinterpret_cast<float4 *>(smem + Stg::BYTES + ms * 2 * MBUF + f32p_off<NCS>(row, q)) = v;
       }
-    if constexpr (INPL) __syncwarp();         // the matrix's threads have read the slot
+      __syncwarp();
 #pragma unroll
-    for (int i = 0; i < RP; ++i)
-      if (r0 + i < N) {
+      for (int i = 0; i < RP; ++i)
 #pragma unroll
-        for (int q = 0; q < NCR; ++q)
-          *reinterpret_cast<float4 *>(b0 + f32p_off<NCS>(r0 + i, q)) =
-              make_float4(m[i][4 * q], m[i][4 * q + 1], m[i][4 * q + 2], m[i][4 * q + 3]);
-      }
-    __syncwarp();
+        for (int q = 0; q < NCR; ++q) {
+          float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          if (r0 + i < N) v = *reinterpret_cast<const float4 *>(b0 + f32p_off<NCS>(r0 + i, q));
+          m[i][4 * q] = v.x; m[i][4 * q + 1] = v.y; m[i][4 * q + 2] = v.z; m[i][4 * q + 3] = v.w;
+        }
+#pragma unroll
+      for (int i = 0; i < RP; ++i)
+#pragma unroll
+        for (int j = 4 * NCR; j < NC; ++j) m[i][j] = 0.0f;
+    } else {
+#pragma unroll
+      for (int i = 0; i < RP; ++i)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const int row = r0 + i;
+          m[i][j] = (live && row < N && j < N) ? sm[row * N + j] : 0.0f;
+        }
+      if constexpr (INPL) __syncwarp();         // the matrix's threads have read the slot
+#pragma unroll
+      for (int i = 0; i < RP; ++i)
+        if (r0 + i < N) {
+#pragma unroll
+          for (int q = 0; q < NCR; ++q)
+            *reinterpret_cast<float4 *>(b0 + f32p_off<NCS>(r0 + i, q)) =
+                make_float4(m[i][4 * q], m[i][4 * q + 1], m[i][4 * q + 2], m[i][4 * q + 3]);
+        }
+      __syncwarp();
+    }
 #pragma unroll 1
     for (int r = 0; r < repeat; ++r) {
       const char *cur = (r & 1) ? b1 : b0;
@@ -1116,7 +1182,16 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
       }
       __syncwarp();
     }
-    if (live) {
+    if constexpr (VCP) {   // the final M is the buffer the last update wrote: back to the packed slots
+      const int fb = (repeat & 1) ? MBUF : 0;
+#pragma unroll 4
+      for (int e = lane; e < MPW * CPM; e += 32) {
+        const int ml = e / CPM, cc = e - ml * CPM, row = cc / NCR, q = cc - row * NCR, ms = warp * MPW + ml;
+        if (ms < cnt)
+          *reinterpret_cast<float4 *>(stage + ms * Stg::SBM + cc * 16) =
+              *reinterpret_cast<const float4 *>(smem + Stg::BYTES + ms * 2 * MBUF + fb + f32p_off<NCS>(row, q));
+      }
+    } else if (live) {
 #pragma unroll
       for (int i = 0; i < RP; ++i)
 #pragma unroll
@@ -1161,14 +1236,15 @@ __device__ __forceinline__ void sts128(unsigned a, float x, float y, float z, fl
 template <int N, Addend A, bool STRM>
 __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__restrict__ out,
                                          long long batch, int repeat) {
-  constexpr F32T TL = f32t_tile(N);
+  constexpr int DT = STRM ? 2 : 0;   // the streaming kernel may have its own shape (jm_plan.h F32TS_TABLE)
+  constexpr F32T TL = f32t_tile(N, DT);
   constexpr int RA = TL.ra, CB = TL.cb, RG = TL.rg, CG = TL.cg, NH = CB / 4, LDM = TL.ldm;
-  constexpr int TPMAT = RG * CG, WPM = f32t_wpm(N), MPW = f32t_mpw(N), WPC = f32t_wpc(N);
-  constexpr int MPC = f32t_mpc(N), NR = f32t_nr(N), NC = CG * CB, SROWS = f32t_srows(N);
-  constexpr int REG = f32t_region(N), ES = 4, MB = N * N * 4, NT = 32 * WPC;
+  constexpr int TPMAT = RG * CG, WPM = f32t_wpm(N, DT), MPW = f32t_mpw(N, DT), WPC = f32t_wpc(N, DT);
+  constexpr int MPC = f32t_mpc(N, DT), NR = f32t_nr(N, DT), NC = CG * CB, SROWS = f32t_srows(N, DT);
+  constexpr int REG = f32t_region(N, DT), ES = 4, MB = N * N * 4, NT = 32 * WPC;
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   constexpr bool PAD = (NR != N) || (NC != N);
-  static_assert(CB % 4 == 0 && NC >= f32t_kp(N), "tile shape");
+  static_assert(CB % 4 == 0 && NC >= f32t_kp(N, DT), "tile shape");
   static_assert(WPC % WPM == 0, "whole matrices per CTA");
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1195,7 +1271,15 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
   // each slot widened to the work region (f32t_ring); odd n keep the
   // double-buffered cp.async stage (the next chunk streams in while this one
   // is updated)
-  typedef typename Pick<STRM && f32t_ring(N), Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, REG>,
+  // (n % 4 == 0: the ring copies each row straight into the work layout (row
+  // pitch LDM), so the matrix is read into the accumulators and written back
+  // with conflict-free 16-B accesses in the publish pattern instead of
+  // element accesses of the packed layout, whose rows 2^k x 16 B apart put a
+  // quarter-warp on one bank: 53 % of the n = 32, R = 1 kernel's wavefronts
+  // conflicted, profiles/r02_ncu_kinds.md)
+  constexpr bool RROWS = STRM && f32t_ring(N) && JM_F32T_RING_ROWS && (N % 4) == 0;
+  typedef typename Pick<STRM && f32t_ring(N),
+                        Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, REG, RROWS ? LDM * 4 : 0>,
                         Stager<N, ES, REG, NT, MPC, AL, STRM>>::type Stg;
   static_assert(Stg::SBM >= REG, "a slot holds the work region");
   Stg sg(in, out, batch, smem);
@@ -1205,17 +1289,29 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
     float *sm = reinterpret_cast<float *>(sg.buf() + (lane_ok ? mi : 0) * Stg::SBM);
     const unsigned sbase = smem_u32(sm);
     float2 p[RA][CB / 2];
-    // own block of the staged matrix (packed, row stride N)
+    if constexpr (RROWS) {   // own block of the staged matrix (row-pitched: already the work layout)
 #pragma unroll
-    for (int i = 0; i < RA; ++i)
+      for (int i = 0; i < RA; ++i)
 #pragma unroll
-      for (int h = 0; h < NH; ++h)
-#pragma unroll
-        for (int e = 0; e < 4; e += 2) {
-          const int row = row_of(i), c0 = chunk_of(h) * 4 + e;
-          p[i][2 * h + e / 2].x = (live && row < N && c0 < N) ? sm[row * N + c0] : 0.0f;
-          p[i][2 * h + e / 2].y = (live && row < N && c0 + 1 < N) ? sm[row * N + c0 + 1] : 0.0f;
+        for (int h = 0; h < NH; ++h) {
+          const int row = row_of(i), c0 = chunk_of(h) * 4;
+          float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          if (live && row < N && c0 < N) v = lds128(sbase + (row * LDM + c0) * 4);
+          p[i][2 * h] = make_float2(v.x, v.y);
+          p[i][2 * h + 1] = make_float2(v.z, v.w);
         }
+    } else {   // own block of the staged matrix (packed, row stride N)
+#pragma unroll
+      for (int i = 0; i < RA; ++i)
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+#pragma unroll
+          for (int e = 0; e < 4; e += 2) {
+            const int row = row_of(i), c0 = chunk_of(h) * 4 + e;
+            p[i][2 * h + e / 2].x = (live && row < N && c0 < N) ? sm[row * N + c0] : 0.0f;
+            p[i][2 * h + e / 2].y = (live && row < N && c0 + 1 < N) ? sm[row * N + c0 + 1] : 0.0f;
+          }
+    }
     sync();                            // staged matrix read: the region becomes the work area
     if constexpr (SROWS > NR) {        // rows read as k padding (k in [NR, KP)) are zero
       if (live)
@@ -1264,7 +1360,7 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
 #pragma unroll
           for (int h = 0; h < NH; ++h) bq[h] = bn[h];
         };
-        constexpr int KU = f32t_kunroll(N);
+        constexpr int KU = f32t_kunroll(N, DT);
 #pragma unroll KU
         for (int kb = 0; kb < KF; ++kb) {
           const bool last = kb == KF - 1;
@@ -1295,7 +1391,19 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
           }
       }
     }
-    if (live) {                        // back to the packed layout for the store
+    if constexpr (RROWS) {             // rows leave from the work layout (the k loop's reads are done)
+      if (live) {
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            const int row = row_of(i), c0 = chunk_of(h) * 4;
+            if (row < N && c0 < N)
+              sts128(sbase + (row * LDM + c0) * 4, p[i][2 * h].x, p[i][2 * h].y, p[i][2 * h + 1].x,
+                     p[i][2 * h + 1].y);
+          }
+      }
+    } else if (live) {                 // back to the packed layout for the store
 #pragma unroll
       for (int i = 0; i < RA; ++i)
 #pragma unroll
@@ -1503,7 +1611,7 @@ __global__ void __maxnreg__(f32t_maxreg(N, sizeof(T) == 8)) k_update_rc(const T 
 }
 
 template <int N, class T, Addend A, Tile K>
-__global__ void __maxnreg__(f32t_maxreg(N, sizeof(T) == 8)) k_update_stream_rc(const T *__restrict__ in, T *__restrict__ out,
+__global__ void __maxnreg__(f32t_maxreg(N, sizeof(T) == 8 ? 1 : 2)) k_update_stream_rc(const T *__restrict__ in, T *__restrict__ out,
                                                                long long batch, int repeat) {
   update_body<N, T, A, K, true>(in, out, batch, repeat);
 }

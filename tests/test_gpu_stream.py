@@ -47,7 +47,7 @@ def _batch_for(n):
 
 # f64 sizes whose resident kernel is the DFMA register tile (jm_plan.h F64T_TABLE)
 # and whose low-repeat kernel is the DMMA ring
-F64_REG_N = (11, 12, 18, 19, 20)
+F64_REG_N = (11, 12, 17, 18, 19, 20)
 
 
 def _same_bits(n, dt):

@@ -173,7 +173,7 @@ class Cand:
         pad = self.n * self.n / (self.nr * self.nc)
         regs = self.regs
         wps = 4 if regs <= 128 else (3 if regs <= 168 else 2)      # warps per SMSP from registers
-        mats_sm = (227 * 1024) // self.region
+        mats_sm = (227 * 1024) // (self.region * (2 if STREAM else 1))   # the streaming kernel double-buffers
         warps_sm_smem = mats_sm * self.wpm // self.mpw if self.wpm > 1 else mats_sm // self.mpw
         wps = min(wps, warps_sm_smem // 4)
         # FP32 pipe vs the register-file return of shared loads (microbench
@@ -188,6 +188,7 @@ class Cand:
 
 
 RA_MAX, CB_MAX = 8, 16   # r02 extended search: tools/f32_search.py --wide sets 13 / 24
+STREAM = False           # score for the low-repeat kernel (two regions per matrix in flight)
 
 
 def candidates(n, maxreg=128, es=4):

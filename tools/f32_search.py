@@ -31,8 +31,8 @@ def row(c: dict) -> str:
             f"{c['qmix']}, {c['maxreg']}, {c['kunroll']}}},")
 
 
-def write_table(rows: list[str], dt: str = "f32") -> None:
-    name = "F32T_TABLE" if dt == "f32" else "F64T_TABLE"
+def write_table(rows: list[str], dt: str = "f32", stream: bool = False) -> None:
+    name = "F32TS_TABLE" if stream else "F32T_TABLE" if dt == "f32" else "F64T_TABLE"
     s = open(PLAN).read()
     a = s.index(f"constexpr F32TRow {name}[] = {{")
     b = s.index("};", a)
@@ -41,12 +41,13 @@ def write_table(rows: list[str], dt: str = "f32") -> None:
     open(PLAN, "w").write(s)
 
 
-def candidates(ns, top, es=4, wide=False):
+def candidates(ns, top, es=4, wide=False, stream=False):
     import f32_layout as L
     if wide:   # r02: register tiles up to 12 (FP64) / 13 (FP32) rows and 12 / 24 columns
         L.RA_MAX, L.CB_MAX = (12, 12) if es == 8 else (13, 24)
+    L.STREAM = stream
     from multiprocessing import Pool
-    with Pool(initializer=_widen, initargs=(L.RA_MAX, L.CB_MAX)) as pool:
+    with Pool(initializer=_widen, initargs=(L.RA_MAX, L.CB_MAX, L.STREAM)) as pool:
         res = pool.starmap(L.best_for, [(n, top, 128, es) for n in ns])
     out = {}
     for n, lst in zip(ns, res):
@@ -62,34 +63,38 @@ def candidates(ns, top, es=4, wide=False):
     return out
 
 
-def _widen(ra_max, cb_max):
+def _widen(ra_max, cb_max, stream=False):
     import f32_layout as L
-    L.RA_MAX, L.CB_MAX = ra_max, cb_max
+    L.RA_MAX, L.CB_MAX, L.STREAM = ra_max, cb_max, stream
 
 
-def run(cands: dict, out: str, steps: int, dt: str = "f32", baseline: bool = False) -> None:
+def run(cands: dict, out: str, steps: int, dt: str = "f32", baseline: bool = False, stream: bool = False) -> None:
+    """stream: the candidates go into F32TS_TABLE (the low-repeat kernel's own
+    shapes) and are timed at R = 1 (fraction of HBM, the library's pick)"""
     ns = sorted(int(n) for n in cands)
     depth = max(len(v) for v in cands.values())
     for j in ([-1] if baseline else []) + list(range(depth)):
         # rank -1: the table empty (FP64: the DMMA / TPMS kinds these sizes use otherwise)
         rows = [] if j < 0 else [row(cands[str(n)][min(j, len(cands[str(n)]) - 1)]) for n in ns]
-        write_table(rows, dt)
+        write_table(rows, dt, stream)
         b = subprocess.run([sys.executable, "-c", "import paper_1904_08555_b200._build as b; b.build(force=True)"],
                            cwd=ROOT, capture_output=True, text=True)
         if b.returncode:
             print(f"rank {j}: build failed: {b.stderr[-2000:]}", file=sys.stderr)
             continue
         p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "stream_sweep.py"), "--sizes",
-                            ",".join(map(str, ns)), "--dtypes", dt, "--repeats", "100", "--gb", "0.25",
+                            ",".join(map(str, ns)), "--dtypes", dt, "--repeats", "1" if stream else "100",
+                            "--gb", "0.5" if stream else "0.25",
                             "--steps", str(steps)], cwd=ROOT, capture_output=True, text=True)
         with open(out, "a") as fh:
             for ln in p.stdout.splitlines():
                 d = json.loads(ln)
                 n = d["n"]
                 c = None if j < 0 else cands[str(n)][min(j, len(cands[str(n)]) - 1)]
-                k = d["kernels"]["0"]
-                rec = dict(rank=j, n=n, dtype=dt, cand=c, frac_pipe=d["resident"]["frac_pipe"], regs=k["regs"],
-                           local=k["local"], smem=k["smem"], tile=k["tile"])
+                k = d["kernels"]["1" if stream else "0"]
+                frac = d["auto"]["frac_hbm"] if stream else d["resident"]["frac_pipe"]
+                rec = dict(rank=j, n=n, dtype=dt, cand=c, frac_pipe=frac, regs=k["regs"],
+                           local=k["local"], smem=k["smem"], tile=k["tile"], stream=stream)
                 fh.write(json.dumps(rec) + "\n")
         print(f"rank {j} done", file=sys.stderr)
 
@@ -129,15 +134,16 @@ def main():
     ap.add_argument("--baseline", action="store_true", help="also time the sizes with the table empty")
     ap.add_argument("--margin", type=float, default=0.0)
     ap.add_argument("--wide", action="store_true", help="larger register tiles (see candidates())")
+    ap.add_argument("--stream", action="store_true", help="search the low-repeat kernel's table (R = 1, HBM)")
     a = ap.parse_args()
     if a.candidates:
         ns = []
         for part in a.candidates.split(","):
             lo, _, hi = part.partition("..")
             ns += list(range(int(lo), int(hi or lo) + 1))
-        print(json.dumps(candidates(ns, a.top, 8 if a.dtype == "f64" else 4, a.wide), indent=0))
+        print(json.dumps(candidates(ns, a.top, 8 if a.dtype == "f64" else 4, a.wide, a.stream), indent=0))
     elif a.run:
-        run(json.load(open(a.run)), a.out, a.steps, a.dtype, a.baseline)
+        run(json.load(open(a.run)), a.out, a.steps, a.dtype, a.baseline, a.stream)
     elif a.pick:
         pick(a.pick, a.margin)
 

@@ -5,7 +5,7 @@
         python tools/ncu_configs.py 16:f64:1048576:100:resident 32:f32:262144:1:streaming ...
 
 Each argument is n:dtype:batch:repeat:variant (variant = resident | streaming |
-auto | generic).  Inputs are the `bench` distribution filled on the device;
+auto | generic | latency).  Inputs are the `bench` distribution filled on the device;
 every configuration is warmed (compiled) before the captured launch, so the
 NVRTC compile never lands inside a capture.  Prints the key info per config
 (regs, smem, tile) as JSON lines so a summary can be matched to its config.
@@ -26,7 +26,8 @@ def main():
     import paper_1904_08555_b200 as jm
     torch.cuda.init()
     jm.jit_mat_init(0)
-    flags = {"resident": jm.JM_FLAG_RESIDENT, "streaming": jm.JM_FLAG_STREAMING, "auto": 0, "generic": 0}
+    flags = {"resident": jm.JM_FLAG_RESIDENT, "streaming": jm.JM_FLAG_STREAMING, "auto": 0, "generic": 0,
+             "latency": jm.JM_FLAG_LATENCY}
     for spec in sys.argv[1:]:
         n, dt, b, r, v = spec.split(":")
         n, b, r = int(n), int(b), int(r)

@@ -112,8 +112,7 @@ def main():
     i = 0   # --algo entries apply to the captured update launches in order, across reports
     for rep in a.reps:
         for d in raw(rep):
-            if "k_update" not in d.get("Kernel Name", "") and "k_matmul" not in d.get("Kernel Name", "") \
-                    and "k_mass" not in d.get("Kernel Name", ""):
+            if not any(k in d.get("Kernel Name", "") for k in ("k_update", "k_matmul", "k_mass", "jm_generic")):
                 continue
             s = summarise(d, algos[i] if i < len(algos) else None)
             i += 1
