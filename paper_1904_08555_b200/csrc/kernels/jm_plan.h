@@ -186,7 +186,7 @@ struct F32T {
 // Per-n choices, measured on B200 (tools/f32_search.py; the layout of each
 // shape from tools/f32_layout.py):
 // {n, RA, CB, row padding (16-B chunks), region padding (16-B chunks), colblk, trfast, qmix, maxreg, kunroll}
-struct F32TRow { int n, ra, cb, ldmpad, pad, colblk, trfast, qmix, maxreg, kunroll; };
+struct F32TRow { int n, ra, cb, ldmpad, pad, colblk, trfast, qmix, maxreg, kunroll, wpc; };   // (wpc 0: 4)
 // FP64 register tiles (DFMA, run_f64t) for the sizes where DMMA's 8 x 8 x 4
 // granularity wastes most of the pipe; the same fields, CB a multiple of 2
 // (a 16-B chunk holds two doubles).  Only the sizes listed take this kind.
@@ -267,6 +267,12 @@ constexpr F32TRow F32T_TABLE[] = {
 // region -- more warps per SM -- can beat the faster k loop); same fields.
 constexpr F32TRow F32TS_TABLE[] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    // r02 stream search v1 (R = 1, fraction of HBM; profiles/r02_f32_stream_search_v1.jsonl)
+    {17, 6, 4, 6, 0, 0, 1, 1, 168, 4},    // 0.432 (0.323 with the resident shape)
+    {18, 5, 12, 4, 1, 1, 1, 0, 168, 4},   // 0.604 (0.480)
+    {22, 5, 8, 5, 1, 0, 0, 1, 168, 5},    // 0.618 (0.428)
+    {25, 7, 8, 1, 1, 1, 0, 1, 168, 6},    // 0.418 (0.365)
+    {33, 6, 8, 1, 0, 1, 1, 0, 168, 8},    // 0.351 (0.290)
 };
 #ifndef JM_F32T_RA                // tuning hooks: force the register-tile shape / layout / knobs
 #define JM_F32T_RA 0
@@ -327,7 +333,7 @@ JM_HD constexpr F32T f32t_tile(int n, int dt = 0) {
   F32T t = f32t_default(n, dt);
   auto take = [&](const F32TRow &r) {
     t = F32T{r.ra, r.cb, cdiv(n, r.ra), cdiv(n, r.cb), cdiv(n, r.cb) * r.cb + tt_vec(dt) * r.ldmpad, r.pad,
-             r.colblk, r.trfast, r.qmix, r.maxreg, r.kunroll, 4};
+             r.colblk, r.trfast, r.qmix, r.maxreg, r.kunroll, r.wpc > 0 ? r.wpc : 4};
   };
   if (dt == 1) {
     for (const F32TRow &r : F64T_TABLE)
@@ -622,14 +628,36 @@ JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8, 
 #define JM_F32T_RING 1
 #endif
 #ifndef JM_F32T_RING_ROWS
-#define JM_F32T_RING_ROWS 1   // n % 4 == 0: row-pitched copies straight into the work layout (run_f32t RROWS)
+#define JM_F32T_RING_ROWS 0   // 1: row-pitched copies straight into the work layout (run_f32t RROWS); measured 2-5x slower at R = 1 (one 80-256 B bulk copy per row, profiles/r02_ab_f32_ring_rows.md)
 #endif
 #ifndef JM_F32T_RING_MAXB
 #define JM_F32T_RING_MAXB (113 * 1024)   // ... while two CTAs still fit on an SM
 #endif
+// JM_F32T_SEP_ALL: every n takes the packed ring with separate work regions
+// (f32t_ring_sep), not the in-place ring.  Measured at R = 1..2 for n = 17..64
+// (profiles/r02_ab_f32_stream_sep.md): the chunk-wise copy into a separate work
+// region removes the conflicted element reads of the packed matrix, but the
+// extra region costs occupancy (n = 20 0.64 -> 0.47, 40 0.50 -> 0.41 of HBM;
+// n = 32 / 48 +2-4 %), and the element-wise copy of rows that are not whole
+// 16-B chunks is slower still (n = 18 0.61 -> 0.23) — off
+#ifndef JM_F32T_SEP_ALL
+#define JM_F32T_SEP_ALL 0
+#endif
 JM_HD constexpr bool f32t_ring(int n) {
-  return JM_F32T_RING && (n * n * 4) % 16 == 0 &&
+  return JM_F32T_RING && !JM_F32T_SEP_ALL && (n * n * 4) % 16 == 0 &&
          ring_bytes(n, 4, f32t_mpc(n, 2), f32t_region(n, 2)) <= JM_F32T_RING_MAXB;
+}
+// odd n: the ring of packed chunk copies (a matrix is not a multiple of 16 B,
+// so it cannot be its own copy into a slot) beside a separate work region per
+// matrix of the round, while that still fits twice on an SM.  Measured slower
+// than the prefetching stage (n = 25 0.37 -> 0.26, 27 0.46 -> 0.23 of HBM at
+// R = 1; profiles/r02_ab_f32_stream_sep.md) — off
+#ifndef JM_F32T_RING_SEP
+#define JM_F32T_RING_SEP 0
+#endif
+JM_HD constexpr bool f32t_ring_sep(int n) {
+  return JM_F32T_RING_SEP && (JM_F32T_SEP_ALL || (n * n * 4) % 16 != 0) &&
+         ring_bytes(n, 4, f32t_mpc(n, 2)) + f32t_mpc(n, 2) * f32t_region(n, 2) <= JM_F32T_RING_MAXB;
 }
 // matrices per round of each kind (the resident plan's chunk)
 JM_HD constexpr int round_mpc(int n, int dtype) {
@@ -662,6 +690,9 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   // the work area; the result goes back packed and leaves by a bulk store)
   if (f32t_ring(n))
     return Plan{(int)Tile::F32, 32 * f32t_wpc(n, 2), chm, ring_bytes(n, es, rm, f32t_region(n, 2)), f32t_wpm(n, 2)};
+  if (f32t_ring_sep(n))
+    return Plan{(int)Tile::F32, 32 * f32t_wpc(n, 2), chm, ring_bytes(n, es, rm) + rm * f32t_region(n, 2),
+                f32t_wpm(n, 2)};
   // F32T, odd n: the resident layout with the double-buffered cp.async stage
   // (the next chunk streams in while this one is updated)
   return Plan{(int)Tile::F32, 32 * f32t_wpc(n, 2), f32t_mpc(n, 2), 2 * rup(f32t_mpc(n, 2) * f32t_region(n, 2), 16),

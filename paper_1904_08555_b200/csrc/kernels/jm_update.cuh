@@ -1278,18 +1278,71 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
   // quarter-warp on one bank: 53 % of the n = 32, R = 1 kernel's wavefronts
   // conflicted, profiles/r02_ncu_kinds.md)
   constexpr bool RROWS = STRM && f32t_ring(N) && JM_F32T_RING_ROWS && (N % 4) == 0;
-  typedef typename Pick<STRM && f32t_ring(N),
-                        Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, REG, RROWS ? LDM * 4 : 0>,
+  // RSEP (f32t_ring_sep): the ring slots hold the packed matrices (one bulk
+  // copy per matrix for even n, one per chunk for odd n) and each matrix of
+  // the round has its own work region beside the ring.  The threads of a
+  // matrix group (a warp, or the warps of one matrix) copy the packed slots
+  // into the work layout with consecutive 16-B (n % 4 == 0) or 4-B accesses
+  // -- bank-conflict free on both sides -- and the matrix is read into the
+  // accumulators, and written back, in the publish pattern; the group copies
+  // the result back to the slots for the bulk store.  Per matrix in flight:
+  // two packed slots + one work region (the in-place ring: two work regions).
+  constexpr bool RSEP = STRM && !f32t_ring(N) && f32t_ring_sep(N);
+  constexpr int GS = 32 * WPM, GM = WPM == 1 ? MPW : 1;   // group threads, group matrices
+  const int gt = WPM == 1 ? lane : (warp % WPM) * 32 + lane;
+  const int gm0 = WPM == 1 ? warp * MPW : warp / WPM;   // the group's first matrix slot
+  typedef typename Pick<STRM && (f32t_ring(N) || RSEP),
+                        Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, RSEP ? 0 : REG, RROWS ? LDM * 4 : 0>,
                         Stager<N, ES, REG, NT, MPC, AL, STRM>>::type Stg;
-  static_assert(Stg::SBM >= REG, "a slot holds the work region");
+  static_assert(RSEP || Stg::SBM >= REG, "a slot holds the work region");
   Stg sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     const bool live = lane_ok && mi < sg.cnt();
-    float *sm = reinterpret_cast<float *>(sg.buf() + (lane_ok ? mi : 0) * Stg::SBM);
-    const unsigned sbase = smem_u32(sm);
+    float *sm = reinterpret_cast<float *>(sg.buf() + (lane_ok ? mi : 0) * Stg::SBM);   // the staged matrix
+    float *wk = RSEP ? reinterpret_cast<float *>(smem + Stg::BYTES + (lane_ok ? mi : 0) * REG) : sm;   // work region
+    const unsigned sbase = smem_u32(wk);
     float2 p[RA][CB / 2];
-    if constexpr (RROWS) {   // own block of the staged matrix (row-pitched: already the work layout)
+    if constexpr (RSEP) {
+      const int cnt = sg.cnt();
+      if constexpr (N % 4 == 0) {
+        constexpr int CPR = N / 4, CPM = N * CPR;
+#pragma unroll 4
+        for (int e = gt; e < GM * CPM; e += GS) {
+          const int ml = e / CPM, cc = e - ml * CPM, row = cc / CPR, q = cc - row * CPR, ms = gm0 + ml;
+          if (ms < cnt)
+            *reinterpret_cast<float4 *>(smem + Stg::BYTES + ms * REG + (row * LDM + 4 * q) * 4) =
+                *reinterpret_cast<const float4 *>(sg.buf() + ms * Stg::SBM + cc * 16);
+        }
+      } else {
+        constexpr int EPM = N * N;
+#pragma unroll 4
+        for (int e = gt; e < GM * EPM; e += GS) {
+          const int ml = e / EPM, cc = e - ml * EPM, row = cc / N, col = cc - row * N, ms = gm0 + ml;
+          if (ms < cnt)
+            reinterpret_cast<float *>(smem + Stg::BYTES + ms * REG)[row * LDM + col] =
+                reinterpret_cast<const float *>(sg.buf() + ms * Stg::SBM)[cc];
+        }
+      }
+      sync();
+#pragma unroll
+      for (int i = 0; i < RA; ++i)
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const int row = row_of(i), c0 = chunk_of(h) * 4;
+          float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          if (live && row < N && c0 < N) {
+            v = lds128(sbase + (row * LDM + c0) * 4);
+            if constexpr (N % 4 != 0) {   // the padding columns of the work region hold stale values
+              if (c0 + 1 >= N) v.y = 0.0f;
+              if (c0 + 2 >= N) v.z = 0.0f;
+              if (c0 + 3 >= N) v.w = 0.0f;
+            }
+          }
+          p[i][2 * h] = make_float2(v.x, v.y);
+          p[i][2 * h + 1] = make_float2(v.z, v.w);
+        }
+    } else if constexpr (RROWS) {   // own block of the staged matrix (row-pitched: already the work layout)
 #pragma unroll
       for (int i = 0; i < RA; ++i)
 #pragma unroll
@@ -1315,7 +1368,7 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
     sync();                            // staged matrix read: the region becomes the work area
     if constexpr (SROWS > NR) {        // rows read as k padding (k in [NR, KP)) are zero
       if (live)
-        for (int e = t; e < (SROWS - NR) * LDM; e += TPMAT) sm[NR * LDM + e] = 0.0f;
+        for (int e = t; e < (SROWS - NR) * LDM; e += TPMAT) wk[NR * LDM + e] = 0.0f;
     }
     for (int r = 0; r < repeat; ++r) {
       if (live) {                      // publish M
@@ -1391,7 +1444,40 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
           }
       }
     }
-    if constexpr (RROWS) {             // rows leave from the work layout (the k loop's reads are done)
+    if constexpr (RSEP) {              // work layout (publish pattern), then the group copies it to the slots
+      if (live) {
+#pragma unroll
+        for (int i = 0; i < RA; ++i)
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            const int row = row_of(i), c0 = chunk_of(h) * 4;
+            if (row < N && c0 < N)
+              sts128(sbase + (row * LDM + c0) * 4, p[i][2 * h].x, p[i][2 * h].y, p[i][2 * h + 1].x,
+                     p[i][2 * h + 1].y);
+          }
+      }
+      sync();
+      const int cnt = sg.cnt();
+      if constexpr (N % 4 == 0) {
+        constexpr int CPR = N / 4, CPM = N * CPR;
+#pragma unroll 4
+        for (int e = gt; e < GM * CPM; e += GS) {
+          const int ml = e / CPM, cc = e - ml * CPM, row = cc / CPR, q = cc - row * CPR, ms = gm0 + ml;
+          if (ms < cnt)
+            *reinterpret_cast<float4 *>(sg.buf() + ms * Stg::SBM + cc * 16) =
+                *reinterpret_cast<const float4 *>(smem + Stg::BYTES + ms * REG + (row * LDM + 4 * q) * 4);
+        }
+      } else {
+        constexpr int EPM = N * N;
+#pragma unroll 4
+        for (int e = gt; e < GM * EPM; e += GS) {
+          const int ml = e / EPM, cc = e - ml * EPM, row = cc / N, col = cc - row * N, ms = gm0 + ml;
+          if (ms < cnt)
+            reinterpret_cast<float *>(sg.buf() + ms * Stg::SBM)[cc] =
+                reinterpret_cast<const float *>(smem + Stg::BYTES + ms * REG)[row * LDM + col];
+        }
+      }
+    } else if constexpr (RROWS) {      // rows leave from the work layout (the k loop's reads are done)
       if (live) {
 #pragma unroll
         for (int i = 0; i < RA; ++i)

@@ -27,8 +27,9 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 
 def row(c: dict) -> str:
+    wpc = f", {c['wpc']}" if c.get("wpc") else ""
     return (f"    {{{c['n']}, {c['ra']}, {c['cb']}, {c['ldmpad']}, {c['pad']}, {c['colblk']}, {c['trfast']}, "
-            f"{c['qmix']}, {c['maxreg']}, {c['kunroll']}}},")
+            f"{c['qmix']}, {c['maxreg']}, {c['kunroll']}{wpc}}},")
 
 
 def write_table(rows: list[str], dt: str = "f32", stream: bool = False) -> None:
