@@ -267,12 +267,45 @@ constexpr F32TRow F32T_TABLE[] = {
 // region -- more warps per SM -- can beat the faster k loop); same fields.
 constexpr F32TRow F32TS_TABLE[] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    // r02 stream search v1 (R = 1, fraction of HBM; profiles/r02_f32_stream_search_v1.jsonl)
-    {17, 6, 4, 6, 0, 0, 1, 1, 168, 4},    // 0.432 (0.323 with the resident shape)
-    {18, 5, 12, 4, 1, 1, 1, 0, 168, 4},   // 0.604 (0.480)
-    {22, 5, 8, 5, 1, 0, 0, 1, 168, 5},    // 0.618 (0.428)
-    {25, 7, 8, 1, 1, 1, 0, 1, 168, 6},    // 0.418 (0.365)
-    {33, 6, 8, 1, 0, 1, 1, 0, 168, 8},    // 0.351 (0.290)
+    // r02 stream search v2 (R = 1, fraction of the HBM bandwidth (bytes moved / time) of the kernel the
+    // library picks, "was" = the resident shape; last field 2 = two-warp CTAs;
+    // profiles/r02_f32_stream_search_v2.jsonl)
+    {17, 6, 4, 6, 0, 0, 1, 1, 168, 4, 2},  // 0.448 at R = 1 (was 0.316), 106 regs
+    {18, 5, 12, 4, 1, 1, 1, 0, 168, 4, 2},  // 0.667 at R = 1 (was 0.475), 138 regs
+    {19, 5, 12, 4, 1, 1, 1, 0, 168, 4, 2},  // 0.413 at R = 1 (was 0.386), 137 regs
+    {20, 5, 12, 4, 1, 1, 1, 0, 168, 5, 2},  // 0.667 at R = 1 (was 0.635), 145 regs
+    {22, 5, 8, 5, 1, 0, 0, 1, 168, 5},  // 0.624 at R = 1 (was 0.428), 114 regs
+    {23, 8, 12, 1, 5, 0, 0, 0, 255, 5, 2},  // 0.433 at R = 1 (was 0.365), 221 regs
+    {24, 6, 12, 1, 4, 0, 1, 0, 168, 6, 2},  // 0.707 at R = 1 (was 0.489), 167 regs
+    {25, 7, 8, 1, 1, 1, 0, 1, 168, 6, 2},  // 0.424 at R = 1 (was 0.365), 132 regs
+    {26, 7, 8, 1, 1, 1, 0, 1, 168, 6, 2},  // 0.656 at R = 1 (was 0.624), 133 regs
+    {27, 7, 8, 1, 1, 1, 0, 1, 168, 6, 2},  // 0.468 at R = 1 (was 0.455), 131 regs
+    {28, 7, 8, 1, 1, 1, 0, 1, 168, 7, 2},  // 0.609 at R = 1 (was 0.572), 131 regs
+    {29, 8, 8, 1, 3, 1, 0, 1, 168, 7, 2},  // 0.440 at R = 1 (was 0.428), 144 regs
+    {30, 8, 8, 1, 3, 1, 0, 1, 168, 7, 2},  // 0.712 at R = 1 (was 0.675), 146 regs
+    {31, 8, 8, 1, 3, 1, 0, 1, 168, 7, 2},  // 0.475 at R = 1 (was 0.428), 141 regs
+    {32, 8, 8, 1, 3, 1, 0, 1, 168, 8, 2},  // 0.650 at R = 1 (was 0.465), 144 regs
+    {33, 6, 8, 1, 0, 1, 1, 0, 168, 8},  // 0.351 at R = 1 (was 0.289), 122 regs
+    {34, 6, 8, 1, 0, 1, 1, 0, 168, 8},  // 0.530 at R = 1 (was 0.512), 124 regs
+    {35, 7, 12, 1, 1, 1, 0, 1, 168, 8, 2},  // 0.394 at R = 1 (was 0.375), 160 regs
+    {36, 6, 8, 1, 0, 1, 1, 0, 168, 9},  // 0.520 at R = 1 (was 0.485), 141 regs
+    {37, 7, 8, 1, 0, 1, 1, 0, 168, 9},  // 0.355 at R = 1 (was 0.334), 138 regs
+    {38, 5, 12, 1, 0, 0, 1, 0, 168, 9, 2},  // 0.513 at R = 1 (was 0.488), 129 regs
+    {39, 7, 8, 1, 0, 1, 1, 0, 168, 9},  // 0.376 at R = 1 (was 0.358), 137 regs
+    {40, 5, 12, 1, 0, 0, 1, 0, 168, 10, 2},  // 0.512 at R = 1 (was 0.496), 129 regs
+    {49, 7, 16, 1, 0, 0, 0, 0, 255, 2},  // 0.258 at R = 1 (was 0.233), 214 regs
+    {50, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.364 at R = 1 (was 0.286), 136 regs
+    {51, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.300 at R = 1 (was 0.241), 146 regs
+    {52, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.358 at R = 1 (was 0.345), 152 regs
+    {53, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.303 at R = 1 (was 0.245), 154 regs
+    {56, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.392 at R = 1 (was 0.316), 134 regs
+    {57, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.303 at R = 1 (was 0.242), 146 regs
+    {58, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.409 at R = 1 (was 0.289), 154 regs
+    {60, 8, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.356 at R = 1 (was 0.293), 164 regs
+    {61, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.324 at R = 1 (was 0.265), 150 regs
+    {62, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.428 at R = 1 (was 0.315), 152 regs
+    {63, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.295 at R = 1 (was 0.229), 153 regs
+    {64, 8, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.283 at R = 1 (was 0.248), 155 regs
 };
 #ifndef JM_F32T_RA                // tuning hooks: force the register-tile shape / layout / knobs
 #define JM_F32T_RA 0
@@ -430,6 +463,15 @@ JM_HD constexpr int f32p_halves(int n) { return n <= 16 ? 1 : cdiv(f32p_ncr(n), 
 // multiple of 64 B, so the two matrices sharing a quarter-warp land in
 // opposite halves of the 128-B bank window
 JM_HD constexpr int f32p_mbuf(int n) { return n * f32p_ncs(n) * 16 + 32; }
+// stride between two matrices' buffer pairs (own two buffers): + JM_F32P_PAIR_SKEW
+// bytes, so the four matrices of a half-warp reading row k (one 16-B address
+// each) land in four bank slots (pair stride 132 chunks = 4 mod 8 put
+// matrices 0/2 and 1/3 on one slot: 40 % of the n = 16 kernel's wavefronts
+// conflicted, profiles/r02_ncu_kinds.md); the publish then pays 2-way
+#ifndef JM_F32P_PAIR_SKEW
+#define JM_F32P_PAIR_SKEW 32
+#endif
+JM_HD constexpr int f32p_pstr(int n) { return 2 * f32p_mbuf(n) + JM_F32P_PAIR_SKEW; }
 // resident kernel: the matrix's stage slot, widened to a row buffer, doubles as
 // the first row buffer (run_f32p INPL), one buffer less per matrix: n = 12
 // 0.52 -> 0.65 and n = 14 0.50 -> 0.60 of the FP32 pipe at R = 100; n = 16
@@ -485,7 +527,7 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   if (f32p_use(n)) {
     const int mpc = F32P_WPC * f32p_mpw(n);
     if (f32p_inplace(n)) return Plan{(int)Tile::F32Rows, 32 * F32P_WPC, mpc, nst * rup(mpc * f32p_slot(n), 16) + mpc * f32p_mbuf(n), 1};
-    return Plan{(int)Tile::F32Rows, 32 * F32P_WPC, mpc, nst * stage_bytes(mpc, n, es) + 2 * mpc * f32p_mbuf(n), 1};
+    return Plan{(int)Tile::F32Rows, 32 * F32P_WPC, mpc, nst * stage_bytes(mpc, n, es) + mpc * f32p_pstr(n), 1};
   }
   // F32 tiles: the stage area IS the per-matrix region (stride f32t_region)
   return Plan{(int)t, 32 * f32t_wpc(n), f32t_mpc(n), f32t_mpc(n) * f32t_region(n), f32t_wpm(n)};
@@ -627,6 +669,9 @@ JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8, 
 #ifndef JM_F32T_RING
 #define JM_F32T_RING 1
 #endif
+#ifndef JM_F32T_PVEC
+#define JM_F32T_PVEC 1   // n % 4 == 0: rotated 16-B one-time reads / write-backs of the packed matrix (run_f32t PVEC)
+#endif
 #ifndef JM_F32T_RING_ROWS
 #define JM_F32T_RING_ROWS 0   // 1: row-pitched copies straight into the work layout (run_f32t RROWS); measured 2-5x slower at R = 1 (one 80-256 B bulk copy per row, profiles/r02_ab_f32_ring_rows.md)
 #endif
@@ -684,7 +729,7 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   if (f32p_use(n))
     return f32p_ring_inplace(n)
                ? Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm, f32p_slot(n)) + rm * f32p_mbuf(n), 1}
-               : Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + 2 * rm * f32p_mbuf(n), 1};
+               : Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + rm * f32p_pstr(n), 1};
   // F32T, even n: the bulk-copy ring, each matrix's slot widened to its work
   // region (the staged matrix is read into the accumulators, then the slot is
   // the work area; the result goes back packed and leaves by a bulk store)

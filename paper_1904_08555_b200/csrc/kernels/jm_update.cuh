@@ -1041,7 +1041,8 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
   const int mw = lane / G, tg = lane - mw * G;
   const int mi = warp * MPW + mw;                      // matrix slot in the chunk
   const int r0 = tg * RP;
-  char *bufs = smem + Stg::BYTES + mi * (INPL ? 1 : 2) * MBUF;
+  constexpr int PSTR = INPL ? MBUF : f32p_pstr(N);   // per-matrix buffer stride
+  char *bufs = smem + Stg::BYTES + mi * PSTR;
   const float c = float(0.00005);
 
   Stg sg(in, out, batch, smem);
@@ -1072,7 +1073,7 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
         const int ml = e / CPM, cc = e - ml * CPM, row = cc / NCR, q = cc - row * NCR, ms = warp * MPW + ml;
         const float4 v = ms < cnt ? *reinterpret_cast<const float4 *>(stage + ms * Stg::SBM + cc * 16)
                                   : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        *reinterpret_cast<float4 *>(smem + Stg::BYTES + ms * 2 * MBUF + f32p_off<NCS>(row, q)) = v;
+        *reinterpret_cast<float4 *>(smem + Stg::BYTES + ms * PSTR + f32p_off<NCS>(row, q)) = v;
       }
       __syncwarp();
 #pragma unroll
@@ -1189,7 +1190,7 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
         const int ml = e / CPM, cc = e - ml * CPM, row = cc / NCR, q = cc - row * NCR, ms = warp * MPW + ml;
         if (ms < cnt)
           *reinterpret_cast<float4 *>(stage + ms * Stg::SBM + cc * 16) =
-              *reinterpret_cast<const float4 *>(smem + Stg::BYTES + ms * 2 * MBUF + fb + f32p_off<NCS>(row, q));
+              *reinterpret_cast<const float4 *>(smem + Stg::BYTES + ms * PSTR + fb + f32p_off<NCS>(row, q));
       }
     } else if (live) {
 #pragma unroll
@@ -1233,6 +1234,27 @@ __device__ __forceinline__ void sts128(unsigned a, float x, float y, float z, fl
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
 }
 
+// v[h] <- v[(h - d) mod NH] (RIGHT: undo a load order that started at chunk
+// d) or v[h] <- v[(h + d) mod NH] (left), d < NH a runtime amount: one
+// compile-time rotation by 2^b per bit of d, selected at run time
+template <int NH, bool RIGHT>
+__device__ __forceinline__ void rot_chunks(float4 (&v)[NH], int d) {
+#pragma unroll
+  for (int b = 1; b < NH; b <<= 1) {
+    const bool on = (d & b) != 0;
+    float4 w[NH];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) w[h] = RIGHT ? v[(h - b % NH + NH) % NH] : v[(h + b) % NH];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      v[h].x = on ? w[h].x : v[h].x;
+      v[h].y = on ? w[h].y : v[h].y;
+      v[h].z = on ? w[h].z : v[h].z;
+      v[h].w = on ? w[h].w : v[h].w;
+    }
+  }
+}
+
 template <int N, Addend A, bool STRM>
 __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__restrict__ out,
                                          long long batch, int repeat) {
@@ -1267,6 +1289,15 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
   };
   auto row_of = [&](int i) { return i * RG + tr; };
   auto chunk_of = [&](int h) { return TL.colblk ? tc * NH + h : h * CG + tc; };
+  // PVEC (r02): the one-time read of the staged (packed, row stride N)
+  // matrix into the accumulators and the write-back go as 16-B accesses when
+  // rows are whole chunks; thread tr takes its NH chunks of a row starting at
+  // chunk tr % NH, so the threads of a quarter-warp that share a column
+  // (rows 2^k x 16 B apart: one bank slot) touch different chunks at a time.
+  // The element accesses were 8-way conflicted at n = 32 (53 % of the R = 1
+  // kernel's wavefronts, profiles/r02_ncu_kinds.md).
+  constexpr bool PVEC = JM_F32T_PVEC && (N % 4) == 0;
+  const int prot = NH > 1 ? tr % NH : 0;
   // STRM (the low-repeat variant): even n run behind the bulk-copy ring with
   // each slot widened to the work region (f32t_ring); odd n keep the
   // double-buffered cp.async stage (the next chunk streams in while this one
@@ -1353,6 +1384,25 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
           p[i][2 * h] = make_float2(v.x, v.y);
           p[i][2 * h + 1] = make_float2(v.z, v.w);
         }
+    } else if constexpr (PVEC) {   // packed, rows of whole 16-B chunks: rotated LDS.128 (PVEC above)
+      const unsigned pbase = smem_u32(sm);
+#pragma unroll
+      for (int i = 0; i < RA; ++i) {
+        const int row = row_of(i);
+        float4 v[NH];
+#pragma unroll
+        for (int st = 0; st < NH; ++st) {
+          const int c0 = chunk_of((st + prot) % NH) * 4;
+          v[st] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          if (live && row < N && c0 < N) v[st] = lds128(pbase + (row * N + c0) * 4);
+        }
+        rot_chunks<NH, true>(v, prot);   // v[h] = chunk h
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          p[i][2 * h] = make_float2(v[h].x, v[h].y);
+          p[i][2 * h + 1] = make_float2(v[h].z, v[h].w);
+        }
+      }
     } else {   // own block of the staged matrix (packed, row stride N)
 #pragma unroll
       for (int i = 0; i < RA; ++i)
@@ -1488,6 +1538,21 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
               sts128(sbase + (row * LDM + c0) * 4, p[i][2 * h].x, p[i][2 * h].y, p[i][2 * h + 1].x,
                      p[i][2 * h + 1].y);
           }
+      }
+    } else if (PVEC && live) {         // back to the packed layout: rotated STS.128
+      const unsigned pbase = smem_u32(sm);
+#pragma unroll
+      for (int i = 0; i < RA; ++i) {
+        const int row = row_of(i);
+        float4 v[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) v[h] = make_float4(p[i][2 * h].x, p[i][2 * h].y, p[i][2 * h + 1].x, p[i][2 * h + 1].y);
+        rot_chunks<NH, false>(v, prot);  // v[st] = chunk (st + prot) % NH
+#pragma unroll
+        for (int st = 0; st < NH; ++st) {
+          const int c0 = chunk_of((st + prot) % NH) * 4;
+          if (row < N && c0 < N) sts128(pbase + (row * N + c0) * 4, v[st].x, v[st].y, v[st].z, v[st].w);
+        }
       }
     } else if (live) {                 // back to the packed layout for the store
 #pragma unroll

@@ -1,10 +1,13 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
 mkdir -p gpurun_out/r02
 O=gpurun_out/r02
-rm -f $O/ab_rt.jsonl $O/f32s_search_v2.jsonl
-timeout 900 python tools/ab.py --sizes 33..56 --dtypes f64 --repeats 1,2 --out $O/ab_rt.jsonl \
-  --variant rt2="JM_DMMA_RT_LARGE=2" --variant rt3="JM_DMMA_RT_LARGE=3" --variant base= 2> $O/ab_rt.err
-python tools/ab.py --table $O/ab_rt.jsonl > $O/ab_rt.md
-timeout 2700 python tools/f32_search.py --stream --baseline --run tools/f32s_candidates_v2.json --out $O/f32s_search_v2.jsonl 2> $O/f32s_search_v2.err
-python tools/f32_search.py --pick $O/f32s_search_v2.jsonl --margin 0.01 > $O/f32s_search_v2_pick.txt
-cat $O/ab_rt.md $O/f32s_search_v2_pick.txt
+timeout 2700 python -m pytest tests -m gpu -q -x 2>&1 | tail -15 > $O/gputest_full7.txt
+rm -f $O/ab_pvec.jsonl $O/ab_skew.jsonl $O/f32_xover.jsonl
+timeout 1500 python tools/ab.py --sizes 17..64 --dtypes f32 --repeats 1,100 --out $O/ab_pvec.jsonl \
+  --variant nopvec="JM_F32T_PVEC=0" --variant pvec= 2> $O/ab_pvec.err
+python tools/ab.py --table $O/ab_pvec.jsonl > $O/ab_pvec.md
+timeout 600 python tools/ab.py --sizes 12..16 --dtypes f32 --repeats 1,100 --out $O/ab_skew.jsonl \
+  --variant noskew="JM_F32P_PAIR_SKEW=0" --variant skew= 2> $O/ab_skew.err
+python tools/ab.py --table $O/ab_skew.jsonl > $O/ab_skew.md
+timeout 900 python tools/stream_sweep.py --sizes 17,20,24,28,32,33,40,48,56,64 --dtypes f32 --repeats 2,3,4,6,8 --gb 0.5 > $O/f32_xover.jsonl 2> $O/f32_xover.err
+tail -3 $O/gputest_full7.txt; cat $O/ab_skew.md; head -52 $O/ab_pvec.md
