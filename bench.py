@@ -260,7 +260,8 @@ def main():
         sys.exit(relaunch(a))
     world, rank, local = resolve_world(a)
     if os.environ.get("JM_BENCH_DRY_RUN"):    # test hook: the launch contract only, no GPU work
-        print(json.dumps({"rank": rank, "world": world, "gpus": a.gpus, "local_rank": local}), flush=True)
+        # one write(2) per record: the ranks share the pipe, and print() may split a line
+        os.write(1, (json.dumps({"rank": rank, "world": world, "gpus": a.gpus, "local_rank": local}) + "\n").encode())
         return
     if a.impl == "reference":     # (rank 0 only; n_gpus = --gpus, as in the GPU arm)
         run_reference(a, rank)

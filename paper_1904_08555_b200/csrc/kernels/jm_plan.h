@@ -217,7 +217,7 @@ constexpr F32TRow F32T_TABLE[] = {
     {18, 6, 20, 2, 1, 0, 1, 0, 255, 4},  // 0.586 of the pipe, 247 regs (r02 wide search; was 0.491)
     {19, 5, 20, 1, 1, 0, 1, 0, 255, 4},  // 0.638 of the pipe, 205 regs (r02 wide search; was 0.487)
     {20, 5, 12, 4, 1, 1, 1, 0, 168, 5},  // 0.618 of the pipe, 146 regs
-    {21, 7, 12, 1, 5, 0, 0, 0, 168, 5},  // 0.563 of the pipe, 160 regs
+    {21, 11, 12, 1, 2, 0, 1, 0, 255, 5, 2},  // 0.574 of the pipe, 220 regs (r02 wpc search; was 0.562)
     {22, 6, 12, 4, 1, 1, 1, 0, 168, 5},  // 0.609 of the pipe, 150 regs
     {23, 6, 12, 4, 1, 1, 1, 0, 168, 5},  // 0.654 of the pipe, 154 regs
     {24, 6, 12, 4, 1, 1, 1, 0, 168, 6},  // 0.721 of the pipe, 158 regs
@@ -233,7 +233,7 @@ constexpr F32TRow F32T_TABLE[] = {
     {34, 7, 12, 1, 1, 1, 0, 1, 168, 8},  // 0.636 of the pipe, 161 regs
     {35, 7, 12, 1, 1, 1, 0, 1, 168, 8},  // 0.662 of the pipe, 156 regs
     {36, 8, 12, 1, 1, 1, 0, 1, 255, 9},  // 0.595 of the pipe, 200 regs
-    {37, 5, 12, 1, 0, 0, 1, 0, 168, 9},  // 0.551 of the pipe, 134 regs
+    {37, 5, 20, 1, 0, 0, 1, 0, 255, 9},  // 0.584 of the pipe, 200 regs (r02 wpc search; was 0.550)
     {38, 5, 12, 1, 0, 0, 1, 0, 168, 9},  // 0.584 of the pipe, 144 regs
     {39, 5, 12, 1, 0, 0, 1, 0, 168, 9},  // 0.613 of the pipe, 134 regs
     {40, 5, 12, 1, 0, 0, 1, 0, 168, 10},  // 0.656 of the pipe, 142 regs
@@ -468,8 +468,10 @@ JM_HD constexpr int f32p_mbuf(int n) { return n * f32p_ncs(n) * 16 + 32; }
 // each) land in four bank slots (pair stride 132 chunks = 4 mod 8 put
 // matrices 0/2 and 1/3 on one slot: 40 % of the n = 16 kernel's wavefronts
 // conflicted, profiles/r02_ncu_kinds.md); the publish then pays 2-way
+// Measured (profiles/r02_ab_skew.md): slower at every n = 12..16 (R = 1 n = 16
+// 0.54 -> 0.51 of HBM, R = 100 0.71 -> 0.70 of the pipe) — off (0)
 #ifndef JM_F32P_PAIR_SKEW
-#define JM_F32P_PAIR_SKEW 32
+#define JM_F32P_PAIR_SKEW 0
 #endif
 JM_HD constexpr int f32p_pstr(int n) { return 2 * f32p_mbuf(n) + JM_F32P_PAIR_SKEW; }
 // resident kernel: the matrix's stage slot, widened to a row buffer, doubles as
@@ -616,10 +618,17 @@ JM_HD constexpr int stream_lo(int n, int dtype) {
 #define JM_F64T_RN 0     // > 0: one switch point for every register-tile size
 #endif
 JM_HD constexpr int f64t_rn(int n) { return JM_F64T_RN > 0 ? JM_F64T_RN : n <= 12 ? 120 : n <= 18 ? 160 : 330; }
-// FP32 register tiles: the streaming kernel (ring / prefetching stage) below this R(n+1)
+// FP32 register tiles: the streaming kernel (ring / prefetching stage, with
+// its own tile shapes, F32TS_TABLE) below this R(n+1).  Measured at R = 2..8
+// (profiles/r02_f32_stream_xover.jsonl): it still wins at R = 8 for n = 20,
+// 28, 32, 33, 40, 48, 56; the crossover is R(n+1) ~ 110 at n = 17, ~125 at 24,
+// ~200 at 64.  JM_F32T_RN > 0: one switch point for every tile size.
 #ifndef JM_F32T_RN
-#define JM_F32T_RN 140
+#define JM_F32T_RN 0
 #endif
+JM_HD constexpr int f32t_rn(int n) {
+  return JM_F32T_RN > 0 ? JM_F32T_RN : n == 17 ? 110 : n == 24 ? 125 : n >= 61 ? 200 : 9 * (n + 1);
+}
 JM_HD constexpr int stream_rn_tpm(int n, int dtype) { return (dtype == 0 && n == 3) ? (1 << 30) : 0; }
 JM_HD constexpr int stream_rn(int n, int dtype) {
   return !stream_ok(n, dtype)               ? 0
@@ -628,7 +637,7 @@ JM_HD constexpr int stream_rn(int n, int dtype) {
          : (dtype == 0 && tile_for(n, dtype) == Tile::Tpms) ? (n == 12 ? 0 : 20)   // R = 1: row-panel ring
          : dtype == 1        ? stream_rn_f64(n)
          : f32p_use(n)       ? 64
-                             : JM_F32T_RN;
+                             : f32t_rn(n);
 }
 // rounds per chunk: >= JM_RING_CHUNK bytes and a chunk a multiple of 16 B
 JM_HD constexpr int ring_k(int rb) {
@@ -669,9 +678,19 @@ JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8, 
 #ifndef JM_F32T_RING
 #define JM_F32T_RING 1
 #endif
+// n % 4 == 0: rotated 16-B one-time reads / write-backs of the packed matrix
+// (run_f32t PVEC).  Measured per n (profiles/r02_ab_pvec.md, R = 1, fraction
+// of HBM): 20 0.67 -> 0.75, 28 0.61 -> 0.66, 32 0.65 -> 0.76, 60 0.36 -> 0.42,
+// but 24 0.71 -> 0.67, 36..48 -0.01..-0.02 (R = 100 unchanged within 0.02);
+// JM_F32T_PVEC = 1: the sizes that gain, 2: every n % 4 == 0, 0: none
 #ifndef JM_F32T_PVEC
-#define JM_F32T_PVEC 1   // n % 4 == 0: rotated 16-B one-time reads / write-backs of the packed matrix (run_f32t PVEC)
+#define JM_F32T_PVEC 1
 #endif
+JM_HD constexpr bool f32t_pvec(int n) {
+  return (n % 4) == 0 &&
+         (JM_F32T_PVEC == 2 || (JM_F32T_PVEC == 1 && (n == 20 || n == 28 || n == 32 || n == 52 || n == 56 ||
+                                                    n == 60 || n == 64)));
+}
 #ifndef JM_F32T_RING_ROWS
 #define JM_F32T_RING_ROWS 0   // 1: row-pitched copies straight into the work layout (run_f32t RROWS); measured 2-5x slower at R = 1 (one 80-256 B bulk copy per row, profiles/r02_ab_f32_ring_rows.md)
 #endif

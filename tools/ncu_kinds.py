@@ -38,10 +38,16 @@ KINDS = [
     ("F32 row panels", 16, "f32", 100, "auto"),
     ("F32 row-panel ring (streaming)", 16, "f32", 1, "auto"),
     ("F32 tiles", 17, "f32", 100, "auto"),
+    ("F32 tiles", 24, "f32", 100, "auto"),
     ("F32 tiles", 32, "f32", 100, "auto"),
+    ("F32 tiles", 48, "f32", 100, "auto"),
     ("F32 tiles", 64, "f32", 100, "auto"),
+    ("F32 tiles, low-repeat kernel (prefetching stage, odd n)", 17, "f32", 1, "auto"),
+    ("F32 tile ring (streaming, even n)", 24, "f32", 1, "auto"),
     ("F32 tile ring (streaming, even n)", 32, "f32", 1, "auto"),
     ("F32 tiles, prefetching stage (streaming, odd n)", 33, "f32", 1, "auto"),
+    ("F32 tile ring (streaming, even n)", 48, "f32", 1, "auto"),
+    ("F32 tiles, low-repeat kernel (compute-bound at R = 1)", 64, "f32", 1, "auto"),
     ("latency kernel (C1: one 4x4, warp per matrix)", 4, "f64", 1000, "latency"),
     ("generic runtime-N kernel", 16, "f64", 100, "generic"),
 ]

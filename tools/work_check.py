@@ -37,11 +37,17 @@ METRICS = ["sm__sass_thread_inst_executed_op_dfma_pred_on.sum",
 CONFIGS = [(2, "f64", "resident", True), (4, "f64", "resident", True), (7, "f64", "resident", True),
            (8, "f64", "resident", True), (16, "f64", "resident", True), (16, "f64", "streaming", True),
            (32, "f64", "resident", True), (32, "f64", "streaming", True), (64, "f64", "resident", True),
-           (12, "f64", "resident", False), (17, "f64", "resident", False), (25, "f64", "resident", False),
-           (41, "f64", "resident", False), (9, "f64", "resident", True), (10, "f64", "resident", True),
+           (9, "f64", "resident", True), (10, "f64", "resident", True),
+           # FP64 register tiles (r02): 12 and 20 tile exactly, 11 and 17 pad to 12 / 18
+           (12, "f64", "resident", True), (20, "f64", "resident", True),
+           (11, "f64", "resident", False), (17, "f64", "resident", False),
+           # DMMA padding: thin border (25), k-compaction (28), CTA kind (41)
+           (25, "f64", "resident", False), (28, "f64", "resident", False), (41, "f64", "resident", False),
            (2, "f32", "resident", True), (3, "f32", "resident", True), (8, "f32", "resident", True),
-           (11, "f32", "resident", True), (12, "f32", "resident", True),
-           (16, "f32", "resident", True), (32, "f32", "resident", False), (64, "f32", "resident", False)]
+           (11, "f32", "resident", True), (12, "f32", "resident", True), (16, "f32", "resident", True),
+           # FP32 register tiles (r02 shapes): 24, 32, 48, 64 tile exactly; 17 pads to 18 x 20
+           (24, "f32", "resident", True), (32, "f32", "resident", True), (48, "f32", "resident", True),
+           (64, "f32", "resident", True), (32, "f32", "streaming", True), (17, "f32", "resident", False)]
 
 
 def child(n, dt, batch, repeat, variant):
