@@ -274,6 +274,8 @@ constexpr F32TRow F32TS_TABLE[] = {
     {18, 5, 12, 4, 1, 1, 1, 0, 168, 4, 2},  // 0.667 at R = 1 (was 0.475), 138 regs
     {19, 5, 12, 4, 1, 1, 1, 0, 168, 4, 2},  // 0.413 at R = 1 (was 0.386), 137 regs
     {20, 5, 12, 4, 1, 1, 1, 0, 168, 5, 2},  // 0.667 at R = 1 (was 0.635), 145 regs
+    {21, 7, 12, 1, 5, 0, 0, 0, 168, 5},   // (the r02 resident shape before the CTA-size search: 0.40 at R = 1;
+                                          //  the new resident 11 x 12 two-warp tile streams at 0.31)
     {22, 5, 8, 5, 1, 0, 0, 1, 168, 5},  // 0.624 at R = 1 (was 0.428), 114 regs
     {23, 8, 12, 1, 5, 0, 0, 0, 255, 5, 2},  // 0.433 at R = 1 (was 0.365), 221 regs
     {24, 6, 12, 1, 4, 0, 1, 0, 168, 6, 2},  // 0.707 at R = 1 (was 0.489), 167 regs
