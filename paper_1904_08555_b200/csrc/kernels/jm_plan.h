@@ -681,18 +681,16 @@ JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8, 
 #define JM_F32T_RING 1
 #endif
 // n % 4 == 0: rotated 16-B one-time reads / write-backs of the packed matrix
-// (run_f32t PVEC).  Measured per n (profiles/r02_ab_pvec.md, R = 1, fraction
-// of HBM): 20 0.67 -> 0.75, 28 0.61 -> 0.66, 32 0.65 -> 0.76, 60 0.36 -> 0.42,
-// but 24 0.71 -> 0.67, 36..48 -0.01..-0.02 (R = 100 unchanged within 0.02);
-// JM_F32T_PVEC = 1: the sizes that gain, 2: every n % 4 == 0, 0: none
+// (run_f32t PVEC), in the low-repeat (streaming) kernel, where the one-time
+// accesses are a large share of the shared-memory traffic (at R = 100 they are
+// noise).  First measured with the resident tile shapes (profiles/r02_ab_pvec.md,
+// R = 1: 20 0.67 -> 0.75, 32 0.65 -> 0.76, but 24 0.71 -> 0.67), then the
+// streaming shapes were searched with the one-time accesses in the layout model
+// (tools/f32_layout.py init_wavefronts) and PVEC on.  JM_F32T_PVEC=0: off.
 #ifndef JM_F32T_PVEC
 #define JM_F32T_PVEC 1
 #endif
-JM_HD constexpr bool f32t_pvec(int n) {
-  return (n % 4) == 0 &&
-         (JM_F32T_PVEC == 2 || (JM_F32T_PVEC == 1 && (n == 20 || n == 28 || n == 32 || n == 52 || n == 56 ||
-                                                    n == 60 || n == 64)));
-}
+JM_HD constexpr bool f32t_pvec(int n, bool strm) { return JM_F32T_PVEC && strm && (n % 4) == 0; }
 #ifndef JM_F32T_RING_ROWS
 #define JM_F32T_RING_ROWS 0   // 1: row-pitched copies straight into the work layout (run_f32t RROWS); measured 2-5x slower at R = 1 (one 80-256 B bulk copy per row, profiles/r02_ab_f32_ring_rows.md)
 #endif

@@ -1296,7 +1296,7 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
   // (rows 2^k x 16 B apart: one bank slot) touch different chunks at a time.
   // The element accesses were 8-way conflicted at n = 32 (53 % of the R = 1
   // kernel's wavefronts, profiles/r02_ncu_kinds.md).
-  constexpr bool PVEC = f32t_pvec(N);
+  constexpr bool PVEC = f32t_pvec(N, STRM);
   const int prot = NH > 1 ? tr % NH : 0;
   // STRM (the low-repeat variant): even n run behind the bulk-copy ring with
   // each slot widened to the work region (f32t_ring); odd n keep the

@@ -164,11 +164,39 @@ class Cand:
             wb += self.n * wavefronts({l: mi * self.region + 16 * self.chunk(h, tc) for l, mi, tr, tc in L})
         return wa, wb, ws
 
+    def init_wavefronts(self, warp=0):
+        """wavefronts of the one-time read of the staged (packed, row stride n)
+        matrix into the accumulators; the write-back costs the same.  Rows of
+        whole 16-B chunks: run_f32t's rotated 16-B accesses (PVEC); else 4-B
+        element accesses (a 32-bit access costs its largest number of distinct
+        addresses in one bank)."""
+        L = self.lanes(warp)
+        nh = self.cb // self.vec
+        tot = 0
+        for i in range(self.ra):
+            if (self.n * self.es) % 16 == 0:
+                for st in range(nh):
+                    tot += wavefronts({l: mi * self.region + (self.row(i, tr) * self.n
+                                                              + self.chunk((st + tr % nh) % nh, tc) * self.vec) * self.es
+                                       for l, mi, tr, tc in L})
+            else:
+                for e in range(self.cb):
+                    banks = {}
+                    for l, mi, tr, tc in L:
+                        a = mi * self.region + (self.row(i, tr) * self.n + self.chunk(e // self.vec, tc) * self.vec
+                                                + e % self.vec) * self.es
+                        banks.setdefault((a // 4) % 32, set()).add(a)
+                    tot += max(len(v) for v in banks.values())
+        return tot
+
     def score(self, maxreg=128):
         wa, wb, ws = self.update_wavefronts()
         # FMA-pipe clocks per update (SM-wide): FP32 2 FFMA2 / clk, FP64 2 DFMA / clk (64 FMA/clk/SM)
         fclk = (self.ra * self.cb // 2 * self.n) / 2.0 if self.es == 4 else (self.ra * self.cb * self.n) / 2.0
-        lsu = (wa + wb + ws) / fclk                        # LSU clocks per FMA clock
+        # the one-time read + write-back, per update at the repeat count scored for
+        # (STREAM: R = 1; resident: R = 100)
+        wi = 2 * self.init_wavefronts() / (1 if STREAM else 100)
+        lsu = (wa + wb + ws + wi) / fclk                   # LSU clocks per FMA clock
         live = len(self.lanes(0)) / 32.0
         pad = self.n * self.n / (self.nr * self.nc)
         regs = self.regs

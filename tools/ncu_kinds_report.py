@@ -9,7 +9,10 @@ Per launch: the kind, the configuration, the roofline side it sits on
 achieved fraction of that roof from ncu's own duration (serialised,
 cold-cache replay, so slightly below the bench numbers), the pipe the kind
 issues to, DRAM bytes against the algorithmic 2·n²·s·batch, shared-memory
-bank conflicts, occupancy and the top stall reasons.
+shared-memory wavefronts above the ideal for the addresses accessed (ncu's
+"excessive" wavefronts; the raw bank-conflict counter also counts the
+second wavefront every 128-bit access needs, so it overstates conflicts),
+occupancy and the top stall reasons.
 """
 from __future__ import annotations
 
@@ -35,7 +38,7 @@ def main(path: str) -> None:
           "(DESIGN.md §6). ncu replays each kernel serialised and cold, so its fractions run a little under "
           "the bench / sweep numbers. DRAM/algo = (dram read + write) / (2·n²·s·batch).\n")
     print("| kind | config | roof | achieved | frac | pipe busy | DRAM/algo | regs | smem KB | warps active % | "
-          "smem conflicts | top stalls |")
+          "smem excess wavefronts | top stalls |")
     print("|---|---|---|---|---|---|---|---|---|---|---|---|")
     for (what, n, dt, r, v), s in zip(ncu_kinds.KINDS, rows):
         hbm = r * (n + 1) < 46
@@ -47,7 +50,7 @@ def main(path: str) -> None:
             ach_s = f"{ach:.2f} TF"
         pipe = (f"FP64 {s['fp64_shared_pipe_pct']:.0f}% (DMMA {s['dmma_pct']:.0f}, DFMA {s['dfma_pct']:.0f})"
                 if dt == "f64" else f"FMA {s['fma_pipe_pct']:.0f}%")
-        conf = s["smem_conflicts"] / s["smem_wavefronts"] if s["smem_wavefronts"] > 0 else 0.0
+        conf = s.get("smem_excessive", float("nan")) / s["smem_wavefronts"] if s["smem_wavefronts"] > 0 else 0.0
         st = ", ".join(f"{k} {v}" for k, v in list(s["stalls_per_issue"].items())[:3])
         name = s["kernel"].replace("void ", "").split("(")[0]
         print(f"| {what} (`{name}`) | n={n} {dt} R={r} batch={s['algo_bytes'] // (2 * n * n * (8 if dt == 'f64' else 4))} "

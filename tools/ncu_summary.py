@@ -26,11 +26,29 @@ STALLS = ["wait", "math_pipe_throttle", "short_scoreboard", "long_scoreboard", "
 
 
 def raw(rep: str) -> list[dict]:
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"],
-                         check=True, capture_output=True, text=True).stdout
+    """rows of the raw page: from a report (ncu -i) or a saved raw CSV (.csv / .csv.gz)"""
+    if rep.endswith(".csv") or rep.endswith(".csv.gz"):
+        import gzip
+        out = gzip.open(rep, "rt").read() if rep.endswith(".gz") else open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"],
+                             check=True, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    head, _units = rows[0], rows[1]
-    return [dict(zip(head, r)) for r in rows[2:]]
+    head, units = rows[0], rows[1]
+    recs = [dict(zip(head, r)) for r in rows[2:]]
+    # a saved page without --print-units base: scale to base units (ns, byte, Hz)
+    scale = {"us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "s": 1e9, "second": 1e9,
+             "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Kbyte/block": 1e3, "Mbyte/block": 1e6,
+             "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9, "Kbyte/second": 1e3, "Mbyte/second": 1e6, "Gbyte/second": 1e9}
+    for k, u in zip(head, units):
+        f = scale.get(u)
+        if f:
+            for d in recs:
+                try:
+                    d[k] = str(float(d[k].replace(",", "")) * f)
+                except (ValueError, KeyError):
+                    pass
+    return recs
 
 
 def num(d: dict, k: str) -> float:
@@ -62,6 +80,11 @@ def summarise(d: dict, algo=None) -> dict:
         "dram_pct": num(d, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
         "smem_wavefronts": num(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
         "smem_conflicts": num(d, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+        # wavefronts above the ideal for the accessed addresses (the source page's
+        # "L1 Wavefronts Shared Excessive"); the bank-conflict counter above also
+        # counts the extra wavefronts every 128-bit access needs, so it is not
+        # the excess
+        "smem_excessive": num(d, "derived__memory_l1_wavefronts_shared_excessive"),
         "smem_pipe_pct": num(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
         "inst": num(d, "smsp__inst_executed.sum"),
     }
@@ -86,10 +109,10 @@ def md_row(s: dict) -> str:
     pipe = (f"shared {s['fp64_shared_pipe_pct']:.1f}% (dmma {s['dmma_pct']:.1f}, dfma {s['dfma_pct']:.1f})"
             if s["fp64_shared_pipe_pct"] > 1 else f"fma {s['fma_pipe_pct']:.1f}%")
     tr = f"{s['traffic_ratio']:.3f}" if "traffic_ratio" in s else "-"
-    conf = s["smem_conflicts"] / s["smem_wavefronts"] if s["smem_wavefronts"] > 0 else 0.0
+    conf = s["smem_excessive"] / s["smem_wavefronts"] if s["smem_wavefronts"] > 0 else 0.0
     return (f"| {s['kernel'].split('(')[0]} | {s['ms']:.3f} | {s['regs']} | {s['smem_kb']:.1f} | "
             f"{s['warps_active_pct']:.1f} | {pipe} | {s['dram_pct']:.1f} | {tr} | "
-            f"{s['smem_wavefronts'] / 1e6:.1f}M ({100 * conf:.0f}% confl) | "
+            f"{s['smem_wavefronts'] / 1e6:.1f}M ({100 * conf:.0f}% excess) | "
             f"{', '.join(f'{k} {v}' for k, v in s['stalls_per_issue'].items())} |")
 
 
