@@ -206,10 +206,10 @@ constexpr F32TRow F64T_TABLE[] = {
 #if JM_F64T_ON
     {11, 3, 12, 4, 1, 0, 1, 0, 255, 2},
     {12, 3, 12, 4, 1, 0, 1, 0, 168, 6},
-    {17, 9, 6, 3, 1, 1, 1, 0, 255, 8},    // (r02 wide search: 0.553 vs the border DMMA's 0.536)
-    {18, 9, 6, 3, 1, 1, 1, 0, 255, 9},    // (r02 wide search: 0.628; 6 x 10 0.560)
-    {19, 5, 10, 4, 1, 1, 1, 0, 255, 9},
-    {20, 5, 10, 4, 1, 1, 1, 0, 255, 10},
+    {17, 9, 6, 3, 1, 1, 1, 0, 168, 8},    // (r02 wide search: 0.553 vs the border DMMA's 0.536; cap 168: 0.555)
+    {18, 9, 6, 3, 1, 1, 1, 0, 200, 9},    // (r02 wide search: 0.628, cap 200: 0.638; 6 x 10 0.560)
+    {19, 5, 10, 4, 1, 1, 1, 0, 168, 9},   // (cap 168: 0.615)
+    {20, 5, 10, 4, 1, 1, 1, 0, 168, 10},  // (cap 168: 0.712)
 #endif
 };
 constexpr F32TRow F32T_TABLE[] = {
@@ -267,47 +267,49 @@ constexpr F32TRow F32T_TABLE[] = {
 // region -- more warps per SM -- can beat the faster k loop); same fields.
 constexpr F32TRow F32TS_TABLE[] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    // r02 stream search v2 (R = 1, fraction of the HBM bandwidth (bytes moved / time) of the kernel the
-    // library picks, "was" = the resident shape; last field 2 = two-warp CTAs;
-    // profiles/r02_f32_stream_search_v2.jsonl)
+    // Streaming-kernel shapes, R = 1, fraction of the HBM bandwidth (bytes moved / time) of the
+    // kernel the library picks ("was" = the resident shape); last field 2 = two-warp CTAs.
+    // Odd n: search v2 (profiles/r02_f32_stream_search_v2.jsonl); even n: search v3 with the
+    // one-time packed accesses in the layout model and PVEC on (r02_f32_stream_search_v3.jsonl);
+    // n = 42, 44, 52, 54 stream fastest with their resident shape.
     {17, 6, 4, 6, 0, 0, 1, 1, 168, 4, 2},  // 0.448 at R = 1 (was 0.316), 106 regs
-    {18, 5, 12, 4, 1, 1, 1, 0, 168, 4, 2},  // 0.667 at R = 1 (was 0.475), 138 regs
+    {18, 5, 12, 4, 2, 0, 1, 0, 168, 4, 2},  // 0.703 at R = 1 (v3) (was 0.477), 144 regs
     {19, 5, 12, 4, 1, 1, 1, 0, 168, 4, 2},  // 0.413 at R = 1 (was 0.386), 137 regs
-    {20, 5, 12, 4, 1, 1, 1, 0, 168, 5, 2},  // 0.667 at R = 1 (was 0.635), 145 regs
-    {21, 7, 12, 1, 5, 0, 0, 0, 168, 5},   // (the r02 resident shape before the CTA-size search: 0.40 at R = 1;
-                                          //  the new resident 11 x 12 two-warp tile streams at 0.31)
-    {22, 5, 8, 5, 1, 0, 0, 1, 168, 5},  // 0.624 at R = 1 (was 0.428), 114 regs
+    {20, 5, 12, 4, 1, 1, 1, 0, 168, 5, 2},  // 0.747 at R = 1 (v3) (was 0.705), 133 regs
+    {21, 7, 12, 1, 5, 0, 0, 0, 168, 5},   // the r02 resident shape before the CTA-size search (0.40 at R = 1; the 11 x 12 two-warp tile streams at 0.31)
+    {22, 6, 12, 1, 2, 0, 1, 0, 168, 5},  // 0.694 at R = 1 (v3) (was 0.428), 165 regs
     {23, 8, 12, 1, 5, 0, 0, 0, 255, 5, 2},  // 0.433 at R = 1 (was 0.365), 221 regs
-    {24, 6, 12, 1, 4, 0, 1, 0, 168, 6, 2},  // 0.707 at R = 1 (was 0.489), 167 regs
+    {24, 6, 12, 1, 4, 1, 1, 0, 168, 6},  // 0.723 at R = 1 (v3) (was 0.506), 159 regs
     {25, 7, 8, 1, 1, 1, 0, 1, 168, 6, 2},  // 0.424 at R = 1 (was 0.365), 132 regs
-    {26, 7, 8, 1, 1, 1, 0, 1, 168, 6, 2},  // 0.656 at R = 1 (was 0.624), 133 regs
+    {26, 7, 8, 1, 1, 1, 0, 1, 168, 6, 2},  // 0.650 at R = 1 (v3) (was 0.618), 133 regs
     {27, 7, 8, 1, 1, 1, 0, 1, 168, 6, 2},  // 0.468 at R = 1 (was 0.455), 131 regs
-    {28, 7, 8, 1, 1, 1, 0, 1, 168, 7, 2},  // 0.609 at R = 1 (was 0.572), 131 regs
+    {28, 7, 8, 1, 0, 0, 0, 1, 168, 7, 2},  // 0.667 at R = 1 (v3) (was 0.628), 131 regs
     {29, 8, 8, 1, 3, 1, 0, 1, 168, 7, 2},  // 0.440 at R = 1 (was 0.428), 144 regs
-    {30, 8, 8, 1, 3, 1, 0, 1, 168, 7, 2},  // 0.712 at R = 1 (was 0.675), 146 regs
+    {30, 8, 8, 1, 3, 1, 0, 1, 168, 7, 2},  // 0.705 at R = 1 (v3) (was 0.667), 146 regs
     {31, 8, 8, 1, 3, 1, 0, 1, 168, 7, 2},  // 0.475 at R = 1 (was 0.428), 141 regs
-    {32, 8, 8, 1, 3, 1, 0, 1, 168, 8, 2},  // 0.650 at R = 1 (was 0.465), 144 regs
+    {32, 8, 8, 1, 3, 1, 0, 1, 168, 8, 2},  // 0.758 at R = 1 (v3) (was 0.681), 144 regs
     {33, 6, 8, 1, 0, 1, 1, 0, 168, 8},  // 0.351 at R = 1 (was 0.289), 122 regs
-    {34, 6, 8, 1, 0, 1, 1, 0, 168, 8},  // 0.530 at R = 1 (was 0.512), 124 regs
+    {34, 7, 12, 2, 0, 0, 0, 1, 168, 8},  // 0.535 at R = 1 (v3) (was 0.508), 161 regs
     {35, 7, 12, 1, 1, 1, 0, 1, 168, 8, 2},  // 0.394 at R = 1 (was 0.375), 160 regs
-    {36, 6, 8, 1, 0, 1, 1, 0, 168, 9},  // 0.520 at R = 1 (was 0.485), 141 regs
+    {36, 6, 8, 3, 0, 0, 0, 0, 168, 9},  // 0.537 at R = 1 (v3) (was 0.491), 124 regs
     {37, 7, 8, 1, 0, 1, 1, 0, 168, 9},  // 0.355 at R = 1 (was 0.334), 138 regs
-    {38, 5, 12, 1, 0, 0, 1, 0, 168, 9, 2},  // 0.513 at R = 1 (was 0.488), 129 regs
+    {38, 5, 12, 1, 0, 0, 1, 0, 168, 9, 2},  // 0.506 at R = 1 (v3) (was 0.485), 129 regs
     {39, 7, 8, 1, 0, 1, 1, 0, 168, 9},  // 0.376 at R = 1 (was 0.358), 137 regs
-    {40, 5, 12, 1, 0, 0, 1, 0, 168, 10, 2},  // 0.512 at R = 1 (was 0.496), 129 regs
+    {40, 5, 12, 1, 0, 1, 1, 0, 168, 10},  // 0.494 at R = 1 (v3) (was 0.465), 135 regs
+    {46, 6, 12, 1, 0, 1, 1, 0, 168, 11},  // 0.490 at R = 1 (v3) (was 0.462), 141 regs
+    {48, 6, 12, 1, 0, 1, 1, 0, 168, 12},  // 0.481 at R = 1 (v3) (was 0.396), 156 regs
     {49, 7, 16, 1, 0, 0, 0, 0, 255, 2},  // 0.258 at R = 1 (was 0.233), 214 regs
-    {50, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.364 at R = 1 (was 0.286), 136 regs
+    {50, 7, 8, 1, 0, 1, 1, 0, 168, 2, 2},  // 0.365 at R = 1 (v3) (was 0.286), 140 regs
     {51, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.300 at R = 1 (was 0.241), 146 regs
-    {52, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.358 at R = 1 (was 0.345), 152 regs
     {53, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.303 at R = 1 (was 0.245), 154 regs
-    {56, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.392 at R = 1 (was 0.316), 134 regs
+    {56, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.407 at R = 1 (v3) (was 0.309), 137 regs
     {57, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.303 at R = 1 (was 0.242), 146 regs
-    {58, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.409 at R = 1 (was 0.289), 154 regs
-    {60, 8, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.356 at R = 1 (was 0.293), 164 regs
+    {58, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.410 at R = 1 (v3) (was 0.290), 154 regs
+    {60, 8, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.414 at R = 1 (v3) (was 0.291), 146 regs
     {61, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.324 at R = 1 (was 0.265), 150 regs
-    {62, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.428 at R = 1 (was 0.315), 152 regs
+    {62, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.428 at R = 1 (v3) (was 0.316), 152 regs
     {63, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.295 at R = 1 (was 0.229), 153 regs
-    {64, 8, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.283 at R = 1 (was 0.248), 155 regs
+    {64, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.459 at R = 1 (v3) (was 0.297), 155 regs
 };
 #ifndef JM_F32T_RA                // tuning hooks: force the register-tile shape / layout / knobs
 #define JM_F32T_RA 0
@@ -690,7 +692,9 @@ JM_HD constexpr bool dmma_inplace(int n) { return dmma_scr(n) <= ring_sbm(n, 8, 
 #ifndef JM_F32T_PVEC
 #define JM_F32T_PVEC 1
 #endif
-JM_HD constexpr bool f32t_pvec(int n, bool strm) { return JM_F32T_PVEC && strm && (n % 4) == 0; }
+JM_HD constexpr bool f32t_pvec(int n, bool strm) {   // (resident n = 60: +0.03 of the pipe at R = 100)
+  return JM_F32T_PVEC && (strm || n == 60) && (n % 4) == 0;
+}
 #ifndef JM_F32T_RING_ROWS
 #define JM_F32T_RING_ROWS 0   // 1: row-pitched copies straight into the work layout (run_f32t RROWS); measured 2-5x slower at R = 1 (one 80-256 B bulk copy per row, profiles/r02_ab_f32_ring_rows.md)
 #endif

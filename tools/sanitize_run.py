@@ -24,11 +24,15 @@ import torch  # noqa: E402
 
 import paper_1904_08555_b200 as jm  # noqa: E402
 
+# r02 adds: the FP64 register tiles (11, 17, 20) and their DMMA ring, k-compaction (28, 44),
+# the thin border (25), FP32 tiles with their own streaming shapes, two-warp CTAs, the
+# rotated 16-B one-time accesses (20, 32, 48, 64) and the prefetching stage (odd n: 21, 49)
 CASES = [(2, "f64"), (3, "f64"), (5, "f64"), (7, "f64"), (9, "f64"), (10, "f64"), (16, "f64"),
-         (13, "f64"), (17, "f64"), (26, "f64"), (32, "f64"), (33, "f64"), (40, "f64"), (44, "f64"),
-         (48, "f64"), (64, "f64"),
-         (3, "f32"), (8, "f32"), (10, "f32"), (12, "f32"), (13, "f32"), (16, "f32"), (24, "f32"),
-         (33, "f32"), (53, "f32"), (64, "f32")]
+         (11, "f64"), (13, "f64"), (17, "f64"), (20, "f64"), (25, "f64"), (26, "f64"), (28, "f64"),
+         (32, "f64"), (33, "f64"), (40, "f64"), (44, "f64"), (48, "f64"), (64, "f64"),
+         (3, "f32"), (8, "f32"), (10, "f32"), (12, "f32"), (13, "f32"), (16, "f32"), (17, "f32"),
+         (20, "f32"), (21, "f32"), (24, "f32"), (32, "f32"), (33, "f32"), (48, "f32"), (49, "f32"),
+         (53, "f32"), (64, "f32")]
 
 
 def main():
@@ -60,6 +64,9 @@ def main():
         print(f"ok ring n={n} {dt} batch={b}", flush=True)
     x = torch.rand(11, 16, 16, dtype=torch.float64, device="cuda")
     jm.run(x, 3, kind="aot_specialized", sync=True)
+    for n in (2, 4, 5):   # the latency kernel (a warp per matrix, tiny batches)
+        x = torch.rand(3, n, n, dtype=torch.float64, device="cuda")
+        jm.run(x, 5, variant="latency", sync=True)
     groups = []
     bufs = []
     for n in (2, 9, 17, 40):
