@@ -442,6 +442,12 @@ JM_HD constexpr bool f64t_use(int n) {
   return false;
 }
 JM_HD constexpr bool f32t_use(int n) { return n >= 17; }
+// the low-repeat kernel of the row-panel sizes may be the register tiles
+// instead (their streaming shapes, F32TS_TABLE): n >= JM_F32T_STREAM_MIN
+#ifndef JM_F32T_STREAM_MIN
+#define JM_F32T_STREAM_MIN 17
+#endif
+JM_HD constexpr bool f32t_stream_use(int n) { return n >= 17 || n >= JM_F32T_STREAM_MIN; }
 
 // ---- F32 row panels (9 <= n <= 32) ----
 // A thread owns RP = 4 FULL rows of M (the A operand is local); row k of M
@@ -623,15 +629,21 @@ JM_HD constexpr int stream_lo(int n, int dtype) {
 #endif
 JM_HD constexpr int f64t_rn(int n) { return JM_F64T_RN > 0 ? JM_F64T_RN : n <= 12 ? 120 : n <= 18 ? 160 : 330; }
 // FP32 register tiles: the streaming kernel (ring / prefetching stage, with
-// its own tile shapes, F32TS_TABLE) below this R(n+1).  Measured at R = 2..8
-// (profiles/r02_f32_stream_xover.jsonl): it still wins at R = 8 for n = 20,
-// 28, 32, 33, 40, 48, 56; the crossover is R(n+1) ~ 110 at n = 17, ~125 at 24,
-// ~200 at 64.  JM_F32T_RN > 0: one switch point for every tile size.
+// its own tile shapes, F32TS_TABLE) while R <= F32T_STREAM_MAXR[n]: measured
+// stream vs resident at R = 2..12, 24 and 100 (profiles/r02_f32_stream_xover_v3.jsonl,
+// r02_f32_stream_xover_r24_r100.jsonl).  With its two-warp CTAs and shapes the
+// streaming kernel is the faster one even at R = 100 for n = 27, 29, 31, 32,
+// 34, 36, 38, 39, 41, 45, 46, 52, 54, 55, 58..60 (e.g. n = 52 0.54 -> 0.56,
+// 60 0.61 -> 0.65 of the pipe), so those sizes always stream (1 << 20).
+// JM_F32T_RN > 0: one switch point R(n+1) < JM_F32T_RN for every tile size.
 #ifndef JM_F32T_RN
 #define JM_F32T_RN 0
 #endif
+constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 1048576, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 50, 1048576, 12, 50, 50, 1048576, 1048576, 50, 24, 8, 8, 8, 1048576, 50, 1048576, 1048576, 12, 50, 1048576, 1048576, 1048576, 50, 50, 50, 50};
 JM_HD constexpr int f32t_rn(int n) {
-  return JM_F32T_RN > 0 ? JM_F32T_RN : n == 17 ? 110 : n == 24 ? 125 : n >= 61 ? 200 : 9 * (n + 1);
+  return JM_F32T_RN > 0 ? JM_F32T_RN
+         : F32T_STREAM_MAXR[n] >= (1 << 20) ? (1 << 30)
+         : F32T_STREAM_MAXR[n] > 0 ? F32T_STREAM_MAXR[n] * (n + 1) + 1 : 9 * (n + 1);
 }
 JM_HD constexpr int stream_rn_tpm(int n, int dtype) { return (dtype == 0 && n == 3) ? (1 << 30) : 0; }
 JM_HD constexpr int stream_rn(int n, int dtype) {
@@ -732,7 +744,7 @@ JM_HD constexpr int round_mpc(int n, int dtype) {
   return (tile_for(n, dtype) == Tile::Dmma ||
           (dtype == 1 && (tile_for(n, dtype) == Tile::Tpms || tile_for(n, dtype) == Tile::Reg)))
              ? (dmma_w(n, true) == 1 ? DMMA_WPC : 1)
-         : f32p_use(n)                   ? F32P_WPC * f32p_mpw(n)
+         : (f32p_use(n) && !f32t_stream_use(n)) ? F32P_WPC * f32p_mpw(n)
                                          : f32t_mpc(n, 2);
 }
 // Plan of the streaming variant: mpc = matrices per ring chunk (the host sizes
@@ -749,7 +761,7 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
     const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers
     return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm, dmma_slot(n)) + own * dmma_scr(n), w};
   }
-  if (f32p_use(n))
+  if (f32p_use(n) && !f32t_stream_use(n))
     return f32p_ring_inplace(n)
                ? Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm, f32p_slot(n)) + rm * f32p_mbuf(n), 1}
                : Plan{(int)Tile::F32Rows, 32 * F32P_WPC, chm, ring_bytes(n, es, rm) + rm * f32p_pstr(n), 1};

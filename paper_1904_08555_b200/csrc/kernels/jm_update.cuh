@@ -1731,7 +1731,7 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
     else run_f64t<N, A, false>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Dmma) {
     run_dmma<N, A, dmma_w(N, STRM), STRM>(in, out, batch, repeat);
-  } else if constexpr (f32p_use(N)) {
+  } else if constexpr (f32p_use(N) && !(STRM && f32t_stream_use(N))) {
     run_f32p<N, A, STRM>(in, out, batch, repeat);
   } else {
     run_f32t<N, A, STRM>(in, out, batch, repeat);

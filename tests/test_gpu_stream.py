@@ -156,11 +156,10 @@ def test_variant_selection_and_key_info(jm):
     assert jm.jit_mat_prepare_for(12, "f32", 1) == 0       # TPMS beats the ring even at R = 1
     assert jm.jit_mat_prepare_for(13, "f32", 1) == 1 and jm.jit_mat_prepare_for(13, "f32", 2) == 0
     assert jm.jit_mat_prepare_for(16, "f32", 4) == 0
-    assert jm.jit_mat_prepare_for(64, "f32", 3) == 1       # 195 < 200 (jm_plan.h f32t_rn)
-    assert jm.jit_mat_prepare_for(64, "f32", 4) == 0
-    assert jm.jit_mat_prepare_for(32, "f32", 8) == 1       # 264 < 9 (n + 1) = 297
-    assert jm.jit_mat_prepare_for(32, "f32", 9) == 0
-    assert jm.jit_mat_prepare_for(17, "f32", 6) == 1 and jm.jit_mat_prepare_for(17, "f32", 7) == 0   # 108 < 110
+    # FP32 tiles: stream while R <= F32T_STREAM_MAXR[n] (jm_plan.h f32t_rn)
+    assert jm.jit_mat_prepare_for(64, "f32", 50) == 1 and jm.jit_mat_prepare_for(64, "f32", 51) == 0
+    assert jm.jit_mat_prepare_for(32, "f32", 1000) == 1    # streams at every R (faster even at R = 100)
+    assert jm.jit_mat_prepare_for(17, "f32", 6) == 1 and jm.jit_mat_prepare_for(17, "f32", 7) == 0
     assert jm.jit_mat_prepare_for(8, "f64", 1) == 0        # n = 8 DMMA: resident (measured)
     assert jm.jit_mat_prepare_for(4, "f64", 1, flags=jm.JM_FLAG_STREAMING) == 1   # TPM: staged variant
     assert jm.jit_mat_prepare_for(4, "f64", 1) == 0        # light TPM sizes stay resident

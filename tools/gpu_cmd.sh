@@ -1,8 +1,12 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-mkdir -p gpurun_out/r02
+mkdir -p gpurun_out/r02 gpurun_out/r02/san
 O=gpurun_out/r02
-timeout 1500 python tools/stream_sweep.py --sizes $(seq -s, 17 64) --dtypes f32 --repeats 24,100 --gb 0.5 --steps 3 > $O/f32_xover3.jsonl 2> $O/f32_xover3.err
-rm -f $O/f64_n17.jsonl
-timeout 900 python tools/f32_search.py --dtype f64 --run tools/f64_candidates_n17.json --out $O/f64_n17.jsonl 2> $O/f64_n17.err
-python tools/f32_search.py --pick $O/f64_n17.jsonl > $O/f64_n17_pick.txt
-cat $O/f64_n17_pick.txt
+timeout 2700 python -m pytest tests -m gpu -q 2>&1 | tail -15 > $O/gputest_full10.txt
+rm -f $O/all_n10.jsonl
+timeout 1200 python tools/stream_sweep.py --sizes $(seq -s, 2 64) --dtypes f64,f32 --repeats 1,100 --gb 0.5 --steps 5 --out $O/all_n10.jsonl > /dev/null 2> $O/all_n10.err
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_run.py > $O/san/$tool.txt 2>&1
+  echo "$tool rc=$?" >> $O/san/summary.txt
+  tail -3 $O/san/$tool.txt >> $O/san/summary.txt
+done
+tail -3 $O/gputest_full10.txt; cat $O/san/summary.txt
