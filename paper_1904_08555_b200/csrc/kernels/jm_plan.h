@@ -272,6 +272,7 @@ constexpr F32TRow F32TS_TABLE[] = {
     // Odd n: search v2 (profiles/r02_f32_stream_search_v2.jsonl); even n: search v3 with the
     // one-time packed accesses in the layout model and PVEC on (r02_f32_stream_search_v3.jsonl);
     // n = 42, 44, 52, 54 stream fastest with their resident shape.
+    {16, 8, 4, 1, 4, 0, 1, 0, 168, 4},     // 0.887 at R = 1 (the row-panel ring: 0.54; r02_f32s_n15_16.jsonl)
     {17, 6, 4, 6, 0, 0, 1, 1, 168, 4, 2},  // 0.448 at R = 1 (was 0.316), 106 regs
     {18, 5, 12, 4, 2, 0, 1, 0, 168, 4, 2},  // 0.703 at R = 1 (v3) (was 0.477), 144 regs
     {19, 5, 12, 4, 1, 1, 1, 0, 168, 4, 2},  // 0.413 at R = 1 (was 0.386), 137 regs
@@ -441,13 +442,16 @@ JM_HD constexpr bool f64t_use(int n) {
     if (r.n == n && r.ra > 0) return true;
   return false;
 }
-JM_HD constexpr bool f32t_use(int n) { return n >= 17; }
-// the low-repeat kernel of the row-panel sizes may be the register tiles
-// instead (their streaming shapes, F32TS_TABLE): n >= JM_F32T_STREAM_MIN
+JM_HD constexpr bool f32p_use(int n);
+JM_HD constexpr bool f32t_use(int n) { return n >= 15 && !f32p_use(n); }   // (resident kernel)
+// The low-repeat kernel of a row-panel size may be the register tiles instead
+// (their streaming shapes, F32TS_TABLE): n >= JM_F32T_STREAM_MIN.  Measured at
+// R = 1 (profiles/r02_f32s_n15_16.jsonl): n = 16 as 8 x 4 tiles 0.89 of HBM
+// against 0.54 for the row-panel ring; n = 15 0.58 against 0.72 (stays).
 #ifndef JM_F32T_STREAM_MIN
-#define JM_F32T_STREAM_MIN 17
+#define JM_F32T_STREAM_MIN 16
 #endif
-JM_HD constexpr bool f32t_stream_use(int n) { return n >= 17 || n >= JM_F32T_STREAM_MIN; }
+JM_HD constexpr bool f32t_stream_use(int n) { return f32t_use(n) || (n >= 15 && n >= JM_F32T_STREAM_MIN); }
 
 // ---- F32 row panels (9 <= n <= 32) ----
 // A thread owns RP = 4 FULL rows of M (the A operand is local); row k of M
@@ -552,7 +556,8 @@ JM_HD constexpr bool use_mb1(int n, int dtype, bool strm = false) {
 }
 // ... or k_update[_stream]_rc (a register cap, __maxnreg__): the F32T tiles
 JM_HD constexpr bool use_rc(int n, int dtype, bool strm = false) {
-  return (void)strm, (dtype == 0 && tile_for(n, dtype) == Tile::F32 && f32t_use(n)) || tile_for(n, dtype) == Tile::Reg;
+  return (dtype == 0 && tile_for(n, dtype) == Tile::F32 && (strm ? f32t_stream_use(n) : f32t_use(n))) ||
+         tile_for(n, dtype) == Tile::Reg;
 }
 
 // ---- streaming variant (low repeat: the HBM-bound side of the roofline) ----
@@ -652,7 +657,7 @@ JM_HD constexpr int stream_rn(int n, int dtype) {
          : tile_for(n, dtype) == Tile::Reg ? f64t_rn(n)
          : (dtype == 0 && tile_for(n, dtype) == Tile::Tpms) ? (n == 12 ? 0 : 20)   // R = 1: row-panel ring
          : dtype == 1        ? stream_rn_f64(n)
-         : f32p_use(n)       ? 64
+         : (f32p_use(n) && !f32t_stream_use(n)) ? 64
                              : f32t_rn(n);
 }
 // rounds per chunk: >= JM_RING_CHUNK bytes and a chunk a multiple of 16 B

@@ -37,17 +37,18 @@ KINDS = [
     ("CTA DMMA ring (streaming)", 64, "f64", 1, "auto"),
     ("F32 row panels", 16, "f32", 100, "auto"),
     ("F32 row-panel ring (streaming)", 16, "f32", 1, "auto"),
-    ("F32 tiles", 17, "f32", 100, "auto"),
-    ("F32 tiles", 24, "f32", 100, "auto"),
-    ("F32 tiles", 32, "f32", 100, "auto"),
-    ("F32 tiles", 48, "f32", 100, "auto"),
-    ("F32 tiles", 64, "f32", 100, "auto"),
-    ("F32 tiles, low-repeat kernel (prefetching stage, odd n)", 17, "f32", 1, "auto"),
-    ("F32 tile ring (streaming, even n)", 24, "f32", 1, "auto"),
-    ("F32 tile ring (streaming, even n)", 32, "f32", 1, "auto"),
-    ("F32 tiles, prefetching stage (streaming, odd n)", 33, "f32", 1, "auto"),
-    ("F32 tile ring (streaming, even n)", 48, "f32", 1, "auto"),
-    ("F32 tiles, low-repeat kernel (compute-bound at R = 1)", 64, "f32", 1, "auto"),
+    ("F32 tiles, resident kernel", 17, "f32", 100, "resident"),
+    ("F32 tiles, resident kernel", 24, "f32", 100, "resident"),
+    ("F32 tiles, resident kernel", 32, "f32", 100, "resident"),
+    ("F32 tiles, resident kernel", 48, "f32", 100, "resident"),
+    ("F32 tiles, resident kernel", 64, "f32", 100, "resident"),
+    ("F32 tiles, streaming kernel at R = 100 (its pick: two-warp 8x8 shape)", 32, "f32", 100, "streaming"),
+    ("F32 tiles, streaming kernel (prefetching stage, odd n)", 17, "f32", 1, "streaming"),
+    ("F32 tile ring (streaming, even n)", 24, "f32", 1, "streaming"),
+    ("F32 tile ring (streaming, even n)", 32, "f32", 1, "streaming"),
+    ("F32 tiles, prefetching stage (streaming, odd n)", 33, "f32", 1, "streaming"),
+    ("F32 tile ring (streaming, even n)", 48, "f32", 1, "streaming"),
+    ("F32 tiles, streaming kernel (compute-bound at R = 1)", 64, "f32", 1, "streaming"),
     ("latency kernel (C1: one 4x4, warp per matrix)", 4, "f64", 1000, "latency"),
     ("generic runtime-N kernel", 16, "f64", 100, "generic"),
 ]
