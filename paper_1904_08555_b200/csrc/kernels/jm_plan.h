@@ -213,6 +213,7 @@ constexpr F32TRow F64T_TABLE[] = {
 #endif
 };
 constexpr F32TRow F32T_TABLE[] = {
+    {16, 4, 16, 2, 1, 0, 1, 0, 168, 4},  // 0.721 of the pipe, 148 regs (row panels 0.708)
     {17, 6, 20, 2, 1, 0, 1, 0, 255, 4},  // 0.515 of the pipe, 200 regs (r02 wide search; was 0.434)
     {18, 6, 20, 2, 1, 0, 1, 0, 255, 4},  // 0.586 of the pipe, 247 regs (r02 wide search; was 0.491)
     {19, 5, 20, 1, 1, 0, 1, 0, 255, 4},  // 0.638 of the pipe, 205 regs (r02 wide search; was 0.487)
@@ -443,7 +444,7 @@ JM_HD constexpr bool f64t_use(int n) {
   return false;
 }
 JM_HD constexpr bool f32p_use(int n);
-JM_HD constexpr bool f32t_use(int n) { return n >= 15 && !f32p_use(n); }   // (resident kernel)
+JM_HD constexpr bool f32t_use(int n) { return n > JM_F32_TPM_MAX && !f32p_use(n); }   // (resident kernel)
 // The low-repeat kernel of a row-panel size may be the register tiles instead
 // (their streaming shapes, F32TS_TABLE): n >= JM_F32T_STREAM_MIN.  Measured at
 // R = 1 (profiles/r02_f32s_n15_16.jsonl): n = 16 as 8 x 4 tiles 0.89 of HBM
@@ -451,7 +452,7 @@ JM_HD constexpr bool f32t_use(int n) { return n >= 15 && !f32p_use(n); }   // (r
 #ifndef JM_F32T_STREAM_MIN
 #define JM_F32T_STREAM_MIN 16
 #endif
-JM_HD constexpr bool f32t_stream_use(int n) { return f32t_use(n) || (n >= 15 && n >= JM_F32T_STREAM_MIN); }
+JM_HD constexpr bool f32t_stream_use(int n) { return f32t_use(n) || (n > JM_F32_TPM_MAX && n >= JM_F32T_STREAM_MIN); }
 
 // ---- F32 row panels (9 <= n <= 32) ----
 // A thread owns RP = 4 FULL rows of M (the A operand is local); row k of M
@@ -462,8 +463,10 @@ constexpr int F32P_RP_MAX = 4;
 constexpr int F32P_WPC = 2;                       // warps per CTA
 constexpr int F32P_KSTEP = 4;                     // k steps between scheduling fences
 // (n > 16 needs more than 4 x 16 resident floats next to the accumulators: spills)
+// r02: n = 16 takes the register tiles (4 x 16: 0.72 of the FP32 pipe at
+// R = 100 against 0.71 for the row panels; profiles/r02_f32_n16_resident_search.jsonl)
 #ifndef JM_F32P_MAX
-#define JM_F32P_MAX 16
+#define JM_F32P_MAX 15
 #endif
 JM_HD constexpr bool f32p_use(int n) { return n >= 9 && n <= JM_F32P_MAX; }
 JM_HD constexpr int f32p_g(int n) { return n <= 16 ? 4 : 8; }                 // threads per matrix
@@ -574,6 +577,9 @@ JM_HD constexpr bool use_rc(int n, int dtype, bool strm = false) {
 #ifndef JM_RING_S
 #define JM_RING_S 2
 #endif
+#ifndef JM_RING_NOWAIT_UNSAFE
+#define JM_RING_NOWAIT_UNSAFE 0   // timing experiment only (wrong results): skip the store-read wait before a refill
+#endif
 #ifndef JM_RING_CHUNK
 #define JM_RING_CHUNK 8192
 #endif
@@ -644,7 +650,7 @@ JM_HD constexpr int f64t_rn(int n) { return JM_F64T_RN > 0 ? JM_F64T_RN : n <= 1
 #ifndef JM_F32T_RN
 #define JM_F32T_RN 0
 #endif
-constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 1048576, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 50, 1048576, 12, 50, 50, 1048576, 1048576, 50, 24, 8, 8, 8, 1048576, 50, 1048576, 1048576, 12, 50, 1048576, 1048576, 1048576, 50, 50, 50, 50};
+constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 24, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 1048576, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 50, 1048576, 12, 50, 50, 1048576, 1048576, 50, 24, 8, 8, 8, 1048576, 50, 1048576, 1048576, 12, 50, 1048576, 1048576, 1048576, 50, 50, 50, 50};
 JM_HD constexpr int f32t_rn(int n) {
   return JM_F32T_RN > 0 ? JM_F32T_RN
          : F32T_STREAM_MAXR[n] >= (1 << 20) ? (1 << 30)

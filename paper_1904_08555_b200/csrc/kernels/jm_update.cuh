@@ -362,7 +362,9 @@ struct Ring {
         store(ch, s);
         const long long nx = ch + (long long)S * gridDim.x;
         if (nx < nchunks && full(nx)) {
+#if !JM_RING_NOWAIT_UNSAFE   // (timing experiment only: the refill may overwrite slots a store still reads)
           bulk_wait_read_all();   // this lane's stores have read their slots: refill
+#endif
           issue(nx, s);
         }
       }

@@ -152,11 +152,12 @@ def test_variant_selection_and_key_info(jm):
     assert jm.jit_mat_prepare_for(64, "f64", 7) == 0
     assert jm.jit_mat_prepare_for(33, "f64", 2) == 1       # 68 < 100: thin-border resident above
     assert jm.jit_mat_prepare_for(33, "f64", 3) == 0
-    assert jm.jit_mat_prepare_for(16, "f32", 3) == 1       # 51 < 64
+    assert jm.jit_mat_prepare_for(15, "f32", 3) == 1       # 48 < 64 (row-panel ring)
+    assert jm.jit_mat_prepare_for(15, "f32", 4) == 0
     assert jm.jit_mat_prepare_for(12, "f32", 1) == 0       # TPMS beats the ring even at R = 1
     assert jm.jit_mat_prepare_for(13, "f32", 1) == 1 and jm.jit_mat_prepare_for(13, "f32", 2) == 0
-    assert jm.jit_mat_prepare_for(16, "f32", 8) == 1       # n = 16 streams through the register tiles
-    assert jm.jit_mat_prepare_for(16, "f32", 9) == 0       # (R <= 8; the row panels above)
+    assert jm.jit_mat_prepare_for(16, "f32", 24) == 1      # n = 16: register tiles, streaming to R = 24
+    assert jm.jit_mat_prepare_for(16, "f32", 25) == 0
     # FP32 tiles: stream while R <= F32T_STREAM_MAXR[n] (jm_plan.h f32t_rn)
     assert jm.jit_mat_prepare_for(64, "f32", 50) == 1 and jm.jit_mat_prepare_for(64, "f32", 51) == 0
     assert jm.jit_mat_prepare_for(32, "f32", 1000) == 1    # streams at every R (faster even at R = 100)

@@ -35,8 +35,10 @@ KINDS = [
     ("CTA DMMA", 64, "f64", 100, "auto"),
     ("CTA DMMA ring (streaming)", 40, "f64", 1, "auto"),
     ("CTA DMMA ring (streaming)", 64, "f64", 1, "auto"),
-    ("F32 row panels", 16, "f32", 100, "auto"),
-    ("F32 row-panel ring (streaming)", 16, "f32", 1, "auto"),
+    ("F32 row panels", 15, "f32", 100, "auto"),
+    ("F32 row-panel ring (streaming)", 15, "f32", 1, "auto"),
+    ("F32 tiles, resident kernel", 16, "f32", 100, "resident"),
+    ("F32 tile ring (streaming), 8 x 4", 16, "f32", 1, "streaming"),
     ("F32 tiles, resident kernel", 17, "f32", 100, "resident"),
     ("F32 tiles, resident kernel", 24, "f32", 100, "resident"),
     ("F32 tiles, resident kernel", 32, "f32", 100, "resident"),
