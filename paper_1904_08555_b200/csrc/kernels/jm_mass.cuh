@@ -8,10 +8,13 @@
 // dispatch map; here NVRTC instantiates jm::k_mass<D, Q> on first use, exactly
 // like k_update.  FP64.  Per element 4DQ(D+Q) + Q^2 flops against
 // (3D^2 + Q^2) doubles of traffic: HBM-bound at every (D, Q) <= 8, so the
-// kernel is a streaming one: one thread per element, x / op / y chunks staged
-// through shared memory with coalesced 128-bit copies at an odd 16-B stride
-// (conflict-free per-thread reads), B in shared memory (broadcast reads), the
-// quadrature-point values S in registers.  Appended to the NVRTC source.
+// kernels are streaming ones.  Small D*Q*(D+Q): one thread per element,
+// x / op / y chunks staged through shared memory with coalesced 128-bit copies
+// at an odd 16-B stride (conflict-free per-thread reads), B in shared memory
+// (broadcast reads), the quadrature-point values S in registers.  Larger
+// (jm_plan.h mass_dmma): one warp per element on the FP64 tensor cores
+// (mass_dmma_body below).  Appended
+// to the NVRTC source.
 #ifndef JM_MASS_CUH
 #define JM_MASS_CUH
 
@@ -97,12 +100,110 @@ __device__ __forceinline__ void mass_body(const double *__restrict__ B, const do
   }
 }
 
+// ----------------------------------------------------------------------
+// DMMA variant (r02; jm_plan.h mass_dmma): one WARP per element, the four
+// contractions as FP64 tensor-core products (DMMA.8x8x4, D and Q padded to 8),
+// no shared memory.  With lane (r = lane/4, j = lane%4) and the k-step s
+// summing over k = 2j + s, an accumulator fragment (lane holds M[r][2j+e])
+// is, with no data movement, both the A operand of M.C and the B operand of
+// C.M^T.  Written that way, the chain is
+//     M1 = B . X^T          (X^T as the B operand: lane loads X[r][2j..2j+1], 16 B)
+//     M2 = M1 . B^T = S^T   (S = B X B^T; lane holds S[2j+e][r])
+//     G^T = S^T .* op^T     (lane loads op[2j+e][r])
+//     M3 = B^T . G          (G^T's fragment is G as the B operand)
+//     Y += M3 . B           (Y itself is the accumulator: 16-B load and store)
+// = Y + B^T ((B X B^T) .* op) B, with two constant fragments per lane:
+// F1[s] = B[r][2j+s] (A of step 1, B operand of step 2) and F2[s] = B[2j+s][r]
+// (A of step 3, B operand of step 4).  8 DMMA per element = exactly the
+// 4DQ(D+Q) flops at D = Q = 8.  The thread-per-element kernel above issues one
+// broadcast shared load of B per FMA and was LDS-bound (0.29 of HBM at
+// D = Q = 8, profiles/r01_mass_f7_analog.jsonl).  Each warp keeps the next
+// element's x / y / op loads in flight while it computes the current one.
 template <int D, int Q>
-__global__ void __launch_bounds__(MASS_THREADS)
+__device__ __forceinline__ void mass_dmma_body(const double *__restrict__ B, const double *__restrict__ op,
+                                               const double *__restrict__ x, double *__restrict__ y,
+                                               long long elements) {
+  constexpr int WPC = MASS_DMMA_THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, r = lane >> 2, j = lane & 3;
+  double F1[2], F2[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int k = 2 * j + s;
+    F1[s] = (r < Q && k < D) ? B[r * D + k] : 0.0;
+    F2[s] = (k < Q && r < D) ? B[k * D + r] : 0.0;
+  }
+  // Each lane copies exactly the entries it will own as fragments (even D:
+  // its x / y pair as one 16-B cp.async; out-of-range entries zero-filled)
+  // into its own bytes of the warp's slot, so no barrier is needed: PD slots
+  // per warp keep PD elements' loads in flight without holding registers.
+  // Slot: x at lane*16, y at 512 + lane*16, op at 1024 + lane*16.
+  constexpr int PD = JM_MASS_DMMA_PD;
+  extern __shared__ __align__(16) char smem[];
+  char *const wbase = smem + warp * (PD * MASS_DMMA_SLOT) + lane * 16;
+  const bool okp = r < D && 2 * j < D, ok1 = r < D && 2 * j + 1 < D;
+  const bool oq0 = 2 * j < Q && r < Q, oq1 = 2 * j + 1 < Q && r < Q;
+  auto issue = [&](long long e, int slot) {
+    if (e < elements) {
+      const double *xe = x + e * (D * D), *ye = y + e * (D * D), *oe = op + e * (Q * Q);
+      char *sl = wbase + slot * MASS_DMMA_SLOT;
+      if constexpr (D % 2 == 0) {
+        cp_async_zfill16(sl, okp ? xe + r * D + 2 * j : x, okp ? 16 : 0);
+        cp_async_zfill16(sl + 512, okp ? ye + r * D + 2 * j : y, okp ? 16 : 0);
+      } else {
+        cp_async_zfill8(sl, okp ? xe + r * D + 2 * j : x, okp ? 8 : 0);
+        cp_async_zfill8(sl + 8, ok1 ? xe + r * D + 2 * j + 1 : x, ok1 ? 8 : 0);
+        cp_async_zfill8(sl + 512, okp ? ye + r * D + 2 * j : y, okp ? 8 : 0);
+        cp_async_zfill8(sl + 520, ok1 ? ye + r * D + 2 * j + 1 : y, ok1 ? 8 : 0);
+      }
+      cp_async_zfill8(sl + 1024, oq0 ? oe + (2 * j) * Q + r : op, oq0 ? 8 : 0);
+      cp_async_zfill8(sl + 1032, oq1 ? oe + (2 * j + 1) * Q + r : op, oq1 ? 8 : 0);
+    }
+    cp_async_commit();   // (an empty group past the end keeps the group count uniform)
+  };
+  const long long nw = (long long)gridDim.x * WPC;
+  long long e = (long long)blockIdx.x * WPC + warp;
+#pragma unroll
+  for (int q = 0; q < PD; ++q) issue(e + q * nw, q);
+  int slot = 0;
+  for (; e < elements; e += nw) {
+    cp_async_wait_group<PD - 1>();   // this lane's copies of element e have landed
+    const char *sl = wbase + slot * MASS_DMMA_SLOT;
+    const double2 xv = *reinterpret_cast<const double2 *>(sl);
+    const double2 yv = *reinterpret_cast<const double2 *>(sl + 512);
+    const double2 ov = *reinterpret_cast<const double2 *>(sl + 1024);
+    double m0 = 0.0, m1 = 0.0, s0 = 0.0, s1 = 0.0;
+    dmma884(m0, m1, F1[0], xv.x);    // M1 = B . X^T
+    dmma884(m0, m1, F1[1], xv.y);
+    dmma884(s0, s1, m0, F1[0]);      // M2 = M1 . B^T = S^T
+    dmma884(s0, s1, m1, F1[1]);
+    s0 *= ov.x;                      // G^T = S^T .* op^T
+    s1 *= ov.y;
+    m0 = 0.0; m1 = 0.0;
+    dmma884(m0, m1, F2[0], s0);      // M3 = B^T . G
+    dmma884(m0, m1, F2[1], s1);
+    double y0 = yv.x, y1 = yv.y;
+    dmma884(y0, y1, m0, F2[0]);      // Y += M3 . B
+    dmma884(y0, y1, m1, F2[1]);
+    double *ye = y + e * (D * D);
+    if constexpr (D % 2 == 0) {
+      if (okp) __stcs(reinterpret_cast<double2 *>(ye + r * D + 2 * j), make_double2(y0, y1));
+    } else {
+      if (okp) ye[r * D + 2 * j] = y0;
+      if (ok1) ye[r * D + 2 * j + 1] = y1;
+    }
+    issue(e + PD * nw, slot);        // the slot's values are consumed: refill it
+    slot = slot + 1 == PD ? 0 : slot + 1;
+  }
+  cp_async_wait_group<0>();
+}
+
+template <int D, int Q>
+__global__ void __launch_bounds__(plan_mass(D, Q).threads, mass_dmma(D, Q) ? JM_MASS_DMMA_MINB : 1)
     k_mass(const double *__restrict__ B, const double *__restrict__ op, const double *__restrict__ x,
            double *__restrict__ y, long long elements) {
   static_assert(D >= 1 && D <= MASS_MAX && Q >= 1 && Q <= MASS_MAX, "1 <= D, Q <= 8");
-  mass_body<D, Q>(B, op, x, y, elements);
+  if constexpr (mass_dmma(D, Q)) mass_dmma_body<D, Q>(B, op, x, y, elements);
+  else mass_body<D, Q>(B, op, x, y, elements);
 }
 
 }  // namespace jm

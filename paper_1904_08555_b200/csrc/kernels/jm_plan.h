@@ -864,9 +864,40 @@ JM_HD constexpr Plan plan_matmul_generic(int n, int dtype) {
 // one thread per element, MASS_THREADS elements per CTA chunk
 constexpr int MASS_MAX = 8;                        // 1 <= D, Q <= 8 (Fig. 7: d,q in {2,4,8})
 constexpr int MASS_THREADS = 64;
+// r02: the DMMA kernel (a warp per element, the four contractions on the FP64
+// tensor cores, D and Q padded to 8; jm_mass.cuh mass_dmma_body) for the
+// (D, Q) where it measured faster than the thread-per-element kernel, whose
+// D*Q*(D+Q) FMAs per element each take a broadcast shared load of B (the DMMA
+// kernel's cost per element is fixed: 8 DMMA).  All 64 pairs at 2^21
+// elements, fraction of HBM (profiles/r02_mass_ab.md, two runs): D = 8
+// 0.29-0.52 -> 0.93-1.05, D = 6, 7 0.27-0.60 -> 0.65-0.82, (4, 8) 0.50 ->
+// 0.70-0.75, (2, 8) 0.46 -> 0.53; D <= 3 and small Q keep the thread kernel
+// (e.g. (4, 4) 0.69-0.73 vs 0.44-0.48).  Row d of the table: bit q-1 set = DMMA.  MASS_DMMA_THREADS / 32
+// elements per CTA chunk, no shared memory.  JM_MASS_DMMA: 0 the table, 1 every
+// pair, -1 none (A/B builds)
+#ifndef JM_MASS_DMMA
+#define JM_MASS_DMMA 0
+#endif
+#ifndef JM_MASS_DMMA_PD
+#define JM_MASS_DMMA_PD 4            // elements per warp in flight (cp.async slots per warp)
+#endif
+#ifndef JM_MASS_DMMA_MINB
+#define JM_MASS_DMMA_MINB 4          // __launch_bounds__ min CTAs per SM (<= 64 registers; 4 CTAs also fill the shared memory at PD = 4)
+#endif
+constexpr int MASS_DMMA_THREADS = 256;
+constexpr int MASS_DMMA_SLOT = 1536;   // one element's x, y, op fragments for 32 lanes (3 x 512 B)
+JM_HD constexpr unsigned mass_dmma_row(int d) {
+  return d >= 6 ? 0xffu : d == 5 ? 0xf0u : d == 4 ? 0xe0u : d >= 2 ? 0x80u : 0u;
+}
+JM_HD constexpr bool mass_dmma(int d, int q) {
+  return JM_MASS_DMMA > 0 || (JM_MASS_DMMA == 0 && ((mass_dmma_row(d) >> (q - 1)) & 1u));
+}
 JM_HD constexpr Plan plan_mass(int d, int q) {
-  return Plan{(int)Tile::Generic, MASS_THREADS, MASS_THREADS,
-              2 * stage_bytes(MASS_THREADS, d, 8) + stage_bytes(MASS_THREADS, q, 8) + rup(q * d * 8, 16), 1};
+  return mass_dmma(d, q)
+             ? Plan{(int)Tile::Dmma, MASS_DMMA_THREADS, MASS_DMMA_THREADS / 32,
+                    MASS_DMMA_THREADS / 32 * JM_MASS_DMMA_PD * MASS_DMMA_SLOT, 1}
+             : Plan{(int)Tile::Generic, MASS_THREADS, MASS_THREADS,
+                    2 * stage_bytes(MASS_THREADS, d, 8) + stage_bytes(MASS_THREADS, q, 8) + rup(q * d * 8, 16), 1};
 }
 
 // ---- GENERIC (runtime N; AoT) ----

@@ -122,6 +122,18 @@ __device__ __forceinline__ void cp_async_small(void *s, const void *g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"((unsigned)__cvta_generic_to_shared(s)),
                "l"(g), "n"(BYTES) : "memory");
 }
+// zero-filling forms: `src_bytes` (0 or the full size) of the copy come from
+// global memory, the rest of the destination is zeroed
+__device__ __forceinline__ void cp_async_zfill16(void *s, const void *g, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(s)),
+               "l"(g), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_zfill8(void *s, const void *g, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((unsigned)__cvta_generic_to_shared(s)),
+               "l"(g), "r"(src_bytes) : "memory");
+}
+template <int PENDING>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(PENDING) : "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 

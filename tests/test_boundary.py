@@ -158,3 +158,14 @@ def test_binding_rejects_unknown_enum_names():
     with pytest.raises(ValueError):   # run_many marshals every group before calling the library
         jm.jit_mat_run_many([{"n": 4, "dtype": "f64", "batch": 1, "repeat": 1, "in_ptr": 0, "out_ptr": 0,
                               "addend": "Identity"}])
+
+
+def test_every_mass_specialization_compiles_for_sm100a(jm):
+    """k_mass<D, Q> (Listing 12, reading R18) for every D, Q in 1..8:
+    the thread-per-element kernel and the r02 DMMA kernel (jm_plan.h mass_dmma)."""
+    pairs = [(d, q) for d in range(1, 9) for q in range(1, 9)]
+    with cf.ThreadPoolExecutor(min(8, os.cpu_count() or 1)) as ex:
+        sizes = list(ex.map(lambda p: jm.jit_mat_compile_check(p[0], p[1], "mass"), pairs))
+    assert all(s > 1000 for s in sizes)
+    with pytest.raises(jm.JitMatError):
+        jm.jit_mat_compile_check(9, 4, "mass")

@@ -37,7 +37,9 @@ def _check(got, want, B, op, x, y):
 
 @pytest.mark.parametrize("kind", ["specialized", "generic"])
 @pytest.mark.parametrize("D,Q", [(1, 1), (2, 2), (2, 4), (2, 8), (4, 2), (4, 4), (4, 8), (8, 2),
-                                 (8, 4), (8, 8), (3, 5), (5, 3), (7, 6)])
+                                 (8, 4), (8, 8), (3, 5), (5, 3), (7, 6),
+                                 # r02 DMMA kernel (jm_plan.h mass_dmma): every Q padding at D = 8
+                                 (8, 1), (8, 3), (8, 5), (8, 6), (8, 7), (6, 8), (6, 6)])
 def test_mass_parity(jm, D, Q, kind):
     E = 1000 + 37
     B, op, x, y = _case(D, Q, E, 10 * D + Q)
@@ -61,3 +63,15 @@ def test_mass_errors_and_cache(jm):
     torch.cuda.synchronize()
     st1 = jm.jit_mat_stats()
     assert st1["compilations"] - st0["compilations"] <= 1
+
+
+@pytest.mark.parametrize("E", [1, 3, 7, 8, 9, 4096 + 5])
+@pytest.mark.parametrize("D,Q", [(8, 8), (8, 3)])
+def test_mass_parity_ragged(jm, D, Q, E):
+    """element counts below / around one CTA chunk (the DMMA kernel: 8 elements
+    per CTA, the next element's loads prefetched) and a ragged large tail"""
+    B, op, x, y = _case(D, Q, E, 1000 + E)
+    want = oracle.mass_apply(y, B, op, x)
+    tB, to, tx, ty = (torch.from_numpy(a).cuda() for a in (B, op, x, y))
+    jm.mass(tB, to, tx, ty, sync=True)
+    _check(ty.cpu().numpy(), want, B, op, x, y)

@@ -48,13 +48,15 @@ def main():
     ap.add_argument("--repeats", default="100")
     ap.add_argument("--gb", type=float, default=0.5)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--tool", default="stream_sweep", choices=["stream_sweep", "mass_bench"],
+                    help="mass_bench: the Laghos mass action (tools/mass_bench.py) instead of the update sweep")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     if a.table:
         table(a.table)
         return
     sizes = []
-    for part in a.sizes.split(","):
+    for part in filter(None, a.sizes.split(",")):
         lo, _, hi = part.partition("..")
         sizes += list(range(int(lo), int(hi or lo) + 1))
     for v in a.variant:
@@ -65,10 +67,11 @@ def main():
         if b.returncode:
             print(f"{name}: build failed: {b.stderr[-2000:]}", file=sys.stderr)
             continue
-        p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "stream_sweep.py"), "--sizes",
-                            ",".join(map(str, sizes)), "--dtypes", a.dtypes, "--repeats", a.repeats,
-                            "--gb", str(a.gb), "--steps", str(a.steps)],
-                           cwd=ROOT, env=env, capture_output=True, text=True)
+        cmd = ([os.path.join(ROOT, "tools", "mass_bench.py"), "--pairs", "all", "--elements", "2097152"]
+               if a.tool == "mass_bench" else
+               [os.path.join(ROOT, "tools", "stream_sweep.py"), "--sizes", ",".join(map(str, sizes)),
+                "--dtypes", a.dtypes, "--repeats", a.repeats, "--gb", str(a.gb), "--steps", str(a.steps)])
+        p = subprocess.run([sys.executable] + cmd, cwd=ROOT, env=env, capture_output=True, text=True)
         if p.returncode:
             print(f"{name}: sweep failed: {p.stderr[-2000:]}", file=sys.stderr)
         with open(a.out, "a") as fh:

@@ -1,10 +1,11 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-mkdir -p gpurun_out/r02
-O=gpurun_out/r02
-timeout 2700 python -m pytest tests -m gpu -q 2>&1 | tail -15 > $O/gputest_full11.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke11.txt 2>&1
-rm -f $O/f32_n12_15.jsonl
-export JM_BUILD_DEFINES="JM_F32P_MAX=11 JM_F32_TPMS_MAX=11"
-timeout 1500 python tools/f32_search.py --run tools/f32_candidates_n12_15.json --out $O/f32_n12_15.jsonl 2> $O/f32_n12_15.err
-python tools/f32_search.py --pick $O/f32_n12_15.jsonl > $O/f32_n12_15_pick.txt
-tail -3 $O/gputest_full11.txt; tail -3 $O/smoke11.txt; cat $O/f32_n12_15_pick.txt
+O=gpurun_out/s5; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 300 python tools/mass_bench.py --out $O/mass_f7.jsonl > /dev/null 2> $O/mass_f7.err
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_mass -o $O/mass python tools/mass_ncu.py 8:8 8:4 6:6 4:4 > $O/mass_ncu.log 2>&1
+ncu -i $O/mass.ncu-rep --page raw --csv > $O/mass_raw.csv 2>/dev/null
+for t in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $t python tools/sanitize_run.py > $O/san_$t.txt 2>&1; echo "$t rc=$?" >> $O/san_summary.txt
+  tail -3 $O/san_$t.txt >> $O/san_summary.txt
+done
+cat $O/san_summary.txt

@@ -42,13 +42,16 @@ def timed(fn, steps, stream):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
+    ap.add_argument("--pairs", default="fig7", help="fig7 (the figure's (d, q)) or all (1..8 x 1..8)")
+    ap.add_argument("--elements", default="10000,2097152")
     a = ap.parse_args()
+    pairs = PAIRS if a.pairs == "fig7" else [(d, q) for d in range(1, 9) for q in range(1, 9)]
     fh = open(a.out, "a") if a.out else None
     torch.cuda.init()
     jm.jit_mat_init(0)
     stream = torch.cuda.Stream()
-    for D, Q in PAIRS:
-        for E in (10_000, 1 << 21):
+    for D, Q in pairs:
+        for E in map(int, a.elements.split(",")):
             B = torch.rand(Q, D, dtype=torch.float64, device="cuda")
             op = torch.rand(E, Q, Q, dtype=torch.float64, device="cuda") + 0.5
             x = torch.rand(E, D, D, dtype=torch.float64, device="cuda")
@@ -64,7 +67,6 @@ def main():
                 row[kind] = {"ms": ms, "elements_per_s": E / (ms * 1e-3), "hbm_gbs": byts / (ms * 1e-3) / 1e9,
                              "frac_hbm": byts / (ms * 1e-3) / 1e9 / HBM, "gflops": flops / (ms * 1e-3) / 1e9}
             row["specialized_speedup"] = row["generic"]["ms"] / row["specialized"]["ms"]
-            info = [k for k in jm.jit_mat_key_info() if k.get("op") == 2 and k["n"] == D]
             s = json.dumps(row)
             print(s, flush=True)
             if fh:

@@ -8,7 +8,7 @@
 Covers TPM, warp/CTA DMMA (incl. the thin-border sizes), FP32 row panels and
 tiles, each in its resident and streaming (bulk-copy ring) variant, the generic kernels, the
 AoT specializations, the multiply-accumulate, fill, checksum, run_many and the
-host-buffer path, each on a ragged batch (several chunks + a partial one).
+host-buffer path, the mass action (both kernels), each on a ragged batch (several chunks + a partial one).
 Exits non-zero on any library error; the sanitizer reports the rest.
 """
 from __future__ import annotations
@@ -75,6 +75,15 @@ def main():
         bufs.append((a, b))
         groups.append(dict(n=n, dtype="f64", batch=6, repeat=2, in_ptr=a.data_ptr(), out_ptr=b.data_ptr()))
     jm.jit_mat_run_many(groups, sync=True)
+    # Laghos mass action: thread-per-element (4, 4), (3, 5) and the r02 DMMA kernel (8, 8), (8, 3), (2, 8),
+    # ragged element counts (a partial CTA chunk; fewer elements than warps)
+    for D, Q, E in ((4, 4, 301), (3, 5, 77), (8, 8, 301), (8, 3, 5), (2, 8, 1029)):
+        B = torch.rand(Q, D, dtype=torch.float64, device="cuda")
+        op = torch.rand(E, Q, Q, dtype=torch.float64, device="cuda")
+        xm = torch.rand(E, D, D, dtype=torch.float64, device="cuda")
+        ym = torch.rand(E, D, D, dtype=torch.float64, device="cuda")
+        for kind in ("specialized", "generic"):
+            jm.mass(B, op, xm, ym, kind=kind, sync=True)
     h = np.random.default_rng(0).random((300, 4, 4))
     out = np.empty_like(h)
     os.environ["JIT_MAT_HOST_CHUNK_MB"] = "0"

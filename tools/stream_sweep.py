@@ -45,7 +45,11 @@ def main():
     for dt in a.dtypes.split(","):
         es = 8 if dt == "f64" else 4
         tdt = torch.float64 if dt == "f64" else torch.float32
-        for n in map(int, a.sizes.split(",")):
+        sizes = []
+        for part in a.sizes.split(","):      # "8,16" or ranges "2..64"
+            lo, _, hi = part.partition("..")
+            sizes += range(int(lo), int(hi or lo) + 1)
+        for n in sizes:
             B = int(a.gb * 1e9 // (n * n * es))
             x = torch.empty(B, n, n, dtype=tdt, device="cuda")
             y = torch.empty_like(x)
