@@ -750,6 +750,25 @@ JM_HD constexpr bool f32t_ring_sep(int n) {
   return JM_F32T_RING_SEP && (JM_F32T_SEP_ALL || (n * n * 4) % 16 != 0) &&
          ring_bytes(n, 4, f32t_mpc(n, 2)) + f32t_mpc(n, 2) * f32t_region(n, 2) <= JM_F32T_RING_MAXB;
 }
+// odd n without the ring (the low-repeat kernel is the prefetching cp.async
+// stage): each matrix is staged at byte (its global offset & 15) of its
+// region, so it moves by 16-B copies instead of one 4-B copy per element each
+// way (run_f32t PSH, Stager SHIFT); needs 12 spare bytes in the region.
+// Measured at R = 1 (profiles/r02_ab_f32_pshift.md, fraction of HBM): a gain
+// only where a CTA holds one or two matrices, n >= 55 (55 0.33 -> 0.37, 59
+// 0.41 -> 0.43, 63 0.42 -> 0.48); for n = 17..23 the per-matrix head / tail
+// work costs more than the element copies it replaces (17 0.45 -> 0.37), and
+// 25..53 are within noise.  JM_F32T_PSHIFT=0: off; JM_F32T_PSHIFT_MIN: the
+// smallest n that takes it.
+#ifndef JM_F32T_PSHIFT
+#define JM_F32T_PSHIFT 1
+#endif
+#ifndef JM_F32T_PSHIFT_MIN
+#define JM_F32T_PSHIFT_MIN 55
+#endif
+JM_HD constexpr bool f32t_pshift(int n) {
+  return JM_F32T_PSHIFT && n >= JM_F32T_PSHIFT_MIN && (n * n * 4) % 16 != 0 && n * n * 4 + 12 <= f32t_region(n, 2);
+}
 // matrices per round of each kind (the resident plan's chunk)
 JM_HD constexpr int round_mpc(int n, int dtype) {
   return (tile_for(n, dtype) == Tile::Dmma ||

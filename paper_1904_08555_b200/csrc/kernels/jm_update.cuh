@@ -201,14 +201,59 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // make this thread's generic-proxy shared-memory writes visible to the async proxy
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Odd n (a matrix is not a whole number of 16-B pieces; r02): matrix m of a
+// chunk, at global byte offset s = (first + m) * MB from the 16-B-aligned
+// base, is staged at byte (s & 15) of its SB-byte slot, so the 16-B-aligned
+// body of its global range lands 16-B aligned in shared memory and moves by
+// 16-B copies; the <= 3 elements before and after the body go one by one.
+// Per matrix PPM + 1 work items: body pieces, then one item for head + tail.
+template <int N, int ES, int SB, int NT>
+__device__ __forceinline__ void stage_in_async_shift(const char *__restrict__ g, long long first, char *s,
+                                                     int cnt, int tid) {
+  constexpr int MB = N * N * ES, PPM = MB / 16;
+  for (int p = tid; p < cnt * (PPM + 1); p += NT) {
+    const int m = p / (PPM + 1), q = p - m * (PPM + 1);
+    const long long s0 = (first + m) * MB;
+    const int sh = (int)(s0 & 15), head = (16 - sh) & 15, nb = (MB - head) >> 4;
+    char *d = s + m * SB + sh;
+    if (q < nb) {
+      cp_async16(d + head + 16 * q, g + s0 + head + 16 * q);
+    } else if (q == PPM) {
+      for (int o = 0; o < head; o += ES) cp_async_small<ES>(d + o, g + s0 + o);
+      for (int o = head + 16 * nb; o < MB; o += ES) cp_async_small<ES>(d + o, g + s0 + o);
+    }
+  }
+}
+template <int N, int ES, int SB, int NT>
+__device__ __forceinline__ void stage_out_shift(char *__restrict__ g, long long first, const char *s, int cnt,
+                                                int tid) {
+  constexpr int MB = N * N * ES, PPM = MB / 16;
+  for (int p = tid; p < cnt * (PPM + 1); p += NT) {
+    const int m = p / (PPM + 1), q = p - m * (PPM + 1);
+    const long long s0 = (first + m) * MB;
+    const int sh = (int)(s0 & 15), head = (16 - sh) & 15, nb = (MB - head) >> 4;
+    const char *d = s + m * SB + sh;
+    if (q < nb) {
+      stg16(g + s0 + head + 16 * q, *reinterpret_cast<const uint4 *>(d + head + 16 * q));
+    } else if (q == PPM) {
+      for (int o = 0; o < head; o += ES) *reinterpret_cast<unsigned *>(g + s0 + o) = *reinterpret_cast<const unsigned *>(d + o);
+      for (int o = head + 16 * nb; o < MB; o += ES)
+        *reinterpret_cast<unsigned *>(g + s0 + o) = *reinterpret_cast<const unsigned *>(d + o);
+    }
+  }
+}
+
 // Chunk scheduler shared by the kernels: a persistent CTA walks chunks of MPC
 // matrices (chunk = blockIdx.x, += gridDim.x).  With PF (prefetch) the stage
 // area is double-buffered: while chunk i is computed, chunk i+gridDim.x is
 // already streaming into the other buffer through cp.async, so the HBM latency
 // of the next load hides behind this chunk's updates (matters at small repeat).
 //   for (sg.start(); sg.valid(); sg.next()) { sg.acquire(); ...use sg.buf()...; sg.release(); }
-template <int N, int ES, int SB, int NT, int MPC, bool AL, bool PF>
+// SHIFT (odd n, PF only): each matrix moves by 16-B pieces at byte shift(mi)
+// of its slot (stage_in_async_shift / stage_out_shift)
+template <int N, int ES, int SB, int NT, int MPC, bool AL, bool PF, bool SHIFT = false>
 struct Stager {
+  static_assert(!SHIFT || (PF && ES == 4), "shifted staging: the prefetching FP32 stage");
   static constexpr int MB = N * N * ES;
   static constexpr int SZ = rup(MPC * SB, 16);   // one stage buffer
   const char *in;
@@ -224,9 +269,12 @@ struct Stager {
     return (int)(r < MPC ? r : MPC);
   }
   __device__ __forceinline__ void issue(long long c, char *dst) {
-    stage_in_async<N, ES, SB, NT, AL>(in + c * MPC * MB, dst, count(c), tid);
+    if constexpr (SHIFT) stage_in_async_shift<N, ES, SB, NT>(in, c * MPC, dst, count(c), tid);
+    else stage_in_async<N, ES, SB, NT, AL>(in + c * MPC * MB, dst, count(c), tid);
     cp_async_commit();
   }
+  // byte offset of matrix mi of the current chunk in its slot (SHIFT)
+  __device__ __forceinline__ int shift(int mi) const { return SHIFT ? (int)(((ch * MPC + mi) * MB) & 15) : 0; }
   __device__ __forceinline__ void start() {
     if (PF && ch < nchunks) issue(ch, base);
   }
@@ -246,7 +294,8 @@ struct Stager {
   }
   __device__ __forceinline__ void release() {
     __syncthreads();
-    stage_out<N, ES, SB, NT, AL>(out + ch * MPC * MB, buf(), cnt(), tid);
+    if constexpr (SHIFT) stage_out_shift<N, ES, SB, NT>(out, ch * MPC, buf(), cnt(), tid);
+    else stage_out<N, ES, SB, NT, AL>(out + ch * MPC * MB, buf(), cnt(), tid);
     if constexpr (!PF) __syncthreads();
   }
   __device__ __forceinline__ void next() {
@@ -1333,19 +1382,27 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
   // the result back to the slots for the bulk store.  Per matrix in flight:
   // two packed slots + one work region (the in-place ring: two work regions).
   constexpr bool RSEP = STRM && !f32t_ring(N) && f32t_ring_sep(N);
+  // PSH (r02, jm_plan.h f32t_pshift): odd n behind the prefetching stage stage
+  // each matrix at byte (global offset & 15) of its region so it moves by
+  // 16-B copies in and out (Stager SHIFT) instead of one 4-B copy per element;
+  // the packed matrix is read from, and the result written back to, that offset
+  constexpr bool PSH = STRM && !f32t_ring(N) && !RSEP && f32t_pshift(N);
   constexpr int GS = 32 * WPM, GM = WPM == 1 ? MPW : 1;   // group threads, group matrices
   const int gt = WPM == 1 ? lane : (warp % WPM) * 32 + lane;
   const int gm0 = WPM == 1 ? warp * MPW : warp / WPM;   // the group's first matrix slot
   typedef typename Pick<STRM && (f32t_ring(N) || RSEP),
                         Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, RSEP ? 0 : REG, RROWS ? LDM * 4 : 0>,
-                        Stager<N, ES, REG, NT, MPC, AL, STRM>>::type Stg;
+                        Stager<N, ES, REG, NT, MPC, AL, STRM, PSH>>::type Stg;
   static_assert(RSEP || Stg::SBM >= REG, "a slot holds the work region");
   Stg sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     const bool live = lane_ok && mi < sg.cnt();
-    float *sm = reinterpret_cast<float *>(sg.buf() + (lane_ok ? mi : 0) * Stg::SBM);   // the staged matrix
-    float *wk = RSEP ? reinterpret_cast<float *>(smem + Stg::BYTES + (lane_ok ? mi : 0) * REG) : sm;   // work region
+    int shb = 0;                       // (PSH) the staged matrix's byte offset in its region
+    if constexpr (PSH) shb = sg.shift(lane_ok ? mi : 0);
+    float *sm = reinterpret_cast<float *>(sg.buf() + (lane_ok ? mi : 0) * Stg::SBM + shb);   // the staged matrix
+    float *wk = RSEP ? reinterpret_cast<float *>(smem + Stg::BYTES + (lane_ok ? mi : 0) * REG)
+                     : reinterpret_cast<float *>(sg.buf() + (lane_ok ? mi : 0) * Stg::SBM);   // work region
     const unsigned sbase = smem_u32(wk);
     float2 p[RA][CB / 2];
     if constexpr (RSEP) {

@@ -1,11 +1,6 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-O=gpurun_out/s5; mkdir -p $O
+O=gpurun_out/s6; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
-timeout 300 python tools/mass_bench.py --out $O/mass_f7.jsonl > /dev/null 2> $O/mass_f7.err
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_mass -o $O/mass python tools/mass_ncu.py 8:8 8:4 6:6 4:4 > $O/mass_ncu.log 2>&1
-ncu -i $O/mass.ncu-rep --page raw --csv > $O/mass_raw.csv 2>/dev/null
-for t in memcheck racecheck synccheck initcheck; do
-  timeout 900 compute-sanitizer --tool $t python tools/sanitize_run.py > $O/san_$t.txt 2>&1; echo "$t rc=$?" >> $O/san_summary.txt
-  tail -3 $O/san_$t.txt >> $O/san_summary.txt
-done
-cat $O/san_summary.txt
+timeout 900 python -m pytest tests/test_gpu_stream.py tests/test_gpu_parity.py -x -q > $O/test.txt 2>&1; tail -2 $O/test.txt
+timeout 1200 python tools/ab.py --variant off="JM_F32T_PSHIFT=0" --variant pshift= --sizes 17,19,21,23,25,27,29,31,33,35,37,39,41,43,45,47,49,51,53,55,57,59,61,63 --dtypes f32 --repeats 1,2 --out $O/ab_pshift.jsonl 2> $O/ab.err
+python tools/ab.py --table $O/ab_pshift.jsonl > $O/ab_pshift.md; cat $O/ab_pshift.md
