@@ -246,10 +246,10 @@ constexpr F32TRow F32T_TABLE[] = {
     {46, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.700 of the pipe, 154 regs
     {47, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.718 of the pipe, 154 regs
     {48, 6, 12, 1, 0, 0, 1, 0, 168, 12},  // 0.750 of the pipe, 154 regs
-    {49, 13, 8, 4, 0, 0, 1, 0, 255, 2},  // 0.518 of the pipe, 227 regs (r02 wide search; was 0.492)
-    {50, 13, 8, 4, 0, 0, 1, 0, 255, 2},  // 0.534 of the pipe, 229 regs (r02 wide search; was 0.509)
+    {49, 13, 8, 4, 0, 0, 1, 0, 232, 4},  // 0.531 of the pipe, 212 regs (r02 neighbourhood search: cap 232, k unroll 4; wide search 0.518)
+    {50, 13, 8, 4, 0, 0, 1, 0, 232, 4},  // 0.551 of the pipe, 215 regs (r02 neighbourhood search: cap 232, k unroll 4; wide search 0.534)
     {51, 13, 8, 4, 0, 0, 1, 0, 255, 2},  // 0.560 of the pipe, 227 regs (r02 wide search; was 0.508)
-    {52, 13, 8, 1, 0, 0, 1, 0, 255, 2},  // 0.533 of the pipe, 230 regs (r02 wide search; was 0.516)
+    {52, 13, 8, 1, 0, 0, 1, 0, 255, 4},  // 0.585 of the pipe, 236 regs (r02 neighbourhood search: k unroll 4; wide search 0.533)
     {53, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.554 of the pipe, 238 regs
     {54, 7, 8, 1, 0, 0, 1, 0, 168, 2},  // 0.581 of the pipe, 160 regs
     {55, 7, 8, 1, 0, 0, 1, 0, 168, 2},  // 0.584 of the pipe, 154 regs

@@ -1,6 +1,9 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-O=gpurun_out/s6; mkdir -p $O
+O=gpurun_out/s8; mkdir -p $O
+PLAN=paper_1904_08555_b200/csrc/kernels/jm_plan.h
+cp $PLAN $O/jm_plan.h.orig
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_stream.py tests/test_gpu_parity.py -x -q > $O/test.txt 2>&1; tail -2 $O/test.txt
-timeout 1200 python tools/ab.py --variant off="JM_F32T_PSHIFT=0" --variant pshift= --sizes 17,19,21,23,25,27,29,31,33,35,37,39,41,43,45,47,49,51,53,55,57,59,61,63 --dtypes f32 --repeats 1,2 --out $O/ab_pshift.jsonl 2> $O/ab.err
-python tools/ab.py --table $O/ab_pshift.jsonl > $O/ab_pshift.md; cat $O/ab_pshift.md
+timeout 3000 python tools/f32_search.py --run tools/f32_candidates_nb2.json --out $O/f32_nb2.jsonl 2> $O/f32_nb2.err
+python tools/f32_search.py --pick $O/f32_nb2.jsonl > $O/f32_nb2_pick.txt
+cp $O/jm_plan.h.orig $PLAN
+cat $O/f32_nb2_pick.txt
