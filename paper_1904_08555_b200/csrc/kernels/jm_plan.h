@@ -234,7 +234,7 @@ constexpr F32TRow F32T_TABLE[] = {
     {34, 7, 12, 1, 1, 1, 0, 1, 168, 8},  // 0.636 of the pipe, 161 regs
     {35, 7, 12, 1, 1, 1, 0, 1, 168, 8},  // 0.662 of the pipe, 156 regs
     {36, 8, 12, 1, 1, 1, 0, 1, 255, 9},  // 0.595 of the pipe, 200 regs
-    {37, 5, 20, 1, 0, 0, 1, 0, 255, 9},  // 0.584 of the pipe, 200 regs (r02 wpc search; was 0.550)
+    {37, 5, 20, 1, 0, 0, 1, 0, 232, 4},  // 0.626 of the pipe (r02 neighbourhood search: cap 232, k unroll 4; was 0.585)
     {38, 5, 12, 1, 0, 0, 1, 0, 168, 9},  // 0.584 of the pipe, 144 regs
     {39, 5, 12, 1, 0, 0, 1, 0, 168, 9},  // 0.613 of the pipe, 134 regs
     {40, 5, 12, 1, 0, 0, 1, 0, 168, 10},  // 0.656 of the pipe, 142 regs
@@ -244,24 +244,24 @@ constexpr F32TRow F32T_TABLE[] = {
     {44, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.644 of the pipe, 160 regs
     {45, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.662 of the pipe, 148 regs
     {46, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.700 of the pipe, 154 regs
-    {47, 6, 12, 1, 0, 0, 1, 0, 168, 11},  // 0.718 of the pipe, 154 regs
+    {47, 6, 12, 1, 0, 0, 1, 0, 168, 4},  // 0.732 of the pipe (r02 neighbourhood search: cap 168, k unroll 4; was 0.719)
     {48, 6, 12, 1, 0, 0, 1, 0, 168, 12},  // 0.750 of the pipe, 154 regs
     {49, 13, 8, 4, 0, 0, 1, 0, 232, 4},  // 0.531 of the pipe, 212 regs (r02 neighbourhood search: cap 232, k unroll 4; wide search 0.518)
     {50, 13, 8, 4, 0, 0, 1, 0, 232, 4},  // 0.551 of the pipe, 215 regs (r02 neighbourhood search: cap 232, k unroll 4; wide search 0.534)
-    {51, 13, 8, 4, 0, 0, 1, 0, 255, 2},  // 0.560 of the pipe, 227 regs (r02 wide search; was 0.508)
+    {51, 13, 8, 4, 0, 0, 1, 0, 232, 4},  // 0.573 of the pipe (r02 neighbourhood search: cap 232, k unroll 4; was 0.560)
     {52, 13, 8, 1, 0, 0, 1, 0, 255, 4},  // 0.585 of the pipe, 236 regs (r02 neighbourhood search: k unroll 4; wide search 0.533)
-    {53, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.554 of the pipe, 238 regs
-    {54, 7, 8, 1, 0, 0, 1, 0, 168, 2},  // 0.581 of the pipe, 160 regs
-    {55, 7, 8, 1, 0, 0, 1, 0, 168, 2},  // 0.584 of the pipe, 154 regs
+    {53, 7, 16, 1, 0, 0, 1, 0, 232, 4},  // 0.588 of the pipe (r02 neighbourhood search: cap 232, k unroll 4; was 0.555)
+    {54, 7, 8, 1, 0, 0, 1, 0, 168, 8},  // 0.610 of the pipe (r02 neighbourhood search: cap 168, k unroll 8; was 0.582)
+    {55, 7, 8, 1, 0, 0, 1, 0, 232, 8},  // 0.620 of the pipe (r02 neighbourhood search: cap 232, k unroll 8; was 0.584)
     {56, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.662 of the pipe, 204 regs
     {57, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.587 of the pipe, 225 regs
-    {58, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.611 of the pipe, 221 regs
+    {58, 8, 16, 1, 0, 0, 1, 0, 255, 4},  // 0.628 of the pipe (r02 neighbourhood search: cap 255, k unroll 4; was 0.611)
     {59, 8, 8, 1, 0, 0, 0, 0, 255, 2},  // 0.640 of the pipe, 154 regs
-    {60, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.604 of the pipe, 233 regs
+    {60, 8, 16, 1, 0, 0, 1, 0, 232, 4},  // 0.676 of the pipe (r02 neighbourhood search: cap 232, k unroll 4; was 0.633)
     {61, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.679 of the pipe, 236 regs
     {62, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.711 of the pipe, 244 regs
     {63, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.730 of the pipe, 236 regs
-    {64, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.762 of the pipe, 217 regs
+    {64, 8, 16, 1, 0, 0, 1, 0, 255, 4},  // 0.781 of the pipe (r02 neighbourhood search: cap 255, k unroll 4; was 0.763)
 };
 // The low-repeat (streaming) kernel's own shapes, where they differ from the
 // resident kernel's (R = 1 is bound by moving the matrices, so a smaller work
