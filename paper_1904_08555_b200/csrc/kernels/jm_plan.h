@@ -676,8 +676,27 @@ JM_HD constexpr int ring_k(int rb) {
 JM_HD constexpr int ring_sbm(int n, int es, int slot = 0) {
   return (n * n * es) % 16 == 0 ? (slot > stage_stride(n, es) ? slot : stage_stride(n, es)) : n * n * es;
 }
+// r02, shifted per-matrix copies: an FP64 matrix of odd n is 8 B short of a
+// whole number of 16-B pieces, so one matrix per round (the CTA-DMMA ring)
+// needed chunks of two matrices (K = 2).  Instead each matrix sits at byte
+// (global offset mod 16) of a slot of n*n*8 + 8 bytes: its 16-B-aligned body is
+// one bulk copy, the 8 bytes outside it one cp.async tied to the same mbarrier
+// (cp.async.mbarrier.arrive) — chunks of ONE matrix, half the ring.
+// JM_RING_SHIFT=0: off.
+#ifndef JM_RING_SHIFT
+#define JM_RING_SHIFT 1
+#endif
+JM_HD constexpr bool ring_shift(int n, int es, int rm) {
+  return JM_RING_SHIFT && es == 8 && rm == 1 && (n * n * es) % 16 == 8;
+}
+JM_HD constexpr int ring_kr(int n, int es, int rm) {   // rounds per chunk
+  return ring_shift(n, es, rm) ? cdiv(JM_RING_CHUNK, n * n * es) : ring_k(rm * n * n * es);
+}
+JM_HD constexpr int ring_sbmr(int n, int es, int rm, int slot = 0) {   // matrix slot stride
+  return ring_shift(n, es, rm) ? (slot > n * n * es + 8 ? slot : n * n * es + 8) : ring_sbm(n, es, slot);
+}
 JM_HD constexpr int ring_bytes(int n, int es, int rm, int slot = 0) {
-  return JM_RING_S * ring_k(rm * n * n * es) * rm * ring_sbm(n, es, slot) + rup(8 * JM_RING_S, 16);
+  return JM_RING_S * ring_kr(n, es, rm) * rm * ring_sbmr(n, es, rm, slot) + rup(8 * JM_RING_S, 16);
 }
 // DMMA in the streaming variant: when the swizzled publish buffer fits in the
 // matrix's ring slot (n a multiple of 16), the slot is reused as that buffer
@@ -781,7 +800,7 @@ JM_HD constexpr int round_mpc(int n, int dtype) {
 // the grid by it); smem = the ring + the kind's own work areas.
 JM_HD constexpr Plan plan_stream(int n, int dtype) {
   const int es = dtype == 1 ? 8 : 4;
-  const int rm = round_mpc(n, dtype), rb = rm * n * n * es, chm = ring_k(rb) * rm;
+  const int rm = round_mpc(n, dtype), chm = ring_kr(n, es, rm) * rm;
   if (!stream_ok(n, dtype)) return plan_specialized(n, dtype);
   if (tile_for(n, dtype) == Tile::TPM)
     return Plan{(int)Tile::TPM, TPM_THREADS, TPM_THREADS, 2 * stage_bytes(TPM_THREADS, n, es), 1};

@@ -195,6 +195,11 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned by
                "r"(bytes)
                : "memory");
 }
+// the stage's mbarrier tracks this thread's prior cp.async copies (one
+// pending arrival added now, its arrive when they have landed)
+__device__ __forceinline__ void cp_async_mbar_arrive(u64 *bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -331,9 +336,14 @@ struct Ring {
   static constexpr bool ROWS = RPB > 0;                   // one copy per row
   static_assert(!ROWS || (ROWB % 16 == 0 && RPB % 16 == 0 && RPB >= ROWB), "row-pitched copies of 16-B rows");
   static constexpr bool PER = (MB % 16) == 0;             // one copy per matrix
-  static constexpr int SBM = ring_sbm(N, ES, SLOT);       // matrix slot stride
+  // SHF (jm_plan.h ring_shift): matrix m of a full chunk sits at byte
+  // shift(m) = (global offset mod 16) of its slot; body by bulk copy, the 8 B
+  // outside it by a cp.async whose completion the stage's mbarrier tracks
+  static constexpr bool SHF = ring_shift(N, ES, MPC) && !ROWS;
+  static constexpr int SBM = ring_sbmr(N, ES, MPC, SLOT);  // matrix slot stride
   static constexpr int RB = MPC * SBM, CHM = K * MPC, CHB = K * RB, GB = CHM * MB;
-  static_assert(GB % 16 == 0 && CHB % 16 == 0, "bulk copies move multiples of 16 bytes");
+  static constexpr int TXB = SHF ? CHM * (MB - 8) : GB;   // bytes the bulk copies of a chunk move
+  static_assert((SHF || GB % 16 == 0) && CHB % 16 == 0 && TXB % 16 == 0, "bulk copies move multiples of 16 bytes");
   static_assert(S >= 2, "ring of at least two stages");
   static constexpr int BYTES = S * CHB + rup(8 * S, 16);
   const char *in;
@@ -353,8 +363,23 @@ struct Ring {
   __device__ __forceinline__ void issue(long long c, int st) {
     const char *g = in + c * GB;
     char *d = base + st * CHB;
-    if (tid == 0) mbar_expect_tx(bar + st, GB);
-    if constexpr (ROWS) {
+    if constexpr (SHF) {
+      // the 8-B pieces first: cp.async.mbarrier.arrive adds a pending arrival
+      // BEFORE the expect_tx arrival below, so the phase cannot complete early
+      for (int m = tid; m < CHM; m += 32) {
+        const int sh = (int)(((c * CHM + m) * MB) & 15), ox = sh ? 0 : MB - 8;
+        cp_async_small<8>(d + m * SBM + sh + ox, g + (size_t)m * MB + ox);
+        cp_async_mbar_arrive(bar + st);
+      }
+      __syncwarp();
+    }
+    if (tid == 0) mbar_expect_tx(bar + st, TXB);
+    if constexpr (SHF) {
+      for (int m = tid; m < CHM; m += 32) {
+        const int sh = (int)(((c * CHM + m) * MB) & 15), ob = sh ? 8 : 0;
+        bulk_g2s(d + m * SBM + sh + ob, g + (size_t)m * MB + ob, MB - 8, bar + st);
+      }
+    } else if constexpr (ROWS) {
       for (int e = tid; e < CHM * N; e += 32) {
         const int m = e / N, r = e - m * N;
         bulk_g2s(d + m * SBM + r * RPB, g + (size_t)e * ROWB, ROWB, bar + st);
@@ -369,7 +394,13 @@ struct Ring {
   __device__ __forceinline__ void store(long long c, int st) {
     char *g = out + c * GB;
     const char *d = base + st * CHB;
-    if constexpr (ROWS) {
+    if constexpr (SHF) {
+      for (int m = tid; m < CHM; m += 32) {
+        const int sh = (int)(((c * CHM + m) * MB) & 15), ob = sh ? 8 : 0, ox = sh ? 0 : MB - 8;
+        bulk_s2g(g + (size_t)m * MB + ob, d + m * SBM + sh + ob, MB - 8);
+        *reinterpret_cast<u64 *>(g + (size_t)m * MB + ox) = *reinterpret_cast<const u64 *>(d + m * SBM + sh + ox);
+      }
+    } else if constexpr (ROWS) {
       for (int e = tid; e < CHM * N; e += 32) {
         const int m = e / N, r = e - m * N;
         bulk_s2g(g + (size_t)e * ROWB, d + m * SBM + r * RPB, ROWB);
@@ -398,6 +429,11 @@ struct Ring {
   }
   __device__ __forceinline__ bool valid() const { return ch < nchunks; }
   __device__ __forceinline__ char *buf() const { return base + s * CHB + sub * RB; }
+  // byte offset of matrix mi of the current round in its slot (SHF; the
+  // ragged last chunk is staged by element copies at offset 0)
+  __device__ __forceinline__ int shift(int mi) const {
+    return (SHF && full(ch)) ? (int)(((ch * CHM + (long long)sub * MPC + mi) * MB) & 15) : 0;
+  }
   __device__ __forceinline__ int cnt() const {
     const long long r = batch - (ch * CHM + (long long)sub * MPC);
     return (int)(r <= 0 ? 0 : (r < MPC ? r : MPC));
@@ -722,7 +758,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   // tiles are skipped by warp-uniform branches
   constexpr bool RAG = RT * W != T8;
   constexpr bool PF = prefetch_for(N, 1);
-  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, dmma_slot(N)>,
+  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_kr(N, ES, MPC), JM_RING_S, dmma_slot(N)>,
                         Stager<N, ES, SB, NT, MPC, AL, PF>>::type Stg;
   // streaming, even n: the matrix's ring slot (widened to the publish buffer
   // when needed, dmma_slot) doubles as its (first) publish buffer once M is in
@@ -796,7 +832,7 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
     char *stage = sg.buf();
     const int cnt = sg.cnt();
     if (mi < cnt) {
-      double *sm = reinterpret_cast<double *>(stage + mi * Stg::SBM);
+      double *sm = reinterpret_cast<double *>(stage + mi * Stg::SBM + sg.shift(mi));   // (odd n: Ring SHF)
       double acc[RT][T8][2];
       if constexpr (N % 2 == 0) {
         // even n: the lane's pair (8J+2t, 8J+2t+1) is one 16-B load; for n a
@@ -1097,7 +1133,7 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   static_assert(G * RP >= N, "row panels must cover the matrix");
   constexpr bool PF = prefetch_for(N, 0);
-  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, INPL ? f32p_slot(N) : 0>,
+  typedef typename Pick<STRM, Ring<N, ES, NT, MPC, ring_kr(N, ES, MPC), JM_RING_S, INPL ? f32p_slot(N) : 0>,
                         Stager<N, ES, SB, NT, MPC, AL, PF>>::type Stg;
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1391,7 +1427,7 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
   const int gt = WPM == 1 ? lane : (warp % WPM) * 32 + lane;
   const int gm0 = WPM == 1 ? warp * MPW : warp / WPM;   // the group's first matrix slot
   typedef typename Pick<STRM && (f32t_ring(N) || RSEP),
-                        Ring<N, ES, NT, MPC, ring_k(MPC * MB), JM_RING_S, RSEP ? 0 : REG, RROWS ? LDM * 4 : 0>,
+                        Ring<N, ES, NT, MPC, ring_kr(N, ES, MPC), JM_RING_S, RSEP ? 0 : REG, RROWS ? LDM * 4 : 0>,
                         Stager<N, ES, REG, NT, MPC, AL, STRM, PSH>>::type Stg;
   static_assert(RSEP || Stg::SBM >= REG, "a slot holds the work region");
   Stg sg(in, out, batch, smem);
