@@ -228,7 +228,10 @@ JM_API int jit_mat_matmul(int n, int dtype, int kind, int64_t batch, const void 
  * doubles, device pointers (op/x/y 16-byte aligned; y must not overlap B, op
  * or x).  kind JM_KIND_SPECIALIZED instantiates jm::k_mass<dofs, quads>
  * through NVRTC (replacing Laghos' ~32-entry dispatch map of explicit
- * instantiations, Listing 12); JM_KIND_GENERIC is the runtime-(dofs, quads)
+ * instantiations, Listing 12) — for the larger (dofs, quads) a warp per
+ * element with the contractions on the FP64 tensor cores (DESIGN.md §10 f4);
+ * the summation order differs from the CPU oracle's (parity is relative to the
+ * contraction's magnitude scale).  JM_KIND_GENERIC is the runtime-(dofs, quads)
  * kernel.  1 <= dofs, quads <= 8 (Fig. 7's d, q in {2, 4, 8}); larger is
  * JM_E_UNSUPPORTED.  Asynchronous on `stream` (NULL = the set stream). */
 JM_API int jit_mat_mass(int dofs, int quads, int kind, int64_t elements, const double *B,

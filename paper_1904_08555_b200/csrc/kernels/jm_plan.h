@@ -683,6 +683,20 @@ JM_HD constexpr int ring_sbm(int n, int es, int slot = 0) {
 // one bulk copy, the 8 bytes outside it one cp.async tied to the same mbarrier
 // (cp.async.mbarrier.arrive) — chunks of ONE matrix, half the ring.
 // JM_RING_SHIFT=0: off.
+// Streaming CTA-DMMA kernels (W > 1, publish buffer not in the ring slot):
+// one publish buffer + one more CTA barrier per update instead of two
+// alternating buffers (run_dmma ONE), where two buffers would leave one CTA
+// per SM (> JM_DMMA_1BUF_MAXB): odd n = 57..63 then fit two.  Measured
+// (profiles/r02_ab_dmma_stream_1buf.md, FP64 pipe at R = 1): 57 0.41 -> 0.55,
+// 59 0.45 -> 0.59, 61 0.47 -> 0.63, 63 0.51 -> 0.68; where it does not change
+// the CTAs per SM the extra barrier costs up to 0.05 (n = 56), so only there.
+// JM_DMMA_STREAM_1BUF=0: two buffers everywhere.
+#ifndef JM_DMMA_STREAM_1BUF
+#define JM_DMMA_STREAM_1BUF 1
+#endif
+#ifndef JM_DMMA_1BUF_MAXB
+#define JM_DMMA_1BUF_MAXB (113 * 1024)
+#endif
 #ifndef JM_RING_SHIFT
 #define JM_RING_SHIFT 1
 #endif
@@ -796,6 +810,10 @@ JM_HD constexpr int round_mpc(int n, int dtype) {
          : (f32p_use(n) && !f32t_stream_use(n)) ? F32P_WPC * f32p_mpw(n)
                                          : f32t_mpc(n, 2);
 }
+JM_HD constexpr bool dmma_stream_1buf(int n) {
+  return JM_DMMA_STREAM_1BUF && dmma_w(n, true) > 1 && !dmma_inplace(n) &&
+         ring_bytes(n, 8, 1, dmma_slot(n)) + 2 * dmma_scr(n) > JM_DMMA_1BUF_MAXB;
+}
 // Plan of the streaming variant: mpc = matrices per ring chunk (the host sizes
 // the grid by it); smem = the ring + the kind's own work areas.
 JM_HD constexpr Plan plan_stream(int n, int dtype) {
@@ -807,7 +825,7 @@ JM_HD constexpr Plan plan_stream(int n, int dtype) {
   if (tile_for(n, dtype) == Tile::Dmma ||
       (dtype == 1 && (tile_for(n, dtype) == Tile::Tpms || tile_for(n, dtype) == Tile::Reg))) {   // (Tpms, Reg: DMMA ring)
     const int w = dmma_w(n, true);
-    const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : 2);   // scratch buffers
+    const int own = dmma_inplace(n) ? (w == 1 ? 0 : 1) : (w == 1 ? DMMA_WPC : (dmma_stream_1buf(n) ? 1 : 2));   // scratch buffers
     return Plan{(int)Tile::Dmma, 32 * (w == 1 ? DMMA_WPC : w), chm, ring_bytes(n, es, rm, dmma_slot(n)) + own * dmma_scr(n), w};
   }
   if (f32p_use(n) && !f32t_stream_use(n))

@@ -791,6 +791,11 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
   const int g = lane >> 2, t = lane & 3;
   const int mi = (W == 1) ? warp : 0;        // matrix slot in the chunk
   const int wr = (W == 1) ? 0 : warp;        // this warp's rank within the matrix
+  // ONE (r02, streaming CTA kernels): a single publish buffer and one more
+  // CTA barrier per update instead of two alternating buffers — at the low
+  // repeat counts this kernel runs (one update at R = 1) the second buffer
+  // was mostly idle shared memory (jm_plan.h JM_DMMA_STREAM_1BUF)
+  constexpr bool ONE = STRM && W > 1 && !INPL && dmma_stream_1buf(N);
   char *scr = smem + Stg::BYTES + ((W == 1 && !INPL) ? warp * SCR : 0);
   const double c = 0.00005;
   // Swizzled-scratch offsets factored into a few lane constants plus
@@ -870,7 +875,10 @@ __device__ __forceinline__ void run_dmma(const double *__restrict__ in, double *
       }
       for (int r = 0; r < repeat; ++r) {
         char *sb = INPL ? ((W > 1 && (r & 1)) ? scr : reinterpret_cast<char *>(sm))
-                        : scr + ((W > 1) ? (r & 1) * SCR : 0);
+                        : scr + ((W > 1 && !ONE) ? (r & 1) * SCR : 0);
+        if constexpr (ONE) {           // every B-fragment read of update r-1 done before this publish
+          if (r > 0) __syncthreads();
+        }
         // publish M (own rows) for the B-fragment reads
 #pragma unroll
         for (int I = 0; I < RT; ++I) {
