@@ -27,21 +27,40 @@ __device__ __forceinline__ void mass_body(const double *__restrict__ B, const do
   constexpr int NT = MASS_THREADS, MPC = MASS_THREADS;
   constexpr int SBX = stage_stride(D, 8), SBQ = stage_stride(Q, 8);
   constexpr int MBX = D * D * 8, MBQ = Q * Q * 8;
+  // r02 (JM_MASS_PF): two stage buffers, the next chunk's x / y / op stream in
+  // by cp.async while this chunk is computed (the single-buffered kernel was
+  // latency-bound: long-scoreboard stalls, profiles/r02_ncu_mass.md)
+  constexpr bool PF = JM_MASS_PF;
+  constexpr int SXB = stage_bytes(MPC, D, 8), STB = 2 * SXB + stage_bytes(MPC, Q, 8);
   extern __shared__ __align__(16) char smem[];
-  char *sx = smem;
-  char *sy = sx + stage_bytes(MPC, D, 8);
-  char *so = sy + stage_bytes(MPC, D, 8);
-  double *sB = reinterpret_cast<double *>(so + stage_bytes(MPC, Q, 8));
+  double *sB = reinterpret_cast<double *>(smem + (PF ? 2 : 1) * STB);
   const int tid = threadIdx.x;
   for (int i = tid; i < Q * D; i += NT) sB[i] = B[i];
   const long long nchunks = (elements + MPC - 1) / MPC;
-  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+  auto count = [&](long long c) { return (int)((elements - c * MPC) < MPC ? (elements - c * MPC) : MPC); };
+  auto issue = [&](long long c, char *st) {
+    const long long e0 = c * MPC;
+    stage_in_async<D, 8, SBX, NT, true>(reinterpret_cast<const char *>(x) + e0 * MBX, st, count(c), tid);
+    stage_in_async<D, 8, SBX, NT, true>(reinterpret_cast<const char *>(y) + e0 * MBX, st + SXB, count(c), tid);
+    stage_in_async<Q, 8, SBQ, NT, true>(reinterpret_cast<const char *>(op) + e0 * MBQ, st + 2 * SXB, count(c), tid);
+    cp_async_commit();
+  };
+  if (PF && blockIdx.x < nchunks) issue(blockIdx.x, smem);
+  int it = 0;
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++it) {
     const long long e0 = ch * MPC;
-    const int cnt = (int)((elements - e0) < MPC ? (elements - e0) : MPC);
-    stage_in<D, 8, SBX, NT, true>(reinterpret_cast<const char *>(x) + e0 * MBX, sx, cnt, tid);
-    stage_in<D, 8, SBX, NT, true>(reinterpret_cast<const char *>(y) + e0 * MBX, sy, cnt, tid);
-    stage_in<Q, 8, SBQ, NT, true>(reinterpret_cast<const char *>(op) + e0 * MBQ, so, cnt, tid);
-    __syncthreads();
+    const int cnt = count(ch);
+    char *sx = smem + (PF ? (it & 1) * STB : 0), *sy = sx + SXB, *so = sx + 2 * SXB;
+    if constexpr (PF) {
+      cp_async_wait_all();
+      __syncthreads();   // chunk ch visible; every thread is done with the other buffer
+      if (ch + gridDim.x < nchunks) issue(ch + gridDim.x, smem + ((it + 1) & 1) * STB);
+    } else {
+      stage_in<D, 8, SBX, NT, true>(reinterpret_cast<const char *>(x) + e0 * MBX, sx, cnt, tid);
+      stage_in<D, 8, SBX, NT, true>(reinterpret_cast<const char *>(y) + e0 * MBX, sy, cnt, tid);
+      stage_in<Q, 8, SBQ, NT, true>(reinterpret_cast<const char *>(op) + e0 * MBQ, so, cnt, tid);
+      __syncthreads();
+    }
     if (tid < cnt) {
       const double *X = reinterpret_cast<const double *>(sx + tid * SBX);
       const double *O = reinterpret_cast<const double *>(so + tid * SBQ);
@@ -96,7 +115,7 @@ __device__ __forceinline__ void mass_body(const double *__restrict__ B, const do
     }
     __syncthreads();
     stage_out<D, 8, SBX, NT, true>(reinterpret_cast<char *>(y) + e0 * MBX, sy, cnt, tid);
-    __syncthreads();
+    if constexpr (!PF) __syncthreads();
   }
 }
 

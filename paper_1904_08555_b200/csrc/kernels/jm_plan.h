@@ -920,6 +920,9 @@ JM_HD constexpr Plan plan_matmul_generic(int n, int dtype) {
 // one thread per element, MASS_THREADS elements per CTA chunk
 constexpr int MASS_MAX = 8;                        // 1 <= D, Q <= 8 (Fig. 7: d,q in {2,4,8})
 constexpr int MASS_THREADS = 64;
+#ifndef JM_MASS_PF
+#define JM_MASS_PF 1                 // thread-per-element kernel: double-buffered cp.async staging
+#endif
 // r02: the DMMA kernel (a warp per element, the four contractions on the FP64
 // tensor cores, D and Q padded to 8; jm_mass.cuh mass_dmma_body) for the
 // (D, Q) where it measured faster than the thread-per-element kernel, whose
@@ -953,7 +956,8 @@ JM_HD constexpr Plan plan_mass(int d, int q) {
              ? Plan{(int)Tile::Dmma, MASS_DMMA_THREADS, MASS_DMMA_THREADS / 32,
                     MASS_DMMA_THREADS / 32 * JM_MASS_DMMA_PD * MASS_DMMA_SLOT, 1}
              : Plan{(int)Tile::Generic, MASS_THREADS, MASS_THREADS,
-                    2 * stage_bytes(MASS_THREADS, d, 8) + stage_bytes(MASS_THREADS, q, 8) + rup(q * d * 8, 16), 1};
+                    (JM_MASS_PF ? 2 : 1) * (2 * stage_bytes(MASS_THREADS, d, 8) + stage_bytes(MASS_THREADS, q, 8)) +
+                        rup(q * d * 8, 16), 1};
 }
 
 // ---- GENERIC (runtime N; AoT) ----
