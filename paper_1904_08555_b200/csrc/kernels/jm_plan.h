@@ -273,9 +273,9 @@ constexpr F32TRow F32TS_TABLE[] = {
     // Odd n: search v2 (profiles/r02_f32_stream_search_v2.jsonl); even n: search v3 with the
     // one-time packed accesses in the layout model and PVEC on (r02_f32_stream_search_v3.jsonl);
     // n = 42, 44, 52, 54 stream fastest with their resident shape.
-    {16, 8, 4, 1, 4, 0, 1, 0, 168, 4},     // 0.887 at R = 1 (the row-panel ring: 0.54; r02_f32s_n15_16.jsonl)
+    {16, 8, 4, 1, 4, 0, 1, 0, 255, 2},  // 0.930 at R = 1 (r02 neighbourhood search: cap 255, k unroll 2; was 0.859)
     {17, 6, 4, 6, 0, 0, 1, 1, 168, 4, 2},  // 0.448 at R = 1 (was 0.316), 106 regs
-    {18, 5, 12, 4, 2, 0, 1, 0, 168, 4, 2},  // 0.703 at R = 1 (v3) (was 0.477), 144 regs
+    {18, 5, 12, 4, 2, 0, 1, 0, 255, 4, 2},  // 0.740 at R = 1 (r02 neighbourhood search: cap 255, k unroll 4; was 0.707)
     {19, 5, 12, 4, 1, 1, 1, 0, 168, 4, 2},  // 0.413 at R = 1 (was 0.386), 137 regs
     {20, 5, 12, 4, 1, 1, 1, 0, 168, 5, 2},  // 0.747 at R = 1 (v3) (was 0.705), 133 regs
     {21, 7, 12, 1, 5, 0, 0, 0, 168, 5},   // the r02 resident shape before the CTA-size search (0.40 at R = 1; the 11 x 12 two-warp tile streams at 0.31)
@@ -301,10 +301,10 @@ constexpr F32TRow F32TS_TABLE[] = {
     {46, 6, 12, 1, 0, 1, 1, 0, 168, 11},  // 0.490 at R = 1 (v3) (was 0.462), 141 regs
     {48, 6, 12, 1, 0, 1, 1, 0, 168, 12},  // 0.481 at R = 1 (v3) (was 0.396), 156 regs
     {49, 7, 16, 1, 0, 0, 0, 0, 255, 2},  // 0.258 at R = 1 (was 0.233), 214 regs
-    {50, 7, 8, 1, 0, 1, 1, 0, 168, 2, 2},  // 0.365 at R = 1 (v3) (was 0.286), 140 regs
+    {50, 7, 8, 1, 0, 1, 1, 0, 255, 4, 2},  // 0.380 at R = 1 (r02 neighbourhood search: cap 255, k unroll 4; was 0.364)
     {51, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.300 at R = 1 (was 0.241), 146 regs
     {53, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.303 at R = 1 (was 0.245), 154 regs
-    {56, 7, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.407 at R = 1 (v3) (was 0.309), 137 regs
+    {56, 7, 8, 1, 0, 0, 1, 0, 168, 8, 2},  // 0.434 at R = 1 (r02 neighbourhood search: cap 168, k unroll 8; was 0.408)
     {57, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.303 at R = 1 (was 0.242), 146 regs
     {58, 8, 8, 1, 0, 0, 0, 0, 168, 2, 2},  // 0.410 at R = 1 (v3) (was 0.290), 154 regs
     {60, 8, 8, 1, 0, 0, 1, 0, 168, 2, 2},  // 0.414 at R = 1 (v3) (was 0.291), 146 regs
@@ -928,12 +928,15 @@ constexpr int MASS_THREADS = 64;
 // (D, Q) where it measured faster than the thread-per-element kernel, whose
 // D*Q*(D+Q) FMAs per element each take a broadcast shared load of B (the DMMA
 // kernel's cost per element is fixed: 8 DMMA).  All 64 pairs at 2^21
-// elements, fraction of HBM (profiles/r02_mass_ab.md, two runs): D = 8
-// 0.29-0.52 -> 0.93-1.05, D = 6, 7 0.27-0.60 -> 0.65-0.82, (4, 8) 0.50 ->
-// 0.70-0.75, (2, 8) 0.46 -> 0.53; D <= 3 and small Q keep the thread kernel
-// (e.g. (4, 4) 0.69-0.73 vs 0.44-0.48).  Row d of the table: bit q-1 set = DMMA.  MASS_DMMA_THREADS / 32
-// elements per CTA chunk, no shared memory.  JM_MASS_DMMA: 0 the table, 1 every
-// pair, -1 none (A/B builds)
+// elements, fraction of HBM (profiles/r02_mass_ab.md): against r01's
+// single-buffered thread kernel D = 8 0.29-0.52 -> 0.93-1.05, D = 6, 7
+// 0.27-0.60 -> 0.65-0.82; the thread kernel then got double-buffered cp.async
+// staging (JM_MASS_PF: median 0.69 -> 0.87 of HBM over all pairs) and wins
+// again below D*Q ~ 30-40: the table is from that comparison
+// (r02_mass_table_ab.jsonl): D = 8 Q >= 2, D = 7 Q >= 4, D = 6 Q >= 6,
+// D = 4, 5 Q = 8.  Row d of the table: bit q-1 set = DMMA.  MASS_DMMA_THREADS
+// / 32 elements per CTA chunk.  JM_MASS_DMMA: 0 the table, 1 every pair, -1
+// none (A/B builds)
 #ifndef JM_MASS_DMMA
 #define JM_MASS_DMMA 0
 #endif
@@ -945,8 +948,8 @@ constexpr int MASS_THREADS = 64;
 #endif
 constexpr int MASS_DMMA_THREADS = 256;
 constexpr int MASS_DMMA_SLOT = 1536;   // one element's x, y, op fragments for 32 lanes (3 x 512 B)
-JM_HD constexpr unsigned mass_dmma_row(int d) {
-  return d >= 6 ? 0xffu : d == 5 ? 0xf0u : d == 4 ? 0xe0u : d >= 2 ? 0x80u : 0u;
+JM_HD constexpr unsigned mass_dmma_row(int d) {   // (r02, against the double-buffered thread kernel)
+  return d == 8 ? 0xfeu : d == 7 ? 0xf8u : d == 6 ? 0xe0u : d >= 4 ? 0x80u : 0u;
 }
 JM_HD constexpr bool mass_dmma(int d, int q) {
   return JM_MASS_DMMA > 0 || (JM_MASS_DMMA == 0 && ((mass_dmma_row(d) >> (q - 1)) & 1u));
