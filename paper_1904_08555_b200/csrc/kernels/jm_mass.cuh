@@ -30,7 +30,7 @@ __device__ __forceinline__ void mass_body(const double *__restrict__ B, const do
   // r02 (JM_MASS_PF): two stage buffers, the next chunk's x / y / op stream in
   // by cp.async while this chunk is computed (the single-buffered kernel was
   // latency-bound: long-scoreboard stalls, profiles/r02_ncu_mass.md)
-  constexpr bool PF = JM_MASS_PF;
+  constexpr bool PF = mass_pf(D, Q);
   constexpr int SXB = stage_bytes(MPC, D, 8), STB = 2 * SXB + stage_bytes(MPC, Q, 8);
   extern __shared__ __align__(16) char smem[];
   double *sB = reinterpret_cast<double *>(smem + (PF ? 2 : 1) * STB);

@@ -923,6 +923,11 @@ constexpr int MASS_THREADS = 64;
 #ifndef JM_MASS_PF
 #define JM_MASS_PF 1                 // thread-per-element kernel: double-buffered cp.async staging
 #endif
+// ... except the tiniest elements, where the doubled stage area costs more
+// residency than the overlap gains ((1, 1) 0.53 -> 0.49, (2, 1) 0.71 -> 0.64,
+// (2, 2) 0.70 -> 0.61 of HBM; every other pair gains, up to 0.41 -> 0.99:
+// profiles/r02_mass_pf_ab.jsonl)
+JM_HD constexpr bool mass_pf(int d, int q) { return JM_MASS_PF && !((d == 1 && q == 1) || (d == 2 && q <= 2)); }
 // r02: the DMMA kernel (a warp per element, the four contractions on the FP64
 // tensor cores, D and Q padded to 8; jm_mass.cuh mass_dmma_body) for the
 // (D, Q) where it measured faster than the thread-per-element kernel, whose
@@ -959,7 +964,7 @@ JM_HD constexpr Plan plan_mass(int d, int q) {
              ? Plan{(int)Tile::Dmma, MASS_DMMA_THREADS, MASS_DMMA_THREADS / 32,
                     MASS_DMMA_THREADS / 32 * JM_MASS_DMMA_PD * MASS_DMMA_SLOT, 1}
              : Plan{(int)Tile::Generic, MASS_THREADS, MASS_THREADS,
-                    (JM_MASS_PF ? 2 : 1) * (2 * stage_bytes(MASS_THREADS, d, 8) + stage_bytes(MASS_THREADS, q, 8)) +
+                    (mass_pf(d, q) ? 2 : 1) * (2 * stage_bytes(MASS_THREADS, d, 8) + stage_bytes(MASS_THREADS, q, 8)) +
                         rup(q * d * 8, 16), 1};
 }
 
