@@ -172,6 +172,44 @@ JM_HD constexpr int dmma_scr(int n) { return 8 * dmma_t8(n) * dmma_rsc(n) * 16; 
 //   0.97 of the FP32 pipe, with one LDS.128 per 16 FFMA2 at 0.91, with two
 //   at 0.77-0.81 (tools/microbench/ffma2_lds_mix.cu) — so bigger register
 //   tiles (fewer loaded registers per FFMA2) win even at two warps per SMSP.
+// Lane packing (r02 late, F32T.pack): a matrix of RG*CG threads that does not
+// divide 32 leaves lanes idle in a warp-per-matrices mapping (9 x 6 FP64
+// tiles: 6 threads, 5 matrices, 2 of 32 lanes idle; 28-thread FP32 tiles: 4
+// of 32).  Packed, thread tid of the CTA is thread tid % (RG*CG) of matrix
+// tid / (RG*CG), and a CTA of WPC warps holds 32*WPC / (RG*CG) matrices; the
+// per-update syncs become CTA barriers.  JM_TILE_PACK=0: off everywhere;
+// JM_TILE_PACK_N / _DT / _WPC: force it for one size (measurement hook).
+#ifndef JM_TILE_PACK
+#define JM_TILE_PACK 1
+#endif
+#ifndef JM_TILE_PACK_N
+#define JM_TILE_PACK_N 0
+#endif
+#ifndef JM_TILE_PACK_DT
+#define JM_TILE_PACK_DT 1
+#endif
+#ifndef JM_TILE_PACK_WPC
+#define JM_TILE_PACK_WPC 0
+#endif
+// JM_TILE_PACK_ALL (measurement hook): pack every resident tile shape that
+// idles lanes, with the smallest (1) or the largest (2) CTA of <= 8 warps
+// that the packing fills
+#ifndef JM_TILE_PACK_ALL
+#define JM_TILE_PACK_ALL 0
+#endif
+#ifndef JM_TILE_PACK_STRM
+#define JM_TILE_PACK_STRM 0   // 1: JM_TILE_PACK_ALL also packs the low-repeat kernels' shapes
+#endif
+JM_HD constexpr int pack_fill_milli(int tpm, int w) { return (32 * w / tpm) * tpm * 1000 / (32 * w); }
+JM_HD constexpr int unpacked_fill_milli(int tpm) {
+  return tpm > 32 ? tpm * 1000 / (32 * ((tpm + 31) / 32)) : (32 / tpm) * tpm * 1000 / 32;
+}
+JM_HD constexpr int pack_wpc_for(int tpm, int mode) {
+  int best = 0;
+  for (int w = 2; w <= 8; ++w)
+    if (32 * w >= tpm && pack_fill_milli(tpm, w) >= 990 && (best == 0 || mode == 2)) best = w;
+  return best;
+}
 struct F32T {
   int ra, cb, rg, cg;   // RA x CB register tile; RG x CG threads per matrix
   int ldm;              // row stride of the published M, floats (multiple of 4)
@@ -182,11 +220,13 @@ struct F32T {
   int maxreg;           // register cap (__maxnreg__ of k_update_rc)
   int kunroll;          // k blocks of four per iteration of the (rolled) k loop
   int wpc;              // warps per CTA
+  int pack;             // 1: lane-packed CTA (matrices of RG*CG threads laid end to end over
+                        // the CTA's threads, straddling warps; a CTA barrier per sync)
 };
 // Per-n choices, measured on B200 (tools/f32_search.py; the layout of each
 // shape from tools/f32_layout.py):
 // {n, RA, CB, row padding (16-B chunks), region padding (16-B chunks), colblk, trfast, qmix, maxreg, kunroll}
-struct F32TRow { int n, ra, cb, ldmpad, pad, colblk, trfast, qmix, maxreg, kunroll, wpc; };   // (wpc 0: 4)
+struct F32TRow { int n, ra, cb, ldmpad, pad, colblk, trfast, qmix, maxreg, kunroll, wpc, pack; };   // (wpc 0: 4)
 // FP64 register tiles (DFMA, run_f64t) for the sizes where DMMA's 8 x 8 x 4
 // granularity wastes most of the pipe; the same fields, CB a multiple of 2
 // (a 16-B chunk holds two doubles).  Only the sizes listed take this kind.
@@ -362,7 +402,7 @@ JM_HD constexpr F32T f32t_default(int n, int dt = 0) {
       const double lane = t > 32 ? (double)t / rup(t, 32) : (double)((32 / t) * t) / 32.0;
       const double core = 1.0 / (1.0 + 0.3 * 4.0 * (ra + cb) / (ra * cb));
       const double sc = pad * lane * core;
-      if (sc > bs + 1e-9) { bs = sc; best = F32T{ra, cb, rg, cg, 0, 0, 0, 1, 0, 168, 2, 4}; }
+      if (sc > bs + 1e-9) { bs = sc; best = F32T{ra, cb, rg, cg, 0, 0, 0, 1, 0, 168, 2, 4, 0}; }
     }
   best.ldm = best.cg * best.cb + v;
   best.maxreg = w * (best.ra * best.cb + v * best.ra + 2 * best.cb) + 24 > 168 ? 255 : 168;
@@ -372,7 +412,7 @@ JM_HD constexpr F32T f32t_tile(int n, int dt = 0) {
   F32T t = f32t_default(n, dt);
   auto take = [&](const F32TRow &r) {
     t = F32T{r.ra, r.cb, cdiv(n, r.ra), cdiv(n, r.cb), cdiv(n, r.cb) * r.cb + tt_vec(dt) * r.ldmpad, r.pad,
-             r.colblk, r.trfast, r.qmix, r.maxreg, r.kunroll, r.wpc > 0 ? r.wpc : 4};
+             r.colblk, r.trfast, r.qmix, r.maxreg, r.kunroll, r.wpc > 0 ? r.wpc : 4, r.pack};
   };
   if (dt == 1) {
     for (const F32TRow &r : F64T_TABLE)
@@ -384,6 +424,16 @@ JM_HD constexpr F32T f32t_tile(int n, int dt = 0) {
       for (const F32TRow &r : F32TS_TABLE)
         if (r.n == n && r.ra > 0) take(r);
   }
+  if (JM_TILE_PACK == 0) t.pack = 0;
+  if (JM_TILE_PACK_N == n && (dt == 1) == (JM_TILE_PACK_DT == 1) && dt != 2) {   // (search hook)
+    t.pack = 1;
+    if (JM_TILE_PACK_WPC > 0) t.wpc = JM_TILE_PACK_WPC;
+  }
+  if (JM_TILE_PACK_ALL > 0 && (dt != 2 || JM_TILE_PACK_STRM) && !t.qmix) {
+    const int tpm = t.rg * t.cg, w = pack_wpc_for(tpm, JM_TILE_PACK_ALL);
+    if (w > 0 && pack_fill_milli(tpm, w) > unpacked_fill_milli(tpm) + 20) { t.pack = 1; t.wpc = w; }
+  }
+  if (t.pack) t.qmix = 0;
   if (dt == 1) {   // (the JM_F32T_* tuning hooks below apply to the FP32 tiles)
     if (t.rg * t.cg > 16 || t.rg * t.cg <= 8) t.qmix = 0;
     return t;
@@ -415,7 +465,8 @@ JM_HD constexpr int f32t_wpc(int n, int dt = 0) {
   return f32t_tile(n, dt).wpc < f32t_wpm(n, dt) ? f32t_wpm(n, dt) : f32t_tile(n, dt).wpc;
 }
 JM_HD constexpr int f32t_mpc(int n, int dt = 0) {   // matrices per CTA
-  return f32t_wpc(n, dt) / f32t_wpm(n, dt) * f32t_mpw(n, dt);
+  return f32t_tile(n, dt).pack ? 32 * f32t_wpc(n, dt) / f32t_tpmat(n, dt)
+                               : f32t_wpc(n, dt) / f32t_wpm(n, dt) * f32t_mpw(n, dt);
 }
 JM_HD constexpr int f32t_nr(int n, int dt = 0) { return f32t_tile(n, dt).rg * f32t_tile(n, dt).ra; }   // padded rows
 JM_HD constexpr int f32t_kp(int n, int dt = 0) { return rup(n, tt_vec(dt)); }   // k blocks of one 16-B chunk

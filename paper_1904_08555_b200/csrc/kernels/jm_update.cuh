@@ -1374,23 +1374,27 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   constexpr bool PAD = (NR != N) || (NC != N);
   static_assert(CB % 4 == 0 && NC >= f32t_kp(N, DT), "tile shape");
-  static_assert(WPC % WPM == 0, "whole matrices per CTA");
+  static_assert(TL.pack || WPC % WPM == 0, "whole matrices per CTA");
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // matrix slot in the chunk (mi) and thread index within the matrix (t)
   // (qmix: the two matrices of a warp alternate by quarter-warp, so the two
   // quarters of a half-warp always read different matrices: disjoint
   // addresses, one wavefront per half for both the A and the B loads)
+  // (PACK, jm_plan.h F32T.pack: matrices laid end to end over the CTA's
+  // threads, straddling warps; CTA barriers)
+  constexpr bool PACK = TL.pack;
   const int m = WPM == 1 ? (TL.qmix ? (lane >> 3) & 1 : lane / TPMAT) : 0;
-  const int t = WPM == 1 ? (TL.qmix ? ((lane >> 4) << 3) + (lane & 7) : lane - m * TPMAT) : (warp % WPM) * 32 + lane;
-  const int mi = WPM == 1 ? warp * MPW + m : warp / WPM;
+  const int t = PACK ? tid % TPMAT : WPM == 1 ? (TL.qmix ? ((lane >> 4) << 3) + (lane & 7) : lane - m * TPMAT) : (warp % WPM) * 32 + lane;
+  const int mi = PACK ? tid / TPMAT : WPM == 1 ? warp * MPW + m : warp / WPM;
   // lanes past the last whole matrix of a warp, or past RG*CG in a multi-warp
   // matrix, idle (but take part in the syncs)
-  const bool lane_ok = WPM > 1 ? t < TPMAT : (m < MPW && t < TPMAT);
+  const bool lane_ok = PACK ? mi < MPC : WPM > 1 ? t < TPMAT : (m < MPW && t < TPMAT);
   const int tr = TL.trfast ? t % RG : t / CG, tc = TL.trfast ? t / RG : t % CG;
   const float c = float(0.00005);
   auto sync = [&]() {
-    if constexpr (WPM == 1) __syncwarp();
+    if constexpr (PACK) __syncthreads();
+    else if constexpr (WPM == 1) __syncwarp();
     else if constexpr (WPM == WPC) __syncthreads();
     else bar_named(1 + mi, 32 * WPM);
   };
@@ -1438,6 +1442,7 @@ __device__ __forceinline__ void run_f32t(const float *__restrict__ in, float *__
                         Ring<N, ES, NT, MPC, ring_kr(N, ES, MPC), JM_RING_S, RSEP ? 0 : REG, RROWS ? LDM * 4 : 0>,
                         Stager<N, ES, REG, NT, MPC, AL, STRM, PSH>>::type Stg;
   static_assert(RSEP || Stg::SBM >= REG, "a slot holds the work region");
+  static_assert(!(RSEP && PACK), "the packed-slot copy assumes warp-aligned matrix groups");
   Stg sg(in, out, batch, smem);
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
@@ -1715,17 +1720,19 @@ __device__ __forceinline__ void run_f64t(const double *__restrict__ in, double *
   constexpr bool AL = ((MPC * MB) % 16) == 0;
   constexpr bool PAD = (NR != N) || (NC != N);
   static_assert(CB % 2 == 0 && NC >= f32t_kp(N, 1), "tile shape");
-  static_assert(WPC % WPM == 0, "whole matrices per CTA");
+  static_assert(TL.pack || WPC % WPM == 0, "whole matrices per CTA");
   extern __shared__ __align__(16) char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr bool PACK = TL.pack;   // (lane-packed CTA, jm_plan.h F32T.pack)
   const int m = WPM == 1 ? (TL.qmix ? (lane >> 3) & 1 : lane / TPMAT) : 0;
-  const int t = WPM == 1 ? (TL.qmix ? ((lane >> 4) << 3) + (lane & 7) : lane - m * TPMAT) : (warp % WPM) * 32 + lane;
-  const int mi = WPM == 1 ? warp * MPW + m : warp / WPM;
-  const bool lane_ok = WPM > 1 ? t < TPMAT : (m < MPW && t < TPMAT);
+  const int t = PACK ? tid % TPMAT : WPM == 1 ? (TL.qmix ? ((lane >> 4) << 3) + (lane & 7) : lane - m * TPMAT) : (warp % WPM) * 32 + lane;
+  const int mi = PACK ? tid / TPMAT : WPM == 1 ? warp * MPW + m : warp / WPM;
+  const bool lane_ok = PACK ? mi < MPC : WPM > 1 ? t < TPMAT : (m < MPW && t < TPMAT);
   const int tr = TL.trfast ? t % RG : t / CG, tc = TL.trfast ? t / RG : t % CG;
   const double c = 0.00005;
   auto sync = [&]() {
-    if constexpr (WPM == 1) __syncwarp();
+    if constexpr (PACK) __syncthreads();
+    else if constexpr (WPM == 1) __syncwarp();
     else if constexpr (WPM == WPC) __syncthreads();
     else bar_named(1 + mi, 32 * WPM);
   };

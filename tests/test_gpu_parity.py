@@ -82,6 +82,29 @@ def test_parity_signed_hard_all_n(jm, n, dt):
         assert_parity(got_i, want_i, what=f"signed identity n={n} {dt} R={r}")
 
 
+IDLE_LANE_SHAPES = [("f64", 17), ("f64", 18), ("f32", 17), ("f32", 18), ("f32", 25), ("f32", 41), ("f32", 42),
+                    ("f32", 49), ("f32", 50), ("f32", 51), ("f32", 52), ("f32", 54), ("f32", 55)]
+
+
+@pytest.mark.parametrize("dt,n", IDLE_LANE_SHAPES)
+def test_parity_register_tiles_many_chunks(jm, dt, n):
+    """The register-tile shapes whose matrices do not fill a warp (6-, 10-,
+    28- and 56-thread matrices: idle lanes, or with JM_TILE_PACK_ALL the
+    lane-packed CTA of jm_plan.h F32T.pack, profiles/r02_ab_lane_pack.md):
+    several whole CTA chunks (up to 85 matrices each) plus a ragged tail, both
+    signs, resident kernel, in place as well."""
+    batch = 3 * 85 + 5 if n <= 25 else 3 * 8 + 5
+    for dist, seed in (("hard", 2000), ("shard", 3000)):
+        x = jm_synth.generate(n, dt, dist, jm_synth.SEED_HARD_BASE + seed + n, 0, batch)
+        for r in (1, 2, 5):
+            want = oracle.run(x, r)
+            xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+            got = jm.run(xd, r, addend="ones", sync=True, variant="resident").cpu().numpy()
+            assert_parity(got, want, what=f"packed {dist} n={n} {dt} R={r}")
+        jm.run(xd, 3, xd, addend="identity", sync=True, variant="resident")
+        assert_parity(xd.cpu().numpy(), oracle.run(x, 3, "identity"), what=f"packed in-place n={n} {dt}")
+
+
 @pytest.mark.parametrize("dt", ["f64", "f32"])
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 8, 9, 13, 16, 17, 24, 32, 33, 40, 48, 57, 64])
 def test_parity_identity_addend(jm, n, dt):
