@@ -291,7 +291,7 @@ constexpr F32TRow F32T_TABLE[] = {
     {51, 13, 8, 4, 0, 0, 1, 0, 232, 4},  // 0.573 of the pipe (r02 neighbourhood search: cap 232, k unroll 4; was 0.560)
     {52, 13, 8, 1, 0, 0, 1, 0, 255, 4},  // 0.585 of the pipe, 236 regs (r02 neighbourhood search: k unroll 4; wide search 0.533)
     {53, 7, 16, 1, 0, 0, 1, 0, 232, 4},  // 0.588 of the pipe (r02 neighbourhood search: cap 232, k unroll 4; was 0.555)
-    {54, 7, 8, 1, 0, 0, 1, 0, 144, 8},  // 0.618 of the pipe (r02 cap A/B, profiles/r02_ab_f32_cap.md: cap 144, 14 warps per SM; cap 168 0.605)
+    {54, 7, 8, 1, 0, 0, 1, 0, 144, 8},  // 0.618 of the pipe (r02 cap A/B, profiles/r02_ab_f32_cap.md: cap 144; cap 168 0.605)
     {55, 7, 8, 1, 0, 0, 1, 0, 144, 8},  // 0.638 of the pipe (r02 cap A/B: cap 144; cap 232 0.620)
     {56, 7, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.662 of the pipe, 204 regs
     {57, 8, 16, 1, 0, 0, 1, 0, 255, 2},  // 0.587 of the pipe, 225 regs
