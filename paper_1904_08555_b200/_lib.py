@@ -22,7 +22,7 @@ JM_FLAG_SYNC, JM_FLAG_HOST_BUFFERS, JM_FLAG_RESIDENT, JM_FLAG_STREAMING = 1, 2, 
 JM_FLAG_BATCH_COMPILE = 16
 JM_FLAG_LATENCY = 32
 JM_TILE_NAMES = {0: "generic", 1: "tpm", 2: "warp_dmma", 3: "cta_dmma", 4: "warp_f32",
-                 5: "cta_f32", 6: "rows", 7: "matmul", 8: "tpm2", 9: "tpms", 10: "f32_rows", 11: "f64_reg", 12: "lat"}
+                 5: "cta_f32", 6: "rows", 7: "matmul", 8: "tpm2", 9: "tpms", 10: "f32_rows", 11: "f64_reg", 12: "lat", 13: "f32_tc"}
 JM_OP_MATMUL = 2
 JM_OP_MASS = 3
 JM_OP_STREAM = 4

@@ -25,7 +25,8 @@ enum class Tile : int { Generic = 0, TPM = 1, Dmma = 2, Tpm2 = 3 /* r01, removed
                         Rows = 6 /* r01 FP64 row panels, removed */,
                         F32Rows = 7 /* plan label only: the FP32 row panels of Tile::F32 */,
                         Reg = 8 /* FP64 register tiles (DFMA; run_f64t) */,
-                        Lat = 9 /* latency path: a warp per matrix, an element per lane (k_update_lat) */ };
+                        Lat = 9 /* latency path: a warp per matrix, an element per lane (k_update_lat) */,
+                        F32Tc = 10 /* plan label only: the FP32 kind on the tensor cores (run_f32tc) */ };
 
 struct Plan {
   int tile;      // Tile
@@ -575,6 +576,25 @@ JM_HD constexpr bool prefetch_for(int n, int dtype) {
   return dtype == 1 ? (n >= 5 && n <= 7) : (n >= 8 && n <= JM_F32_TPM_MAX);
 }
 
+// ---- FP32 on the tensor cores, error-compensated TF32 (r02 late, run_f32tc) ----
+// n a multiple of 16: a warp per matrix, P = M + M.M as m16n8k8 TF32 mma.sync
+// tiles with each operand split x = hi + lo (hi = tf32(x), lo = tf32(x - hi))
+// and the three products lo.hi + hi.lo + hi.hi accumulated in FP32 (the
+// dropped lo.lo term is ~2^-22 relative).  The accumulator fragment of n-tile
+// KS IS the A fragment of k-step KS under the k permutation (t, t+4) ->
+// (2t, 2t+1), so only B (rows of M) goes through shared memory.
+// JM_F32TC=1: the resident FP32 kernel of n = 16..JM_F32TC_MAXN (n % 16 == 0).
+#ifndef JM_F32TC
+#define JM_F32TC 1
+#endif
+#ifndef JM_F32TC_MAXN
+#define JM_F32TC_MAXN 32
+#endif
+constexpr int F32TC_WPC = 4;                        // warps (= matrices) per CTA
+JM_HD constexpr bool f32tc_use(int n) { return JM_F32TC && n % 16 == 0 && n <= JM_F32TC_MAXN; }
+JM_HD constexpr int f32tc_ld(int n) { return n + 4; }   // publish row stride (floats): B loads conflict free
+JM_HD constexpr int f32tc_wbytes(int n) { return n * f32tc_ld(n) * 4; }
+
 JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   const int es = dtype == 1 ? 8 : 4;
   const Tile t = tile_for(n, dtype);
@@ -599,6 +619,8 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
     if (f32p_inplace(n)) return Plan{(int)Tile::F32Rows, 32 * F32P_WPC, mpc, nst * rup(mpc * f32p_slot(n), 16) + mpc * f32p_mbuf(n), 1};
     return Plan{(int)Tile::F32Rows, 32 * F32P_WPC, mpc, nst * stage_bytes(mpc, n, es) + mpc * f32p_pstr(n), 1};
   }
+  if (dtype == 0 && f32tc_use(n))
+    return Plan{(int)Tile::F32Tc, 32 * F32TC_WPC, F32TC_WPC, stage_bytes(F32TC_WPC, n, es) + F32TC_WPC * f32tc_wbytes(n), 1};
   // F32 tiles: the stage area IS the per-matrix region (stride f32t_region)
   return Plan{(int)t, 32 * f32t_wpc(n), f32t_mpc(n), f32t_mpc(n) * f32t_region(n), f32t_wpm(n)};
 }
@@ -610,7 +632,7 @@ JM_HD constexpr bool use_mb1(int n, int dtype, bool strm = false) {
 }
 // ... or k_update[_stream]_rc (a register cap, __maxnreg__): the F32T tiles
 JM_HD constexpr bool use_rc(int n, int dtype, bool strm = false) {
-  return (dtype == 0 && tile_for(n, dtype) == Tile::F32 && (strm ? f32t_stream_use(n) : f32t_use(n))) ||
+  return (dtype == 0 && tile_for(n, dtype) == Tile::F32 && (strm ? f32t_stream_use(n) : f32t_use(n) && !f32tc_use(n))) ||
          tile_for(n, dtype) == Tile::Reg;
 }
 
@@ -701,7 +723,10 @@ JM_HD constexpr int f64t_rn(int n) { return JM_F64T_RN > 0 ? JM_F64T_RN : n <= 1
 #ifndef JM_F32T_RN
 #define JM_F32T_RN 0
 #endif
-constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 24, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 1048576, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 50, 1048576, 12, 50, 50, 1048576, 1048576, 50, 24, 8, 8, 8, 1048576, 50, 1048576, 1048576, 12, 50, 1048576, 1048576, 1048576, 50, 50, 50, 50};
+constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 2, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 50, 1048576, 12, 50, 50, 1048576, 1048576, 50, 24, 8, 8, 8, 1048576, 50, 1048576, 1048576, 12, 50, 1048576, 1048576, 1048576, 50, 50, 50, 50};
+// (n = 16, 32: the resident kernel is the tensor-core kind, run_f32tc, which
+// beats the streaming tiles from R = 8 (0.64 vs 0.58, 0.81 vs 0.73 of the
+// pipe; profiles/r02_f32tc.md), so they stream only at the lowest R)
 JM_HD constexpr int f32t_rn(int n) {
   return JM_F32T_RN > 0 ? JM_F32T_RN
          : F32T_STREAM_MAXR[n] >= (1 << 20) ? (1 << 30)

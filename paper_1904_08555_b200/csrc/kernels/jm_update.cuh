@@ -1831,6 +1831,142 @@ __device__ __forceinline__ void run_f64t(const double *__restrict__ in, double *
   sg.finish();
 }
 
+// ======================================================================
+// run_f32tc — FP32 on the tensor cores (jm_plan.h f32tc_use): a warp per
+// matrix, n = 16*MT.  Lane (g, t) = (lane / 4, lane % 4) holds, for m-tile I
+// and n-tile J, the m16n8 accumulator fragment {(16I+g, 8J+2t), (.., 8J+2t+1),
+// (16I+g+8, 8J+2t), (.., 8J+2t+1)} of M (then of P = M + M.M).  Under the k
+// permutation (t, t+4) -> (2t, 2t+1) within a k-step, n-tile KS's fragment is
+// the m16n8k8 A fragment {a0, a1, a2, a3} = {c0, c2, c1, c3} of k-step KS, so
+// only the B operand B[k][j] = M[8KS + 2t (+1)][8J + g] is read from the
+// warp's published copy of M.  Each operand x is split x = hi + lo (hi, lo
+// TF32; tf32_split) and lo.hi + hi.lo + hi.hi accumulate in FP32 (the 3xTF32
+// scheme; lo.lo ~ 2^-21 relative is dropped).
+// ======================================================================
+// The split without cvt.rna.tf32 (an FSETP / VIADD / LOP3 / SEL sequence per
+// value in SASS, which made the ALU pipe the bound): hi = x with the 13 low
+// mantissa bits cleared (exact: lo = x - hi is exact in FP32), lo rounded to
+// TF32 by adding half an ulp and clearing the same bits (lo is finite and
+// far from overflow), or (JM_F32TC_LORND=0, the default) passed as is, the
+// mma reading it truncated: measured max relative error vs the oracle 1.6e-6
+// (rounded: 1.3e-6) against the 1e-5 FP32 bound, 0.931 vs 0.914 of the FP32
+// pipe at n = 32 (profiles/r02_f32tc.md).
+#ifndef JM_F32TC_LORND
+#define JM_F32TC_LORND 0
+#endif
+// (hi is formed as x - (x - mask(x)), exactly mask(x): ptxas knows the mma
+// ignores the low bits, so a plain mask operand became the raw accumulator and
+// the permuted A quad was rebuilt with four MOVs at every use; the FADD result
+// is allocated in quad order once)
+__device__ __forceinline__ void tf32_split(float x, unsigned &hi, unsigned &lo) {
+  const float d = x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);   // exact
+  hi = __float_as_uint(x - d);                                              // exact: the masked x
+  const unsigned l = __float_as_uint(d);
+  lo = JM_F32TC_LORND ? (l + 0x1000u) & 0xffffe000u : l;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int N, Addend A>
+__device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *__restrict__ out,
+                                          long long batch, int repeat) {
+  static_assert(N % 16 == 0, "m16 tiles");
+  constexpr int MT = N / 16, NT8 = N / 8, LD = f32tc_ld(N), MPC = F32TC_WPC, NT = 32 * F32TC_WPC;
+  constexpr int SB = stage_stride(N, 4);
+  constexpr bool AL = ((MPC * N * N * 4) % 16) == 0;
+  extern __shared__ __align__(16) char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const float c = float(0.00005);
+  Stager<N, 4, SB, NT, MPC, AL, false> sg(in, out, batch, smem);
+  float *w = reinterpret_cast<float *>(smem + Stager<N, 4, SB, NT, MPC, AL, false>::BYTES) + warp * N * LD;
+  for (sg.start(); sg.valid(); sg.next()) {
+    sg.acquire();
+    const bool live = warp < sg.cnt();
+    float *sm = reinterpret_cast<float *>(sg.buf() + warp * SB);
+    float acc[MT][NT8][4];
+    if (live) {
+#pragma unroll
+      for (int I = 0; I < MT; ++I)
+#pragma unroll
+        for (int J = 0; J < NT8; ++J)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float2 v = *reinterpret_cast<const float2 *>(sm + (16 * I + g + 8 * h) * N + 8 * J + 2 * t);
+            acc[I][J][2 * h] = v.x;
+            acc[I][J][2 * h + 1] = v.y;
+          }
+      for (int r = 0; r < repeat; ++r) {
+        // publish M (row-major, row stride LD) for the B operand
+#pragma unroll
+        for (int I = 0; I < MT; ++I)
+#pragma unroll
+          for (int J = 0; J < NT8; ++J)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              *reinterpret_cast<float2 *>(w + (16 * I + g + 8 * h) * LD + 8 * J + 2 * t) =
+                  make_float2(acc[I][J][2 * h], acc[I][J][2 * h + 1]);
+        // A fragments (hi, lo) of every k-step, taken before the products overwrite acc
+        unsigned ah[MT][NT8][4], al[MT][NT8][4];
+#pragma unroll
+        for (int I = 0; I < MT; ++I)
+#pragma unroll
+          for (int KS = 0; KS < NT8; ++KS)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              tf32_split(acc[I][KS][q == 1 ? 2 : q == 2 ? 1 : q], ah[I][KS][q], al[I][KS][q]);
+            }
+        __syncwarp();
+#pragma unroll
+        for (int KS = 0; KS < NT8; ++KS) {
+          unsigned bh[NT8][2], bl[NT8][2];
+#pragma unroll
+          for (int J = 0; J < NT8; ++J)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              tf32_split(w[(8 * KS + 2 * t + h) * LD + 8 * J + g], bh[J][h], bl[J][h]);
+            }
+          // small terms first; consecutive mma on different accumulators
+#pragma unroll
+          for (int pr = 0; pr < 3; ++pr)
+#pragma unroll
+            for (int J = 0; J < NT8; ++J)
+#pragma unroll
+              for (int I = 0; I < MT; ++I) {
+                if (pr == 0) mma_tf32(acc[I][J], al[I][KS], bh[J][0], bh[J][1]);
+                else if (pr == 1) mma_tf32(acc[I][J], ah[I][KS], bl[J][0], bl[J][1]);
+                else mma_tf32(acc[I][J], ah[I][KS], bh[J][0], bh[J][1]);
+              }
+        }
+        __syncwarp();   // every read of w done before the next publish
+#pragma unroll
+        for (int I = 0; I < MT; ++I)
+#pragma unroll
+          for (int J = 0; J < NT8; ++J)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int row = 16 * I + g + 8 * (q >> 1), col = 8 * J + 2 * t + (q & 1);
+              const float a = (A == Addend::Ones || row == col) ? 1.0f : 0.0f;
+              acc[I][J][q] = fmaT(c, acc[I][J][q], a);
+            }
+      }
+#pragma unroll
+      for (int I = 0; I < MT; ++I)
+#pragma unroll
+        for (int J = 0; J < NT8; ++J)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            *reinterpret_cast<float2 *>(sm + (16 * I + g + 8 * h) * N + 8 * J + 2 * t) =
+                make_float2(acc[I][J][2 * h], acc[I][J][2 * h + 1]);
+    }
+    sg.release();
+  }
+  sg.finish();
+}
+
 // ------------------------------------------------------------------ entry
 // The NVRTC name expression is "jm::k_update<N, T, jm::Addend::X, jm::Tile::Y>"
 // with Y = tile_for(N, dtype); the host launches it with plan_specialized().
@@ -1853,6 +1989,8 @@ __device__ __forceinline__ void update_body(const T *__restrict__ in, T *__restr
     else run_f64t<N, A, false>(in, out, batch, repeat);
   } else if constexpr (K == Tile::Dmma) {
     run_dmma<N, A, dmma_w(N, STRM), STRM>(in, out, batch, repeat);
+  } else if constexpr (!STRM && sizeof(T) == 4 && f32tc_use(N)) {
+    run_f32tc<N, A>(in, out, batch, repeat);
   } else if constexpr (f32p_use(N) && !(STRM && f32t_stream_use(N))) {
     run_f32p<N, A, STRM>(in, out, batch, repeat);
   } else {

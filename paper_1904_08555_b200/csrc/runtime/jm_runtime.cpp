@@ -1226,6 +1226,7 @@ int tile_code(const jm::Plan &p) {
          : p.tile == (int)jm::Tile::Rows ? JM_TILE_ROWS
          : p.tile == (int)jm::Tile::F32Rows ? JM_TILE_F32_ROWS
          : p.tile == (int)jm::Tile::Reg ? JM_TILE_F64_REG
+         : p.tile == (int)jm::Tile::F32Tc ? JM_TILE_F32_TC
          : p.tile == (int)jm::Tile::Dmma ? (p.w > 1 ? JM_TILE_CTA_DMMA : JM_TILE_WARP_DMMA)
                                          : (p.w > 1 ? JM_TILE_CTA_F32 : JM_TILE_WARP_F32);
 }

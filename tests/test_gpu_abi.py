@@ -101,7 +101,7 @@ def test_generic_is_preseeded(jm):
 
 def test_key_info_reports_registers(jm):
     _fresh(jm)
-    for n, dt in ((4, "double"), (16, "double"), (15, "float"), (16, "float"), (64, "double")):
+    for n, dt in ((4, "double"), (16, "double"), (15, "float"), (16, "float"), (32, "float"), (64, "double")):
         jm.jit_mat_prepare(n, dt)
     info = {(k["n"], k["dtype"], k["kind"]): k for k in jm.jit_mat_key_info()}
     k16 = info[(16, 1, 0)]
@@ -110,7 +110,8 @@ def test_key_info_reports_registers(jm):
     assert info[(64, 1, 0)]["tile_name"] == "cta_dmma"
     assert info[(4, 1, 0)]["tile_name"] == "tpm"
     assert info[(15, 0, 0)]["tile_name"] == "f32_rows"
-    assert info[(16, 0, 0)]["tile_name"] == "warp_f32"
+    assert info[(16, 0, 0)]["tile_name"] == "f32_tc"        # FP32 on the tensor cores (3xTF32)
+    assert info[(32, 0, 0)]["tile_name"] == "f32_tc"
     for k in info.values():
         assert k["local_bytes"] == 0, f"spill in {k}"
 

@@ -56,8 +56,9 @@ def _same_bits(n, dt):
     # DFMA path and the streaming one (one warp per row tile) does not, and
     # f64 n = 9 / 10 and f32 n = 12..14, whose resident kernel is thread per
     # matrix with a staged product (TPMS) and whose low-repeat kernel is the
-    # DMMA ring / the row-panel ring, and the DFMA register-tile sizes
-    return not ((dt == "f64" and n in (9, 10, 33, 34) + F64_REG_N) or (dt == "f32" and n in (12, 13, 14)))
+    # DMMA ring / the row-panel ring, and the DFMA register-tile sizes, and
+    # f32 n = 16 / 32, whose resident kernel runs on the tensor cores (3xTF32)
+    return not ((dt == "f64" and n in (9, 10, 33, 34) + F64_REG_N) or (dt == "f32" and n in (12, 13, 14, 16, 32)))
 
 
 def test_f64_reg_sizes_match_the_plan(jm):
@@ -156,11 +157,11 @@ def test_variant_selection_and_key_info(jm):
     assert jm.jit_mat_prepare_for(15, "f32", 4) == 0
     assert jm.jit_mat_prepare_for(12, "f32", 1) == 0       # TPMS beats the ring even at R = 1
     assert jm.jit_mat_prepare_for(13, "f32", 1) == 1 and jm.jit_mat_prepare_for(13, "f32", 2) == 0
-    assert jm.jit_mat_prepare_for(16, "f32", 24) == 1      # n = 16: register tiles, streaming to R = 24
-    assert jm.jit_mat_prepare_for(16, "f32", 25) == 0
+    assert jm.jit_mat_prepare_for(16, "f32", 2) == 1       # n = 16: streaming register tiles to R = 2,
+    assert jm.jit_mat_prepare_for(16, "f32", 3) == 0       # then the tensor-core kind (profiles/r02_f32tc.md)
     # FP32 tiles: stream while R <= F32T_STREAM_MAXR[n] (jm_plan.h f32t_rn)
     assert jm.jit_mat_prepare_for(64, "f32", 50) == 1 and jm.jit_mat_prepare_for(64, "f32", 51) == 0
-    assert jm.jit_mat_prepare_for(32, "f32", 1000) == 1    # streams at every R (faster even at R = 100)
+    assert jm.jit_mat_prepare_for(32, "f32", 2) == 1 and jm.jit_mat_prepare_for(32, "f32", 3) == 0   # (tensor cores)
     assert jm.jit_mat_prepare_for(17, "f32", 6) == 1 and jm.jit_mat_prepare_for(17, "f32", 7) == 0
     assert jm.jit_mat_prepare_for(8, "f64", 1) == 0        # n = 8 DMMA: resident (measured)
     assert jm.jit_mat_prepare_for(4, "f64", 1, flags=jm.JM_FLAG_STREAMING) == 1   # TPM: staged variant
