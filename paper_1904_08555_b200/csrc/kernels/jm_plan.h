@@ -588,10 +588,24 @@ JM_HD constexpr bool prefetch_for(int n, int dtype) {
 #define JM_F32TC 1
 #endif
 #ifndef JM_F32TC_MAXN
-#define JM_F32TC_MAXN 32
+#define JM_F32TC_MAXN 64
 #endif
-constexpr int F32TC_WPC = 4;                        // warps (= matrices) per CTA
-JM_HD constexpr bool f32tc_use(int n) { return JM_F32TC && n % 16 == 0 && n <= JM_F32TC_MAXN; }
+// m-tiles (16 rows) per warp: the warps of a matrix split its rows (WPM =
+// (n / 16) / MTW warps per matrix, a named barrier per matrix); each warp
+// keeps its m-tiles' accumulators and A splits in registers
+#ifndef JM_F32TC_MTW
+#define JM_F32TC_MTW 0    // > 0: one value for every size
+#endif
+// n = 16, 32, 64 (profiles/r02_f32tc.md: 0.72 -> 0.74, 0.77 -> 0.93, 0.78 -> 0.94
+// of the FP32 pipe at R = 100); n = 48 stays on the FFMA2 tiles (three warps
+// per matrix reach 0.66 against 0.76)
+JM_HD constexpr bool f32tc_use(int n) { return JM_F32TC && n % 16 == 0 && n <= JM_F32TC_MAXN && n != 48; }
+JM_HD constexpr int f32tc_mtw(int n) {
+  return (JM_F32TC_MTW > 0 && (n / 16) % JM_F32TC_MTW == 0) ? JM_F32TC_MTW : n <= 32 ? n / 16 : 2;   // (n = 64: two warps, 0.94 vs 0.89 for four)
+}
+JM_HD constexpr int f32tc_wpm(int n) { return n / 16 / f32tc_mtw(n); }                       // warps per matrix
+JM_HD constexpr int f32tc_mpc(int n) { return f32tc_wpm(n) >= 4 ? 1 : 4 / f32tc_wpm(n); }   // matrices per CTA
+JM_HD constexpr int f32tc_wpc(int n) { return f32tc_wpm(n) * f32tc_mpc(n); }
 JM_HD constexpr int f32tc_ld(int n) { return n + 4; }   // publish row stride (floats): B loads conflict free
 JM_HD constexpr int f32tc_wbytes(int n) { return n * f32tc_ld(n) * 4; }
 
@@ -620,7 +634,8 @@ JM_HD constexpr Plan plan_specialized(int n, int dtype) {
     return Plan{(int)Tile::F32Rows, 32 * F32P_WPC, mpc, nst * stage_bytes(mpc, n, es) + mpc * f32p_pstr(n), 1};
   }
   if (dtype == 0 && f32tc_use(n))
-    return Plan{(int)Tile::F32Tc, 32 * F32TC_WPC, F32TC_WPC, stage_bytes(F32TC_WPC, n, es) + F32TC_WPC * f32tc_wbytes(n), 1};
+    return Plan{(int)Tile::F32Tc, 32 * f32tc_wpc(n), f32tc_mpc(n), stage_bytes(f32tc_mpc(n), n, es) + f32tc_mpc(n) * f32tc_wbytes(n),
+                f32tc_wpm(n)};
   // F32 tiles: the stage area IS the per-matrix region (stride f32t_region)
   return Plan{(int)t, 32 * f32t_wpc(n), f32t_mpc(n), f32t_mpc(n) * f32t_region(n), f32t_wpm(n)};
 }
@@ -723,10 +738,11 @@ JM_HD constexpr int f64t_rn(int n) { return JM_F64T_RN > 0 ? JM_F64T_RN : n <= 1
 #ifndef JM_F32T_RN
 #define JM_F32T_RN 0
 #endif
-constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 2, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 50, 1048576, 12, 50, 50, 1048576, 1048576, 50, 24, 8, 8, 8, 1048576, 50, 1048576, 1048576, 12, 50, 1048576, 1048576, 1048576, 50, 50, 50, 50};
-// (n = 16, 32: the resident kernel is the tensor-core kind, run_f32tc, which
-// beats the streaming tiles from R = 8 (0.64 vs 0.58, 0.81 vs 0.73 of the
-// pipe; profiles/r02_f32tc.md), so they stream only at the lowest R)
+constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 2, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 50, 1048576, 12, 50, 50, 1048576, 1048576, 50, 24, 8, 8, 8, 1048576, 50, 1048576, 1048576, 12, 50, 1048576, 1048576, 1048576, 50, 50, 50, 3};
+// (n = 16, 32, 64: the resident kernel is the tensor-core kind, run_f32tc,
+// which ties the streaming tiles at R = 3 and wins above (R = 8: 0.65 vs 0.58,
+// 0.82 vs 0.74, 0.83 vs 0.75 of the pipe; profiles/r02_f32tc.md), so they
+// stream at R <= 2 (n = 64: R <= 3))
 JM_HD constexpr int f32t_rn(int n) {
   return JM_F32T_RN > 0 ? JM_F32T_RN
          : F32T_STREAM_MAXR[n] >= (1 << 20) ? (1 << 30)

@@ -1875,18 +1875,24 @@ template <int N, Addend A>
 __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *__restrict__ out,
                                           long long batch, int repeat) {
   static_assert(N % 16 == 0, "m16 tiles");
-  constexpr int MT = N / 16, NT8 = N / 8, LD = f32tc_ld(N), MPC = F32TC_WPC, NT = 32 * F32TC_WPC;
-  constexpr int SB = stage_stride(N, 4);
+  // MT m-tiles of this warp (MTW of the matrix's N/16; WPM warps per matrix)
+  constexpr int MT = f32tc_mtw(N), WPM = f32tc_wpm(N), NT8 = N / 8, LD = f32tc_ld(N), MPC = f32tc_mpc(N);
+  constexpr int NT = 32 * f32tc_wpc(N), SB = stage_stride(N, 4);
   constexpr bool AL = ((MPC * N * N * 4) % 16) == 0;
   extern __shared__ __align__(16) char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int mi = warp / WPM, r0 = 16 * MT * (warp % WPM);   // matrix slot, first row of this warp
   const float c = float(0.00005);
+  auto msync = [&]() {
+    if constexpr (WPM == 1) __syncwarp();
+    else bar_named(1 + mi, 32 * WPM);
+  };
   Stager<N, 4, SB, NT, MPC, AL, false> sg(in, out, batch, smem);
-  float *w = reinterpret_cast<float *>(smem + Stager<N, 4, SB, NT, MPC, AL, false>::BYTES) + warp * N * LD;
+  float *w = reinterpret_cast<float *>(smem + Stager<N, 4, SB, NT, MPC, AL, false>::BYTES) + mi * N * LD;
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
-    const bool live = warp < sg.cnt();
-    float *sm = reinterpret_cast<float *>(sg.buf() + warp * SB);
+    const bool live = mi < sg.cnt();
+    float *sm = reinterpret_cast<float *>(sg.buf() + mi * SB);
     float acc[MT][NT8][4];
     if (live) {
 #pragma unroll
@@ -1895,7 +1901,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
         for (int J = 0; J < NT8; ++J)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const float2 v = *reinterpret_cast<const float2 *>(sm + (16 * I + g + 8 * h) * N + 8 * J + 2 * t);
+            const float2 v = *reinterpret_cast<const float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t);
             acc[I][J][2 * h] = v.x;
             acc[I][J][2 * h + 1] = v.y;
           }
@@ -1907,7 +1913,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
           for (int J = 0; J < NT8; ++J)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              *reinterpret_cast<float2 *>(w + (16 * I + g + 8 * h) * LD + 8 * J + 2 * t) =
+              *reinterpret_cast<float2 *>(w + (r0 + 16 * I + g + 8 * h) * LD + 8 * J + 2 * t) =
                   make_float2(acc[I][J][2 * h], acc[I][J][2 * h + 1]);
         // A fragments (hi, lo) of every k-step, taken before the products overwrite acc
         unsigned ah[MT][NT8][4], al[MT][NT8][4];
@@ -1919,7 +1925,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
             for (int q = 0; q < 4; ++q) {
               tf32_split(acc[I][KS][q == 1 ? 2 : q == 2 ? 1 : q], ah[I][KS][q], al[I][KS][q]);
             }
-        __syncwarp();
+        msync();
 #pragma unroll
         for (int KS = 0; KS < NT8; ++KS) {
           unsigned bh[NT8][2], bl[NT8][2];
@@ -1941,14 +1947,14 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
                 else mma_tf32(acc[I][J], ah[I][KS], bh[J][0], bh[J][1]);
               }
         }
-        __syncwarp();   // every read of w done before the next publish
+        msync();   // every read of w done before the next publish
 #pragma unroll
         for (int I = 0; I < MT; ++I)
 #pragma unroll
           for (int J = 0; J < NT8; ++J)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const int row = 16 * I + g + 8 * (q >> 1), col = 8 * J + 2 * t + (q & 1);
+              const int row = r0 + 16 * I + g + 8 * (q >> 1), col = 8 * J + 2 * t + (q & 1);
               const float a = (A == Addend::Ones || row == col) ? 1.0f : 0.0f;
               acc[I][J][q] = fmaT(c, acc[I][J][q], a);
             }
@@ -1959,7 +1965,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
         for (int J = 0; J < NT8; ++J)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            *reinterpret_cast<float2 *>(sm + (16 * I + g + 8 * h) * N + 8 * J + 2 * t) =
+            *reinterpret_cast<float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t) =
                 make_float2(acc[I][J][2 * h], acc[I][J][2 * h + 1]);
     }
     sg.release();

@@ -1,15 +1,15 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-# FP32 n = 16, 32 on the tensor cores by default: GPU suite, smoke, resident/streaming crossover, ncu of the kind
-O=gpurun_out/s22; mkdir -p $O
-python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
-timeout 2000 python -m pytest tests -m gpu -q > $O/gputest.txt 2>&1; tail -3 $O/gputest.txt; grep -E "^FAILED" $O/gputest.txt | head
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; grep -E "f32|Error" $O/smoke.txt
-timeout 600 python tools/stream_sweep.py --sizes 16,32 --dtypes f32 --repeats 1,2,3,4,6,8,100 --out $O/xover.jsonl > /dev/null 2> $O/xover.err
+# tensor-core FP32 kind for n = 48, 64 (warps split the rows) and the warps-per-matrix choice; error, parity, A/B, crossover
+O=gpurun_out/s23; mkdir -p $O
+JM_BUILD_DEFINES="JM_F32TC_MAXN=64" python -c "import paper_1904_08555_b200._build as b; b.build(force=True)" > $O/build64.log 2>&1
+timeout 600 python tools/tc_err.py 48,64 2>&1 | tee $O/tc_err_48_64.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "f32 and (48 or 64)" > $O/parity64.txt 2>&1; tail -2 $O/parity64.txt
+timeout 900 python tools/stream_sweep.py --sizes 48,64 --dtypes f32 --repeats 1,2,3,4,6,8,100 --out $O/xover64.jsonl > /dev/null 2> $O/xover64.err
+timeout 1500 python tools/ab.py --variant mtw1="JM_F32TC_MAXN=64 JM_F32TC_MTW=1" --variant mtw2="JM_F32TC_MAXN=64 JM_F32TC_MTW=2" \
+  --variant ffma="JM_F32TC_MAXN=32" --variant tc64="JM_F32TC_MAXN=64" --sizes 32,48,64 --dtypes f32 --repeats 100,8 --out $O/ab64.jsonl > $O/ab64.log 2>&1
 python - <<'PY'
 import json
-for l in open('gpurun_out/s22/xover.jsonl'):
-    d=json.loads(l); print(d['n'], d['repeat'], {k:(d[k].get('frac_pipe'), d[k].get('frac_hbm'), d[k].get('ms')) for k in ('resident','streaming','auto') if k in d})
+for f in ('xover64', 'ab64'):
+    for l in open(f'gpurun_out/s23/{f}.jsonl'):
+        d=json.loads(l); print(f, d.get('ab',''), d['n'], d['repeat'], {k:(d[k].get('frac_pipe'), d[k].get('frac_hbm')) for k in ('resident','streaming','auto') if k in d})
 PY
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_update -o $O/prof_f32tc \
-  python tools/ncu_configs.py 16:f32:262144:100:resident 32:f32:65536:100:resident > $O/ncu.log 2>&1; tail -1 $O/ncu.log
-ncu -i $O/prof_f32tc.ncu-rep --page raw --csv > $O/prof_f32tc_raw.csv 2>/dev/null
