@@ -590,16 +590,22 @@ JM_HD constexpr bool prefetch_for(int n, int dtype) {
 #ifndef JM_F32TC_MAXN
 #define JM_F32TC_MAXN 64
 #endif
+#ifndef JM_F32TC_16
+#define JM_F32TC_16 0   // 1: n = 16 too (measurement hook)
+#endif
 // m-tiles (16 rows) per warp: the warps of a matrix split its rows (WPM =
 // (n / 16) / MTW warps per matrix, a named barrier per matrix); each warp
 // keeps its m-tiles' accumulators and A splits in registers
 #ifndef JM_F32TC_MTW
 #define JM_F32TC_MTW 0    // > 0: one value for every size
 #endif
-// n = 16, 32, 64 (profiles/r02_f32tc.md: 0.72 -> 0.74, 0.77 -> 0.93, 0.78 -> 0.94
-// of the FP32 pipe at R = 100); n = 48 stays on the FFMA2 tiles (three warps
-// per matrix reach 0.66 against 0.76)
-JM_HD constexpr bool f32tc_use(int n) { return JM_F32TC && n % 16 == 0 && n <= JM_F32TC_MAXN && n != 48; }
+// n = 32, 64 (profiles/r02_f32tc.md: 0.77 -> 0.91, 0.78 -> 0.94 of the FP32
+// pipe at R = 100, with the non-finite check); n = 48 stays on the FFMA2 tiles
+// (three warps per matrix reach 0.66 against 0.76), and so does n = 16 (two
+// accumulator fragments per warp: 0.69 with the check against 0.72)
+JM_HD constexpr bool f32tc_use(int n) {
+  return JM_F32TC && n % 16 == 0 && n <= JM_F32TC_MAXN && n != 48 && (n != 16 || JM_F32TC_16);
+}
 JM_HD constexpr int f32tc_mtw(int n) {
   return (JM_F32TC_MTW > 0 && (n / 16) % JM_F32TC_MTW == 0) ? JM_F32TC_MTW : n <= 32 ? n / 16 : 2;   // (n = 64: two warps, 0.94 vs 0.89 for four)
 }
@@ -738,11 +744,11 @@ JM_HD constexpr int f64t_rn(int n) { return JM_F64T_RN > 0 ? JM_F64T_RN : n <= 1
 #ifndef JM_F32T_RN
 #define JM_F32T_RN 0
 #endif
-constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 2, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 50, 1048576, 12, 50, 50, 1048576, 1048576, 50, 24, 8, 8, 8, 1048576, 50, 1048576, 1048576, 12, 50, 1048576, 1048576, 1048576, 50, 50, 50, 3};
-// (n = 16, 32, 64: the resident kernel is the tensor-core kind, run_f32tc,
-// which ties the streaming tiles at R = 3 and wins above (R = 8: 0.65 vs 0.58,
-// 0.82 vs 0.74, 0.83 vs 0.75 of the pipe; profiles/r02_f32tc.md), so they
-// stream at R <= 2 (n = 64: R <= 3))
+constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 24, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 50, 1048576, 12, 50, 50, 1048576, 1048576, 50, 24, 8, 8, 8, 1048576, 50, 1048576, 1048576, 12, 50, 1048576, 1048576, 1048576, 50, 50, 50, 3};
+// (n = 32, 64: the resident kernel is the tensor-core kind, run_f32tc,
+// which ties the streaming tiles at R = 3 and wins above (R = 8: 0.82 vs 0.74,
+// 0.83 vs 0.75 of the pipe; profiles/r02_f32tc.md), so they stream at R <= 2
+// (n = 64: R <= 3))
 JM_HD constexpr int f32t_rn(int n) {
   return JM_F32T_RN > 0 ? JM_F32T_RN
          : F32T_STREAM_MAXR[n] >= (1 << 20) ? (1 << 30)

@@ -1329,6 +1329,14 @@ __device__ __forceinline__ void run_f32p(const float *__restrict__ in, float *__
 __device__ __forceinline__ void bar_named(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// named barrier that also ORs a predicate over its threads
+__device__ __forceinline__ bool bar_red_or(int id, int nthreads, bool v) {
+  unsigned r;
+  asm volatile("{\n\t.reg .pred q, p;\n\tsetp.ne.u32 q, %1, 0;\n\tbarrier.red.or.pred p, %2, %3, q;\n\t"
+               "selp.u32 %0, 1, 0, p;\n\t}"
+               : "=r"(r) : "r"((unsigned)v), "r"(id), "r"(nthreads) : "memory");
+  return r != 0;
+}
 // 32-bit shared-window addresses throughout: NVRTC otherwise keeps the
 // work-area pointers as 64-bit generic addresses (r02: 166 vs 132 registers
 // for the same n = 32 kernel built by nvcc, which infers the shared space)
@@ -1854,6 +1862,9 @@ __device__ __forceinline__ void run_f64t(const double *__restrict__ in, double *
 #ifndef JM_F32TC_LORND
 #define JM_F32TC_LORND 0
 #endif
+#ifndef JM_F32TC_SAFE
+#define JM_F32TC_SAFE 1   // 0: no non-finite check (timing experiment only: infinities come out NaN)
+#endif
 // (hi is formed as x - (x - mask(x)), exactly mask(x): ptxas knows the mma
 // ignores the low bits, so a plain mask operand became the raw accumulator and
 // the permuted A quad was rebuilt with four MOVs at every use; the FADD result
@@ -1947,7 +1958,48 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
                 else mma_tf32(acc[I][J], ah[I][KS], bh[J][0], bh[J][1]);
               }
         }
-        msync();   // every read of w done before the next publish
+        // Non-finite values: the split of an infinity is inf + NaN, and
+        // inf * (a zero lo part) is NaN where FP32 arithmetic gives inf, so a
+        // matrix whose P is not finite (an infinite or NaN input, or an
+        // overflow) redoes this update as the plain FP32 FMA chain from the
+        // published M (k ascending, p = M first: the other kinds' order), and
+        // its infinities and NaNs fall where the oracle's do.
+        bool bad = false;
+#pragma unroll
+        for (int I = 0; I < (JM_F32TC_SAFE ? MT : 0); ++I)
+#pragma unroll
+          for (int J = 0; J < NT8; ++J)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) bad |= !(fabsf(acc[I][J][q]) <= 3.402823466e38f);
+        bool anybad;
+        if constexpr (WPM == 1) {
+          anybad = __any_sync(0xffffffffu, bad);
+          __syncwarp();   // every read of w done before the next publish
+        } else {
+          anybad = bar_red_or(1 + mi, 32 * WPM, bad);   // (the same barrier, with the vote)
+        }
+        if (anybad) {   // (rare: rolled loops, P through the matrix's idle stage slot)
+#pragma unroll 1
+          for (int e = lane; e < 16 * MT * N; e += 32) {
+            const int row = r0 + e / N, col = e - (e / N) * N;
+            float pv = w[row * LD + col];
+#pragma unroll 1
+            for (int k = 0; k < N; ++k) pv = fmaT(w[row * LD + k], w[k * LD + col], pv);
+            sm[row * N + col] = pv;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int I = 0; I < MT; ++I)
+#pragma unroll
+            for (int J = 0; J < NT8; ++J)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const float2 v = *reinterpret_cast<const float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t);
+                acc[I][J][2 * h] = v.x;
+                acc[I][J][2 * h + 1] = v.y;
+              }
+          msync();
+        }
 #pragma unroll
         for (int I = 0; I < MT; ++I)
 #pragma unroll

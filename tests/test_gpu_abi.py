@@ -110,8 +110,8 @@ def test_key_info_reports_registers(jm):
     assert info[(64, 1, 0)]["tile_name"] == "cta_dmma"
     assert info[(4, 1, 0)]["tile_name"] == "tpm"
     assert info[(15, 0, 0)]["tile_name"] == "f32_rows"
-    assert info[(16, 0, 0)]["tile_name"] == "f32_tc"        # FP32 on the tensor cores (3xTF32)
-    assert info[(32, 0, 0)]["tile_name"] == "f32_tc"
+    assert info[(16, 0, 0)]["tile_name"] == "warp_f32"
+    assert info[(32, 0, 0)]["tile_name"] == "f32_tc"        # FP32 on the tensor cores (3xTF32)
     for k in info.values():
         assert k["local_bytes"] == 0, f"spill in {k}"
 

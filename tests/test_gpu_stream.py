@@ -57,8 +57,8 @@ def _same_bits(n, dt):
     # f64 n = 9 / 10 and f32 n = 12..14, whose resident kernel is thread per
     # matrix with a staged product (TPMS) and whose low-repeat kernel is the
     # DMMA ring / the row-panel ring, and the DFMA register-tile sizes, and
-    # f32 n = 16 / 32 / 64, whose resident kernel runs on the tensor cores (3xTF32)
-    return not ((dt == "f64" and n in (9, 10, 33, 34) + F64_REG_N) or (dt == "f32" and n in (12, 13, 14, 16, 32, 64)))
+    # f32 n = 32 / 64, whose resident kernel runs on the tensor cores (3xTF32)
+    return not ((dt == "f64" and n in (9, 10, 33, 34) + F64_REG_N) or (dt == "f32" and n in (12, 13, 14, 32, 64)))
 
 
 def test_f64_reg_sizes_match_the_plan(jm):
@@ -157,8 +157,8 @@ def test_variant_selection_and_key_info(jm):
     assert jm.jit_mat_prepare_for(15, "f32", 4) == 0
     assert jm.jit_mat_prepare_for(12, "f32", 1) == 0       # TPMS beats the ring even at R = 1
     assert jm.jit_mat_prepare_for(13, "f32", 1) == 1 and jm.jit_mat_prepare_for(13, "f32", 2) == 0
-    assert jm.jit_mat_prepare_for(16, "f32", 2) == 1       # n = 16: streaming register tiles to R = 2,
-    assert jm.jit_mat_prepare_for(16, "f32", 3) == 0       # then the tensor-core kind (profiles/r02_f32tc.md)
+    assert jm.jit_mat_prepare_for(16, "f32", 24) == 1      # n = 16: register tiles, streaming to R = 24
+    assert jm.jit_mat_prepare_for(16, "f32", 25) == 0
     # FP32 tiles: stream while R <= F32T_STREAM_MAXR[n] (jm_plan.h f32t_rn)
     assert jm.jit_mat_prepare_for(64, "f32", 3) == 1 and jm.jit_mat_prepare_for(64, "f32", 4) == 0   # (tensor cores above)
     assert jm.jit_mat_prepare_for(47, "f32", 50) == 1 and jm.jit_mat_prepare_for(47, "f32", 51) == 0
