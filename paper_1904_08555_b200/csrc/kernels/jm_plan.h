@@ -599,21 +599,31 @@ JM_HD constexpr bool prefetch_for(int n, int dtype) {
 #ifndef JM_F32TC_MTW
 #define JM_F32TC_MTW 0    // > 0: one value for every size
 #endif
-// n = 32, 64 (profiles/r02_f32tc.md: 0.77 -> 0.91, 0.78 -> 0.94 of the FP32
-// pipe at R = 100, with the non-finite check); n = 48 stays on the FFMA2 tiles
-// (three warps per matrix reach 0.66 against 0.76), and so does n = 16 (two
-// accumulator fragments per warp: 0.69 with the check against 0.72)
+// n = 32, 40, 48, 56, 64 (profiles/r02_f32tc.md, fraction of the FP32 pipe
+// at R = 100, with the non-finite check, FFMA2 tiles in brackets: 0.91 (0.77),
+// 0.82 (0.66), 0.97 (0.76), 0.84 (0.66), 0.94 (0.78)); n = 16 (two accumulator
+// fragments per warp: 0.69 against 0.72) and n = 24 (a half-padding m-tile:
+// 0.67 against 0.73) stay on the FFMA2 tiles
+#ifndef JM_F32TC_ALL
+#define JM_F32TC_ALL 0   // 1: every multiple of 8 in 24..JM_F32TC_MAXN (measurement hook)
+#endif
 JM_HD constexpr bool f32tc_use(int n) {
-  return JM_F32TC && n % 16 == 0 && n <= JM_F32TC_MAXN && n != 48 && (n != 16 || JM_F32TC_16);
+  return JM_F32TC && n <= JM_F32TC_MAXN &&
+         ((n % 8 == 0 && n >= 32) || (n == 16 && JM_F32TC_16) || (JM_F32TC_ALL && n % 8 == 0 && n >= 24));
 }
+// (n a multiple of 8 but not of 16: the last m-tile is half padding rows,
+// which never reach a real row: A row m only feeds P row m, and B reads rows k < n)
+JM_HD constexpr int f32tc_mt(int n) { return (n + 15) / 16; }                                  // m-tiles of a matrix
 JM_HD constexpr int f32tc_mtw(int n) {
-  return (JM_F32TC_MTW > 0 && (n / 16) % JM_F32TC_MTW == 0) ? JM_F32TC_MTW : n <= 32 ? n / 16 : 2;   // (n = 64: two warps, 0.94 vs 0.89 for four)
+  return (JM_F32TC_MTW > 0 && f32tc_mt(n) % JM_F32TC_MTW == 0) ? JM_F32TC_MTW
+         : n <= 48 ? f32tc_mt(n) : 2;   // one warp per matrix up to n = 48 (48: 0.97 vs 0.66 for three
+                                        // warps, 40: 0.82 vs 0.54), two above (64: 0.94 vs 0.89 for four)
 }
-JM_HD constexpr int f32tc_wpm(int n) { return n / 16 / f32tc_mtw(n); }                       // warps per matrix
+JM_HD constexpr int f32tc_wpm(int n) { return f32tc_mt(n) / f32tc_mtw(n); }                  // warps per matrix
 JM_HD constexpr int f32tc_mpc(int n) { return f32tc_wpm(n) >= 4 ? 1 : 4 / f32tc_wpm(n); }   // matrices per CTA
 JM_HD constexpr int f32tc_wpc(int n) { return f32tc_wpm(n) * f32tc_mpc(n); }
 JM_HD constexpr int f32tc_ld(int n) { return n + 4; }   // publish row stride (floats): B loads conflict free
-JM_HD constexpr int f32tc_wbytes(int n) { return n * f32tc_ld(n) * 4; }
+JM_HD constexpr int f32tc_wbytes(int n) { return 16 * f32tc_mt(n) * f32tc_ld(n) * 4; }
 
 JM_HD constexpr Plan plan_specialized(int n, int dtype) {
   const int es = dtype == 1 ? 8 : 4;
@@ -744,11 +754,11 @@ JM_HD constexpr int f64t_rn(int n) { return JM_F64T_RN > 0 ? JM_F64T_RN : n <= 1
 #ifndef JM_F32T_RN
 #define JM_F32T_RN 0
 #endif
-constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 24, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 50, 1048576, 12, 50, 50, 1048576, 1048576, 50, 24, 8, 8, 8, 1048576, 50, 1048576, 1048576, 12, 50, 1048576, 1048576, 1048576, 50, 50, 50, 3};
-// (n = 32, 64: the resident kernel is the tensor-core kind, run_f32tc,
-// which ties the streaming tiles at R = 3 and wins above (R = 8: 0.82 vs 0.74,
-// 0.83 vs 0.75 of the pipe; profiles/r02_f32tc.md), so they stream at R <= 2
-// (n = 64: R <= 3))
+constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 24, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 2, 1048576, 12, 50, 50, 1048576, 1048576, 50, 2, 8, 8, 8, 1048576, 50, 1048576, 1048576, 2, 50, 1048576, 1048576, 1048576, 50, 50, 50, 3};
+// (n = 32, 40, 48, 56, 64: the resident kernel is the tensor-core kind,
+// run_f32tc, which ties the streaming tiles at R = 3 and wins above (R = 8:
+// 0.82 vs 0.74, 0.73 vs 0.61, 0.84 vs 0.70, 0.78 vs 0.64, 0.83 vs 0.75 of the
+// pipe; profiles/r02_f32tc.md), so they stream at R <= 2 (n = 64: R <= 3))
 JM_HD constexpr int f32t_rn(int n) {
   return JM_F32T_RN > 0 ? JM_F32T_RN
          : F32T_STREAM_MAXR[n] >= (1 << 20) ? (1 << 30)

@@ -1885,7 +1885,7 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], 
 template <int N, Addend A>
 __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *__restrict__ out,
                                           long long batch, int repeat) {
-  static_assert(N % 16 == 0, "m16 tiles");
+  static_assert(N % 8 == 0, "m16n8 tiles (the last m-tile may be half padding)");
   // MT m-tiles of this warp (MTW of the matrix's N/16; WPM warps per matrix)
   constexpr int MT = f32tc_mtw(N), WPM = f32tc_wpm(N), NT8 = N / 8, LD = f32tc_ld(N), MPC = f32tc_mpc(N);
   constexpr int NT = 32 * f32tc_wpc(N), SB = stage_stride(N, 4);
@@ -1899,7 +1899,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
     else bar_named(1 + mi, 32 * WPM);
   };
   Stager<N, 4, SB, NT, MPC, AL, false> sg(in, out, batch, smem);
-  float *w = reinterpret_cast<float *>(smem + Stager<N, 4, SB, NT, MPC, AL, false>::BYTES) + mi * N * LD;
+  float *w = reinterpret_cast<float *>(smem + Stager<N, 4, SB, NT, MPC, AL, false>::BYTES) + mi * (16 * f32tc_mt(N)) * LD;
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
     const bool live = mi < sg.cnt();
@@ -1912,7 +1912,9 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
         for (int J = 0; J < NT8; ++J)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const float2 v = *reinterpret_cast<const float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t);
+            const float2 v = (N % 16 == 0 || r0 + 16 * I + 8 * h < N)
+                                ? *reinterpret_cast<const float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t)
+                                : make_float2(0.0f, 0.0f);
             acc[I][J][2 * h] = v.x;
             acc[I][J][2 * h + 1] = v.y;
           }
@@ -1982,6 +1984,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
 #pragma unroll 1
           for (int e = lane; e < 16 * MT * N; e += 32) {
             const int row = r0 + e / N, col = e - (e / N) * N;
+            if (N % 16 != 0 && row >= N) break;   // (padding rows: rows only grow with e)
             float pv = w[row * LD + col];
 #pragma unroll 1
             for (int k = 0; k < N; ++k) pv = fmaT(w[row * LD + k], w[k * LD + col], pv);
@@ -1994,7 +1997,9 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
             for (int J = 0; J < NT8; ++J)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                const float2 v = *reinterpret_cast<const float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t);
+                const float2 v = (N % 16 == 0 || r0 + 16 * I + 8 * h < N)
+                                    ? *reinterpret_cast<const float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t)
+                                    : make_float2(0.0f, 0.0f);
                 acc[I][J][2 * h] = v.x;
                 acc[I][J][2 * h + 1] = v.y;
               }
@@ -2017,8 +2022,9 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
         for (int J = 0; J < NT8; ++J)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            *reinterpret_cast<float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t) =
-                make_float2(acc[I][J][2 * h], acc[I][J][2 * h + 1]);
+            if (N % 16 == 0 || r0 + 16 * I + 8 * h < N)
+              *reinterpret_cast<float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t) =
+                  make_float2(acc[I][J][2 * h], acc[I][J][2 * h + 1]);
     }
     sg.release();
   }

@@ -57,8 +57,8 @@ def _same_bits(n, dt):
     # f64 n = 9 / 10 and f32 n = 12..14, whose resident kernel is thread per
     # matrix with a staged product (TPMS) and whose low-repeat kernel is the
     # DMMA ring / the row-panel ring, and the DFMA register-tile sizes, and
-    # f32 n = 32 / 64, whose resident kernel runs on the tensor cores (3xTF32)
-    return not ((dt == "f64" and n in (9, 10, 33, 34) + F64_REG_N) or (dt == "f32" and n in (12, 13, 14, 32, 64)))
+    # f32 n = 32, 40, 48, 56, 64, whose resident kernel runs on the tensor cores (3xTF32)
+    return not ((dt == "f64" and n in (9, 10, 33, 34) + F64_REG_N) or (dt == "f32" and n in (12, 13, 14, 32, 40, 48, 56, 64)))
 
 
 def test_f64_reg_sizes_match_the_plan(jm):
