@@ -754,11 +754,12 @@ JM_HD constexpr int f64t_rn(int n) { return JM_F64T_RN > 0 ? JM_F64T_RN : n <= 1
 #ifndef JM_F32T_RN
 #define JM_F32T_RN 0
 #endif
-constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 24, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 2, 1048576, 12, 50, 50, 1048576, 1048576, 50, 2, 8, 8, 8, 1048576, 50, 1048576, 1048576, 2, 50, 1048576, 1048576, 1048576, 50, 50, 50, 3};
+constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 24, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 1, 1048576, 12, 50, 50, 1048576, 1048576, 50, 1, 8, 8, 8, 1048576, 50, 1048576, 1048576, 1, 50, 1048576, 1048576, 1048576, 50, 50, 50, 3};
 // (n = 32, 40, 48, 56, 64: the resident kernel is the tensor-core kind,
-// run_f32tc, which ties the streaming tiles at R = 3 and wins above (R = 8:
-// 0.82 vs 0.74, 0.73 vs 0.61, 0.84 vs 0.70, 0.78 vs 0.64, 0.83 vs 0.75 of the
-// pipe; profiles/r02_f32tc.md), so they stream at R <= 2 (n = 64: R <= 3))
+// run_f32tc; measured crossovers (profiles/r02_f32tc_xover*.jsonl): n = 32 and
+// 64 tie the streaming tiles at R = 3, n = 40, 48, 56 win from R = 2 (0.58 vs
+// 0.49, 0.64 vs 0.62, 0.66 vs 0.60 of the pipe) — so 32 streams at R <= 2,
+// 64 at R <= 3, 40 / 48 / 56 at R = 1 only)
 JM_HD constexpr int f32t_rn(int n) {
   return JM_F32T_RN > 0 ? JM_F32T_RN
          : F32T_STREAM_MAXR[n] >= (1 << 20) ? (1 << 30)
