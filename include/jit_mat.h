@@ -293,7 +293,7 @@ enum { JM_TILE_GENERIC = 0, JM_TILE_TPM = 1, JM_TILE_WARP_DMMA = 2, JM_TILE_CTA_
        JM_TILE_F32_ROWS = 10 /* FP32 row panels: 4 threads per matrix own full rows (n = 15, 16) */,
        JM_TILE_F64_REG = 11 /* FP64 register tiles with DFMA (sizes DMMA pads badly) */,
        JM_TILE_LAT = 12 /* latency kernel: a warp per matrix, an element per lane (tiny batches) */,
-       JM_TILE_F32_TC = 13 /* FP32 on the tensor cores: m16n8k8 TF32 mma, operands split hi + lo (3xTF32; n = 32, 40, 48, 56, 64) */ };
+       JM_TILE_F32_TC = 13 /* FP32 on the tensor cores: m16n8k8 TF32 mma, operands split hi + lo (3xTF32; n = 32 and 37..64, zero-padded to a multiple of 8) */ };
 
 JM_API int jit_mat_stats(jm_stats *out);
 /* Copy up to `cap` non-empty slots into `keys`; returns the number of

@@ -607,22 +607,31 @@ JM_HD constexpr bool prefetch_for(int n, int dtype) {
 #ifndef JM_F32TC_ALL
 #define JM_F32TC_ALL 0   // 1: every multiple of 8 in 24..JM_F32TC_MAXN (measurement hook)
 #endif
+// n >= JM_F32TC_ODD that are not multiples of 8 take it too, zero-padded to
+// 8*ceil(n/8) (profiles/r02_f32tc.md, R = 100: 38 0.60 -> 0.69, 41 0.55 ->
+// 0.59, 44 0.65 -> 0.74, 47 0.73 -> 0.90, 50 0.56 -> 0.60, 53 0.59 -> 0.69,
+// 57 0.59 -> 0.65, 60 0.65 -> 0.78, 63 0.73 -> 0.88; n = 35, padded to 40,
+// loses: 0.67 -> 0.55).  0: off.
+#ifndef JM_F32TC_ODD
+#define JM_F32TC_ODD 37
+#endif
 JM_HD constexpr bool f32tc_use(int n) {
   return JM_F32TC && n <= JM_F32TC_MAXN &&
-         ((n % 8 == 0 && n >= 32) || (n == 16 && JM_F32TC_16) || (JM_F32TC_ALL && n % 8 == 0 && n >= 24));
+         ((n % 8 == 0 && n >= 32) || (n == 16 && JM_F32TC_16) || (JM_F32TC_ALL && n % 8 == 0 && n >= 24) ||
+          (JM_F32TC_ODD > 0 && n % 8 != 0 && n >= JM_F32TC_ODD));
 }
 // (n a multiple of 8 but not of 16: the last m-tile is half padding rows,
 // which never reach a real row: A row m only feeds P row m, and B reads rows k < n)
-JM_HD constexpr int f32tc_mt(int n) { return (n + 15) / 16; }                                  // m-tiles of a matrix
+JM_HD constexpr int f32tc_mt(int n) { return ((n + 7) / 8 * 8 + 15) / 16; }                                  // m-tiles of a matrix
 JM_HD constexpr int f32tc_mtw(int n) {
   return (JM_F32TC_MTW > 0 && f32tc_mt(n) % JM_F32TC_MTW == 0) ? JM_F32TC_MTW
-         : n <= 48 ? f32tc_mt(n) : 2;   // one warp per matrix up to n = 48 (48: 0.97 vs 0.66 for three
+         : n <= 48 ? f32tc_mt(n) : f32tc_mt(n) % 2 == 0 ? 2 : 1;   // one warp per matrix up to n = 48 (48: 0.97 vs 0.66 for three
                                         // warps, 40: 0.82 vs 0.54), two above (64: 0.94 vs 0.89 for four)
 }
 JM_HD constexpr int f32tc_wpm(int n) { return f32tc_mt(n) / f32tc_mtw(n); }                  // warps per matrix
 JM_HD constexpr int f32tc_mpc(int n) { return f32tc_wpm(n) >= 4 ? 1 : 4 / f32tc_wpm(n); }   // matrices per CTA
 JM_HD constexpr int f32tc_wpc(int n) { return f32tc_wpm(n) * f32tc_mpc(n); }
-JM_HD constexpr int f32tc_ld(int n) { return n + 4; }   // publish row stride (floats): B loads conflict free
+JM_HD constexpr int f32tc_ld(int n) { return (n + 7) / 8 * 8 + 4; }   // publish row stride (floats): B loads conflict free
 JM_HD constexpr int f32tc_wbytes(int n) { return 16 * f32tc_mt(n) * f32tc_ld(n) * 4; }
 
 JM_HD constexpr Plan plan_specialized(int n, int dtype) {
@@ -754,12 +763,14 @@ JM_HD constexpr int f64t_rn(int n) { return JM_F64T_RN > 0 ? JM_F64T_RN : n <= 1
 #ifndef JM_F32T_RN
 #define JM_F32T_RN 0
 #endif
-constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 24, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 50, 1048576, 1048576, 1, 1048576, 12, 50, 50, 1048576, 1048576, 50, 1, 8, 8, 8, 1048576, 50, 1048576, 1048576, 1, 50, 1048576, 1048576, 1048576, 50, 50, 50, 3};
+constexpr int F32T_STREAM_MAXR[65] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 24, 6, 10, 8, 50, 50, 12, 8, 10, 8, 50, 1048576, 12, 1048576, 50, 1048576, 2, 8, 1048576, 24, 1048576, 4, 4, 4, 1, 4, 4, 4, 4, 4, 4, 4, 1, 4, 4, 4, 4, 4, 4, 4, 1, 8, 8, 8, 8, 8, 8, 8, 3};
 // (n = 32, 40, 48, 56, 64: the resident kernel is the tensor-core kind,
 // run_f32tc; measured crossovers (profiles/r02_f32tc_xover*.jsonl): n = 32 and
 // 64 tie the streaming tiles at R = 3, n = 40, 48, 56 win from R = 2 (0.58 vs
 // 0.49, 0.64 vs 0.62, 0.66 vs 0.60 of the pipe) — so 32 streams at R <= 2,
-// 64 at R <= 3, 40 / 48 / 56 at R = 1 only)
+// 64 at R <= 3, 40 / 48 / 56 at R = 1 only; the zero-padded sizes 37..63
+// stream to R = 4 (<= 56) / 8 (57..63): at R = 8 the padded kernel wins
+// except n = 57 (0.51 vs 0.55) and 63 (a tie))
 JM_HD constexpr int f32t_rn(int n) {
   return JM_F32T_RN > 0 ? JM_F32T_RN
          : F32T_STREAM_MAXR[n] >= (1 << 20) ? (1 << 30)

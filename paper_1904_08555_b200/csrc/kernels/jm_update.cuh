@@ -1885,9 +1885,11 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], 
 template <int N, Addend A>
 __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *__restrict__ out,
                                           long long batch, int repeat) {
-  static_assert(N % 8 == 0, "m16n8 tiles (the last m-tile may be half padding)");
+  // (n not a multiple of 8: M is held zero-padded to NP = 8*ceil(n/8), the
+  // padding re-zeroed by every epilogue, so it never reaches a real entry)
+  constexpr int NP = (N + 7) / 8 * 8;
   // MT m-tiles of this warp (MTW of the matrix's N/16; WPM warps per matrix)
-  constexpr int MT = f32tc_mtw(N), WPM = f32tc_wpm(N), NT8 = N / 8, LD = f32tc_ld(N), MPC = f32tc_mpc(N);
+  constexpr int MT = f32tc_mtw(N), WPM = f32tc_wpm(N), NT8 = NP / 8, LD = f32tc_ld(N), MPC = f32tc_mpc(N);
   constexpr int NT = 32 * f32tc_wpc(N), SB = stage_stride(N, 4);
   constexpr bool AL = ((MPC * N * N * 4) % 16) == 0;
   extern __shared__ __align__(16) char smem[];
@@ -1899,6 +1901,14 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
     else bar_named(1 + mi, 32 * WPM);
   };
   Stager<N, 4, SB, NT, MPC, AL, false> sg(in, out, batch, smem);
+  // entries (row, col), (row, col + 1) of the staged (packed, row stride N) matrix; zero outside it
+  auto ld2 = [&](const float *sm, int row, int col) {
+    if constexpr (N % 8 == 0) {
+      return (N % 16 == 0 || row < N) ? *reinterpret_cast<const float2 *>(sm + row * N + col) : make_float2(0.0f, 0.0f);
+    } else {
+      return make_float2(row < N && col < N ? sm[row * N + col] : 0.0f, row < N && col + 1 < N ? sm[row * N + col + 1] : 0.0f);
+    }
+  };
   float *w = reinterpret_cast<float *>(smem + Stager<N, 4, SB, NT, MPC, AL, false>::BYTES) + mi * (16 * f32tc_mt(N)) * LD;
   for (sg.start(); sg.valid(); sg.next()) {
     sg.acquire();
@@ -1912,9 +1922,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
         for (int J = 0; J < NT8; ++J)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const float2 v = (N % 16 == 0 || r0 + 16 * I + 8 * h < N)
-                                ? *reinterpret_cast<const float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t)
-                                : make_float2(0.0f, 0.0f);
+            const float2 v = ld2(sm, r0 + 16 * I + g + 8 * h, 8 * J + 2 * t);
             acc[I][J][2 * h] = v.x;
             acc[I][J][2 * h + 1] = v.y;
           }
@@ -1997,9 +2005,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
             for (int J = 0; J < NT8; ++J)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                const float2 v = (N % 16 == 0 || r0 + 16 * I + 8 * h < N)
-                                    ? *reinterpret_cast<const float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t)
-                                    : make_float2(0.0f, 0.0f);
+                const float2 v = ld2(sm, r0 + 16 * I + g + 8 * h, 8 * J + 2 * t);
                 acc[I][J][2 * h] = v.x;
                 acc[I][J][2 * h + 1] = v.y;
               }
@@ -2014,6 +2020,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
               const int row = r0 + 16 * I + g + 8 * (q >> 1), col = 8 * J + 2 * t + (q & 1);
               const float a = (A == Addend::Ones || row == col) ? 1.0f : 0.0f;
               acc[I][J][q] = fmaT(c, acc[I][J][q], a);
+              if constexpr (N % 8 != 0) acc[I][J][q] = (row < N && col < N) ? acc[I][J][q] : 0.0f;
             }
       }
 #pragma unroll
@@ -2021,10 +2028,16 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
 #pragma unroll
         for (int J = 0; J < NT8; ++J)
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (N % 16 == 0 || r0 + 16 * I + 8 * h < N)
-              *reinterpret_cast<float2 *>(sm + (r0 + 16 * I + g + 8 * h) * N + 8 * J + 2 * t) =
-                  make_float2(acc[I][J][2 * h], acc[I][J][2 * h + 1]);
+          for (int h = 0; h < 2; ++h) {
+            const int row = r0 + 16 * I + g + 8 * h, col = 8 * J + 2 * t;
+            if constexpr (N % 8 == 0) {
+              if (N % 16 == 0 || row < N)
+                *reinterpret_cast<float2 *>(sm + row * N + col) = make_float2(acc[I][J][2 * h], acc[I][J][2 * h + 1]);
+            } else {
+              if (row < N && col < N) sm[row * N + col] = acc[I][J][2 * h];
+              if (row < N && col + 1 < N) sm[row * N + col + 1] = acc[I][J][2 * h + 1];
+            }
+          }
     }
     sg.release();
   }

@@ -57,8 +57,8 @@ def _same_bits(n, dt):
     # f64 n = 9 / 10 and f32 n = 12..14, whose resident kernel is thread per
     # matrix with a staged product (TPMS) and whose low-repeat kernel is the
     # DMMA ring / the row-panel ring, and the DFMA register-tile sizes, and
-    # f32 n = 32, 40, 48, 56, 64, whose resident kernel runs on the tensor cores (3xTF32)
-    return not ((dt == "f64" and n in (9, 10, 33, 34) + F64_REG_N) or (dt == "f32" and n in (12, 13, 14, 32, 40, 48, 56, 64)))
+    # f32 n = 32 and 37..64, whose resident kernel runs on the tensor cores (3xTF32)
+    return not ((dt == "f64" and n in (9, 10, 33, 34) + F64_REG_N) or (dt == "f32" and (n in (12, 13, 14, 32) or n >= 37)))
 
 
 def test_f64_reg_sizes_match_the_plan(jm):
@@ -161,7 +161,8 @@ def test_variant_selection_and_key_info(jm):
     assert jm.jit_mat_prepare_for(16, "f32", 25) == 0
     # FP32 tiles: stream while R <= F32T_STREAM_MAXR[n] (jm_plan.h f32t_rn)
     assert jm.jit_mat_prepare_for(64, "f32", 3) == 1 and jm.jit_mat_prepare_for(64, "f32", 4) == 0   # (tensor cores above)
-    assert jm.jit_mat_prepare_for(47, "f32", 50) == 1 and jm.jit_mat_prepare_for(47, "f32", 51) == 0
+    assert jm.jit_mat_prepare_for(47, "f32", 4) == 1 and jm.jit_mat_prepare_for(47, "f32", 5) == 0     # (tensor cores above)
+    assert jm.jit_mat_prepare_for(30, "f32", 50) == 1 and jm.jit_mat_prepare_for(30, "f32", 51) == 0
     assert jm.jit_mat_prepare_for(32, "f32", 2) == 1 and jm.jit_mat_prepare_for(32, "f32", 3) == 0   # (tensor cores)
     assert jm.jit_mat_prepare_for(17, "f32", 6) == 1 and jm.jit_mat_prepare_for(17, "f32", 7) == 0
     assert jm.jit_mat_prepare_for(8, "f64", 1) == 0        # n = 8 DMMA: resident (measured)
