@@ -68,7 +68,12 @@ def test_mass_writes_stay_in_bounds(jm, D, Q, E):
 @pytest.mark.parametrize("n,dt,R,variant", [(55, "f32", 1, "streaming"), (63, "f32", 1, "streaming"),
                                             (57, "f32", 2, "streaming"), (17, "f32", 1, "streaming"),
                                             (16, "f32", 1, "streaming"), (17, "f64", 3, "resident"),
-                                            (33, "f64", 1, "streaming"), (5, "f64", 2, "resident")])
+                                            (33, "f64", 1, "streaming"), (5, "f64", 2, "resident"),
+                                            # the tensor-core FP32 kind: padded last m-tile (40), zero-padded
+                                            # ragged rows (37, 47, 63), two warps per matrix (57, 64)
+                                            (37, "f32", 3, "resident"), (40, "f32", 3, "resident"),
+                                            (47, "f32", 3, "resident"), (57, "f32", 3, "resident"),
+                                            (63, "f32", 3, "resident"), (64, "f32", 3, "resident")])
 def test_update_writes_stay_in_bounds(jm, n, dt, R, variant):
     G, batch = 4, 37   # 4 guard matrices keep the view 16-B aligned for odd n
     tdt = torch.float64 if dt == "f64" else torch.float32

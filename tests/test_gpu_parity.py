@@ -138,7 +138,7 @@ def test_divergence_to_inf(jm, n, rep, kind):
         assert_parity(_gpu_run(jm, x, r, kind=kind), oracle.run(x, r), what=f"pre-divergence R={r}")
 
 
-@pytest.mark.parametrize("n", [17, 24, 32, 33, 48, 64])
+@pytest.mark.parametrize("n", [17, 24, 32, 33, 37, 40, 47, 48, 57, 63, 64])
 def test_f32_overflow_positions_match(jm, n):
     # FP32 paper init overflows within a few updates at these n; the tiles pad
     # to multiples of 8 / 4, and the padding must never leak NaN or inf into
