@@ -1863,7 +1863,7 @@ __device__ __forceinline__ void run_f64t(const double *__restrict__ in, double *
 #define JM_F32TC_LORND 0
 #endif
 #ifndef JM_F32TC_SAFE
-#define JM_F32TC_SAFE 1   // 0: no non-finite check (timing experiment only: infinities come out NaN)
+#define JM_F32TC_SAFE 1   // 0: no exact-path check (timing experiment only: wrong near overflow / infinities)
 #endif
 // (hi is formed as x - (x - mask(x)), exactly mask(x): ptxas knows the mma
 // ignores the low bits, so a plain mask operand became the raw accumulator and
@@ -1926,6 +1926,23 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
             acc[I][J][2 * h] = v.x;
             acc[I][J][2 * h + 1] = v.y;
           }
+      // Exact-path flag (matrix-uniform after the vote below): a matrix with
+      // an entry |m| > TM = 1 / (2 c n), or a non-finite one, is expanding
+      // (c (1 + 2|M|) > 1: every update amplifies earlier rounding errors),
+      // and the 3xTF32 products' small biased error then grows past the bound
+      // within a few updates (paper-init inputs: 2e-5 one update before they
+      // overflow, FFMA 3e-7; tools/tc_diag_paper.py); such an update runs as
+      // the plain FP32 FMA chain instead (k ascending, p = M first: the other
+      // kinds' order, so IEEE infinities and NaNs also fall where the
+      // oracle's do).  Contracting inputs (c rho < 1) never reach TM.
+      constexpr float TM = 0.5f / (0.00005f * N);
+      bool bad = false;
+#pragma unroll
+      for (int I = 0; I < (JM_F32TC_SAFE ? MT : 0); ++I)
+#pragma unroll
+        for (int J = 0; J < NT8; ++J)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) bad |= !(fabsf(acc[I][J][q]) <= TM);
       for (int r = 0; r < repeat; ++r) {
         // publish M (row-major, row stride LD) for the B operand
 #pragma unroll
@@ -1946,7 +1963,14 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
             for (int q = 0; q < 4; ++q) {
               tf32_split(acc[I][KS][q == 1 ? 2 : q == 2 ? 1 : q], ah[I][KS][q], al[I][KS][q]);
             }
-        msync();
+        bool exact;
+        if constexpr (WPM == 1) {
+          exact = __any_sync(0xffffffffu, bad);
+          __syncwarp();
+        } else {
+          exact = bar_red_or(1 + mi, 32 * WPM, bad);   // (the publish barrier, with the vote)
+        }
+        if (!exact) {
 #pragma unroll
         for (int KS = 0; KS < NT8; ++KS) {
           unsigned bh[NT8][2], bl[NT8][2];
@@ -1968,27 +1992,10 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
                 else mma_tf32(acc[I][J], ah[I][KS], bh[J][0], bh[J][1]);
               }
         }
-        // Non-finite values: the split of an infinity is inf + NaN, and
-        // inf * (a zero lo part) is NaN where FP32 arithmetic gives inf, so a
-        // matrix whose P is not finite (an infinite or NaN input, or an
-        // overflow) redoes this update as the plain FP32 FMA chain from the
-        // published M (k ascending, p = M first: the other kinds' order), and
-        // its infinities and NaNs fall where the oracle's do.
-        bool bad = false;
-#pragma unroll
-        for (int I = 0; I < (JM_F32TC_SAFE ? MT : 0); ++I)
-#pragma unroll
-          for (int J = 0; J < NT8; ++J)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) bad |= !(fabsf(acc[I][J][q]) <= 3.402823466e38f);
-        bool anybad;
-        if constexpr (WPM == 1) {
-          anybad = __any_sync(0xffffffffu, bad);
-          __syncwarp();   // every read of w done before the next publish
-        } else {
-          anybad = bar_red_or(1 + mi, 32 * WPM, bad);   // (the same barrier, with the vote)
         }
-        if (anybad) {   // (rare: rolled loops, P through the matrix's idle stage slot)
+        if constexpr (WPM == 1) __syncwarp();   // every read of w done before the next publish
+        else msync();
+        if (exact) {   // (rare: rolled loops, P through the matrix's idle stage slot)
 #pragma unroll 1
           for (int e = lane; e < 16 * MT * N; e += 32) {
             const int row = r0 + e / N, col = e - (e / N) * N;
@@ -2011,6 +2018,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
               }
           msync();
         }
+        bad = false;
 #pragma unroll
         for (int I = 0; I < MT; ++I)
 #pragma unroll
@@ -2021,6 +2029,7 @@ __device__ __forceinline__ void run_f32tc(const float *__restrict__ in, float *_
               const float a = (A == Addend::Ones || row == col) ? 1.0f : 0.0f;
               acc[I][J][q] = fmaT(c, acc[I][J][q], a);
               if constexpr (N % 8 != 0) acc[I][J][q] = (row < N && col < N) ? acc[I][J][q] : 0.0f;
+              if constexpr (JM_F32TC_SAFE) bad |= !(fabsf(acc[I][J][q]) <= TM);
             }
       }
 #pragma unroll
