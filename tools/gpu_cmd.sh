@@ -1,5 +1,5 @@
 # scratch driver for one gpurun call (overwritten per experiment; the committed copy is the last one run)
-# tensor-core FP32 kind with the |P| > 2^64 exact fallback: paper-init error, then the GPU suite
+# tensor-core FP32 kind with the expansion check (exact FP32 path when max|m| > 1/(2cn)): paper-init error, GPU suite, smoke, perf
 O=gpurun_out/s34; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 timeout 300 python tools/tc_diag_paper.py 2>&1 | tee $O/diag_paper.txt
